@@ -1,0 +1,329 @@
+"""Pins of the CPU oracle against things other than itself (-m "not gpu").
+
+Each test names the passage it follows.  Library routines (sklearn Murmur3,
+numpy mt19937), closed forms and brute force on explicitly sampled subgraphs
+(tests/brute.py) are the independent references.
+"""
+import json
+import math
+import os
+import struct
+
+import numpy as np
+import pytest
+from sklearn.utils import murmurhash3_32
+
+import oracle
+from tests import brute
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# ---------------------------------------------------------------- hashing (Eq. 4)
+def test_murmur3_matches_library():
+    """MurmurHash3 x86_32 (Eq. 4) vs sklearn.utils.murmurhash3_32."""
+    rng = np.random.default_rng(0)
+    assert oracle.murmur3_32(b"", 0) == 0
+    for _ in range(400):
+        ln = int(rng.integers(0, 18))
+        data = bytes(rng.integers(0, 256, ln, dtype=np.uint8))
+        seed = int(rng.integers(0, 2**32))
+        assert oracle.murmur3_32(data, seed) == murmurhash3_32(data, seed=seed, positive=True)
+
+
+def test_edge_hash_golden():
+    """h(u,v) = Murmur3(LE32 u || LE32 v, 0) mod 2^31 (Eq. 4, reading R4)."""
+    with open(os.path.join(GOLDEN, "edge_hash.json")) as f:
+        g = json.load(f)
+    for (u, v), h in zip(g["pairs"], g["hash"]):
+        assert oracle.edge_hash(u, v) == h == brute.edge_hash(u, v)
+    rng = np.random.default_rng(1)
+    for _ in range(300):
+        u, v = (int(x) for x in rng.integers(0, 2**31 - 1, 2))
+        h = oracle.edge_hash(u, v)
+        assert h == brute.edge_hash(u, v) and 0 <= h < 2**31
+    assert oracle.edge_hash(1, 2) != oracle.edge_hash(2, 1)  # directed
+
+
+# ---------------------------------------------------------------- mt19937 / salts
+def test_mt19937_matches_numpy_and_std_check_value():
+    """PAPER.md:472 names mt19937.  C++ [rand.predef]: 10000th draw of default seed 5489 = 4123659995."""
+    assert int(oracle.mt_draws(5489, 10000)[-1]) == 4123659995
+    for seed in (0, 1, 2, 5489, 2**32 - 1):
+        ref = np.random.RandomState(seed)._bit_generator.random_raw(2000).astype(np.uint32)
+        assert np.array_equal(oracle.mt_draws(seed, 2000), ref)
+
+
+def test_salts_stream():
+    """R2/R3: seed_V, seed_J, then X_r = draw & (2^31-1); values from the numpy stream."""
+    sv, sj, X = oracle.salts(1, 1024)
+    bv, bj, BX = brute.salts(1, 1024)
+    assert (sv, sj) == (bv, bj) == (1791095845, 4282876139)
+    assert np.array_equal(X, BX)
+    assert list(X[:4]) == [946286476, 1857819720, 491263, 550290313]
+    assert X.max() < 2**31
+    # J-prefix property (R3): sims 0..J1-1 identical for any J >= J1
+    assert np.array_equal(oracle.salts(1, 64)[2], X[:64])
+    # the C-ABI seed is uint64; only its low 32 bits seed mt19937 (R3)
+    assert np.array_equal(oracle.salts(1 + 2**32, 16)[2], X[:16])
+
+
+# ---------------------------------------------------------------- live test (Eq. 5)
+PAPER_W = [0.005, 0.01, 0.1, 0.05, 0.3, 0.5, 1.0, 0.0]
+
+
+def test_live_closed_forms():
+    """Eq. 5 strict '<': w = 0 never live; w = 1 live iff X xor h != h_max."""
+    rng = np.random.default_rng(2)
+    for _ in range(2000):
+        X, h = (int(x) for x in rng.integers(0, 2**31, 2))
+        assert not oracle.live(X, h, 0.0)
+        assert oracle.live(X, h, 1.0) == ((X ^ h) != brute.HMAX)
+    assert not oracle.live(0, brute.HMAX, 1.0)
+    assert oracle.live(5, 5, 1e-30)  # P = 0 < w
+
+
+def test_live_equals_exact_rational_threshold():
+    """The double-precision Eq. 5 vs the exact rational x/h_max < w, at and around every threshold."""
+    ws = PAPER_W + [1.0 / d for d in range(1, 400)] + list(np.random.default_rng(3).random(300))
+    for w in ws:
+        w32 = float(np.float32(w))
+        T = brute.threshold(w32)
+        for x in {0, T - 2, T - 1, T, T + 1, brute.HMAX - 1, brute.HMAX}:
+            if 0 <= x <= brute.HMAX:
+                assert oracle.live(x, 0, w32) == (x < T), (w32, x, T)
+    # printed integer thresholds (SURVEY finding 4)
+    assert [brute.threshold(w) for w in (0.005, 0.01, 0.05, 0.1, 1.0)] == [10737418, 21474836, 107374184, 214748368, 2147483647]
+
+
+def test_live_rate_and_capture_probability():
+    """Sampling rate within binomial 3 sigma; P(live in >= 1 of J=256 sims at w=0.005)
+    = 1-(1-0.005)^256 = 0.72."""
+    _, _, X = oracle.salts(1, 256)
+    rng = np.random.default_rng(4)
+    hs = rng.integers(0, 2**31, 4000)
+    L = np.array([[oracle.live(int(x), int(h), 0.1) for x in X[:64]] for h in hs[:1500]])
+    N = L.size
+    assert abs(L.mean() - 0.1) < 3 * math.sqrt(0.1 * 0.9 / N)
+    cap = np.array([any(oracle.live(int(x), int(h), 0.005) for x in X) for h in hs])
+    p = 1 - (1 - 0.005) ** 256
+    assert abs(p - 0.7229) < 1e-3
+    assert abs(cap.mean() - p) < 4 * math.sqrt(p * (1 - p) / len(hs))
+
+
+# ---------------------------------------------------------------- init (Alg. 1 lines 2-5)
+def test_init_registers_vs_library_hash():
+    """M_v[j] = clz(hash(v) xor hash(j)), R5/R6; clz via int.bit_length."""
+    for seed, n, J in ((1, 1000, 64), (7, 50, 256), (2**40 + 3, 20, 32)):
+        assert np.array_equal(oracle.init_registers(n, J, seed), brute.init_registers(n, J, seed))
+    M = oracle.init_registers(1000, 64, 1)
+    assert (M[0, 0], M[0, 1], M[1, 0], M[1, 63], M[999, 0]) == (0, 1, 3, 3, 1)
+    assert M.max() <= 32
+
+
+def test_init_geometric_tail():
+    """P(register >= k) = 2^-k for a uniform 32-bit word."""
+    M = oracle.init_registers(20000, 64, 9).astype(np.int64)
+    for k in range(1, 7):
+        frac = (M >= k).mean()
+        assert abs(frac - 2.0**-k) < 4 * math.sqrt(2.0**-k / M.size)
+
+
+# ---------------------------------------------------------------- estimate (Eq. 2)
+def test_estimate_closed_forms():
+    """e = 2^{mean}/phi, phi = 0.77351; SPEC.md:234-235 values."""
+    assert abs(oracle.estimate_row(np.zeros(64, np.uint8)) - 1.29281) < 1e-5
+    assert abs(oracle.estimate_row(np.full(256, 10, np.uint8)) - 1323.84) < 1e-2
+    assert oracle.estimate_row(np.array([0, 2], np.uint8)) == 2.0 / 0.77351
+    assert oracle.estimate_row(np.array([1, 2, 3, 6], np.uint8)) == 2.0**3 / 0.77351
+    rng = np.random.default_rng(5)
+    M = rng.integers(0, 33, (50, 96)).astype(np.uint8)
+    e = oracle.estimate(M)
+    for v in range(50):
+        assert abs(e[v] - brute.estimate(M[v])) <= 1e-12 * e[v]
+
+
+def test_estimate_bias_of_max_clz_register():
+    """Statistical check of Eq. 2 with this register definition (SURVEY finding 3): for a set of
+    c items, E[max clz] = sum_k 1-(1-2^-k)^c; the estimator is biased high (~1.6x at c >= 100)."""
+    rng = np.random.default_rng(6)
+    J = 256
+    for c in (100, 1000):
+        words = rng.integers(0, 2**32, (c, J), dtype=np.uint64)
+        regs = brute.clz32(words).max(axis=0)
+        ratio = oracle.estimate_row(regs) / c
+        expect = 2 ** sum(1 - (1 - 2.0**-k) ** c for k in range(1, 33)) / 0.77351 / c
+        assert 1.3 < ratio < 2.1 and abs(math.log(ratio / expect)) < 0.35
+
+
+# ---------------------------------------------------------------- Simulate (Alg. 2)
+def test_simulate_equals_bruteforce_reach_max():
+    """SPEC.md:500 acceptance #1: >= 100 random graphs (n <= 120), eps_c = 0: every converged
+    register equals the max init register over the reach set in the sampled subgraph."""
+    rng = np.random.default_rng(7)
+    for g in range(100):
+        n = int(rng.integers(2, 120))
+        m = int(rng.integers(0, 4 * n))
+        J = int(rng.choice([32, 64]))
+        seed = int(rng.integers(0, 2**32))
+        p = None if g % 3 == 0 else float(rng.choice([0.05, 0.2, 0.5, 1.0]))
+        off, tgt, pr = brute.random_graph(rng, n, m, p)
+        M, st = oracle.simulate(n, off, tgt, pr, J, seed)
+        assert np.array_equal(M, brute.registers(n, off, tgt, pr, J, seed)), g
+        assert st["changed"][-1] == 0
+
+
+def test_simulate_with_blocked_equals_bruteforce():
+    """Alg. 2 line 'u not in R_S[j]', reading R12: blocked u never pulls in sim j."""
+    rng = np.random.default_rng(8)
+    for g in range(30):
+        n = int(rng.integers(2, 80))
+        off, tgt, pr = brute.random_graph(rng, n, int(rng.integers(0, 4 * n)), float(rng.choice([0.3, 1.0])))
+        J = 32
+        seed = int(rng.integers(0, 2**32))
+        blocked = (rng.random((n, J)) < 0.3).astype(np.uint8)
+        M, _ = oracle.simulate(n, off, tgt, pr, J, seed, blocked=blocked)
+        assert np.array_equal(M, brute.registers(n, off, tgt, pr, J, seed, blocked=blocked.astype(bool)))
+
+
+def test_simulate_special_cases():
+    """No edges -> M unchanged after one sweep; path a->b->c with w = 1 -> pairwise max."""
+    n, J, seed = 5, 64, 3
+    M, st = oracle.simulate(n, np.zeros(n + 1, np.int32), np.zeros(0, np.int32), np.zeros(0, np.float32), J, seed)
+    assert np.array_equal(M, oracle.init_registers(n, J, seed)) and st["sweeps"] == 1
+    off = np.array([0, 1, 2, 2], np.int32)
+    tgt = np.array([1, 2], np.int32)
+    M, _ = oracle.simulate(3, off, tgt, np.ones(2, np.float32), J, seed)
+    I = oracle.init_registers(3, J, seed)
+    # w = 1 is dead only when X xor h = h_max (probability 2^-31); check it is not the case here
+    _, _, X = oracle.salts(seed, J)
+    assert all((int(x) ^ brute.edge_hash(0, 1)) != brute.HMAX and (int(x) ^ brute.edge_hash(1, 2)) != brute.HMAX for x in X)
+    assert np.array_equal(M[0], I.max(axis=0)) and np.array_equal(M[1], I[1:].max(axis=0)) and np.array_equal(M[2], I[2])
+
+
+def test_fig5_shape():
+    """Fig. 5 caption: edge (1,4) live in both sims, (4,3) live only in sim 2;
+    4's sim-2 register rises in sweep 1, 1 re-pulls from 4 in sweep 2, then the process stops.
+    Synchronous sweeps + the Gamma^-(L) frontier give changed sets {1,4}, {1}, {} (readings R10, R11).
+    The toy graph's other edges and its register values are in the missing image (unpinned)."""
+    J = 2
+    for seed in range(1, 100000):
+        sv, sj, X = brute.salts(seed, J)
+        I = brute.init_registers(5, J, seed).astype(int)
+        h43 = brute.edge_hash(4, 3)
+        P = [(int(X[j]) ^ h43) / brute.HMAX for j in range(2)]
+        if not P[1] < P[0]:
+            continue
+        if I[3, 1] > I[4, 1] and I[3, 1] > I[1, 1] and (I[4] > I[1]).any():
+            break
+    w43 = np.float32((P[0] + P[1]) / 2)
+    off = np.array([0, 0, 1, 1, 1, 2], np.int32)  # vertices 0..4; 0 is isolated
+    tgt = np.array([4, 3], np.int32)
+    pr = np.array([1.0, w43], np.float32)
+    M, st = oracle.simulate(5, off, tgt, pr, J, seed)
+    assert st["changed"] == [2, 1, 0] and st["sweeps"] == 3
+    assert M[4, 1] == I[3, 1] and M[4, 0] == I[4, 0] and M[1, 1] == I[3, 1]
+    assert np.array_equal(M, brute.registers(5, off, tgt, pr, J, seed))
+
+
+# ---------------------------------------------------------------- definitions used for sampled parity
+def test_reach_register_and_seed_sigma_vs_bruteforce():
+    rng = np.random.default_rng(9)
+    for g in range(20):
+        n = int(rng.integers(2, 100))
+        off, tgt, pr = brute.random_graph(rng, n, int(rng.integers(0, 4 * n)), None)
+        J, seed = 32, int(rng.integers(0, 2**32))
+        R = brute.registers(n, off, tgt, pr, J, seed)
+        us = rng.integers(0, n, 50)
+        js = rng.integers(0, J, 50)
+        assert np.array_equal(oracle.reach_register(n, off, tgt, pr, J, seed, us, js), R[us, js])
+        seeds = rng.choice(n, min(n, 5), replace=False)
+        cnt = oracle.seed_sigma(n, off, tgt, pr, J, seed, seeds)
+        for k in range(len(seeds)):
+            assert cnt[k] == brute.reach_masks(n, off, tgt, pr, J, seed, seeds[: k + 1]).sum()
+
+
+# ---------------------------------------------------------------- Alg. 1
+def star(n_leaves, center=0, base=0):
+    """edges center -> leaves, ids base..base+n_leaves"""
+    return [(base + center, base + i) for i in range(n_leaves + 1) if i != center]
+
+
+def csr_from_edges(n, edges, w=1.0):
+    edges = sorted(edges)
+    off = np.zeros(n + 1, np.int32)
+    for u, _ in edges:
+        off[u + 1] += 1
+    off = np.cumsum(off).astype(np.int32)
+    tgt = np.array([v for _, v in edges], np.int32)
+    return off, tgt, np.full(len(tgt), w, np.float32)
+
+
+def test_select_star_and_two_stars():
+    """SPEC.md:352 (star, K=1 -> centre) and SPEC.md:427 (two disjoint stars, K=2 -> both centres, larger first)."""
+    off, tgt, pr = csr_from_edges(51, star(50))
+    for t in (0.0, 0.05, math.inf):
+        assert list(oracle.select_seeds(51, off, tgt, pr, 64, 1, 1, t)["seeds"]) == [0]
+    edges = star(5, base=0) + star(10, base=6)  # small star centre 0 (5 leaves), big star centre 6 (10 leaves)
+    off, tgt, pr = csr_from_edges(17, edges)
+    for t in (0.0, 0.05, math.inf):
+        r = oracle.select_seeds(17, off, tgt, pr, 256, 1, 2, t)
+        assert list(r["seeds"]) == [6, 0], t
+        assert list(r["scores"]) == [11.0, 17.0]
+
+
+def test_select_reductions_and_variants():
+    """K=1 with t=inf reduces to argmax of the first-build estimates; t=0 rebuilds at
+    every step (strict '<'), t=inf never (Fig. 6 variants)."""
+    rng = np.random.default_rng(10)
+    for g in range(8):
+        n = int(rng.integers(20, 120))
+        off, tgt, pr = brute.random_graph(rng, n, 4 * n, float(rng.choice([0.1, 0.3])), allow_dups=False, allow_loops=False)
+        J, seed = 64, int(rng.integers(0, 2**32))
+        M, _ = oracle.simulate(n, off, tgt, pr, J, seed)
+        r = oracle.select_seeds(n, off, tgt, pr, J, seed, 1, math.inf)
+        rows = M.astype(np.int64).sum(axis=1)
+        assert r["seeds"][0] == int(np.argmax(rows)) and r["steps"][0]["score"] == rows.max()
+        K = 6
+        r0 = oracle.select_seeds(n, off, tgt, pr, J, seed, K, 0.0)
+        assert all(s["rebuilt"] == 1 for s in r0["steps"]) and r0["stats"]["builds"] == K
+        assert [s["executed"] for s in r0["steps"]] == [1] * (K - 1) + [0]
+        ri = oracle.select_seeds(n, off, tgt, pr, J, seed, K, math.inf)
+        assert all(s["rebuilt"] == 0 for s in ri["steps"]) and ri["stats"]["builds"] == 1
+
+
+def test_select_sigma_and_masks_vs_bruteforce():
+    """R_G(S) and sigma (Alg. 1 lines 13-14) equal brute-force reach of the chosen seeds; sigma is
+    non-decreasing and <= n; seeds are distinct; decisions follow the keep rule of line 18."""
+    rng = np.random.default_rng(11)
+    for g in range(10):
+        n = int(rng.integers(10, 90))
+        off, tgt, pr = brute.random_graph(rng, n, 3 * n, None if g % 2 else 0.2)
+        J, seed, K = 32, int(rng.integers(0, 2**32)), min(n, 6)
+        t = float(rng.choice([0.0, 0.05, 0.3, math.inf]))
+        r = oracle.select_seeds(n, off, tgt, pr, J, seed, K, t, want_vis=True)
+        seeds = list(r["seeds"])
+        assert len(set(seeds)) == K
+        vis = brute.reach_masks(n, off, tgt, pr, J, seed, seeds)
+        assert np.array_equal(r["vis"].astype(bool), vis)
+        for k in range(K):
+            assert r["steps"][k]["sigma_count"] == brute.reach_masks(n, off, tgt, pr, J, seed, seeds[: k + 1]).sum()
+            assert r["scores"][k] == r["steps"][k]["sigma_count"] / J
+            s = r["steps"][k]
+            assert s["rebuilt"] == (not (s["err_l"] < t or s["err_g"] < t))
+        assert all(np.diff(r["scores"]) >= 0) and r["scores"][-1] <= n
+
+
+def test_rebuilt_registers_vs_bruteforce():
+    """After a rebuild (t = 0, K = 2) the registers are the reach-max on G_j^S with S's reach blocked
+    (lines 21-24), and no register exceeds its first-build value."""
+    rng = np.random.default_rng(12)
+    for g in range(10):
+        n = int(rng.integers(10, 80))
+        off, tgt, pr = brute.random_graph(rng, n, 3 * n, 0.4)
+        J, seed = 32, int(rng.integers(0, 2**32))
+        r = oracle.select_seeds(n, off, tgt, pr, J, seed, 2, 0.0, want_final=True)
+        blocked = brute.reach_masks(n, off, tgt, pr, J, seed, r["seeds"][:1])
+        assert np.array_equal(r["M_final"], brute.registers(n, off, tgt, pr, J, seed, blocked=blocked))
+        M1, _ = oracle.simulate(n, off, tgt, pr, J, seed)
+        assert (r["M_final"] <= M1).all()
