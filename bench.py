@@ -1,0 +1,299 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path (one JSON line on rank 0).
+
+A step = one pass of the whole hot path over one synthetic workload:
+edge prep (im_load_csr*), sketch build (im_build_sketches), per-vertex estimate
+(im_estimate*), and the K-step error-adaptive selection with its BFS diffusions and rebuilds
+(im_select_seeds).
+
+value : processed edge x simulation updates per second over the whole step
+        (sum over every sweep of every build/rebuild of [enumerated edges x J] / step time),
+        inputs resident in HBM when the timed region starts.
+e2e   : the same metric through the C ABI with HOST (pinned) buffers: H2D of the CSR and the
+        D2H of estimates and seeds inside the timed region.
+roofline : the sweep kernel (dominant), algorithmic bytes / CUDA-event
+        kernel time vs the measured HBM copy bandwidth of MEASURED_PEAKS.json.
+cpu_baseline : the oracle (oracle/, plain single-threaded C) on a bounded sample of the same
+        workload: the first Alg. 2 sweep over a vertex range, on the host.
+
+    python bench.py [--config c4] [--steps 3] [--warmup 3] [--gpus N] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import gen  # noqa: E402
+
+METRIC = "sketch-build G edge·sims/s (processed edge x simulation updates per second, whole K-seed IM step)"
+UNIT = "G edge·sims/s"
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured", float(d.get("sm_max_mhz", 1965.0))
+    return 6650.0, "fallback", 1965.0
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, gpu_index: int):
+        self.path = tempfile.mktemp(prefix="clocks", suffix=".csv")
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def oracle_sample(cfg, n, off, tgt, pr, target_s=12.0):
+    """cpu_baseline: the oracle's first Alg. 2 sweep over a vertex range sized to ~target_s seconds."""
+    import oracle
+
+    J = cfg.J
+    # calibrate on a small range, then size the timed sample
+    u0 = n // 3
+    e_small = 200_000 // max(1, J // 64)
+    u1 = int(np.searchsorted(off, off[u0] + e_small))
+    u1 = max(u0 + 1, min(u1, n))
+    pe, dt, _ = oracle.first_sweep_sample(n, off, tgt, pr, J, cfg.salt_seed, u0, u1)
+    rate = max(pe, 1) / max(dt, 1e-6)  # edges / s
+    want = int(rate * target_s)
+    u2 = int(np.searchsorted(off, off[u0] + want))
+    u2 = max(u0 + 1, min(u2, n))
+    pe, dt, _ = oracle.first_sweep_sample(n, off, tgt, pr, J, cfg.salt_seed, u0, u2)
+    return {"value": pe * J / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"first Alg. 2 sweep (synchronous, all u processed) over vertices [{u0},{u2}) = {pe} edges x J={J}, "
+                      f"{dt:.1f} s single-threaded, gcc {' '.join(oracle.CFLAGS)}",
+            "seconds": dt}
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    cfg = gen.CONFIGS[args.config]
+    n, off, tgt, pr = gen.workload(cfg)
+    vals = []
+    for _ in range(args.warmup):
+        pass  # the oracle has no warm-up effects beyond page faults handled inside its setup
+    for _ in range(args.steps):
+        vals.append(oracle_sample(cfg, n, off, tgt, pr, target_s=args.ref_seconds))
+    v = statistics.median([x["value"] for x in vals])
+    cb = dict(vals[-1])
+    cb["value"] = v
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": statistics.median([x["seconds"] for x in vals]) * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/u32", "data": "synthetic",
+            "config": config_dict(cfg, n, len(tgt), args), "cpu_baseline": cb,
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(cfg, n, m, args):
+    return {"workload": f"{cfg.name}: {cfg.note}", "n": int(n), "m": int(m), "J": cfg.J, "K": cfg.K, "t": cfg.t,
+            "p": cfg.p if cfg.p is not None else "weighted-cascade 1/indeg", "salt_seed": cfg.salt_seed,
+            "parallelism": "replicas" if args.gpus > 1 else "single-gpu",
+            "l2": "inputs (CSR+hash records) larger than L2" if m * 16 > 126e6 else "L2 flushed (256 MB write) between steps"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=os.environ.get("IM_BENCH_CONFIG", "c4"))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-seconds", type=float, default=12.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        return run_reference(args, rank)
+
+    import torch
+
+    import paper_2105_04023_b200 as im
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = gen.CONFIGS[args.config]
+    t0 = time.time()
+    n, off, tgt, pr = gen.workload(cfg)
+    gen_s = time.time() - t0
+    m = len(tgt)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    im.im_set_stream(stream)
+    d_off = torch.from_numpy(off).to(dev)
+    d_tgt = torch.from_numpy(tgt).to(dev)
+    d_pr = torch.from_numpy(pr).to(dev)
+    d_est = torch.empty(n, dtype=torch.float64, device=dev)
+    h_off = torch.from_numpy(off).pin_memory()
+    h_tgt = torch.from_numpy(tgt).pin_memory()
+    h_pr = torch.from_numpy(pr).pin_memory()
+    h_est = torch.empty(n, dtype=torch.float64).pin_memory()
+    h_seeds = torch.empty(cfg.K, dtype=torch.int32).pin_memory()
+    h_scores = torch.empty(cfg.K, dtype=torch.float64).pin_memory()
+    flush = None if m * 16 > 126e6 else torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if dist is not None:
+            dist.barrier()
+
+    def step_device():
+        im.im_load_csr_device(n, m, d_off, d_tgt, d_pr)
+        im.im_build_sketches(cfg.J, cfg.salt_seed)
+        sb = im.im_get_stats()
+        im.im_estimate_device(d_est)
+        seeds, scores = im.im_select_seeds(cfg.K, cfg.t)
+        ss = im.im_get_stats()
+        return sb, ss, seeds, scores
+
+    def step_e2e():
+        im.lib().im_load_csr(n, h_off.data_ptr(), h_tgt.data_ptr(), h_pr.data_ptr())
+        im.im_build_sketches(cfg.J, cfg.salt_seed)
+        sb = im.im_get_stats()
+        im.lib().im_estimate(h_est.data_ptr())
+        im.im_select_seeds_into(cfg.K, cfg.t, h_seeds.numpy(), h_scores.numpy())
+        ss = im.im_get_stats()
+        return sb, ss
+
+    for _ in range(args.warmup):
+        step_device()
+    times, edges, wedges, sweep_ms, sweeps, launches_sweep, rebuilds, launches = [], [], [], [], [], [], [], []
+    first_build = {}
+    clocks = Clocks(int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[0]) if os.environ.get("CUDA_VISIBLE_DEVICES", "").strip().isdigit() else local)
+    for i in range(args.steps):
+        if flush is not None:
+            flush.fill_(i & 0xFF)
+        barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0 = im.im_kernel_launch_count()
+        ev0.record(stream)
+        sb, ss, seeds, scores = step_device()
+        ev1.record(stream)
+        barrier()
+        launches.append(im.im_kernel_launch_count() - l0)
+        times.append(ev0.elapsed_time(ev1))
+        edges.append(sb["total_edges"] + ss["total_edges"])
+        wedges.append(sb["window_edges"] + ss["window_edges"])
+        sweep_ms.append(sb["sweep_kernel_ms"] + ss["sweep_kernel_ms"])
+        sweeps.append(sb["total_sweeps"] + ss["total_sweeps"])
+        launches_sweep.append(sb["sweep_launches"] + ss["sweep_launches"])
+        rebuilds.append(ss["rebuilds"])
+        first_build = {"ms": sb["last_build_ms"], "sweeps": sb["last_build_sweeps"], "edges": sb["last_build_edges"],
+                       "sweep_kernel_ms": sb["sweep_kernel_ms"], "prep_ms": sb["prep_ms"]}
+    clk = clocks.stop()
+    # e2e through the host-pointer ABI (pinned host buffers), same metric
+    e2e_times = []
+    if not args.no_e2e:
+        for i in range(max(1, args.steps)):
+            if flush is not None:
+                flush.fill_(i & 0xFF)
+            barrier()
+            t = time.perf_counter()
+            step_e2e()
+            torch.cuda.synchronize(dev)
+            e2e_times.append((time.perf_counter() - t) * 1e3)
+    # max over ranks
+    ms = statistics.mean(times)
+    if dist is not None:
+        tt = torch.tensor([ms, statistics.mean(e2e_times) if e2e_times else 0.0], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms, e2e_ms = float(tt[0]), float(tt[1])
+    else:
+        e2e_ms = statistics.mean(e2e_times) if e2e_times else None
+    J = cfg.J
+    work = statistics.mean(edges) * J  # edge x sim updates per step (deterministic count up to in-place order)
+    value = world * work / (ms / 1e3) / 1e9
+    hbm_peak, peak_kind, _ = load_peaks()
+    const_t = 1 if cfg.p is not None else 0
+    alg_bytes = statistics.mean(edges) * (8 + 4 * (1 - const_t)) + statistics.mean(wedges) * 32
+    sweep_s = statistics.mean(sweep_ms) / 1e3
+    achieved = alg_bytes / sweep_s / 1e9 if sweep_s > 0 else None
+    roof = {"bound": "hbm", "kernel": "k_sweep (Simulate sweeps, all builds of the step)",
+            "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak if achieved else None,
+            "peak_kind": peak_kind, "traffic": None,
+            "alg_bytes_per_step": alg_bytes, "sweep_kernel_ms_per_step": statistics.mean(sweep_ms),
+            "sweep_share_of_step": statistics.mean(sweep_ms) / ms,
+            "unit_def": "per enumerated in-edge: 8 B record (+4 B threshold when w varies) + 32 B sector of the puller's "
+                        "register row when the edge's candidate window is non-empty after the change filter"}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/u32",
+            "data": "synthetic", "config": config_dict(cfg, n, m, args), "clocks": clk,
+            "gpu_launches": int(statistics.mean(launches)), "roofline": roof,
+            "im_time_s": ms / 1e3,
+            "sketch_build": {"first_build_ms": first_build.get("ms"), "first_build_sweeps": first_build.get("sweeps"),
+                             "first_build_gedge_sims_per_s": first_build.get("edges", 0) * J / max(first_build.get("sweep_kernel_ms", 1e-9), 1e-9) / 1e6,
+                             "prep_ms": first_build.get("prep_ms"), "sweeps_per_step": statistics.mean(sweeps),
+                             "sweep_launches_per_step": statistics.mean(launches_sweep), "rebuilds_per_step": statistics.mean(rebuilds)},
+            "seeds_head": [int(x) for x in seeds[:5]], "sigma_final": float(scores[-1]) if len(scores) else None,
+            "gen_seconds": gen_s}
+    if e2e_ms is not None:
+        line["e2e"] = {"value": world * work / (e2e_ms / 1e3) / 1e9, "unit": UNIT,
+                       "h2d_bytes_per_step": int((n + 1) * 4 + m * 8), "d2h_bytes_per_step": int(n * 8 + cfg.K * 12),
+                       "ms_per_step": e2e_ms}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = oracle_sample(cfg, n, off, tgt, pr)
+        line["cpu_baseline"].pop("seconds", None)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    im.im_free()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

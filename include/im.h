@@ -1,0 +1,145 @@
+/*
+ * im.h -- C ABI of the B200-native (sm_100a) hot path of
+ *   "Fast and Error-Adaptive Influence Maximization based on Count-Distinct
+ *    Sketches" (arxiv 2105.04023; PAPER.md).
+ *
+ * Problem: find K seed vertices maximising the expected
+ * number of vertices influenced under the Independent Cascade model.  Method:
+ * hash-based fused sampling (Eq. 4-5), one 8-bit
+ * Flajolet-Martin register per (vertex, simulation) (Eq. 1-3),
+ * Simulate to the fixpoint (Alg. 2), greedy selection with
+ * error-adaptive rebuilds (Alg. 1).  Readings of the paper
+ * (R1..R21) are listed in DESIGN.md.
+ *
+ * Conventions (all entry points):
+ *  - Return 0 on success, a negative IM_E* code on error; im_last_error() then
+ *    returns a message.  On error, caller-owned outputs are left untouched.
+ *  - Calls are synchronous: outputs are on the host when the call returns.
+ *  - One global context, not thread-safe.  The library owns all device state
+ *    from im_load_csr* until im_free() or the next im_load_csr*.
+ *  - Host pointers are caller-owned and only read/written during the call.
+ *  - All work runs on one CUDA stream (im_set_stream, default: a library stream)
+ *    on the current CUDA device, which must be sm_100 (B200); otherwise IM_ECUDA.
+ *    There is no CPU fallback.
+ */
+#ifndef IM_H
+#define IM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IM_OK 0
+#define IM_EINVAL (-1) /* argument or graph validation failed */
+#define IM_ESTATE (-2) /* wrong call order (e.g. im_estimate before im_build_sketches) */
+#define IM_ENOMEM (-3) /* device or host allocation failed */
+#define IM_ECUDA (-4)  /* CUDA error, or no sm_100 device */
+
+/* One greedy step of Alg. 1. */
+typedef struct {
+    int32_t vertex;      /* s chosen at this step */
+    int32_t pad;
+    int64_t score;       /* sum_j max(M_S'[j], M_s[j]): integer numerator of Estimate(Merge(M_S', M_s)) */
+    double e;            /* 2^(score/J) / 0.77351 (Eq. 2, line 12) */
+    int64_t sigma_count; /* sum_j |R_G(S)[j]| after adding s */
+    double sigma;        /* sigma_count / J (line 14) */
+    double delta;        /* sigma - varsigma (line 15) */
+    double err_l;        /* |(e - delta) / delta|, +inf when delta == 0 (line 16) */
+    double err_g;        /* |(e - delta) / sigma| (line 17) */
+    int32_t rebuilt;     /* 1: the else branch (rebuild) was decided (line 18 test false) */
+    int32_t executed;    /* 1: the rebuild was executed (skipped after the last pick, reading R18) */
+} im_step;
+
+typedef struct {
+    int32_t n;
+    int32_t J;                 /* 0 before im_build_sketches */
+    int64_t m;
+    int32_t const_threshold;   /* 1 if every edge has the same w (one scalar integer threshold) */
+    uint32_t threshold;        /* that threshold T: live iff (X_j xor h) < T (exactly Eq. 5 in double) */
+    int32_t builds;            /* Simulate runs since load (first build + executed rebuilds) */
+    int32_t last_build_sweeps; /* sweeps of the most recent Simulate */
+    int64_t last_build_edges;  /* edges enumerated by the most recent Simulate */
+    int64_t total_sweeps;      /* since the last im_select_seeds / im_build_sketches call began */
+    int64_t total_edges;       /* edges enumerated by all sweeps in the same window */
+    int32_t rebuilds;          /* rebuilds executed by the last im_select_seeds */
+    int32_t bfs_levels;        /* BFS levels run by the last im_select_seeds */
+    int64_t bfs_edges;         /* out-edges enumerated by those BFS levels */
+    double prep_ms;            /* im_load_csr*: device edge prep (hash, threshold, transpose) */
+    double last_build_ms;      /* most recent Simulate incl. register init */
+    double last_select_ms;     /* last im_select_seeds, wall time inside the call */
+    double sweep_kernel_ms;    /* summed sweep-kernel time in the window (CUDA events) */
+    int64_t sweep_launches;    /* sweep kernel launches in the window */
+    int64_t window_edges;      /* enumerated edges whose candidate window was non-empty after the change filter */
+    int64_t kernel_launches;   /* all kernel launches in the window */
+} im_stats;
+
+/*
+ * Load a directed graph in CSR form and run the one-off edge preparation:
+ *   h(u,v) = Murmur3_x86_32(LE32 u || LE32 v, seed 0) mod 2^31   (Eq. 4; R4)
+ *   per-edge integer threshold T_e with  (X xor h)/h_max < w  <=>  (X xor h) < T_e  (Eq. 5; R1, R7)
+ *   and the transpose (in-edges) used by the sweeps.
+ * n        : number of vertices, n >= 1.
+ * offsets  : HOST int32[n+1], offsets[0] = 0, non-decreasing; m = offsets[n].
+ * targets  : HOST int32[m], out-neighbours, each in [0, n).  Self loops and
+ *            duplicate edges are allowed and result-neutral (R19).
+ * probs    : HOST float32[m], IC probability w_uv of each edge, finite, in [0, 1].
+ * Resets all state.  IM_EINVAL on validation failure, IM_ENOMEM, IM_ECUDA.
+ */
+int im_load_csr(int32_t n, const int32_t *offsets, const int32_t *targets, const float *probs);
+
+/* Same, with DEVICE pointers (already resident in HBM; read during the call only). m must equal offsets[n]. */
+int im_load_csr_device(int32_t n, int64_t m, const int32_t *d_offsets, const int32_t *d_targets, const float *d_probs);
+
+/*
+ * Alg. 1 lines 2-6: salts from mt19937(low 32 bits of seed)
+ * (R2, R3), registers M_v[j] = clz(Murmur3(v, seed_V) xor Murmur3(j, seed_J))
+ * (R5, R6), then Simulate to the fixpoint with R_S = {} (eps_c = 0, R10, R11).
+ * J       : number of simulations, a multiple of 32 in [32, 1024].
+ * Requires a loaded graph (IM_ESTATE otherwise).
+ */
+int im_build_sketches(int32_t J, uint64_t seed);
+
+/* e_v = 2^{mean_j M_v[j]} / 0.77351 for every vertex (Eq. 2, R8).  out: HOST double[n]. */
+int im_estimate(double *out);
+/* Same into DEVICE memory: d_out double[n]. */
+int im_estimate_device(double *d_out);
+
+/*
+ * Alg. 1 lines 7-30 with eps_l = eps_g = err_threshold (R17): K greedy steps,
+ * each an argmax of Estimate(Merge(M_S', M_v)) (lowest id on ties, R14), a
+ * multi-simulation BFS for R_G(S) and sigma over the same samples (R13), the
+ * error test and either M_S' merge or a rebuild on the residual graph.
+ * Always starts from S = {}, varsigma = 0, M_S' = 0 and freshly built sketches.
+ * K                : 0 <= K <= n (K = 0 writes nothing).
+ * err_threshold    : >= 0, not NaN; +inf = never rebuild; 0 = always rebuild.
+ * out_seeds        : HOST int32[K]; out_scores: HOST double[K], sigma after k+1 seeds (R21).
+ */
+int im_select_seeds(int32_t K, double err_threshold, int32_t *out_seeds, double *out_scores);
+/* Same with separate local / global thresholds. */
+int im_select_seeds_ex(int32_t K, double eps_l, double eps_g, int32_t *out_seeds, double *out_scores);
+
+/* ---- test / diagnostic extras ---- */
+/* registers after the most recent Simulate, HOST uint8[n*J] row-major, simulation order j = 0..J-1 */
+int im_get_registers(uint8_t *out);
+/* the same for nrows listed vertices: out uint8[nrows*J] */
+int im_get_register_rows(int64_t nrows, const int32_t *rows, uint8_t *out);
+/* R_G(S) after the last selection: HOST uint32[n*(J/32)], bit j%32 of word j/32 of row v */
+int im_get_reach(uint32_t *out);
+/* step log of the last selection: HOST im_step[cap]; returns the number of steps written (>= 0) */
+int im_get_step_log(im_step *out, int32_t cap);
+int im_get_stats(im_stats *out);
+/* run all device work on this cudaStream_t (NULL: the library's own stream) */
+int im_set_stream(void *cuda_stream);
+/* number of kernel launches issued by the library since load (diagnostic) */
+int64_t im_kernel_launch_count(void);
+void im_free(void);
+const char *im_last_error(void);
+/* ABI version (major*100 + minor) */
+int32_t im_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IM_H */

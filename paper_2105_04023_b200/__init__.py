@@ -1,0 +1,208 @@
+"""Thin Python binding of the C ABI in include/im.h (argument marshalling only).
+
+Every step of the method runs in the sm_100a kernels of libim_b200.so; this
+module only converts arrays to pointers and raises on negative return codes.
+There is no fallback: if the CUDA library is missing or the device is not a
+B200 (sm_100), calls raise.  PyTorch is optional and only used to pass device
+pointers / streams (tensors are accepted wherever a device pointer is).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libim_b200.so")
+
+IM_OK, IM_EINVAL, IM_ESTATE, IM_ENOMEM, IM_ECUDA = 0, -1, -2, -3, -4
+
+
+class IMError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+class im_step(ctypes.Structure):
+    _fields_ = [
+        ("vertex", ctypes.c_int32), ("pad", ctypes.c_int32), ("score", ctypes.c_int64),
+        ("e", ctypes.c_double), ("sigma_count", ctypes.c_int64), ("sigma", ctypes.c_double),
+        ("delta", ctypes.c_double), ("err_l", ctypes.c_double), ("err_g", ctypes.c_double),
+        ("rebuilt", ctypes.c_int32), ("executed", ctypes.c_int32),
+    ]
+
+
+class im_stats(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_int32), ("J", ctypes.c_int32), ("m", ctypes.c_int64),
+        ("const_threshold", ctypes.c_int32), ("threshold", ctypes.c_uint32),
+        ("builds", ctypes.c_int32), ("last_build_sweeps", ctypes.c_int32), ("last_build_edges", ctypes.c_int64),
+        ("total_sweeps", ctypes.c_int64), ("total_edges", ctypes.c_int64),
+        ("rebuilds", ctypes.c_int32), ("bfs_levels", ctypes.c_int32), ("bfs_edges", ctypes.c_int64),
+        ("prep_ms", ctypes.c_double), ("last_build_ms", ctypes.c_double), ("last_select_ms", ctypes.c_double),
+        ("sweep_kernel_ms", ctypes.c_double), ("sweep_launches", ctypes.c_int64), ("window_edges", ctypes.c_int64),
+        ("kernel_launches", ctypes.c_int64),
+    ]
+
+
+# (restype, argtypes) of every symbol declared in include/im.h
+_vp, _i32, _i64, _u64, _f64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double
+SIGNATURES = {
+    "im_load_csr": (ctypes.c_int, [_i32, _vp, _vp, _vp]),
+    "im_load_csr_device": (ctypes.c_int, [_i32, _i64, _vp, _vp, _vp]),
+    "im_build_sketches": (ctypes.c_int, [_i32, _u64]),
+    "im_estimate": (ctypes.c_int, [_vp]),
+    "im_estimate_device": (ctypes.c_int, [_vp]),
+    "im_select_seeds": (ctypes.c_int, [_i32, _f64, _vp, _vp]),
+    "im_select_seeds_ex": (ctypes.c_int, [_i32, _f64, _f64, _vp, _vp]),
+    "im_get_registers": (ctypes.c_int, [_vp]),
+    "im_get_register_rows": (ctypes.c_int, [_i64, _vp, _vp]),
+    "im_get_reach": (ctypes.c_int, [_vp]),
+    "im_get_step_log": (ctypes.c_int, [_vp, _i32]),
+    "im_get_stats": (ctypes.c_int, [_vp]),
+    "im_set_stream": (ctypes.c_int, [_vp]),
+    "im_kernel_launch_count": (_i64, []),
+    "im_free": (None, []),
+    "im_last_error": (ctypes.c_char_p, []),
+    "im_version": (_i32, []),
+}
+
+_lib = None
+
+
+def lib():
+    """Load libim_b200.so (raises if it was not built: there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(rc: int) -> int:
+    if rc < 0:
+        raise IMError(rc, lib().im_last_error().decode(errors="replace"))
+    return rc
+
+
+def _host(a, dtype):
+    a = np.ascontiguousarray(a, dtype=dtype)
+    return a, a.ctypes.data
+
+
+def _dptr(x) -> int:
+    """device pointer of a torch CUDA tensor, or an int"""
+    if x is None:
+        return 0
+    if isinstance(x, int):
+        return x
+    return int(x.data_ptr())
+
+
+def im_load_csr(n: int, offsets, targets, probs) -> None:
+    """Host arrays (copied to the device inside the call)."""
+    o, po = _host(offsets, np.int32)
+    t, pt = _host(targets, np.int32)
+    p, pp = _host(probs, np.float32)
+    if len(o) != n + 1 or len(t) != int(o[-1]) or len(p) != len(t):
+        raise IMError(IM_EINVAL, "array lengths do not match n / offsets[n]")
+    _check(lib().im_load_csr(n, po, pt or None, pp or None))
+
+
+def im_load_csr_device(n: int, m: int, d_offsets, d_targets, d_probs) -> None:
+    """Device arrays (torch CUDA tensors or raw pointers), already resident in HBM."""
+    _check(lib().im_load_csr_device(n, m, _dptr(d_offsets), _dptr(d_targets) or None, _dptr(d_probs) or None))
+
+
+def im_build_sketches(J: int, seed: int) -> None:
+    _check(lib().im_build_sketches(J, seed & 0xFFFFFFFFFFFFFFFF))
+
+
+def im_estimate(n: int) -> np.ndarray:
+    out = np.empty(n, dtype=np.float64)
+    _check(lib().im_estimate(out.ctypes.data))
+    return out
+
+
+def im_estimate_device(d_out) -> None:
+    _check(lib().im_estimate_device(_dptr(d_out)))
+
+
+def im_select_seeds(K: int, err_threshold: float, eps_g: float | None = None):
+    """Returns (seeds int32[K], scores float64[K]).  eps_g given -> im_select_seeds_ex(K, eps_l, eps_g)."""
+    seeds = np.zeros(max(K, 1), dtype=np.int32)
+    scores = np.zeros(max(K, 1), dtype=np.float64)
+    if eps_g is None:
+        _check(lib().im_select_seeds(K, float(err_threshold), seeds.ctypes.data, scores.ctypes.data))
+    else:
+        _check(lib().im_select_seeds_ex(K, float(err_threshold), float(eps_g), seeds.ctypes.data, scores.ctypes.data))
+    return seeds[:K].copy(), scores[:K].copy()
+
+
+def im_select_seeds_into(K: int, err_threshold: float, seeds: np.ndarray, scores: np.ndarray) -> None:
+    """Allocation-free variant writing into caller arrays (e.g. pinned host buffers)."""
+    _check(lib().im_select_seeds(K, float(err_threshold), seeds.ctypes.data, scores.ctypes.data))
+
+
+def im_get_registers(n: int, J: int) -> np.ndarray:
+    out = np.empty((n, J), dtype=np.uint8)
+    _check(lib().im_get_registers(out.ctypes.data))
+    return out
+
+
+def im_get_register_rows(rows, J: int) -> np.ndarray:
+    r, pr = _host(rows, np.int32)
+    out = np.empty((len(r), J), dtype=np.uint8)
+    _check(lib().im_get_register_rows(len(r), pr, out.ctypes.data))
+    return out
+
+
+def im_get_reach(n: int, J: int) -> np.ndarray:
+    out = np.empty((n, J // 32), dtype=np.uint32)
+    _check(lib().im_get_reach(out.ctypes.data))
+    return out
+
+
+def im_get_step_log(K: int) -> list[dict]:
+    arr = (im_step * max(K, 1))()
+    k = _check(lib().im_get_step_log(ctypes.cast(arr, ctypes.c_void_p), K))
+    return [{f: getattr(arr[i], f) for f, _ in im_step._fields_ if f != "pad"} for i in range(k)]
+
+
+def im_get_stats() -> dict:
+    s = im_stats()
+    _check(lib().im_get_stats(ctypes.byref(s)))
+    return {f: getattr(s, f) for f, _ in im_stats._fields_}
+
+
+def im_set_stream(stream) -> None:
+    """torch.cuda.Stream, raw cudaStream_t int, or None (library stream)."""
+    h = 0 if stream is None else (stream if isinstance(stream, int) else int(stream.cuda_stream))
+    _check(lib().im_set_stream(h or None))
+
+
+def im_kernel_launch_count() -> int:
+    return int(lib().im_kernel_launch_count())
+
+
+def im_free() -> None:
+    lib().im_free()
+
+
+def im_version() -> int:
+    return int(lib().im_version())
+
+
+def reach_bits_to_bool(words: np.ndarray, J: int) -> np.ndarray:
+    """uint32[n, J/32] (bit j%32 of word j/32) -> bool[n, J] (marshalling helper)."""
+    n = words.shape[0]
+    bits = (words[:, :, None] >> np.arange(32, dtype=np.uint32)) & 1
+    return bits.reshape(n, J).astype(bool)

@@ -1,0 +1,590 @@
+// im_abi.cu -- the C ABI of include/im.h: validation, device state, and the host
+// control loops of Alg. 1 / Alg. 2 (sweep-to-fixpoint, greedy K loop).  Every step of
+// the method runs in the kernels of im_kernels.cu; the host only sequences launches
+// and reads back iteration counters (a few bytes per sweep / BFS level / greedy step).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "im_device.cuh"
+#include "im_internal.h"
+
+namespace im {
+int occupancy_sweep(int* blocks_per_sm_sweep, int* blocks_per_sm_bfs);
+}
+
+using namespace im;
+
+namespace {
+
+Ctx g;
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(call)                                                                                            \
+    do {                                                                                                    \
+        cudaError_t e_ = (call);                                                                            \
+        if (e_ != cudaSuccess) {                                                                            \
+            if (e_ == cudaErrorMemoryAllocation) { cudaGetLastError(); return fail(IM_ENOMEM, "%s: %s", #call, cudaGetErrorString(e_)); } \
+            return fail(IM_ECUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_));    \
+        }                                                                                                   \
+    } while (0)
+
+#define TRY(x)                 \
+    do {                       \
+        int r_ = (x);          \
+        if (r_) return r_;     \
+    } while (0)
+
+template <class T>
+void dfree(T*& p) {
+    if (p) cudaFree((void*)p);
+    p = nullptr;
+}
+
+template <class T>
+int dalloc(T*& p, size_t count) {
+    dfree(p);
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMalloc((void**)&p, count * sizeof(T));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        p = nullptr;
+        return fail(IM_ENOMEM, "cudaMalloc of %zu bytes failed: %s", count * sizeof(T), cudaGetErrorString(e));
+    }
+    return 0;
+}
+
+using clk = std::chrono::steady_clock;
+double ms_since(clk::time_point t0) { return std::chrono::duration<double, std::milli>(clk::now() - t0).count(); }
+
+int ensure_device() {
+    if (g.dev >= 0) return 0;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return fail(IM_ECUDA, "no CUDA device: %s", cudaGetErrorString(e));
+    cudaDeviceProp p;
+    CK(cudaGetDeviceProperties(&p, dev));
+    if (p.major != 10 || p.minor != 0)
+        return fail(IM_ECUDA, "this library is built for sm_100a (B200); device %d is sm_%d%d (%s)", dev, p.major, p.minor, p.name);
+    g.dev = dev;
+    g.num_sms = p.multiProcessorCount;
+    int bs = 0, bb = 0;
+    CK((cudaError_t)occupancy_sweep(&bs, &bb));
+    g.max_blocks_sweep = std::max(1, bs) * g.num_sms;
+    g.max_blocks_bfs = std::max(1, bb) * g.num_sms;
+    if (!g.own_stream) CK(cudaStreamCreateWithFlags(&g.own_stream, cudaStreamNonBlocking));
+    if (!g.stream) g.stream = g.own_stream;
+    if (!g.hpin) CK(cudaMallocHost(&g.hpin, 4096));
+    if (!g.ev[0]) {
+        CK(cudaEventCreate(&g.ev[0]));
+        CK(cudaEventCreate(&g.ev[1]));
+    }
+    return 0;
+}
+
+void free_sketch_state() {
+    dfree(g.Xs); dfree(g.s12); dfree(g.permd); dfree(g.M); dfree(g.vis);
+    for (int i = 0; i < 2; i++) { dfree(g.items[i]); dfree(g.chg[i]); dfree(g.delta[i]); dfree(g.bitems[i]); dfree(g.bvl[i]); }
+    dfree(g.inS); dfree(g.MS); dfree(g.btag);
+    g.J = 0;
+    g.built = g.fresh = g.any_blocked = false;
+    g.perm.clear();
+}
+
+void free_graph_state() {
+    free_sketch_state();
+    dfree(g.off); dfree(g.fwd); dfree(g.fwdT); dfree(g.roff); dfree(g.rev); dfree(g.revT); dfree(g.ritems);
+    dfree(g.ctr); dfree(g.rec); dfree(g.varsigma); dfree(g.key); dfree(g.first); dfree(g.sigma_count);
+    g.loaded = false;
+    g.n = 0;
+    g.m = 0;
+    g.steps.clear();
+    g.st = im_stats{};
+}
+
+int sync() {
+    CK(cudaStreamSynchronize(g.stream));
+    return 0;
+}
+
+// read `bytes` of device memory to the pinned scratch (synchronous)
+int readback(const void* dptr, size_t bytes, void* host) {
+    CK(cudaMemcpyAsync(g.hpin, dptr, bytes, cudaMemcpyDeviceToHost, g.stream));
+    TRY(sync());
+    memcpy(host, g.hpin, bytes);
+    return 0;
+}
+
+// ----------------------------------------------------------- a0: load + edge prep
+int load_common(int32_t n, int64_t m, const int32_t* d_off_src, const int32_t* d_tgt, const float* d_prob) {
+    auto t0 = clk::now();
+    int64_t launches0 = g.launches;
+    // offsets: own copy
+    TRY(dalloc(g.off, (size_t)n + 1));
+    CK(cudaMemcpyAsync(g.off, d_off_src, ((size_t)n + 1) * sizeof(int32_t), cudaMemcpyDeviceToDevice, g.stream));
+    int* dflags = nullptr;
+    TRY(dalloc(dflags, 4));
+    CK(cudaMemsetAsync(dflags, 0, 4 * sizeof(int), g.stream));
+    CK(launch_validate(g, g.off, d_tgt, d_prob, dflags));
+    if (m > 0) CK(launch_const_check(g, d_prob, dflags + 1));
+    int hf[4];
+    TRY(readback(dflags, sizeof hf, hf));
+    if (hf[0]) {
+        dfree(dflags);
+        return fail(IM_EINVAL, "invalid graph:%s%s%s", (hf[0] & 1) ? " offsets (offsets[0]!=0, decreasing, or offsets[n]!=m)" : "",
+                    (hf[0] & 2) ? " targets out of [0,n)" : "", (hf[0] & 4) ? " probabilities not finite in [0,1]" : "");
+    }
+    g.constT = (m == 0) || hf[1] == 0;
+    g.T0 = 0;
+    if (g.constT && m > 0) {
+        float w0;
+        TRY(readback(d_prob, sizeof(float), &w0));
+        g.T0 = live_threshold(w0);
+    }
+    // forward records {target, h}, per-edge thresholds, in-degrees
+    TRY(dalloc(g.fwd, (size_t)m));
+    if (!g.constT) TRY(dalloc(g.fwdT, (size_t)m));
+    int32_t* indeg = nullptr;
+    TRY(dalloc(indeg, 2 * ((size_t)n + 1)));
+    CK(cudaMemsetAsync(indeg, 0, 2 * ((size_t)n + 1) * sizeof(int32_t), g.stream));
+    if (m > 0) CK(launch_edge_prep(g, d_tgt, d_prob, indeg));
+    // reverse offsets = exclusive scan of in-degrees
+    TRY(dalloc(g.roff, (size_t)n + 1));
+    size_t tmp_bytes = 0;
+    CK(scan_exclusive(g, indeg, g.roff, n + 1, nullptr, tmp_bytes));
+    tmp_bytes += 256;
+    char* tmp = nullptr;
+    TRY(dalloc(tmp, tmp_bytes));
+    CK(scan_exclusive(g, indeg, g.roff, n + 1, tmp, tmp_bytes));
+    // transpose
+    TRY(dalloc(g.rev, (size_t)m));
+    if (!g.constT) TRY(dalloc(g.revT, (size_t)m));
+    CK(cudaMemsetAsync(indeg, 0, ((size_t)n + 1) * sizeof(int32_t), g.stream));
+    if (m > 0) CK(launch_transpose(g, indeg));
+    // work items: reverse segments of every vertex (sweep 1), forward item capacity (BFS)
+    int32_t* nseg = nullptr;
+    TRY(dalloc(nseg, 2 * ((size_t)n + 1)));
+    CK(launch_build_items(g, g.roff, nullptr, nseg, tmp, tmp_bytes));
+    int32_t total[2];
+    TRY(readback(nseg + (n + 1) + n, sizeof(int32_t), &total[0]));
+    g.n_ritems = total[0];
+    TRY(dalloc(g.ritems, (size_t)g.n_ritems));
+    CK(launch_build_items(g, g.roff, g.ritems, nseg, tmp, tmp_bytes));
+    CK(launch_build_items(g, g.off, nullptr, nseg, tmp, tmp_bytes));
+    TRY(readback(nseg + (n + 1) + n, sizeof(int32_t), &total[1]));
+    g.n_fitems_cap = total[1];
+    TRY(sync());
+    dfree(tmp);
+    dfree(nseg);
+    dfree(indeg);
+    dfree(dflags);
+    // small per-graph state
+    TRY(dalloc(g.ctr, 2));
+    TRY(dalloc(g.rec, 1));
+    TRY(dalloc(g.varsigma, 1));
+    TRY(dalloc(g.key, 1));
+    TRY(dalloc(g.first, 1));
+    TRY(dalloc(g.sigma_count, 1));
+    g.loaded = true;
+    g.st = im_stats{};
+    g.st.n = n;
+    g.st.m = m;
+    g.st.const_threshold = g.constT ? 1 : 0;
+    g.st.threshold = g.T0;
+    g.st.prep_ms = ms_since(t0);
+    g.st.kernel_launches = g.launches - launches0;
+    return 0;
+}
+
+int check_csr_args(int32_t n, int64_t m) {
+    if (n < 1) return fail(IM_EINVAL, "n must be >= 1 (got %d)", n);
+    if (m < 0 || m > 2147483647LL) return fail(IM_EINVAL, "m must be in [0, 2^31-1] (got %lld)", (long long)m);
+    return 0;
+}
+
+// ----------------------------------------------------------- a1-a4: build
+int alloc_sketch_state(int32_t J) {
+    if (g.J == J && g.M) return 0;
+    free_sketch_state();
+    size_t n = (size_t)g.n, W = (size_t)J / 32;
+    TRY(dalloc(g.Xs, (size_t)J));
+    TRY(dalloc(g.s12, 4097));
+    TRY(dalloc(g.permd, (size_t)J));
+    TRY(dalloc(g.M, n * (size_t)J));
+    TRY(dalloc(g.vis, n * W));
+    for (int i = 0; i < 2; i++) {
+        TRY(dalloc(g.items[i], (size_t)std::max(g.n_ritems, 1)));
+        TRY(dalloc(g.chg[i], n));
+        CK(cudaMemsetAsync(g.chg[i], 0, n * sizeof(ull), g.stream));
+        TRY(dalloc(g.delta[i], n * W));
+        CK(cudaMemsetAsync(g.delta[i], 0, n * W * sizeof(uint32_t), g.stream));
+        TRY(dalloc(g.bitems[i], (size_t)std::max(g.n_fitems_cap, 1)));
+        TRY(dalloc(g.bvl[i], n));
+    }
+    TRY(dalloc(g.inS, n));
+    TRY(dalloc(g.MS, (size_t)J));
+    TRY(dalloc(g.btag, n));
+    CK(cudaMemsetAsync(g.btag, 0, n * sizeof(uint32_t), g.stream));
+    g.tag = 0;
+    g.bt = 0;
+    g.J = J;
+    return 0;
+}
+
+// Alg. 1 salts (R2, R3): mt19937(low 32 bits of seed): seed_V, seed_J, X_j = draw & (2^31-1).
+// Internally simulations are ordered by ascending salt.
+int setup_salts(int32_t J, uint64_t seed) {
+    std::mt19937 gen((uint32_t)seed);
+    g.seedV = gen();
+    g.seedJ = gen();
+    std::vector<uint32_t> X(J);
+    for (int j = 0; j < J; j++) X[j] = gen() & 0x7FFFFFFFu;
+    g.perm.resize(J);
+    for (int j = 0; j < J; j++) g.perm[j] = j;
+    std::stable_sort(g.perm.begin(), g.perm.end(), [&](int a, int b) { return X[a] < X[b]; });
+    std::vector<uint32_t> Xs(J);
+    for (int i = 0; i < J; i++) Xs[i] = X[g.perm[i]];
+    std::vector<uint16_t> s12(4097);
+    for (uint32_t b = 0, i = 0; b <= 4096; b++) {
+        while ((int)i < J && (Xs[i] >> 19) < b) i++;
+        s12[b] = (uint16_t)i;
+    }
+    CK(cudaMemcpyAsync(g.Xs, Xs.data(), J * sizeof(uint32_t), cudaMemcpyHostToDevice, g.stream));
+    CK(cudaMemcpyAsync(g.s12, s12.data(), 4097 * sizeof(uint16_t), cudaMemcpyHostToDevice, g.stream));
+    CK(cudaMemcpyAsync(g.permd, g.perm.data(), J * sizeof(int32_t), cudaMemcpyHostToDevice, g.stream));
+    TRY(sync());  // host vectors go out of scope
+    g.seed = seed;
+    return 0;
+}
+
+// Alg. 1 lines 2-5 / 21-25 + Alg. 2 to the fixpoint (eps_c = 0).  blocked: R_S = current visited bits.
+int simulate(bool blocked) {
+    auto t0 = clk::now();
+    CK(launch_init_registers(g));
+    IterCounters hc;
+    int sweeps = 0;
+    int64_t edges = 0;
+    float kms = 0.f;
+    // sweep 1: every in-edge of every vertex
+    uint32_t tag = ++g.tag;
+    int out = 0;
+    CK(cudaMemsetAsync(&g.ctr[out], 0, sizeof(IterCounters), g.stream));
+    CK(cudaEventRecord(g.ev[0], g.stream));
+    CK(launch_sweep(g, true, g.ritems, g.n_ritems, 0u, tag, out, blocked));
+    CK(cudaEventRecord(g.ev[1], g.stream));
+    TRY(readback(&g.ctr[out], sizeof hc, &hc));
+    int64_t wedges = (int64_t)hc.win_edges;
+    float t;
+    CK(cudaEventElapsedTime(&t, g.ev[0], g.ev[1]));
+    kms += t;
+    sweeps = 1;
+    edges = g.m;
+    int64_t launches = 1;
+    while (hc.next_items > 0) {
+        uint32_t tag_in = tag;
+        tag = ++g.tag;
+        int cur = out;
+        out ^= 1;
+        int n_items = hc.next_items;
+        edges += (int64_t)hc.next_edges;
+        CK(cudaMemsetAsync(&g.ctr[out], 0, sizeof(IterCounters), g.stream));
+        CK(cudaEventRecord(g.ev[0], g.stream));
+        CK(launch_sweep(g, false, g.items[cur], n_items, tag_in, tag, out, blocked));
+        CK(cudaEventRecord(g.ev[1], g.stream));
+        TRY(readback(&g.ctr[out], sizeof hc, &hc));
+        wedges += (int64_t)hc.win_edges;
+        CK(cudaEventElapsedTime(&t, g.ev[0], g.ev[1]));
+        kms += t;
+        sweeps++;
+        launches++;
+    }
+    g.st.builds++;
+    g.st.last_build_sweeps = sweeps;
+    g.st.last_build_edges = edges;
+    g.st.total_sweeps += sweeps;
+    g.st.total_edges += edges;
+    g.st.sweep_kernel_ms += kms;
+    g.st.sweep_launches += launches;
+    g.st.window_edges += wedges;
+    g.st.last_build_ms = ms_since(t0);
+    g.built = true;
+    g.fresh = !blocked;
+    return 0;
+}
+
+int build_fresh() {
+    CK(cudaMemsetAsync(g.vis, 0, (size_t)g.n * (g.J / 32) * sizeof(uint32_t), g.stream));
+    g.any_blocked = false;
+    return simulate(false);
+}
+
+}  // namespace
+
+// =========================================================== C ABI
+extern "C" {
+
+int32_t im_version(void) { return 100; }
+
+const char* im_last_error(void) { return g_err.c_str(); }
+
+int64_t im_kernel_launch_count(void) { return g.launches; }
+
+int im_set_stream(void* s) {
+    TRY(ensure_device());
+    g.stream = s ? (cudaStream_t)s : g.own_stream;
+    return 0;
+}
+
+void im_free(void) {
+    if (g.dev >= 0) cudaStreamSynchronize(g.stream);
+    free_graph_state();
+}
+
+int im_load_csr(int32_t n, const int32_t* offsets, const int32_t* targets, const float* probs) {
+    TRY(ensure_device());
+    if (!offsets || (n >= 1 && !targets && offsets[n] > 0) || (!probs && n >= 1 && offsets[n] > 0))
+        return fail(IM_EINVAL, "null pointer argument");
+    TRY(check_csr_args(n, offsets[n]));
+    if (offsets[0] != 0) return fail(IM_EINVAL, "offsets[0] must be 0");
+    int64_t m = offsets[n];
+    free_graph_state();
+    int32_t* d_off = nullptr;
+    int32_t* d_tgt = nullptr;
+    float* d_prob = nullptr;
+    TRY(dalloc(d_off, (size_t)n + 1));
+    TRY(dalloc(d_tgt, (size_t)m));
+    TRY(dalloc(d_prob, (size_t)m));
+    CK(cudaMemcpyAsync(d_off, offsets, ((size_t)n + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, g.stream));
+    if (m) {
+        CK(cudaMemcpyAsync(d_tgt, targets, (size_t)m * sizeof(int32_t), cudaMemcpyHostToDevice, g.stream));
+        CK(cudaMemcpyAsync(d_prob, probs, (size_t)m * sizeof(float), cudaMemcpyHostToDevice, g.stream));
+    }
+    g.n = n;
+    g.m = m;
+    int r = load_common(n, m, d_off, d_tgt, d_prob);
+    cudaStreamSynchronize(g.stream);
+    dfree(d_off);
+    dfree(d_tgt);
+    dfree(d_prob);
+    if (r) free_graph_state();
+    return r;
+}
+
+int im_load_csr_device(int32_t n, int64_t m, const int32_t* d_offsets, const int32_t* d_targets, const float* d_probs) {
+    TRY(ensure_device());
+    if (!d_offsets || (m > 0 && (!d_targets || !d_probs))) return fail(IM_EINVAL, "null pointer argument");
+    TRY(check_csr_args(n, m));
+    free_graph_state();
+    g.n = n;
+    g.m = m;
+    int r = load_common(n, m, d_offsets, d_targets, d_probs);
+    if (r) free_graph_state();
+    return r;
+}
+
+int im_build_sketches(int32_t J, uint64_t seed) {
+    if (!g.loaded) return fail(IM_ESTATE, "im_build_sketches: no graph loaded");
+    if (J < 32 || J > 1024 || J % 32) return fail(IM_EINVAL, "J must be a multiple of 32 in [32, 1024] (got %d)", J);
+    g.st.total_sweeps = 0;
+    g.st.total_edges = 0;
+    g.st.sweep_kernel_ms = 0;
+    g.st.sweep_launches = 0;
+    g.st.window_edges = 0;
+    int64_t l0 = g.launches;
+    TRY(alloc_sketch_state(J));
+    TRY(setup_salts(J, seed));
+    TRY(build_fresh());
+    g.st.J = J;
+    g.st.kernel_launches = g.launches - l0;
+    return 0;
+}
+
+int im_estimate_device(double* d_out) {
+    if (!g.built) return fail(IM_ESTATE, "im_estimate: sketches not built");
+    if (!d_out) return fail(IM_EINVAL, "null output");
+    CK(launch_estimate(g, d_out));
+    return sync();
+}
+
+int im_estimate(double* out) {
+    if (!g.built) return fail(IM_ESTATE, "im_estimate: sketches not built");
+    if (!out) return fail(IM_EINVAL, "null output");
+    double* d = nullptr;
+    TRY(dalloc(d, (size_t)g.n));
+    CK(launch_estimate(g, d));
+    CK(cudaMemcpyAsync(out, d, (size_t)g.n * sizeof(double), cudaMemcpyDeviceToHost, g.stream));
+    int r = sync();
+    dfree(d);
+    return r;
+}
+
+int im_select_seeds_ex(int32_t K, double eps_l, double eps_g, int32_t* out_seeds, double* out_scores) {
+    if (!g.built) return fail(IM_ESTATE, "im_select_seeds: sketches not built");
+    if (K < 0 || K > g.n) return fail(IM_EINVAL, "K must be in [0, n] (got %d, n = %d)", K, g.n);
+    if (std::isnan(eps_l) || std::isnan(eps_g) || eps_l < 0 || eps_g < 0) return fail(IM_EINVAL, "thresholds must be >= 0 and not NaN");
+    if (K > 0 && (!out_seeds || !out_scores)) return fail(IM_EINVAL, "null output");
+    auto t0 = clk::now();
+    int64_t l0 = g.launches;
+    g.st.total_sweeps = 0;
+    g.st.total_edges = 0;
+    g.st.sweep_kernel_ms = 0;
+    g.st.sweep_launches = 0;
+    g.st.window_edges = 0;
+    g.st.rebuilds = 0;
+    g.st.bfs_levels = 0;
+    g.st.bfs_edges = 0;
+    g.steps.clear();
+    if (K == 0) return 0;
+    // start from S = {}, varsigma = 0, M_S' = 0 and freshly built sketches
+    if (!g.fresh) TRY(build_fresh());
+    const size_t n = (size_t)g.n, W = (size_t)g.J / 32;
+    CK(cudaMemsetAsync(g.vis, 0, n * W * sizeof(uint32_t), g.stream));
+    CK(cudaMemsetAsync(g.inS, 0, n, g.stream));
+    CK(cudaMemsetAsync(g.MS, 0, (size_t)g.J, g.stream));
+    CK(cudaMemsetAsync(g.varsigma, 0, sizeof(double), g.stream));
+    CK(cudaMemsetAsync(g.sigma_count, 0, sizeof(ull), g.stream));
+    std::vector<int32_t> seeds(K);
+    std::vector<double> scores(K);
+    bool pool_check = false;
+    for (int k = 0; k < K; k++) {
+        // line 10: argmax over the pool
+        CK(cudaMemsetAsync(g.key, 0, sizeof(ull), g.stream));
+        CK(cudaMemsetAsync(g.first, 0x7F, sizeof(int), g.stream));
+        CK(launch_argmax(g, pool_check));
+        // lines 11, 13-14: S <- S + s, BFS for R_G(S), sigma
+        CK(cudaMemsetAsync(&g.ctr[0], 0, sizeof(IterCounters), g.stream));
+        CK(launch_seed_start(g, k));
+        IterCounters hc;
+        TRY(readback(&g.ctr[0], sizeof hc, &hc));
+        int cur = 0;
+        while (hc.next_items > 0) {
+            int n_items = hc.next_items, n_v = hc.changed;
+            g.st.bfs_edges += (int64_t)hc.next_edges;
+            uint32_t tag = ++g.bt;
+            CK(cudaMemsetAsync(&g.ctr[cur ^ 1], 0, sizeof(IterCounters), g.stream));
+            CK(launch_bfs_level(g, cur, n_items, tag));
+            CK(launch_bfs_clear(g, cur, n_v));
+            TRY(readback(&g.ctr[cur ^ 1], sizeof hc, &hc));
+            cur ^= 1;
+            g.st.bfs_levels++;
+        }
+        if (hc.changed > 0) CK(launch_bfs_clear(g, cur, hc.changed));  // last frontier: only out-degree-0 vertices
+        pool_check = true;
+        g.any_blocked = true;
+        // lines 12, 15-27: error test, M_S' merge or rebuild decision
+        CK(launch_error_check(g, k, K, eps_l, eps_g));
+        StepDev rec;
+        TRY(readback(g.rec, sizeof rec, &rec));
+        im_step s;
+        static_assert(sizeof(im_step) == sizeof(StepDev), "im_step layout");
+        memcpy(&s, &rec, sizeof s);
+        g.steps.push_back(s);
+        seeds[k] = rec.vertex;
+        scores[k] = rec.sigma;
+        if (rec.executed) {  // lines 21-25: rebuild on the residual graph, R_S = R_G(S)
+            TRY(simulate(true));
+            g.st.rebuilds++;
+        }
+    }
+    memcpy(out_seeds, seeds.data(), K * sizeof(int32_t));
+    memcpy(out_scores, scores.data(), K * sizeof(double));
+    g.st.last_select_ms = ms_since(t0);
+    g.st.kernel_launches = g.launches - l0;
+    return 0;
+}
+
+int im_select_seeds(int32_t K, double err_threshold, int32_t* out_seeds, double* out_scores) {
+    return im_select_seeds_ex(K, err_threshold, err_threshold, out_seeds, out_scores);
+}
+
+static void unpermute_rows(const uint8_t* in, uint8_t* out, int64_t nrows) {
+    const int J = g.J;
+    for (int64_t r = 0; r < nrows; r++)
+        for (int jj = 0; jj < J; jj++) out[r * J + g.perm[jj]] = in[r * J + jj];
+}
+
+int im_get_register_rows(int64_t nrows, const int32_t* rows, uint8_t* out) {
+    if (!g.built) return fail(IM_ESTATE, "registers not built");
+    if (nrows < 0 || (nrows > 0 && (!rows || !out))) return fail(IM_EINVAL, "bad arguments");
+    for (int64_t i = 0; i < nrows; i++)
+        if (rows[i] < 0 || rows[i] >= g.n) return fail(IM_EINVAL, "row %lld out of range", (long long)i);
+    if (nrows == 0) return 0;
+    int32_t* drows = nullptr;
+    uint8_t* dout = nullptr;
+    TRY(dalloc(drows, (size_t)nrows));
+    TRY(dalloc(dout, (size_t)nrows * g.J));
+    CK(cudaMemcpyAsync(drows, rows, nrows * sizeof(int32_t), cudaMemcpyHostToDevice, g.stream));
+    CK(launch_gather_rows(g, drows, nrows, dout));
+    std::vector<uint8_t> tmp((size_t)nrows * g.J);
+    CK(cudaMemcpyAsync(tmp.data(), dout, tmp.size(), cudaMemcpyDeviceToHost, g.stream));
+    TRY(sync());
+    dfree(drows);
+    dfree(dout);
+    unpermute_rows(tmp.data(), out, nrows);
+    return 0;
+}
+
+int im_get_registers(uint8_t* out) {
+    if (!g.built) return fail(IM_ESTATE, "registers not built");
+    if (!out) return fail(IM_EINVAL, "null output");
+    std::vector<uint8_t> tmp((size_t)g.n * g.J);
+    CK(cudaMemcpyAsync(tmp.data(), g.M, tmp.size(), cudaMemcpyDeviceToHost, g.stream));
+    TRY(sync());
+    unpermute_rows(tmp.data(), out, g.n);
+    return 0;
+}
+
+int im_get_reach(uint32_t* out) {
+    if (!g.built) return fail(IM_ESTATE, "sketches not built");
+    if (!out) return fail(IM_EINVAL, "null output");
+    const size_t W = (size_t)g.J / 32, n = (size_t)g.n;
+    std::vector<uint32_t> tmp(n * W);
+    CK(cudaMemcpyAsync(tmp.data(), g.vis, tmp.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost, g.stream));
+    TRY(sync());
+    for (size_t v = 0; v < n; v++) {
+        uint32_t* o = out + v * W;
+        for (size_t w = 0; w < W; w++) o[w] = 0;
+        for (int jj = 0; jj < g.J; jj++)
+            if (tmp[v * W + (jj >> 5)] >> (jj & 31) & 1u) {
+                int j = g.perm[jj];
+                o[j >> 5] |= 1u << (j & 31);
+            }
+    }
+    return 0;
+}
+
+int im_get_step_log(im_step* out, int32_t cap) {
+    if (cap < 0 || (cap > 0 && !out)) return fail(IM_EINVAL, "bad arguments");
+    int k = (int)std::min<size_t>((size_t)cap, g.steps.size());
+    if (k) memcpy(out, g.steps.data(), k * sizeof(im_step));
+    return k;
+}
+
+int im_get_stats(im_stats* out) {
+    if (!out) return fail(IM_EINVAL, "null output");
+    *out = g.st;
+    out->n = g.n;
+    out->J = g.J;
+    out->m = g.m;
+    return 0;
+}
+
+}  // extern "C"

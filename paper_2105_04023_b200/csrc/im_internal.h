@@ -1,0 +1,116 @@
+// im_internal.h -- library-private state and kernel launchers (host side).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/im.h"
+
+namespace im {
+
+typedef unsigned long long ull;
+
+constexpr int SEG = 256;        // max edges per work item (a segment of one vertex's edge list)
+constexpr int DENSE_WIN = 32;   // windows wider than this many simulations take the warp-cooperative path
+constexpr int BLOCK = 256;      // threads per block of the persistent work-list kernels
+
+// device-side counters of one sweep / BFS level (one 32-byte D2H per iteration)
+struct IterCounters {
+    int next_items;     // work items appended for the next iteration
+    int changed;        // vertices that changed (first change per iteration)
+    ull next_edges;     // edges covered by the appended items
+    int batch;          // dynamic batch cursor of the persistent kernel
+    int pad;
+    ull new_bits;       // BFS: newly visited (vertex, simulation) pairs
+    ull win_edges;      // sweep: edges with a non-empty candidate window (after the change filter)
+};
+
+struct StepDev {  // mirrors im_step
+    int32_t vertex, pad;
+    int64_t score;
+    double e;
+    int64_t sigma_count;
+    double sigma, delta, err_l, err_g;
+    int32_t rebuilt, executed;
+};
+
+struct Ctx {
+    int dev = -1, num_sms = 0;
+    cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;
+    // graph (Sec. 3.3 CSR) + edge prep (Eq. 4-5)
+    bool loaded = false;
+    int32_t n = 0;
+    int64_t m = 0;
+    int32_t* off = nullptr;     // n+1 forward offsets
+    uint2* fwd = nullptr;       // m {target, h}
+    uint32_t* fwdT = nullptr;   // m per-edge thresholds (null when constant)
+    int32_t* roff = nullptr;    // n+1 reverse offsets
+    uint2* rev = nullptr;       // m {source, h} grouped by target
+    uint32_t* revT = nullptr;
+    bool constT = true;
+    uint32_t T0 = 0;
+    int4* ritems = nullptr;     // all reverse segments {v, eb, ee, 0}
+    int32_t n_ritems = 0;
+    int32_t n_fitems_cap = 0;   // sum_v ceil(outdeg/SEG)
+    // sketches
+    int32_t J = 0;
+    uint64_t seed = 0;
+    uint32_t seedV = 0, seedJ = 0;
+    std::vector<int32_t> perm;  // internal (ascending salt) index -> simulation j
+    uint32_t* Xs = nullptr;     // sorted salts [J]
+    uint16_t* s12 = nullptr;    // [4097]
+    int32_t* permd = nullptr;   // [J]
+    uint8_t* M = nullptr;       // n*J registers, row-major, internal simulation order
+    uint32_t* vis = nullptr;    // n*(J/32) R_G(S) bits, internal order
+    bool built = false, fresh = false, any_blocked = false;
+    // sweep buffers
+    int4* items[2] = {nullptr, nullptr};
+    ull* chg[2] = {nullptr, nullptr};
+    uint32_t tag = 0;
+    IterCounters* ctr = nullptr;   // [2]
+    // selection buffers
+    uint8_t* inS = nullptr;
+    uint8_t* MS = nullptr;
+    uint32_t* delta[2] = {nullptr, nullptr};
+    int4* bitems[2] = {nullptr, nullptr};
+    int32_t* bvl[2] = {nullptr, nullptr};
+    uint32_t* btag = nullptr;
+    uint32_t bt = 0;
+    StepDev* rec = nullptr;
+    double* varsigma = nullptr;
+    ull* key = nullptr;
+    int* first = nullptr;
+    ull* sigma_count = nullptr;
+    // host pinned scratch
+    void* hpin = nullptr;
+    // bookkeeping
+    im_stats st{};
+    std::vector<im_step> steps;
+    int64_t launches = 0;
+    int max_blocks_sweep = 0, max_blocks_bfs = 0;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+};
+
+// ---- launchers (im_kernels.cu); all enqueue on c.stream, return cudaError_t ----
+cudaError_t launch_validate(Ctx& c, const int32_t* off, const int32_t* tgt, const float* prob, int* flags);
+cudaError_t launch_const_check(Ctx& c, const float* prob, int* flag);
+cudaError_t launch_edge_prep(Ctx& c, const int32_t* tgt, const float* prob, int32_t* indeg);
+cudaError_t launch_transpose(Ctx& c, int32_t* cursor);
+cudaError_t launch_build_items(Ctx& c, const int32_t* offs, int4* items, int32_t* nseg_scratch, void* tmp, size_t tmp_bytes);
+cudaError_t scan_exclusive(Ctx& c, const int32_t* in, int32_t* out, int n, void* tmp, size_t& tmp_bytes);
+cudaError_t launch_salt_tables(Ctx& c);
+cudaError_t launch_init_registers(Ctx& c);
+cudaError_t launch_sweep(Ctx& c, bool first, const int4* items, int n_items, uint32_t tag_in, uint32_t tag_out,
+                         int out_buf, bool blocked);
+cudaError_t launch_estimate(Ctx& c, double* out);
+cudaError_t launch_argmax(Ctx& c, bool pool);
+cudaError_t launch_seed_start(Ctx& c, int k);
+cudaError_t launch_bfs_level(Ctx& c, int cur, int n_items, uint32_t tag);
+cudaError_t launch_bfs_clear(Ctx& c, int cur, int n_v);
+cudaError_t launch_error_check(Ctx& c, int k, int K, double eps_l, double eps_g);
+cudaError_t launch_gather_rows(Ctx& c, const int32_t* rows, int64_t nrows, uint8_t* out);
+
+}  // namespace im

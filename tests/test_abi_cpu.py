@@ -1,0 +1,63 @@
+"""Host-side checks that need no GPU: the C-ABI library loads, exports every symbol that
+include/im.h declares, and rejects bad call order / arguments before touching the device."""
+import os
+import re
+import subprocess
+
+import pytest
+
+import paper_2105_04023_b200 as im
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "im.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(im_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_header_declares_the_boundary():
+    syms = declared_symbols()
+    for s in ("im_load_csr", "im_build_sketches", "im_estimate", "im_select_seeds"):
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol():
+    out = subprocess.run(["nm", "-D", "--defined-only", im.LIB_PATH], capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (im_\w+)", out))
+    missing = [s for s in declared_symbols() if s not in exported]
+    assert not missing, missing
+    assert set(declared_symbols()) == set(im.SIGNATURES), "binding and header disagree"
+
+
+def test_library_loads_and_binds():
+    L = im.lib()
+    for name in declared_symbols():
+        assert hasattr(L, name)
+    assert im.im_version() == 100
+
+
+def test_call_order_errors_without_gpu():
+    im.im_free()
+    with pytest.raises(im.IMError) as e:
+        im.im_build_sketches(64, 1)
+    assert e.value.code == im.IM_ESTATE
+    with pytest.raises(im.IMError) as e:
+        im.im_estimate(4)
+    assert e.value.code == im.IM_ESTATE
+    with pytest.raises(im.IMError) as e:
+        im.im_select_seeds(1, 0.05)
+    assert e.value.code == im.IM_ESTATE
+
+
+def test_no_oracle_in_product_path():
+    """The product package never imports or links the oracle."""
+    pkg = os.path.join(ROOT, "paper_2105_04023_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, f), errors="replace").read()
+                assert "import oracle" not in txt and "liboracle" not in txt and "from oracle" not in txt, f
+    out = subprocess.run(["ldd", im.LIB_PATH], capture_output=True, text=True).stdout
+    assert "oracle" not in out
