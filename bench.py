@@ -192,13 +192,22 @@ def main():
         if dist is not None:
             dist.barrier()
 
+    phase_ms = {"load": [], "build": [], "estimate": [], "select": []}
+
     def step_device():
+        t = time.perf_counter()
         im.im_load_csr_device(n, m, d_off, d_tgt, d_pr)
+        t1 = time.perf_counter()
         im.im_build_sketches(cfg.J, cfg.salt_seed)
         sb = im.im_get_stats()
+        t2 = time.perf_counter()
         im.im_estimate_device(d_est)
+        t3 = time.perf_counter()
         seeds, scores = im.im_select_seeds(cfg.K, cfg.t)
         ss = im.im_get_stats()
+        t4 = time.perf_counter()
+        for k, a, b in (("load", t, t1), ("build", t1, t2), ("estimate", t2, t3), ("select", t3, t4)):
+            phase_ms[k].append((b - a) * 1e3)
         return sb, ss, seeds, scores
 
     def step_e2e():
@@ -279,6 +288,8 @@ def main():
                              "first_build_gedge_sims_per_s": first_build.get("edges", 0) * J / max(first_build.get("sweep_kernel_ms", 1e-9), 1e-9) / 1e6,
                              "prep_ms": first_build.get("prep_ms"), "sweeps_per_step": statistics.mean(sweeps),
                              "sweep_launches_per_step": statistics.mean(launches_sweep), "rebuilds_per_step": statistics.mean(rebuilds)},
+            "phase_ms": {k: statistics.mean(v[-args.steps:]) for k, v in phase_ms.items()}, "step_ms_all": times,
+            "bfs": {"levels": ss["bfs_levels"], "edges": ss["bfs_edges"]},
             "seeds_head": [int(x) for x in seeds[:5]], "sigma_final": float(scores[-1]) if len(scores) else None,
             "gen_seconds": gen_s}
     if e2e_ms is not None:

@@ -12,6 +12,7 @@
 #include <cstring>
 #include <random>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "im_device.cuh"
@@ -53,22 +54,35 @@ int fail(int code, const char* fmt, ...) {
         if (r_) return r_;     \
     } while (0)
 
+// Device buffers are capacity-managed: a buffer is only reallocated when a call needs more
+// bytes than it holds, so repeated loads / builds of the same workload never hit cudaMalloc /
+// cudaFree.  Keys are the addresses of the Ctx pointer members.  im_free() releases all.
+std::unordered_map<void*, size_t> g_cap;
+
 template <class T>
 void dfree(T*& p) {
     if (p) cudaFree((void*)p);
     p = nullptr;
+    g_cap.erase((void*)&p);
 }
 
 template <class T>
-int dalloc(T*& p, size_t count) {
+int dalloc(T*& p, size_t count, bool* fresh = nullptr) {
+    size_t bytes = (count ? count : 1) * sizeof(T);
+    auto it = g_cap.find((void*)&p);
+    if (p && it != g_cap.end() && it->second >= bytes) {
+        if (fresh) *fresh = false;
+        return 0;
+    }
     dfree(p);
-    if (count == 0) count = 1;
-    cudaError_t e = cudaMalloc((void**)&p, count * sizeof(T));
+    cudaError_t e = cudaMalloc((void**)&p, bytes);
     if (e != cudaSuccess) {
         cudaGetLastError();
         p = nullptr;
-        return fail(IM_ENOMEM, "cudaMalloc of %zu bytes failed: %s", count * sizeof(T), cudaGetErrorString(e));
+        return fail(IM_ENOMEM, "cudaMalloc of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
     }
+    g_cap[(void*)&p] = bytes;
+    if (fresh) *fresh = true;
     return 0;
 }
 
@@ -100,24 +114,31 @@ int ensure_device() {
     return 0;
 }
 
-void free_sketch_state() {
-    dfree(g.Xs); dfree(g.s12); dfree(g.permd); dfree(g.M); dfree(g.vis);
-    for (int i = 0; i < 2; i++) { dfree(g.items[i]); dfree(g.chg[i]); dfree(g.delta[i]); dfree(g.bitems[i]); dfree(g.bvl[i]); }
-    dfree(g.inS); dfree(g.MS); dfree(g.btag);
+void reset_sketch_state() {
     g.J = 0;
     g.built = g.fresh = g.any_blocked = false;
     g.perm.clear();
 }
 
-void free_graph_state() {
-    free_sketch_state();
-    dfree(g.off); dfree(g.fwd); dfree(g.fwdT); dfree(g.roff); dfree(g.rev); dfree(g.revT); dfree(g.ritems);
-    dfree(g.ctr); dfree(g.rec); dfree(g.varsigma); dfree(g.key); dfree(g.first); dfree(g.sigma_count);
+// forget the loaded graph (device buffers are kept for reuse; im_free releases them)
+void reset_graph_state() {
+    reset_sketch_state();
     g.loaded = false;
     g.n = 0;
     g.m = 0;
     g.steps.clear();
     g.st = im_stats{};
+}
+
+void release_all() {
+    dfree(g.Xs); dfree(g.s12); dfree(g.permd); dfree(g.M); dfree(g.vis);
+    for (int i = 0; i < 2; i++) { dfree(g.items[i]); dfree(g.chg[i]); dfree(g.delta[i]); dfree(g.bitems[i]); dfree(g.bvl[i]); }
+    dfree(g.inS); dfree(g.MS); dfree(g.btag);
+    dfree(g.off); dfree(g.fwd); dfree(g.fwdT); dfree(g.roff); dfree(g.rev); dfree(g.revT); dfree(g.ritems);
+    dfree(g.ctr); dfree(g.rec); dfree(g.varsigma); dfree(g.key); dfree(g.first); dfree(g.sigma_count);
+    dfree(g.t_flags); dfree(g.t_indeg); dfree(g.t_nseg); dfree(g.t_scan); dfree(g.t_off); dfree(g.t_tgt); dfree(g.t_prob);
+    dfree(g.t_est); dfree(g.t_rows); dfree(g.t_rowsout);
+    reset_graph_state();
 }
 
 int sync() {
@@ -140,7 +161,7 @@ int load_common(int32_t n, int64_t m, const int32_t* d_off_src, const int32_t* d
     // offsets: own copy
     TRY(dalloc(g.off, (size_t)n + 1));
     CK(cudaMemcpyAsync(g.off, d_off_src, ((size_t)n + 1) * sizeof(int32_t), cudaMemcpyDeviceToDevice, g.stream));
-    int* dflags = nullptr;
+    int*& dflags = g.t_flags;
     TRY(dalloc(dflags, 4));
     CK(cudaMemsetAsync(dflags, 0, 4 * sizeof(int), g.stream));
     CK(launch_validate(g, g.off, d_tgt, d_prob, dflags));
@@ -148,7 +169,6 @@ int load_common(int32_t n, int64_t m, const int32_t* d_off_src, const int32_t* d
     int hf[4];
     TRY(readback(dflags, sizeof hf, hf));
     if (hf[0]) {
-        dfree(dflags);
         return fail(IM_EINVAL, "invalid graph:%s%s%s", (hf[0] & 1) ? " offsets (offsets[0]!=0, decreasing, or offsets[n]!=m)" : "",
                     (hf[0] & 2) ? " targets out of [0,n)" : "", (hf[0] & 4) ? " probabilities not finite in [0,1]" : "");
     }
@@ -162,7 +182,7 @@ int load_common(int32_t n, int64_t m, const int32_t* d_off_src, const int32_t* d
     // forward records {target, h}, per-edge thresholds, in-degrees
     TRY(dalloc(g.fwd, (size_t)m));
     if (!g.constT) TRY(dalloc(g.fwdT, (size_t)m));
-    int32_t* indeg = nullptr;
+    int32_t*& indeg = g.t_indeg;
     TRY(dalloc(indeg, 2 * ((size_t)n + 1)));
     CK(cudaMemsetAsync(indeg, 0, 2 * ((size_t)n + 1) * sizeof(int32_t), g.stream));
     if (m > 0) CK(launch_edge_prep(g, d_tgt, d_prob, indeg));
@@ -171,7 +191,7 @@ int load_common(int32_t n, int64_t m, const int32_t* d_off_src, const int32_t* d
     size_t tmp_bytes = 0;
     CK(scan_exclusive(g, indeg, g.roff, n + 1, nullptr, tmp_bytes));
     tmp_bytes += 256;
-    char* tmp = nullptr;
+    char*& tmp = g.t_scan;
     TRY(dalloc(tmp, tmp_bytes));
     CK(scan_exclusive(g, indeg, g.roff, n + 1, tmp, tmp_bytes));
     // transpose
@@ -180,7 +200,7 @@ int load_common(int32_t n, int64_t m, const int32_t* d_off_src, const int32_t* d
     CK(cudaMemsetAsync(indeg, 0, ((size_t)n + 1) * sizeof(int32_t), g.stream));
     if (m > 0) CK(launch_transpose(g, indeg));
     // work items: reverse segments of every vertex (sweep 1), forward item capacity (BFS)
-    int32_t* nseg = nullptr;
+    int32_t*& nseg = g.t_nseg;
     TRY(dalloc(nseg, 2 * ((size_t)n + 1)));
     CK(launch_build_items(g, g.roff, nullptr, nseg, tmp, tmp_bytes));
     int32_t total[2];
@@ -192,10 +212,6 @@ int load_common(int32_t n, int64_t m, const int32_t* d_off_src, const int32_t* d
     TRY(readback(nseg + (n + 1) + n, sizeof(int32_t), &total[1]));
     g.n_fitems_cap = total[1];
     TRY(sync());
-    dfree(tmp);
-    dfree(nseg);
-    dfree(indeg);
-    dfree(dflags);
     // small per-graph state
     TRY(dalloc(g.ctr, 2));
     TRY(dalloc(g.rec, 1));
@@ -222,9 +238,8 @@ int check_csr_args(int32_t n, int64_t m) {
 
 // ----------------------------------------------------------- a1-a4: build
 int alloc_sketch_state(int32_t J) {
-    if (g.J == J && g.M) return 0;
-    free_sketch_state();
     size_t n = (size_t)g.n, W = (size_t)J / 32;
+    bool fr = false;
     TRY(dalloc(g.Xs, (size_t)J));
     TRY(dalloc(g.s12, 4097));
     TRY(dalloc(g.permd, (size_t)J));
@@ -232,19 +247,18 @@ int alloc_sketch_state(int32_t J) {
     TRY(dalloc(g.vis, n * W));
     for (int i = 0; i < 2; i++) {
         TRY(dalloc(g.items[i], (size_t)std::max(g.n_ritems, 1)));
-        TRY(dalloc(g.chg[i], n));
-        CK(cudaMemsetAsync(g.chg[i], 0, n * sizeof(ull), g.stream));
-        TRY(dalloc(g.delta[i], n * W));
-        CK(cudaMemsetAsync(g.delta[i], 0, n * W * sizeof(uint32_t), g.stream));
+        // tags only grow (g.tag, g.bt are never reset), so reused buffers need no clearing
+        TRY(dalloc(g.chg[i], n, &fr));
+        if (fr) CK(cudaMemsetAsync(g.chg[i], 0, n * sizeof(ull), g.stream));
+        TRY(dalloc(g.delta[i], n * W, &fr));
+        if (fr || g.J != J) CK(cudaMemsetAsync(g.delta[i], 0, n * W * sizeof(uint32_t), g.stream));
         TRY(dalloc(g.bitems[i], (size_t)std::max(g.n_fitems_cap, 1)));
         TRY(dalloc(g.bvl[i], n));
     }
     TRY(dalloc(g.inS, n));
     TRY(dalloc(g.MS, (size_t)J));
-    TRY(dalloc(g.btag, n));
-    CK(cudaMemsetAsync(g.btag, 0, n * sizeof(uint32_t), g.stream));
-    g.tag = 0;
-    g.bt = 0;
+    TRY(dalloc(g.btag, n, &fr));
+    if (fr) CK(cudaMemsetAsync(g.btag, 0, n * sizeof(uint32_t), g.stream));
     g.J = J;
     return 0;
 }
@@ -355,7 +369,7 @@ int im_set_stream(void* s) {
 
 void im_free(void) {
     if (g.dev >= 0) cudaStreamSynchronize(g.stream);
-    free_graph_state();
+    release_all();
 }
 
 int im_load_csr(int32_t n, const int32_t* offsets, const int32_t* targets, const float* probs) {
@@ -365,10 +379,10 @@ int im_load_csr(int32_t n, const int32_t* offsets, const int32_t* targets, const
     TRY(check_csr_args(n, offsets[n]));
     if (offsets[0] != 0) return fail(IM_EINVAL, "offsets[0] must be 0");
     int64_t m = offsets[n];
-    free_graph_state();
-    int32_t* d_off = nullptr;
-    int32_t* d_tgt = nullptr;
-    float* d_prob = nullptr;
+    reset_graph_state();
+    int32_t*& d_off = g.t_off;
+    int32_t*& d_tgt = g.t_tgt;
+    float*& d_prob = g.t_prob;
     TRY(dalloc(d_off, (size_t)n + 1));
     TRY(dalloc(d_tgt, (size_t)m));
     TRY(dalloc(d_prob, (size_t)m));
@@ -380,11 +394,7 @@ int im_load_csr(int32_t n, const int32_t* offsets, const int32_t* targets, const
     g.n = n;
     g.m = m;
     int r = load_common(n, m, d_off, d_tgt, d_prob);
-    cudaStreamSynchronize(g.stream);
-    dfree(d_off);
-    dfree(d_tgt);
-    dfree(d_prob);
-    if (r) free_graph_state();
+    if (r) reset_graph_state();
     return r;
 }
 
@@ -392,11 +402,11 @@ int im_load_csr_device(int32_t n, int64_t m, const int32_t* d_offsets, const int
     TRY(ensure_device());
     if (!d_offsets || (m > 0 && (!d_targets || !d_probs))) return fail(IM_EINVAL, "null pointer argument");
     TRY(check_csr_args(n, m));
-    free_graph_state();
+    reset_graph_state();
     g.n = n;
     g.m = m;
     int r = load_common(n, m, d_offsets, d_targets, d_probs);
-    if (r) free_graph_state();
+    if (r) reset_graph_state();
     return r;
 }
 
@@ -427,13 +437,11 @@ int im_estimate_device(double* d_out) {
 int im_estimate(double* out) {
     if (!g.built) return fail(IM_ESTATE, "im_estimate: sketches not built");
     if (!out) return fail(IM_EINVAL, "null output");
-    double* d = nullptr;
+    double*& d = g.t_est;
     TRY(dalloc(d, (size_t)g.n));
     CK(launch_estimate(g, d));
     CK(cudaMemcpyAsync(out, d, (size_t)g.n * sizeof(double), cudaMemcpyDeviceToHost, g.stream));
-    int r = sync();
-    dfree(d);
-    return r;
+    return sync();
 }
 
 int im_select_seeds_ex(int32_t K, double eps_l, double eps_g, int32_t* out_seeds, double* out_scores) {
@@ -527,8 +535,8 @@ int im_get_register_rows(int64_t nrows, const int32_t* rows, uint8_t* out) {
     for (int64_t i = 0; i < nrows; i++)
         if (rows[i] < 0 || rows[i] >= g.n) return fail(IM_EINVAL, "row %lld out of range", (long long)i);
     if (nrows == 0) return 0;
-    int32_t* drows = nullptr;
-    uint8_t* dout = nullptr;
+    int32_t*& drows = g.t_rows;
+    uint8_t*& dout = g.t_rowsout;
     TRY(dalloc(drows, (size_t)nrows));
     TRY(dalloc(dout, (size_t)nrows * g.J));
     CK(cudaMemcpyAsync(drows, rows, nrows * sizeof(int32_t), cudaMemcpyHostToDevice, g.stream));
@@ -536,8 +544,6 @@ int im_get_register_rows(int64_t nrows, const int32_t* rows, uint8_t* out) {
     std::vector<uint8_t> tmp((size_t)nrows * g.J);
     CK(cudaMemcpyAsync(tmp.data(), dout, tmp.size(), cudaMemcpyDeviceToHost, g.stream));
     TRY(sync());
-    dfree(drows);
-    dfree(dout);
     unpermute_rows(tmp.data(), out, nrows);
     return 0;
 }

@@ -84,6 +84,17 @@ struct Ctx {
     ull* key = nullptr;
     int* first = nullptr;
     ull* sigma_count = nullptr;
+    // reused temporaries (edge prep, host-pointer loads, diagnostics)
+    int* t_flags = nullptr;
+    int32_t* t_indeg = nullptr;
+    int32_t* t_nseg = nullptr;
+    char* t_scan = nullptr;
+    int32_t* t_off = nullptr;
+    int32_t* t_tgt = nullptr;
+    float* t_prob = nullptr;
+    double* t_est = nullptr;
+    int32_t* t_rows = nullptr;
+    uint8_t* t_rowsout = nullptr;
     // host pinned scratch
     void* hpin = nullptr;
     // bookkeeping

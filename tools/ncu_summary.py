@@ -1,0 +1,65 @@
+"""Summarise ncu outputs into small text files for profiles/ (run here, no GPU needed).
+
+    python tools/ncu_summary.py launches gpurun_out/launches_c3.csv  > profiles/r01_launches_c3.txt
+    python tools/ncu_summary.py report   gpurun_out/sweep_c4.ncu-rep > profiles/r01_sweep_c4.txt
+"""
+import collections
+import csv
+import io
+import subprocess
+import sys
+
+UNIT = {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0, "second": 1e3, "s": 1e3}
+
+
+def launches(path):
+    rows = [r for r in csv.reader(open(path)) if len(r) > 5]
+    hdr = rows[0]
+    ik, iv, iu = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    for r in rows[1:]:
+        if r[iu] not in UNIT:
+            continue
+        name = r[ik].split("(")[0].replace("void ", "")
+        agg[name][0] += 1
+        agg[name][1] += float(r[iv].replace(",", "")) * UNIT[r[iu]]
+    tot = sum(x[1] for x in agg.values())
+    print(f"# ncu launch list {path}: gpu__time_duration.sum per kernel (cold-cache, serialised; compare shares)")
+    print(f"# total {tot:.2f} ms over {sum(x[0] for x in agg.values())} launches")
+    for k, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        print(f"{t:10.3f} ms {t / tot * 100:5.1f}%  n={c:5d}  avg={t / c * 1e3:9.1f} us  {k}")
+
+
+def report(path):
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    want = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+            "dram__throughput.avg.pct_of_peak_sustained_elapsed", "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
+            "sm__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sector_hit_rate.pct", "l1tex__t_sector_hit_rate.pct",
+            "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum",
+            "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread", "launch__grid_size",
+            "smsp__issue_active.avg.pct_of_peak_sustained_active", "lts__t_requests_srcunit_tex_op_atom_dot_cas.sum"]
+    for r in rows[2:]:
+        d = dict(zip(hdr, r))
+        u = dict(zip(hdr, units))
+        print(f"# ncu --set full {path}")
+        for k in want:
+            if k in d:
+                print(f"{k:70s} {d[k]:>22s} {u.get(k, '')}")
+        stalls = [(k, float(d[k])) for k in hdr if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio")
+                  and d[k] not in ("", "n/a")]
+        stalls.sort(key=lambda x: -x[1])
+        print("# top stall reasons (warps per issue)")
+        for k, v in stalls[:8]:
+            print(f"  {k.replace('smsp__average_warps_issue_stalled_', '').replace('_per_issue_active.ratio', ''):30s} {v:8.3f}")
+        try:
+            rd = float(d["dram__bytes_read.sum"].replace(",", ""))
+            wr = float(d["dram__bytes_write.sum"].replace(",", ""))
+            print(f"# traffic per launch = {rd + wr:.4g} {u['dram__bytes_read.sum']}")
+        except (KeyError, ValueError):
+            pass
+
+
+if __name__ == "__main__":
+    {"launches": launches, "report": report}[sys.argv[1]](sys.argv[2])
