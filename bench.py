@@ -290,6 +290,7 @@ def main():
                              "sweep_launches_per_step": statistics.mean(launches_sweep), "rebuilds_per_step": statistics.mean(rebuilds)},
             "phase_ms": {k: statistics.mean(v[-args.steps:]) for k, v in phase_ms.items()}, "step_ms_all": times,
             "bfs": {"levels": ss["bfs_levels"], "edges": ss["bfs_edges"]},
+            "argmax": {"full_passes": ss["argmax_full"], "lazy_passes": ss["argmax_lazy"], "sorted_rows": ss["sorted_rows"]},
             "seeds_head": [int(x) for x in seeds[:5]], "sigma_final": float(scores[-1]) if len(scores) else None,
             "gen_seconds": gen_s}
     if e2e_ms is not None:

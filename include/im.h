@@ -73,6 +73,10 @@ typedef struct {
     int64_t sweep_launches;    /* sweep kernel launches in the window */
     int64_t window_edges;      /* enumerated edges whose candidate window was non-empty after the change filter */
     int64_t kernel_launches;   /* all kernel launches in the window */
+    int32_t argmax_full;       /* full argmax passes in the last selection (exact lazy argmax) */
+    int32_t argmax_lazy;       /* candidate-list argmax evaluations in the last selection */
+    int32_t sorted_rows;       /* 1 if adjacency rows are sorted by edge hash (constant threshold) */
+    int32_t pad2;
 } im_stats;
 
 /*

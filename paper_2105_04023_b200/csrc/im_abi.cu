@@ -19,7 +19,6 @@
 #include "im_internal.h"
 
 namespace im {
-int occupancy_sweep(int* blocks_per_sm_sweep, int* blocks_per_sm_bfs);
 }
 
 using namespace im;
@@ -101,7 +100,8 @@ int ensure_device() {
     g.dev = dev;
     g.num_sms = p.multiProcessorCount;
     int bs = 0, bb = 0;
-    CK((cudaError_t)occupancy_sweep(&bs, &bb));
+    CK((cudaError_t)occupancy_sweep(&bs));
+    CK((cudaError_t)occupancy_bfs(&bb));
     g.max_blocks_sweep = std::max(1, bs) * g.num_sms;
     g.max_blocks_bfs = std::max(1, bb) * g.num_sms;
     if (!g.own_stream) CK(cudaStreamCreateWithFlags(&g.own_stream, cudaStreamNonBlocking));
@@ -132,12 +132,13 @@ void reset_graph_state() {
 
 void release_all() {
     dfree(g.Xs); dfree(g.s12); dfree(g.permd); dfree(g.M); dfree(g.vis);
-    for (int i = 0; i < 2; i++) { dfree(g.items[i]); dfree(g.chg[i]); dfree(g.delta[i]); dfree(g.bitems[i]); dfree(g.bvl[i]); }
-    dfree(g.inS); dfree(g.MS); dfree(g.btag);
+    for (int i = 0; i < 2; i++) { dfree(g.items[i]); dfree(g.bits[i]); dfree(g.delta[i]); dfree(g.bitems[i]); dfree(g.bvl[i]); }
+    dfree(g.inS); dfree(g.MS); dfree(g.btag); dfree(g.gain); dfree(g.list); dfree(g.lcount); dfree(g.hist);
     dfree(g.off); dfree(g.fwd); dfree(g.fwdT); dfree(g.roff); dfree(g.rev); dfree(g.revT); dfree(g.ritems);
     dfree(g.ctr); dfree(g.rec); dfree(g.varsigma); dfree(g.key); dfree(g.first); dfree(g.sigma_count);
     dfree(g.t_flags); dfree(g.t_indeg); dfree(g.t_nseg); dfree(g.t_scan); dfree(g.t_off); dfree(g.t_tgt); dfree(g.t_prob);
     dfree(g.t_est); dfree(g.t_rows); dfree(g.t_rowsout);
+    for (int i = 0; i < 5; i++) dfree(g.t_prep[i]);
     reset_graph_state();
 }
 
@@ -179,27 +180,33 @@ int load_common(int32_t n, int64_t m, const int32_t* d_off_src, const int32_t* d
         TRY(readback(d_prob, sizeof(float), &w0));
         g.T0 = live_threshold(w0);
     }
-    // forward records {target, h}, per-edge thresholds, in-degrees
+    // constant threshold: rows ordered by h >> B0 (im_prep.cu)
+    g.B0 = g.T0 <= 1u ? 0 : 32 - __builtin_clz(g.T0 - 1u);
+    g.sorted_h = g.constT && m > 1;
+    // forward records {target, h}, thresholds, reverse records {source, h}
     TRY(dalloc(g.fwd, (size_t)m));
-    if (!g.constT) TRY(dalloc(g.fwdT, (size_t)m));
+    TRY(dalloc(g.rev, (size_t)m));
+    if (!g.constT) {
+        TRY(dalloc(g.fwdT, (size_t)m));
+        TRY(dalloc(g.revT, (size_t)m));
+    }
+    TRY(dalloc(g.roff, (size_t)n + 1));
     int32_t*& indeg = g.t_indeg;
     TRY(dalloc(indeg, 2 * ((size_t)n + 1)));
-    CK(cudaMemsetAsync(indeg, 0, 2 * ((size_t)n + 1) * sizeof(int32_t), g.stream));
-    if (m > 0) CK(launch_edge_prep(g, d_tgt, d_prob, indeg));
-    // reverse offsets = exclusive scan of in-degrees
-    TRY(dalloc(g.roff, (size_t)n + 1));
+    size_t sz[5];
+    CK(prep_scratch_sizes(g, sz));
+    void* scr[5];
+    for (int i = 0; i < 5; i++) {
+        TRY(dalloc(g.t_prep[i], sz[i]));
+        scr[i] = g.t_prep[i];
+    }
+    CK(prep_edges(g, d_tgt, d_prob, indeg, nullptr, scr, sz));
+    // work items: reverse segments of every vertex (sweep 1), forward item capacity (BFS)
     size_t tmp_bytes = 0;
     CK(scan_exclusive(g, indeg, g.roff, n + 1, nullptr, tmp_bytes));
     tmp_bytes += 256;
     char*& tmp = g.t_scan;
     TRY(dalloc(tmp, tmp_bytes));
-    CK(scan_exclusive(g, indeg, g.roff, n + 1, tmp, tmp_bytes));
-    // transpose
-    TRY(dalloc(g.rev, (size_t)m));
-    if (!g.constT) TRY(dalloc(g.revT, (size_t)m));
-    CK(cudaMemsetAsync(indeg, 0, ((size_t)n + 1) * sizeof(int32_t), g.stream));
-    if (m > 0) CK(launch_transpose(g, indeg));
-    // work items: reverse segments of every vertex (sweep 1), forward item capacity (BFS)
     int32_t*& nseg = g.t_nseg;
     TRY(dalloc(nseg, 2 * ((size_t)n + 1)));
     CK(launch_build_items(g, g.roff, nullptr, nseg, tmp, tmp_bytes));
@@ -246,18 +253,22 @@ int alloc_sketch_state(int32_t J) {
     TRY(dalloc(g.M, n * (size_t)J));
     TRY(dalloc(g.vis, n * W));
     for (int i = 0; i < 2; i++) {
-        TRY(dalloc(g.items[i], (size_t)std::max(g.n_ritems, 1)));
-        // tags only grow (g.tag, g.bt are never reset), so reused buffers need no clearing
-        TRY(dalloc(g.chg[i], n, &fr));
-        if (fr) CK(cudaMemsetAsync(g.chg[i], 0, n * sizeof(ull), g.stream));
+        TRY(dalloc(g.items[i], (size_t)g.n_ritems + 4 * n + 1));  // slices add <= 3 partial segments per vertex
+        // a completed build leaves both change-bit buffers zero; fresh ones are cleared here
+        TRY(dalloc(g.bits[i], n, &fr));
+        if (fr) CK(cudaMemsetAsync(g.bits[i], 0, n * sizeof(uint32_t), g.stream));
         TRY(dalloc(g.delta[i], n * W, &fr));
         if (fr || g.J != J) CK(cudaMemsetAsync(g.delta[i], 0, n * W * sizeof(uint32_t), g.stream));
-        TRY(dalloc(g.bitems[i], (size_t)std::max(g.n_fitems_cap, 1)));
+        TRY(dalloc(g.bitems[i], (size_t)g.n_fitems_cap + 4 * n + 1));
         TRY(dalloc(g.bvl[i], n));
     }
     TRY(dalloc(g.inS, n));
     TRY(dalloc(g.MS, (size_t)J));
-    TRY(dalloc(g.btag, n, &fr));
+    TRY(dalloc(g.gain, n));
+    TRY(dalloc(g.list, n));
+    TRY(dalloc(g.lcount, 2));
+    TRY(dalloc(g.hist, 4096));
+    TRY(dalloc(g.btag, n, &fr));  // BFS tags only grow (g.bt is never reset)
     if (fr) CK(cudaMemsetAsync(g.btag, 0, n * sizeof(uint32_t), g.stream));
     g.J = J;
     return 0;
@@ -290,45 +301,38 @@ int setup_salts(int32_t J, uint64_t seed) {
 }
 
 // Alg. 1 lines 2-5 / 21-25 + Alg. 2 to the fixpoint (eps_c = 0).  blocked: R_S = current visited bits.
+// Sweep s consumes the items of the vertices changed in sweep s-1 (all in-edge segments for s = 1),
+// filters by their chunk-change bits bits[(s-1)&1], records its own changes in bits[s&1]; the
+// compaction then emits the next items and clears bits[(s-1)&1] for sweep s+1.
 int simulate(bool blocked) {
     auto t0 = clk::now();
     CK(launch_init_registers(g));
+    CK(cudaMemsetAsync(g.bits[1], 0, (size_t)g.n * sizeof(uint32_t), g.stream));
     IterCounters hc;
     int sweeps = 0;
-    int64_t edges = 0;
+    int64_t edges = 0, wedges = 0, launches = 0;
     float kms = 0.f;
-    // sweep 1: every in-edge of every vertex
-    uint32_t tag = ++g.tag;
-    int out = 0;
-    CK(cudaMemsetAsync(&g.ctr[out], 0, sizeof(IterCounters), g.stream));
-    CK(cudaEventRecord(g.ev[0], g.stream));
-    CK(launch_sweep(g, true, g.ritems, g.n_ritems, 0u, tag, out, blocked));
-    CK(cudaEventRecord(g.ev[1], g.stream));
-    TRY(readback(&g.ctr[out], sizeof hc, &hc));
-    int64_t wedges = (int64_t)hc.win_edges;
-    float t;
-    CK(cudaEventElapsedTime(&t, g.ev[0], g.ev[1]));
-    kms += t;
-    sweeps = 1;
+    const int4* items = g.ritems;
+    int n_items = g.n_ritems;
     edges = g.m;
-    int64_t launches = 1;
-    while (hc.next_items > 0) {
-        uint32_t tag_in = tag;
-        tag = ++g.tag;
-        int cur = out;
-        out ^= 1;
-        int n_items = hc.next_items;
-        edges += (int64_t)hc.next_edges;
-        CK(cudaMemsetAsync(&g.ctr[out], 0, sizeof(IterCounters), g.stream));
+    for (int s = 1;; s++) {
+        IterCounters* ctr = &g.ctr[s & 1];
+        CK(cudaMemsetAsync(ctr, 0, sizeof(IterCounters), g.stream));
         CK(cudaEventRecord(g.ev[0], g.stream));
-        CK(launch_sweep(g, false, g.items[cur], n_items, tag_in, tag, out, blocked));
+        CK(launch_sweep(g, items, n_items, s == 1 ? nullptr : g.bits[(s - 1) & 1], g.bits[s & 1], ctr, blocked));
         CK(cudaEventRecord(g.ev[1], g.stream));
-        TRY(readback(&g.ctr[out], sizeof hc, &hc));
-        wedges += (int64_t)hc.win_edges;
+        CK(launch_compact(g, g.bits[s & 1], g.bits[(s - 1) & 1], g.items[s & 1], ctr));
+        TRY(readback(ctr, sizeof hc, &hc));
+        float t;
         CK(cudaEventElapsedTime(&t, g.ev[0], g.ev[1]));
         kms += t;
         sweeps++;
         launches++;
+        wedges += (int64_t)hc.win_edges;
+        if (hc.next_items == 0) break;
+        items = g.items[s & 1];
+        n_items = hc.next_items;
+        edges += (int64_t)hc.next_edges;
     }
     g.st.builds++;
     g.st.last_build_sweeps = sweeps;
@@ -459,6 +463,7 @@ int im_select_seeds_ex(int32_t K, double eps_l, double eps_g, int32_t* out_seeds
     g.st.rebuilds = 0;
     g.st.bfs_levels = 0;
     g.st.bfs_edges = 0;
+    g.st_argmax_full = g.st_argmax_list = 0;
     g.steps.clear();
     if (K == 0) return 0;
     // start from S = {}, varsigma = 0, M_S' = 0 and freshly built sketches
@@ -471,15 +476,31 @@ int im_select_seeds_ex(int32_t K, double eps_l, double eps_g, int32_t* out_seeds
     CK(cudaMemsetAsync(g.sigma_count, 0, sizeof(ull), g.stream));
     std::vector<int32_t> seeds(K);
     std::vector<double> scores(K);
-    bool pool_check = false;
+    bool pool_check = false, need_full = true;
+    const int T = (int)std::min<int64_t>(g.n, std::max<int64_t>(1024, std::min<int64_t>(65536, g.n / 256)));
+    int list_len = 0, theta = 0;
     for (int k = 0; k < K; k++) {
-        // line 10: argmax over the pool
-        CK(cudaMemsetAsync(g.key, 0, sizeof(ull), g.stream));
-        CK(cudaMemsetAsync(g.first, 0x7F, sizeof(int), g.stream));
-        CK(launch_argmax(g, pool_check));
+        // line 10: argmax over the pool (exact lazy evaluation, im_kernels.cu "a6")
+        if (!need_full) {
+            CK(launch_argmax_list(g, list_len));
+            ull hk;
+            TRY(readback(g.key, sizeof hk, &hk));
+            if (hk == 0 || (int64_t)(hk >> 32) < theta) need_full = true;
+            g.st_argmax_list++;
+        }
+        if (need_full) {
+            CK(launch_argmax_full(g, pool_check, T));
+            int lc[2];
+            TRY(readback(g.lcount, sizeof lc, lc));
+            list_len = lc[0];
+            theta = lc[1];
+            need_full = false;
+            g.st_argmax_full++;
+        }
         // lines 11, 13-14: S <- S + s, BFS for R_G(S), sigma
         CK(cudaMemsetAsync(&g.ctr[0], 0, sizeof(IterCounters), g.stream));
         CK(launch_seed_start(g, k));
+        CK(launch_bfs_items(g, 0));
         IterCounters hc;
         TRY(readback(&g.ctr[0], sizeof hc, &hc));
         int cur = 0;
@@ -490,11 +511,12 @@ int im_select_seeds_ex(int32_t K, double eps_l, double eps_g, int32_t* out_seeds
             CK(cudaMemsetAsync(&g.ctr[cur ^ 1], 0, sizeof(IterCounters), g.stream));
             CK(launch_bfs_level(g, cur, n_items, tag));
             CK(launch_bfs_clear(g, cur, n_v));
+            CK(launch_bfs_items(g, cur ^ 1));
             TRY(readback(&g.ctr[cur ^ 1], sizeof hc, &hc));
             cur ^= 1;
             g.st.bfs_levels++;
         }
-        if (hc.changed > 0) CK(launch_bfs_clear(g, cur, hc.changed));  // last frontier: only out-degree-0 vertices
+        if (hc.changed > 0) CK(launch_bfs_clear(g, cur, hc.changed));  // frontier without work items
         pool_check = true;
         g.any_blocked = true;
         // lines 12, 15-27: error test, M_S' merge or rebuild decision
@@ -510,6 +532,7 @@ int im_select_seeds_ex(int32_t K, double eps_l, double eps_g, int32_t* out_seeds
         if (rec.executed) {  // lines 21-25: rebuild on the residual graph, R_S = R_G(S)
             TRY(simulate(true));
             g.st.rebuilds++;
+            need_full = true;
         }
     }
     memcpy(out_seeds, seeds.data(), K * sizeof(int32_t));
@@ -587,6 +610,9 @@ int im_get_step_log(im_step* out, int32_t cap) {
 int im_get_stats(im_stats* out) {
     if (!out) return fail(IM_EINVAL, "null output");
     *out = g.st;
+    out->argmax_full = g.st_argmax_full;
+    out->argmax_lazy = g.st_argmax_list;
+    out->sorted_rows = g.sorted_h ? 1 : 0;
     out->n = g.n;
     out->J = g.J;
     out->m = g.m;

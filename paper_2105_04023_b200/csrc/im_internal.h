@@ -52,6 +52,8 @@ struct Ctx {
     uint32_t* revT = nullptr;
     bool constT = true;
     uint32_t T0 = 0;
+    int B0 = 0;                 // thr_bits(T0): candidate windows are salt blocks of 2^B0
+    bool sorted_h = false;      // adjacency rows sorted by h (constant threshold only)
     int4* ritems = nullptr;     // all reverse segments {v, eb, ee, 0}
     int32_t n_ritems = 0;
     int32_t n_fitems_cap = 0;   // sum_v ceil(outdeg/SEG)
@@ -68,8 +70,7 @@ struct Ctx {
     bool built = false, fresh = false, any_blocked = false;
     // sweep buffers
     int4* items[2] = {nullptr, nullptr};
-    ull* chg[2] = {nullptr, nullptr};
-    uint32_t tag = 0;
+    uint32_t* bits[2] = {nullptr, nullptr};  // per-vertex 32-simulation-chunk change bits, ping-pong
     IterCounters* ctr = nullptr;   // [2]
     // selection buffers
     uint8_t* inS = nullptr;
@@ -83,6 +84,10 @@ struct Ctx {
     double* varsigma = nullptr;
     ull* key = nullptr;
     int* first = nullptr;
+    int32_t* gain = nullptr;     // stored gains of the last full argmax pass (-1: not in the pool)
+    int32_t* list = nullptr;     // candidate list of the lazy argmax
+    int* lcount = nullptr;       // [0] list length, [1] theta
+    uint32_t* hist = nullptr;    // gain histogram of the full pass
     ull* sigma_count = nullptr;
     // reused temporaries (edge prep, host-pointer loads, diagnostics)
     int* t_flags = nullptr;
@@ -94,6 +99,7 @@ struct Ctx {
     float* t_prob = nullptr;
     double* t_est = nullptr;
     int32_t* t_rows = nullptr;
+    char* t_prep[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // edge-prep scratch (src, keys, vals, cub)
     uint8_t* t_rowsout = nullptr;
     // host pinned scratch
     void* hpin = nullptr;
@@ -101,26 +107,44 @@ struct Ctx {
     im_stats st{};
     std::vector<im_step> steps;
     int64_t launches = 0;
+    int st_argmax_full = 0, st_argmax_list = 0;
     int max_blocks_sweep = 0, max_blocks_bfs = 0;
     cudaEvent_t ev[2] = {nullptr, nullptr};
 };
 
-// ---- launchers (im_kernels.cu); all enqueue on c.stream, return cudaError_t ----
+// grid for a grid-stride kernel over `work` threads, capped at 8 resident blocks per SM
+inline int grid_for(Ctx& c, int64_t work, int per_block = BLOCK) {
+    int64_t g = (work + per_block - 1) / per_block;
+    int64_t cap = (int64_t)c.num_sms * 8;
+    if (g > cap) g = cap;
+    return (int)(g < 1 ? 1 : g);
+}
+#define LAUNCHED(c) ((c).launches++, cudaGetLastError())
+
+// ---- launchers (im_kernels.cu, im_sweep.cu); all enqueue on c.stream, return cudaError_t ----
+cudaError_t launch_compact(Ctx& c, const uint32_t* bits_new, uint32_t* bits_clear, int4* items_out, IterCounters* ctr);
+int occupancy_sweep(int* blocks_per_sm);
+int occupancy_bfs(int* blocks_per_sm);
 cudaError_t launch_validate(Ctx& c, const int32_t* off, const int32_t* tgt, const float* prob, int* flags);
 cudaError_t launch_const_check(Ctx& c, const float* prob, int* flag);
-cudaError_t launch_edge_prep(Ctx& c, const int32_t* tgt, const float* prob, int32_t* indeg);
-cudaError_t launch_transpose(Ctx& c, int32_t* cursor);
+cudaError_t prep_scratch_sizes(Ctx& c, size_t* sz);  // 5 sizes (bytes) for prep_edges scratch
+cudaError_t prep_edges(Ctx& c, const int32_t* tgt, const float* prob, int32_t* indeg, int32_t* unused, void** scr,
+                       const size_t* sz);
 cudaError_t launch_build_items(Ctx& c, const int32_t* offs, int4* items, int32_t* nseg_scratch, void* tmp, size_t tmp_bytes);
 cudaError_t scan_exclusive(Ctx& c, const int32_t* in, int32_t* out, int n, void* tmp, size_t& tmp_bytes);
 cudaError_t launch_salt_tables(Ctx& c);
 cudaError_t launch_init_registers(Ctx& c);
-cudaError_t launch_sweep(Ctx& c, bool first, const int4* items, int n_items, uint32_t tag_in, uint32_t tag_out,
-                         int out_buf, bool blocked);
+// one sweep over `items`; bits_in: chunk-change bits of the previous sweep (null: no filter, sweep 1);
+// bits_out: this sweep's chunk-change bits (red.or); counters in *ctr (zeroed by the caller)
+cudaError_t launch_sweep(Ctx& c, const int4* items, int n_items, const uint32_t* bits_in, uint32_t* bits_out,
+                         IterCounters* ctr, bool blocked);
 cudaError_t launch_estimate(Ctx& c, double* out);
-cudaError_t launch_argmax(Ctx& c, bool pool);
+cudaError_t launch_argmax_full(Ctx& c, bool pool, int T);
+cudaError_t launch_argmax_list(Ctx& c, int list_len);
 cudaError_t launch_seed_start(Ctx& c, int k);
 cudaError_t launch_bfs_level(Ctx& c, int cur, int n_items, uint32_t tag);
 cudaError_t launch_bfs_clear(Ctx& c, int cur, int n_v);
+cudaError_t launch_bfs_items(Ctx& c, int buf);
 cudaError_t launch_error_check(Ctx& c, int k, int K, double eps_l, double eps_g);
 cudaError_t launch_gather_rows(Ctx& c, const int32_t* rows, int64_t nrows, uint8_t* out);
 

@@ -1,301 +1,18 @@
 // im_kernels.cu -- sm_100a kernels of the hot path.
 //
-//   k_validate / k_const_check / k_edge_prep / k_transpose / k_items   a0 edge prep (Eq. 4-5, Sec. 3.3)
-//   k_init_registers                                                   a2 register init (Alg. 1 lines 2-5)
-//   k_sweep<...>                                                       a3+a4 Simulate sweeps (Alg. 2)
+//   (edge prep and register init: im_prep.cu)                          a0, a2
+//   (k_sweep / k_compact: im_sweep.cu)                                 a3+a4 Simulate sweeps (Alg. 2)
 //   k_estimate                                                         a5 Eq. 2
 //   k_argmax / k_seed_start / k_bfs_level / k_bfs_clear / k_error_check a6-a8 Alg. 1 loop body
 //
 // No tensor cores: the path is integer gather / byte-max, bound by HBM and the
 // INT pipes.  All work-list kernels are persistent (grid <= resident blocks)
 // and pull 32-item batches from a device cursor.
-#include <cub/device/device_scan.cuh>
 
 #include "im_device.cuh"
 #include "im_internal.h"
 
 namespace im {
-
-// ============================================================ a0: edge prep
-__global__ void k_validate(int32_t n, int64_t m, const int32_t* __restrict__ off, const int32_t* __restrict__ tgt,
-                           const float* __restrict__ prob, int* flags) {
-    int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
-    int f = 0;
-    if (tid == 0) {
-        if (off[0] != 0) f |= 1;
-        if ((int64_t)off[n] != m) f |= 1;
-    }
-    for (int64_t i = tid; i < n; i += stride)
-        if (off[i] > off[i + 1]) f |= 1;
-    for (int64_t e = tid; e < m; e += stride) {
-        int32_t v = tgt[e];
-        if (v < 0 || v >= n) f |= 2;
-        float w = prob[e];
-        if (!(w >= 0.0f && w <= 1.0f)) f |= 4;  // also rejects NaN
-    }
-    if (f) atomicOr(flags, f);
-}
-
-__global__ void k_const_check(int64_t m, const float* __restrict__ prob, int* flag) {
-    int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
-    uint32_t p0 = __float_as_uint(prob[0]);
-    bool diff = false;
-    for (int64_t e = tid; e < m; e += stride) diff |= __float_as_uint(prob[e]) != p0;
-    if (__any_sync(IM_FULL, diff) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
-}
-
-__device__ __forceinline__ int32_t edge_source(const int32_t* __restrict__ off, int32_t n, int64_t e) {
-    int32_t lo = 0, hi = n - 1;  // largest u with off[u] <= e
-    while (lo < hi) {
-        int32_t mid = (lo + hi + 1) >> 1;
-        if ((int64_t)off[mid] <= e) lo = mid; else hi = mid - 1;
-    }
-    return lo;
-}
-
-// h(u,v) (Eq. 4) and T_e (Eq. 5) per forward edge; in-degree histogram for the transpose
-__global__ void k_edge_prep(int32_t n, int64_t m, const int32_t* __restrict__ off, const int32_t* __restrict__ tgt,
-                            const float* __restrict__ prob, uint2* __restrict__ fwd, uint32_t* __restrict__ fwdT,
-                            int32_t* __restrict__ indeg) {
-    int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += stride) {
-        int32_t u = edge_source(off, n, e), v = tgt[e];
-        fwd[e] = make_uint2((uint32_t)v, edge_hash((uint32_t)u, (uint32_t)v));
-        if (fwdT) fwdT[e] = live_threshold(prob[e]);
-        atomicAdd(&indeg[v], 1);
-    }
-}
-
-__global__ void k_transpose(int32_t n, int64_t m, const int32_t* __restrict__ off, const uint2* __restrict__ fwd,
-                            const uint32_t* __restrict__ fwdT, const int32_t* __restrict__ roff, int32_t* __restrict__ cursor,
-                            uint2* __restrict__ rev, uint32_t* __restrict__ revT) {
-    int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += stride) {
-        int32_t u = edge_source(off, n, e);
-        uint2 f = fwd[e];
-        int32_t pos = roff[f.x] + atomicAdd(&cursor[f.x], 1);
-        rev[pos] = make_uint2((uint32_t)u, f.y);
-        if (revT) revT[pos] = fwdT[e];
-    }
-}
-
-__global__ void k_nseg(int32_t n, const int32_t* __restrict__ offs, int32_t* __restrict__ nseg) {
-    int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
-    if (v < n) nseg[v] = (offs[v + 1] - offs[v] + SEG - 1) / SEG;
-    if (v == n) nseg[n] = 0;
-}
-
-__global__ void k_fill_items(int32_t n, const int32_t* __restrict__ offs, const int32_t* __restrict__ base,
-                             int4* __restrict__ items) {
-    int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= n) return;
-    int32_t b = offs[v], e = offs[v + 1], p = base[v];
-    for (int32_t s = b; s < e; s += SEG) items[p++] = make_int4(v, s, min(s + SEG, e), 0);
-}
-
-// ============================================================ a2: register init
-// M_v[jj] = clz(Murmur3(v, seed_V) xor Murmur3(perm[jj], seed_J)), clz(0) = 32 (Alg. 1 lines 2-5; R5, R6)
-__global__ void k_init_registers(int32_t n, int32_t J, uint32_t seedV, uint32_t seedJ, const int32_t* __restrict__ perm,
-                                 uint4* __restrict__ M) {
-    __shared__ uint32_t HJ[1024];
-    for (int j = threadIdx.x; j < J; j += blockDim.x) HJ[j] = murmur_word((uint32_t)perm[j], seedJ);
-    __syncthreads();
-    const int cpr = J >> 4;  // 16-byte chunks per row
-    const int64_t total = (int64_t)n * cpr, stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += stride) {
-        uint32_t v = (uint32_t)(idx / cpr);
-        int c = (int)(idx - (int64_t)v * cpr) << 4;
-        uint32_t hv = murmur_word(v, seedV);
-        uint32_t w[4];
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-            uint32_t x = 0;
-#pragma unroll
-            for (int b = 0; b < 4; b++) x |= (uint32_t)__clz(hv ^ HJ[c + 4 * q + b]) << (8 * b);
-            w[q] = x;
-        }
-        M[idx] = make_uint4(w[0], w[1], w[2], w[3]);
-    }
-}
-
-// ============================================================ a3/a4: Simulate sweeps
-// Alg. 2 realised as an edge-parallel, in-place pass over the in-edges of
-// the vertices whose registers changed in the previous sweep (all vertices in sweep 1):
-// for in-edge (u,v) of such a v, every simulation j with (X_j xor h_uv) < T_uv and u not in
-// R_S[j] gets M_u[j] <- max(M_u[j], M_v[j]) (line 'update', pull direction R9).  Edges of
-// Gamma^-(L) into vertices outside L are skipped: pulling an unchanged row is a no-op.  The
-// fixpoint is unique, so the in-place order reaches exactly the oracle's registers.
-struct SweepArgs {
-    const int4* items;
-    int n_items;
-    IterCounters* ctr_next; // zeroed before launch: batch cursor + appends for the next sweep
-    const int32_t* roff;
-    const uint2* rev;
-    const uint32_t* revT;
-    uint32_t T0;
-    const uint32_t* Xs;
-    const uint16_t* s12;
-    int J;
-    uint32_t* M32;
-    const uint32_t* vis;
-    const ull* chg_in;
-    ull* chg_out;
-    uint32_t tag_in, tag_out;
-    int4* next_items;
-};
-
-template <bool BLOCKED>
-__device__ __forceinline__ uint32_t pull_word(const SweepArgs& a, const uint32_t* sX, uint32_t u, uint32_t v, int w,
-                                              uint32_t h, uint32_t T, int lo, int hi) {
-    uint32_t live = 0;
-#pragma unroll
-    for (int b = 0; b < 4; b++) {
-        int i = 4 * w + b;
-        bool ok = (i >= lo) & (i < hi) & ((sX[i] ^ h) < T);
-        live |= ok ? (0xFFu << (8 * b)) : 0u;
-    }
-    if (BLOCKED && live) {
-        uint32_t vb = (a.vis[(size_t)u * (a.J >> 5) + (w >> 3)] >> ((w & 7) << 2)) & 0xFu;
-        live &= ~expand4(vb);
-    }
-    if (!live) return 0u;
-    const int Jw = a.J >> 2;
-    uint32_t mv = __ldcg(&a.M32[(size_t)v * Jw + w]) & live;
-    if (!mv) return 0u;
-    return atomic_vmax4(&a.M32[(size_t)u * Jw + w], mv) ? (1u << (w >> 3)) : 0u;
-}
-
-template <bool CONST_T, bool BLOCKED, bool FILTER>
-__global__ void __launch_bounds__(BLOCK) k_sweep(SweepArgs a) {
-    __shared__ uint32_t sX[1024];
-    __shared__ uint16_t sS[4098];
-    __shared__ int sSlot[BLOCK / 32][32];
-    for (int i = threadIdx.x; i < a.J; i += blockDim.x) sX[i] = a.Xs[i];
-    for (int i = threadIdx.x; i < 4097; i += blockDim.x) sS[i] = a.s12[i];
-    __syncthreads();
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int J = a.J;
-
-    for (;;) {
-        int base = 0;
-        if (lane == 0) base = atomicAdd(&a.ctr_next->batch, 32);
-        base = __shfl_sync(IM_FULL, base, 0);
-        if (base >= a.n_items) break;
-        int it = base + lane;
-        int v = 0, eb = 0, cnt = 0;
-        uint32_t vbits = IM_FULL;
-        if (it < a.n_items) {
-            int4 I = a.items[it];
-            v = I.x;
-            eb = I.y;
-            cnt = I.z - I.y;
-            if (FILTER) {
-                ull w = a.chg_in[v];
-                vbits = ((uint32_t)(w >> 32) == a.tag_in) ? (uint32_t)w : 0u;
-                if (!vbits) cnt = 0;
-            }
-        }
-        int incl = warp_incl_scan(cnt, lane);
-        int total = __shfl_sync(IM_FULL, incl, 31);
-        int start = incl - cnt;
-        int carry = 0;
-        for (int e0 = 0; e0 < total; e0 += 32) {
-            // owner item of edge slot e0+lane: the last non-empty item starting at or before it
-            bool starts = cnt > 0 && start >= e0 && start < e0 + 32;
-            if (starts) sSlot[wib][start - e0] = lane;
-            uint32_t smask = __reduce_or_sync(IM_FULL, starts ? (1u << (start - e0)) : 0u);
-            __syncwarp();
-            uint32_t below = smask & ((2u << lane) - 1u);
-            int owner = below ? sSlot[wib][31 - __clz(below)] : carry;
-            __syncwarp();
-            carry = __shfl_sync(IM_FULL, owner, 31);
-            int ov = __shfl_sync(IM_FULL, v, owner);
-            int oeb = __shfl_sync(IM_FULL, eb, owner);
-            int ost = __shfl_sync(IM_FULL, start, owner);
-            uint32_t obits = __shfl_sync(IM_FULL, vbits, owner);
-            int idx = e0 + lane;
-
-            uint32_t u = 0, h = 0, T = 0, chg = 0;
-            int lo = 0, hi = 0;
-            bool dense = false;
-            if (idx < total) {
-                int e = oeb + (idx - ost);
-                uint2 r = a.rev[e];
-                u = r.x;
-                h = r.y;
-                T = CONST_T ? a.T0 : a.revT[e];
-                if (T) {
-                    edge_window(h, T, sX, sS, J, lo, hi);
-                    if (FILTER && lo < hi && !(obits & bit_range(lo >> 5, (hi - 1) >> 5))) hi = lo;
-                    if (hi - lo > DENSE_WIN) {
-                        dense = true;
-                    } else if (lo < hi) {
-                        for (int w = lo >> 2; w <= (hi - 1) >> 2; ++w) chg |= pull_word<BLOCKED>(a, sX, u, (uint32_t)ov, w, h, T, lo, hi);
-                    }
-                }
-            }
-            uint32_t wmask = __ballot_sync(IM_FULL, lo < hi);
-            if (lane == 0 && wmask) atomicAdd(&a.ctr_next->win_edges, (ull)__popc(wmask));
-            // wide windows (e.g. w close to 1): the whole warp walks the window, one word per lane
-            uint32_t dmask = __ballot_sync(IM_FULL, dense);
-            while (dmask) {
-                int l = __ffs(dmask) - 1;
-                dmask &= dmask - 1;
-                uint32_t du = __shfl_sync(IM_FULL, u, l), dh = __shfl_sync(IM_FULL, h, l), dT = __shfl_sync(IM_FULL, T, l);
-                int dlo = __shfl_sync(IM_FULL, lo, l), dhi = __shfl_sync(IM_FULL, hi, l);
-                uint32_t dv = (uint32_t)__shfl_sync(IM_FULL, ov, l);
-                uint32_t c = 0;
-                for (int w = (dlo >> 2) + lane; w <= (dhi - 1) >> 2; w += 32) c |= pull_word<BLOCKED>(a, sX, du, dv, w, dh, dT, dlo, dhi);
-                c = __reduce_or_sync(IM_FULL, c);
-                if (lane == l) chg |= c;
-            }
-            // record the change of u: chunk bits under this sweep's tag; the first recorder appends u's items
-            bool first = false;
-            if (chg) {
-                ull* p = &a.chg_out[u];
-                ull old = __ldcg(p);
-                for (;;) {
-                    uint32_t otag = (uint32_t)(old >> 32), ob = (uint32_t)old;
-                    bool same = otag == a.tag_out;
-                    uint32_t nb = same ? (ob | chg) : chg;
-                    if (same && nb == ob) break;
-                    ull want = ((ull)a.tag_out << 32) | nb;
-                    ull prev = atomicCAS(p, old, want);
-                    if (prev == old) {
-                        first = !same;
-                        break;
-                    }
-                    old = prev;
-                }
-            }
-            int rd = 0, ns = 0;
-            if (first) {
-                int rb = a.roff[u];
-                rd = a.roff[u + 1] - rb;
-                ns = (rd + SEG - 1) / SEG;
-            }
-            int ninc = warp_incl_scan(ns, lane);
-            int ntot = __shfl_sync(IM_FULL, ninc, 31);
-            uint32_t fmask = __ballot_sync(IM_FULL, first);
-            if (fmask) {
-                int pos = 0;
-                if (lane == 31) {
-                    if (ntot) pos = atomicAdd(&a.ctr_next->next_items, ntot);
-                    atomicAdd(&a.ctr_next->changed, __popc(fmask));
-                }
-                pos = __shfl_sync(IM_FULL, pos, 31);
-                long long esum = rd;
-#pragma unroll
-                for (int o = 16; o; o >>= 1) esum += __shfl_xor_sync(IM_FULL, esum, o);
-                if (lane == 0 && esum) atomicAdd(&a.ctr_next->next_edges, (ull)esum);
-                if (ns) {
-                    int rb = a.roff[u], re = rb + rd, p = pos + ninc - ns;
-                    for (int s = rb; s < re; s += SEG) a.next_items[p++] = make_int4((int)u, s, min(s + SEG, re), 0);
-                }
-            }
-        }
-    }
-}
 
 // ============================================================ a5: Eq. 2 estimate
 __global__ void k_estimate(int32_t n, int32_t J, const uint32_t* __restrict__ M32, double* __restrict__ out) {
@@ -311,83 +28,157 @@ __global__ void k_estimate(int32_t n, int32_t J, const uint32_t* __restrict__ M3
 }
 
 // ============================================================ a6: greedy argmax
-// score_v = sum_j max(M_S'[j], M_v[j]) over the pool (R14); key = score<<32 | (2^32-1-v) so the
-// 64-bit max picks the lowest id among equal scores.  Also the lowest id not in S (pool-empty fallback).
-template <bool POOL>
-__global__ void __launch_bounds__(BLOCK) k_argmax(int32_t n, int32_t J, const uint32_t* __restrict__ M32,
+// Alg. 1 line 10: s = argmax_v Estimate(Merge(M_S', M_v)).  Estimate is monotone in the integer
+// score_v = sum_j max(M_S'[j], M_v[j]) = sum_j M_S'[j] + gain_v with gain_v = sum_j (M_v[j] - M_S'[j])^+,
+// so the argmax over the pool (R14) is the argmax of gain_v, lowest id on ties via the 64-bit key
+// gain<<32 | (2^32-1-v).  gain_v only shrinks while M_S' grows (between rebuilds), so an exact lazy
+// argmax is used: a full pass stores every gain (an upper bound for later steps) and the list of
+// vertices with stored gain >= theta (about T of them); later steps evaluate only that list, and the
+// result is exact whenever its best current gain is >= theta (every vertex outside the list has
+// current gain <= stored gain < theta).  Otherwise the host runs a new full pass.
+// A row is read as 16-byte chunks by L lanes, 32/L vertices per warp, two groups in flight.
+__device__ __forceinline__ uint32_t gain16(uint4 x, uint4 m) {
+    return __vsadu4(__vsubus4(x.x, m.x), 0u) + __vsadu4(__vsubus4(x.y, m.y), 0u) + __vsadu4(__vsubus4(x.z, m.z), 0u) +
+           __vsadu4(__vsubus4(x.w, m.w), 0u);
+}
+
+constexpr int HIST_BINS = 4096;
+
+// LIST = false: every vertex (full pass: stores gains + histogram); LIST = true: the vertices in list[0..*count)
+template <bool POOL, bool LIST>
+__global__ void __launch_bounds__(BLOCK) k_argmax(int32_t n, int32_t J, int L, int C, const uint4* __restrict__ M16,
                                                   const uint8_t* __restrict__ MS, const uint32_t* __restrict__ vis,
-                                                  const uint8_t* __restrict__ inS, ull* key, int* first) {
-    __shared__ uint32_t sMS[256];
+                                                  ull* key, int32_t* gain_out, uint32_t* hist, int shift,
+                                                  const int32_t* __restrict__ list, const int* list_count) {
+    __shared__ uint4 sMS[64];
     __shared__ ull sKey[BLOCK / 32];
-    __shared__ int sFirst[BLOCK / 32];
-    const int Jw = J >> 2, W = J >> 5;
-    for (int i = threadIdx.x; i < Jw; i += blockDim.x) sMS[i] = reinterpret_cast<const uint32_t*>(MS)[i];
+    __shared__ uint32_t sHist[LIST ? 1 : HIST_BINS];
+    const int nch = J >> 4, W = J >> 5;
+    for (int i = threadIdx.x; i < nch; i += blockDim.x) sMS[i] = reinterpret_cast<const uint4*>(MS)[i];
+    if (!LIST)
+        for (int i = threadIdx.x; i < HIST_BINS; i += blockDim.x) sHist[i] = 0u;
     __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    ull best = 0;
-    int fst = 0x7FFFFFFF;
-    for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < n; v += warps) {
-        bool inpool = true;
-        if (POOL) {
-            bool full = true;
-            for (int w = lane; w < W; w += 32) full &= __ldcs(&vis[v * W + w]) == IM_FULL;
-            inpool = !__all_sync(IM_FULL, full);
-        }
-        if (inpool) {
-            uint32_t s = 0;
-            for (int w = lane; w < Jw; w += 32) s += __vsadu4(__vmaxu4(__ldcs(&M32[v * Jw + w]), sMS[w]), 0u);
+    const int nv = LIST ? *list_count : n;
+    const int lane = threadIdx.x & 31, q = lane & (L - 1), sub = lane / L, VPW = 32 / L;
+    uint4 ms[2];
 #pragma unroll
-            for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(IM_FULL, s, o);
-            ull k = ((ull)s << 32) | (ull)(0xFFFFFFFFu - (uint32_t)v);
-            best = k > best ? k : best;
+    for (int c = 0; c < 2; c++) {
+        int ci = q * C + c;
+        ms[c] = (c < C && ci < nch) ? sMS[ci] : make_uint4(0, 0, 0, 0);
+    }
+    const int64_t groups = ((int64_t)nv + VPW - 1) / VPW;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    ull best = 0;
+    for (int64_t g0 = gw; g0 < groups; g0 += 2 * nwarps) {
+        uint4 x[2][2];
+        int64_t vv[2];
+        bool ok[2];
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+            int64_t idx = (g0 + u * nwarps) * VPW + sub;
+            ok[u] = (g0 + u * nwarps) < groups && idx < nv;
+            vv[u] = ok[u] ? (LIST ? (int64_t)list[idx] : idx) : 0;
+#pragma unroll
+            for (int c = 0; c < 2; c++) {
+                int ci = q * C + c;
+                x[u][c] = (ok[u] && c < C && ci < nch) ? __ldcs(&M16[vv[u] * nch + ci]) : make_uint4(0, 0, 0, 0);
+            }
         }
-        if (lane == 0 && fst == 0x7FFFFFFF && !inS[v]) fst = (int)v;
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+            uint32_t gn = gain16(x[u][0], ms[0]) + gain16(x[u][1], ms[1]);
+            int full = 1;
+            if (POOL && ok[u])
+                for (int w = q; w < W; w += L) full &= __ldcs(&vis[vv[u] * W + w]) == IM_FULL;
+            for (int o = L >> 1; o; o >>= 1) {
+                gn += __shfl_xor_sync(IM_FULL, gn, o);
+                if (POOL) full &= __shfl_xor_sync(IM_FULL, full, o);
+            }
+            bool inpool = ok[u] && (!POOL || !full);
+            if (ok[u] && q == 0) {
+                if (inpool) {
+                    ull k = ((ull)gn << 32) | (ull)(0xFFFFFFFFu - (uint32_t)vv[u]);
+                    best = k > best ? k : best;
+                }
+                if (!LIST) {
+                    gain_out[vv[u]] = inpool ? (int32_t)gn : -1;
+                    if (inpool) atomicAdd(&sHist[min((int)(gn >> shift), HIST_BINS - 1)], 1u);
+                }
+            }
+        }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
         ull ob = __shfl_xor_sync(IM_FULL, best, o);
         best = ob > best ? ob : best;
     }
-    fst = __reduce_min_sync(IM_FULL, fst);
-    if (lane == 0) {
-        sKey[threadIdx.x >> 5] = best;
-        sFirst[threadIdx.x >> 5] = fst;
-    }
+    if (lane == 0) sKey[threadIdx.x >> 5] = best;
     __syncthreads();
     if (threadIdx.x == 0) {
         ull b = 0;
-        int f = 0x7FFFFFFF;
-        for (int i = 0; i < BLOCK / 32; i++) {
-            b = sKey[i] > b ? sKey[i] : b;
-            f = min(f, sFirst[i]);
-        }
+        for (int i = 0; i < BLOCK / 32; i++) b = sKey[i] > b ? sKey[i] : b;
         if (b) atomicMax(key, b);
-        if (f != 0x7FFFFFFF) atomicMin(first, f);
+    }
+    if (!LIST)
+        for (int i = threadIdx.x; i < HIST_BINS; i += blockDim.x)
+            if (sHist[i]) atomicAdd(&hist[i], sHist[i]);
+}
+
+// theta = lower edge of the highest histogram bin at which the suffix count reaches T
+__global__ void k_theta(const uint32_t* __restrict__ hist, int shift, int T, int* theta) {
+    if (threadIdx.x == 0) {
+        long long acc = 0;
+        int b = HIST_BINS - 1;
+        for (; b > 0; --b) {
+            acc += hist[b];
+            if (acc >= T) break;
+        }
+        *theta = b << shift;
+    }
+}
+
+__global__ void k_list_build(int32_t n, const int32_t* __restrict__ gain, const int* theta, int32_t* list, int* count) {
+    const int th = *theta, lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+        int64_t v = base + threadIdx.x;
+        bool take = v < n && gain[v] >= th;
+        uint32_t m = __ballot_sync(IM_FULL, take);
+        if (!m) continue;
+        int pos = 0;
+        if (lane == 0) pos = atomicAdd(count, __popc(m));
+        pos = __shfl_sync(IM_FULL, pos, 0);
+        if (take) list[pos + __popc(m & ((1u << lane) - 1u))] = (int32_t)v;
     }
 }
 
 // ============================================================ a7: seed diffusion
 // Alg. 1 lines 11, 13-14: S <- S + s; R_G(S) by a multi-simulation BFS from s over live edges
 // (same samples as the sketches, R13) carrying J-bit masks; visited bits only ever set.
-__global__ void k_seed_start(int32_t J, const ull* key, const int* first, const uint32_t* __restrict__ M32,
+__global__ void k_seed_start(int32_t n, int32_t J, const ull* key, const uint32_t* __restrict__ M32,
                              const uint8_t* __restrict__ MS, uint8_t* inS, uint32_t* vis, uint32_t* delta0,
                              const int32_t* __restrict__ off, int4* items0, int32_t* vl0, IterCounters* ctr0,
                              ull* sigma_count, StepDev* rec) {
     const int lane = threadIdx.x, W = J >> 5, Jw = J >> 2;
     ull k = *key;
-    uint32_t s = k ? (0xFFFFFFFFu - (uint32_t)k) : (uint32_t)*first;
-    int64_t score;
-    if (k) {
-        score = (int64_t)(k >> 32);
-    } else {  // pool empty: lowest id not in S (R14); its merged score is still reported
-        uint32_t acc = 0;
-        for (int w = lane; w < Jw; w += 32)
-            acc += __vsadu4(__vmaxu4(M32[(size_t)s * Jw + w], reinterpret_cast<const uint32_t*>(MS)[w]), 0u);
-#pragma unroll
-        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(IM_FULL, acc, o);
-        score = acc;
+    uint32_t s = k ? (0xFFFFFFFFu - (uint32_t)k) : 0u;
+    if (!k) {  // pool empty (every vertex covered in every simulation): lowest id not in S (R14)
+        for (int b = 0; b < n; b += 32) {
+            uint32_t z = __ballot_sync(IM_FULL, b + lane < n && !inS[b + lane]);
+            if (z) {
+                s = (uint32_t)(b + __ffs(z) - 1);
+                break;
+            }
+        }
     }
+    // integer numerator of Estimate(Merge(M_S', M_s)) (Alg. 1 line 12)
+    uint32_t acc = 0;
+    for (int w = lane; w < Jw; w += 32)
+        acc += __vsadu4(__vmaxu4(M32[(size_t)s * Jw + w], reinterpret_cast<const uint32_t*>(MS)[w]), 0u);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(IM_FULL, acc, o);
+    const int64_t score = acc;
     uint32_t bits = 0, any = 0;
     for (int w = lane; w < W; w += 32) {
         uint32_t d = ~vis[(size_t)s * W + w];
@@ -401,15 +192,12 @@ __global__ void k_seed_start(int32_t J, const ull* key, const int* first, const 
         bits += __shfl_xor_sync(IM_FULL, bits, o);
         any |= __shfl_xor_sync(IM_FULL, any, o);
     }
-    int b = off[s], e = off[s + 1];
-    int ns = any ? (e - b + SEG - 1) / SEG : 0;
-    for (int i = lane; i < ns; i += 32) items0[i] = make_int4((int)s, b + i * SEG, min(b + (i + 1) * SEG, e), 0);
+    (void)off;
+    (void)items0;
     if (lane == 0) {
         inS[s] = 1;
         *sigma_count += bits;
-        ctr0->next_items = ns;
         ctr0->changed = any ? 1 : 0;
-        ctr0->next_edges = any ? (ull)(e - b) : 0ull;
         if (any) vl0[0] = (int32_t)s;
         rec->vertex = (int32_t)s;
         rec->score = score;
@@ -526,32 +314,14 @@ __global__ void __launch_bounds__(BLOCK) k_bfs_level(BfsArgs a) {
                 if (lane == l) got += c;
             }
             newbits += (uint32_t)got;
+            // first new bit of v in this level: v joins the next frontier (its slices are built after the level)
             bool first = got > 0 && atomicMax(&a.btag[v], a.tag) < a.tag;
-            int rd = 0, ns = 0;
-            if (first) {
-                rd = a.off[v + 1] - a.off[v];
-                ns = (rd + SEG - 1) / SEG;
-            }
-            int ninc = warp_incl_scan(ns, lane);
-            int ntot = __shfl_sync(IM_FULL, ninc, 31);
             uint32_t fmask = __ballot_sync(IM_FULL, first);
             if (fmask) {
-                int pos = 0, vpos = 0;
-                if (lane == 31) {
-                    if (ntot) pos = atomicAdd(&a.ctr_next->next_items, ntot);
-                    vpos = atomicAdd(&a.ctr_next->changed, __popc(fmask));
-                }
-                pos = __shfl_sync(IM_FULL, pos, 31);
+                int vpos = 0;
+                if (lane == 31) vpos = atomicAdd(&a.ctr_next->changed, __popc(fmask));
                 vpos = __shfl_sync(IM_FULL, vpos, 31);
-                long long esum = rd;
-#pragma unroll
-                for (int o = 16; o; o >>= 1) esum += __shfl_xor_sync(IM_FULL, esum, o);
-                if (lane == 0 && esum) atomicAdd(&a.ctr_next->next_edges, (ull)esum);
-                if (first) {
-                    a.next_vl[vpos + __popc(fmask & ((1u << lane) - 1u))] = (int32_t)v;
-                    int b = a.off[v], e = b + rd, p = pos + ninc - ns;
-                    for (int s = b; s < e; s += SEG) a.next_items[p++] = make_int4((int)v, s, min(s + SEG, e), 0);
-                }
+                if (first) a.next_vl[vpos + __popc(fmask & ((1u << lane) - 1u))] = (int32_t)v;
             }
         }
     }
@@ -559,6 +329,68 @@ __global__ void __launch_bounds__(BLOCK) k_bfs_level(BfsArgs a) {
     if (lane == 0 && newbits) {
         atomicAdd(&a.ctr_next->new_bits, (ull)newbits);
         atomicAdd(a.sigma_count, (ull)newbits);
+    }
+}
+
+// Work items of a BFS frontier: for every vertex v of vl, the out-edges whose candidate window can
+// meet a simulation in Delta_v (<= 4 hash-sorted slices of its row for a constant threshold, the
+// whole row otherwise).
+__global__ void k_bfs_items(int J, int B, bool sorted, const uint32_t* __restrict__ Xs, const int32_t* __restrict__ vl,
+                            const uint32_t* __restrict__ delta, const int32_t* __restrict__ off, const uint2* __restrict__ fwd,
+                            int4* __restrict__ items, IterCounters* ctr) {
+    const int lane = threadIdx.x & 31, W = J >> 5, NQ = W < 4 ? W : 4;
+    const int nv = ctr->changed;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < nv; base += stride) {
+        int64_t i = base + threadIdx.x;
+        bool in = i < nv;
+        int eb[4], ee[4], k = 0, ns = 0, es = 0;
+        int v = in ? vl[i] : 0;
+        if (in) {
+            int rb = off[v], re = off[v + 1];
+            if (sorted) {
+                int sa[4], sb[4];
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    sa[q] = sb[q] = -1;
+                    if (q < NQ)
+                        for (int w = q * W / NQ; w < (q + 1) * W / NQ; w++) {
+                            uint32_t d = delta[(size_t)v * W + w];
+                            if (!d) continue;
+                            if (sa[q] < 0) sa[q] = 32 * w + __ffs(d) - 1;
+                            sb[q] = 32 * w + 31 - __clz(d);
+                        }
+                }
+                k = slices_for(fwd, rb, re, Xs, B, sa, sb, eb, ee);
+            } else if (rb < re) {
+                eb[0] = rb;
+                ee[0] = re;
+                k = 1;
+            }
+#pragma unroll
+            for (int t = 0; t < 4; t++)
+                if (t < k) {
+                    ns += (ee[t] - eb[t] + SEG - 1) / SEG;
+                    es += ee[t] - eb[t];
+                }
+        }
+        int ninc = warp_incl_scan(ns, lane);
+        int ntot = __shfl_sync(IM_FULL, ninc, 31);
+        if (!ntot) continue;
+        long long esum = es;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) esum += __shfl_xor_sync(IM_FULL, esum, o);
+        int pos = 0;
+        if (lane == 31) {
+            pos = atomicAdd(&ctr->next_items, ntot);
+            atomicAdd(&ctr->next_edges, (ull)esum);
+        }
+        pos = __shfl_sync(IM_FULL, pos, 31);
+        int p = pos + ninc - ns;
+#pragma unroll
+        for (int t = 0; t < 4; t++)
+            if (t < k)
+                for (int s0 = eb[t]; s0 < ee[t]; s0 += SEG) items[p++] = make_int4(v, s0, min(s0 + SEG, ee[t]), 0);
     }
 }
 
@@ -612,109 +444,58 @@ __global__ void k_gather_rows(int64_t nrows, int32_t J, const int32_t* __restric
 }
 
 // ============================================================ launchers
-static inline int grid_for(Ctx& c, int64_t work, int per_block = BLOCK) {
-    int64_t g = (work + per_block - 1) / per_block;
-    int64_t cap = (int64_t)c.num_sms * 8;
-    if (g > cap) g = cap;
-    return (int)(g < 1 ? 1 : g);
-}
-#define LAUNCHED(c) ((c).launches++, cudaGetLastError())
 
-cudaError_t launch_validate(Ctx& c, const int32_t* off, const int32_t* tgt, const float* prob, int* flags) {
-    k_validate<<<grid_for(c, c.m > c.n ? c.m : c.n), BLOCK, 0, c.stream>>>(c.n, c.m, off, tgt, prob, flags);
-    return LAUNCHED(c);
-}
-cudaError_t launch_const_check(Ctx& c, const float* prob, int* flag) {
-    k_const_check<<<grid_for(c, c.m), BLOCK, 0, c.stream>>>(c.m, prob, flag);
-    return LAUNCHED(c);
-}
-cudaError_t launch_edge_prep(Ctx& c, const int32_t* tgt, const float* prob, int32_t* indeg) {
-    k_edge_prep<<<grid_for(c, c.m), BLOCK, 0, c.stream>>>(c.n, c.m, c.off, tgt, prob, c.fwd, c.fwdT, indeg);
-    return LAUNCHED(c);
-}
-cudaError_t launch_transpose(Ctx& c, int32_t* cursor) {
-    k_transpose<<<grid_for(c, c.m), BLOCK, 0, c.stream>>>(c.n, c.m, c.off, c.fwd, c.fwdT, c.roff, cursor, c.rev, c.revT);
-    return LAUNCHED(c);
-}
-cudaError_t scan_exclusive(Ctx& c, const int32_t* in, int32_t* out, int n, void* tmp, size_t& tmp_bytes) {
-    cudaError_t e = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, in, out, n, c.stream);
-    if (tmp) c.launches++;
-    return e;
-}
-cudaError_t launch_build_items(Ctx& c, const int32_t* offs, int4* items, int32_t* nseg, void* tmp, size_t tmp_bytes) {
-    // nseg has n+1 entries; base = exclusive scan written in place into nseg+? -> use the second half
-    int32_t* base = nseg + (c.n + 1);
-    k_nseg<<<(c.n + 1 + BLOCK - 1) / BLOCK, BLOCK, 0, c.stream>>>(c.n, offs, nseg);
-    cudaError_t e = LAUNCHED(c);
-    if (e) return e;
-    e = scan_exclusive(c, nseg, base, c.n + 1, tmp, tmp_bytes);
-    if (e) return e;
-    if (items) {
-        k_fill_items<<<(c.n + BLOCK - 1) / BLOCK, BLOCK, 0, c.stream>>>(c.n, offs, base, items);
-        e = LAUNCHED(c);
-    }
-    return e;
-}
-cudaError_t launch_init_registers(Ctx& c) {
-    int64_t chunks = (int64_t)c.n * (c.J >> 4);
-    k_init_registers<<<grid_for(c, chunks), BLOCK, 0, c.stream>>>(c.n, c.J, c.seedV, c.seedJ, c.permd,
-                                                                  reinterpret_cast<uint4*>(c.M));
-    return LAUNCHED(c);
-}
-
-template <bool C, bool B, bool F>
-static void sweep_inst(int grid, cudaStream_t s, const SweepArgs& a) {
-    k_sweep<C, B, F><<<grid, BLOCK, 0, s>>>(a);
-}
-
-cudaError_t launch_sweep(Ctx& c, bool first, const int4* items, int n_items, uint32_t tag_in, uint32_t tag_out,
-                         int out_buf, bool blocked) {
-    SweepArgs a;
-    a.items = items;
-    a.n_items = n_items;
-    a.ctr_next = &c.ctr[out_buf];
-    a.roff = c.roff;
-    a.rev = c.rev;
-    a.revT = c.revT;
-    a.T0 = c.T0;
-    a.Xs = c.Xs;
-    a.s12 = c.s12;
-    a.J = c.J;
-    a.M32 = reinterpret_cast<uint32_t*>(c.M);
-    a.vis = c.vis;
-    a.chg_in = c.chg[tag_in & 1];
-    a.chg_out = c.chg[tag_out & 1];
-    a.tag_in = tag_in;
-    a.tag_out = tag_out;
-    a.next_items = c.items[out_buf];
-    int64_t want = ((int64_t)n_items + 32 * (BLOCK / 32) - 1) / (32 * (BLOCK / 32));
-    int grid = (int)(want < 1 ? 1 : (want > c.max_blocks_sweep ? c.max_blocks_sweep : want));
-    bool ct = c.constT;
-    if (first) {
-        if (ct) { if (blocked) sweep_inst<true, true, false>(grid, c.stream, a); else sweep_inst<true, false, false>(grid, c.stream, a); }
-        else { if (blocked) sweep_inst<false, true, false>(grid, c.stream, a); else sweep_inst<false, false, false>(grid, c.stream, a); }
-    } else {
-        if (ct) { if (blocked) sweep_inst<true, true, true>(grid, c.stream, a); else sweep_inst<true, false, true>(grid, c.stream, a); }
-        else { if (blocked) sweep_inst<false, true, true>(grid, c.stream, a); else sweep_inst<false, false, true>(grid, c.stream, a); }
-    }
-    return LAUNCHED(c);
-}
 
 cudaError_t launch_estimate(Ctx& c, double* out) {
     k_estimate<<<grid_for(c, (int64_t)c.n * 32), BLOCK, 0, c.stream>>>(c.n, c.J, reinterpret_cast<const uint32_t*>(c.M), out);
     return LAUNCHED(c);
 }
-cudaError_t launch_argmax(Ctx& c, bool pool) {
-    int g = grid_for(c, (int64_t)c.n * 32);
-    if (pool)
-        k_argmax<true><<<g, BLOCK, 0, c.stream>>>(c.n, c.J, reinterpret_cast<const uint32_t*>(c.M), c.MS, c.vis, c.inS, c.key, c.first);
-    else
-        k_argmax<false><<<g, BLOCK, 0, c.stream>>>(c.n, c.J, reinterpret_cast<const uint32_t*>(c.M), c.MS, c.vis, c.inS, c.key, c.first);
+static void argmax_geometry(const Ctx& c, int& L, int& C) {
+    const int nch = c.J >> 4;
+    C = nch > 32 ? 2 : 1;
+    L = 1;
+    while (L * C < nch) L <<= 1;
+}
+static int hist_shift(const Ctx& c) {
+    int sh = 0;
+    while (((32 * c.J) >> sh) >= HIST_BINS) sh++;
+    return sh;
+}
+
+// full pass: exact argmax into c.key (zeroed here) + stored gains + candidate list for later steps
+cudaError_t launch_argmax_full(Ctx& c, bool pool, int T) {
+    int L, C;
+    argmax_geometry(c, L, C);
+    const int sh = hist_shift(c);
+    cudaError_t e = cudaMemsetAsync(c.key, 0, sizeof(ull), c.stream);
+    if (!e) e = cudaMemsetAsync(c.hist, 0, HIST_BINS * sizeof(uint32_t), c.stream);
+    if (!e) e = cudaMemsetAsync(c.lcount, 0, 2 * sizeof(int), c.stream);
+    if (e) return e;
+    int g = grid_for(c, (int64_t)c.n * L / 2);
+    const uint4* M16 = reinterpret_cast<const uint4*>(c.M);
+    if (pool) k_argmax<true, false><<<g, BLOCK, 0, c.stream>>>(c.n, c.J, L, C, M16, c.MS, c.vis, c.key, c.gain, c.hist, sh, nullptr, nullptr);
+    else k_argmax<false, false><<<g, BLOCK, 0, c.stream>>>(c.n, c.J, L, C, M16, c.MS, c.vis, c.key, c.gain, c.hist, sh, nullptr, nullptr);
+    if ((e = LAUNCHED(c))) return e;
+    k_theta<<<1, 32, 0, c.stream>>>(c.hist, sh, T, c.lcount + 1);
+    if ((e = LAUNCHED(c))) return e;
+    k_list_build<<<grid_for(c, c.n), BLOCK, 0, c.stream>>>(c.n, c.gain, c.lcount + 1, c.list, c.lcount);
+    return LAUNCHED(c);
+}
+
+// lazy step: exact gains over the candidate list only; valid iff best gain >= theta (checked by the host)
+cudaError_t launch_argmax_list(Ctx& c, int list_len) {
+    int L, C;
+    argmax_geometry(c, L, C);
+    cudaError_t e = cudaMemsetAsync(c.key, 0, sizeof(ull), c.stream);
+    if (e) return e;
+    int g = grid_for(c, (int64_t)list_len * L / 2);
+    const uint4* M16 = reinterpret_cast<const uint4*>(c.M);
+    k_argmax<true, true><<<g, BLOCK, 0, c.stream>>>(c.n, c.J, L, C, M16, c.MS, c.vis, c.key, nullptr, nullptr, 0, c.list, c.lcount);
     return LAUNCHED(c);
 }
 cudaError_t launch_seed_start(Ctx& c, int k) {
     (void)k;
-    k_seed_start<<<1, 32, 0, c.stream>>>(c.J, c.key, c.first, reinterpret_cast<const uint32_t*>(c.M), c.MS, c.inS, c.vis,
+    k_seed_start<<<1, 32, 0, c.stream>>>(c.n, c.J, c.key, reinterpret_cast<const uint32_t*>(c.M), c.MS, c.inS, c.vis,
                                           c.delta[0], c.off, c.bitems[0], c.bvl[0], &c.ctr[0], c.sigma_count, c.rec);
     return LAUNCHED(c);
 }
@@ -744,6 +525,11 @@ cudaError_t launch_bfs_level(Ctx& c, int cur, int n_items, uint32_t tag) {
     else k_bfs_level<false><<<grid, BLOCK, 0, c.stream>>>(a);
     return LAUNCHED(c);
 }
+cudaError_t launch_bfs_items(Ctx& c, int buf) {
+    k_bfs_items<<<c.num_sms * 4, BLOCK, 0, c.stream>>>(c.J, c.B0, c.sorted_h, c.Xs, c.bvl[buf], c.delta[buf], c.off, c.fwd,
+                                                        c.bitems[buf], &c.ctr[buf]);
+    return LAUNCHED(c);
+}
 cudaError_t launch_bfs_clear(Ctx& c, int cur, int n_v) {
     int W = c.J >> 5;
     k_bfs_clear<<<grid_for(c, (int64_t)n_v * W), BLOCK, 0, c.stream>>>(n_v, W, c.bvl[cur], c.delta[cur]);
@@ -759,10 +545,8 @@ cudaError_t launch_gather_rows(Ctx& c, const int32_t* rows, int64_t nrows, uint8
     return LAUNCHED(c);
 }
 
-int occupancy_sweep(int* blocks_per_sm_sweep, int* blocks_per_sm_bfs) {
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm_sweep, k_sweep<true, true, true>, BLOCK, 0);
-    if (e) return (int)e;
-    return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm_bfs, k_bfs_level<true>, BLOCK, 0);
+int occupancy_bfs(int* blocks_per_sm) {
+    return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_bfs_level<true>, BLOCK, 0);
 }
 
 }  // namespace im

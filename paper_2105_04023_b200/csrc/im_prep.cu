@@ -1,0 +1,269 @@
+// im_prep.cu -- a0 edge preparation (Eq. 4-5, Sec. 3.3) and a2 register init (Alg. 1 lines 2-5).
+//
+// Edge prep, once per graph:
+//   validate the CSR; detect a constant w; per edge h(u,v) = Murmur3(u||v) mod 2^31 and the exact
+//   integer threshold T_e (im_device.cuh); build the forward rows {v, h} and the reverse rows {u, h}
+//   (grouped by target) used by the sweeps.  With a constant threshold T (2^(B-1) < T <= 2^B) every
+//   row is additionally ordered by h >> B, so the slice of a row whose candidate windows meet a
+//   given simulation range is contiguous (im_device.cuh "hash-sorted adjacency ranges").  Both
+//   orders come from one LSD radix sort of the composite key (row << (31-B)) | (h >> B); the row
+//   part keeps CSR rows contiguous, so the sort doubles as the transpose.  Per-edge thresholds
+//   (weighted cascade) keep the input row order and use an atomic-cursor transpose.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "im_device.cuh"
+#include "im_internal.h"
+
+namespace im {
+
+__global__ void k_validate(int32_t n, int64_t m, const int32_t* __restrict__ off, const int32_t* __restrict__ tgt,
+                           const float* __restrict__ prob, int* flags) {
+    int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+    int f = 0;
+    if (tid == 0) {
+        if (off[0] != 0) f |= 1;
+        if ((int64_t)off[n] != m) f |= 1;
+    }
+    for (int64_t i = tid; i < n; i += stride)
+        if (off[i] > off[i + 1]) f |= 1;
+    for (int64_t e = tid; e < m; e += stride) {
+        int32_t v = tgt[e];
+        if (v < 0 || v >= n) f |= 2;
+        float w = prob[e];
+        if (!(w >= 0.0f && w <= 1.0f)) f |= 4;  // also rejects NaN
+    }
+    if (f) atomicOr(flags, f);
+}
+
+__global__ void k_const_check(int64_t m, const float* __restrict__ prob, int* flag) {
+    int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+    uint32_t p0 = __float_as_uint(prob[0]);
+    bool diff = false;
+    for (int64_t e = tid; e < m; e += stride) diff |= __float_as_uint(prob[e]) != p0;
+    if (__any_sync(IM_FULL, diff) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+// source vertex of every edge: the start position of each non-empty row gets its id, then a max-scan
+__global__ void k_row_markers(int32_t n, const int32_t* __restrict__ off, int32_t* __restrict__ mark) {
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += stride)
+        if (off[u] < off[u + 1]) mark[off[u]] = (int32_t)u;
+}
+
+struct MaxOp {
+    __device__ __forceinline__ int32_t operator()(int32_t a, int32_t b) const { return a > b ? a : b; }
+};
+
+// forward records (+ composite sort keys when SORTED); in-degree histogram
+template <typename K, bool SORTED>
+__global__ void k_edge_prep(int64_t m, const int32_t* __restrict__ src, const int32_t* __restrict__ tgt,
+                            const float* __restrict__ prob, int B, int KB, K* __restrict__ keys, uint2* __restrict__ rec,
+                            uint32_t* __restrict__ recT, int32_t* __restrict__ indeg) {
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += stride) {
+        uint32_t u = (uint32_t)src[e], v = (uint32_t)tgt[e];
+        uint32_t h = edge_hash(u, v);
+        rec[e] = make_uint2(v, h);
+        if (SORTED) keys[e] = ((K)u << KB) | (K)(h >> B);
+        else recT[e] = live_threshold(prob[e]);
+        atomicAdd(&indeg[v], 1);
+    }
+}
+
+// reverse records {u, h} keyed by (v << KB) | (h >> B); fwd is already row-ordered, so src[e] is its row
+template <typename K>
+__global__ void k_rev_keys(int64_t m, const int32_t* __restrict__ src, const uint2* __restrict__ fwd, int B, int KB,
+                           K* __restrict__ keys, uint2* __restrict__ rec) {
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += stride) {
+        uint2 f = fwd[e];
+        keys[e] = ((K)f.x << KB) | (K)(f.y >> B);
+        rec[e] = make_uint2((uint32_t)src[e], f.y);
+    }
+}
+
+// per-edge thresholds: atomic-cursor transpose (row order inside reverse rows is immaterial)
+__global__ void k_transpose(int64_t m, const int32_t* __restrict__ src, const uint2* __restrict__ fwd,
+                            const uint32_t* __restrict__ fwdT, const int32_t* __restrict__ roff, int32_t* __restrict__ cursor,
+                            uint2* __restrict__ rev, uint32_t* __restrict__ revT) {
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += stride) {
+        uint2 f = fwd[e];
+        int32_t pos = roff[f.x] + atomicAdd(&cursor[f.x], 1);
+        rev[pos] = make_uint2((uint32_t)src[e], f.y);
+        revT[pos] = fwdT[e];
+    }
+}
+
+__global__ void k_nseg(int32_t n, const int32_t* __restrict__ offs, int32_t* __restrict__ nseg) {
+    int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < n) nseg[v] = (offs[v + 1] - offs[v] + SEG - 1) / SEG;
+    if (v == n) nseg[n] = 0;
+}
+
+__global__ void k_fill_items(int32_t n, const int32_t* __restrict__ offs, const int32_t* __restrict__ base,
+                             int4* __restrict__ items) {
+    int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    int32_t b = offs[v], e = offs[v + 1], p = base[v];
+    for (int32_t s = b; s < e; s += SEG) items[p++] = make_int4(v, s, min(s + SEG, e), 0);
+}
+
+// ------------------------------------------------------------------ a2: register init
+// M_v[jj] = clz(Murmur3(v, seed_V) xor Murmur3(perm[jj], seed_J)), clz(0) = 32 (Alg. 1 lines 2-5; R5, R6).
+// One thread per 4-register word; hash(j) of the 4 simulations is read as one 16-byte shared load.
+__global__ void k_init_registers(int32_t n, int32_t J, uint32_t seedV, uint32_t seedJ, const int32_t* __restrict__ perm,
+                                 uint32_t* __restrict__ M32) {
+    __shared__ uint4 HJ4[256];
+    uint32_t* HJ = reinterpret_cast<uint32_t*>(HJ4);
+    for (int j = threadIdx.x; j < J; j += blockDim.x) HJ[j] = murmur_word((uint32_t)perm[j], seedJ);
+    __syncthreads();
+    const int wpr = J >> 2;  // words per row
+    const int64_t total = (int64_t)n * wpr, stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += stride) {
+        uint32_t v = (uint32_t)(idx / wpr);
+        int w = (int)(idx - (int64_t)v * wpr);
+        uint32_t hv = murmur_word(v, seedV);
+        uint4 hj = HJ4[w];
+        M32[idx] = (uint32_t)__clz(hv ^ hj.x) | ((uint32_t)__clz(hv ^ hj.y) << 8) | ((uint32_t)__clz(hv ^ hj.z) << 16) |
+                   ((uint32_t)__clz(hv ^ hj.w) << 24);
+    }
+}
+
+// ------------------------------------------------------------------ launchers
+cudaError_t launch_validate(Ctx& c, const int32_t* off, const int32_t* tgt, const float* prob, int* flags) {
+    k_validate<<<grid_for(c, c.m > c.n ? c.m : c.n), BLOCK, 0, c.stream>>>(c.n, c.m, off, tgt, prob, flags);
+    return LAUNCHED(c);
+}
+cudaError_t launch_const_check(Ctx& c, const float* prob, int* flag) {
+    k_const_check<<<grid_for(c, c.m), BLOCK, 0, c.stream>>>(c.m, prob, flag);
+    return LAUNCHED(c);
+}
+cudaError_t scan_exclusive(Ctx& c, const int32_t* in, int32_t* out, int n, void* tmp, size_t& tmp_bytes) {
+    cudaError_t e = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, in, out, n, c.stream);
+    if (tmp) c.launches++;
+    return e;
+}
+cudaError_t launch_build_items(Ctx& c, const int32_t* offs, int4* items, int32_t* nseg, void* tmp, size_t tmp_bytes) {
+    int32_t* base = nseg + (c.n + 1);  // nseg holds 2(n+1) entries: counts, then their exclusive scan
+    k_nseg<<<(c.n + 1 + BLOCK - 1) / BLOCK, BLOCK, 0, c.stream>>>(c.n, offs, nseg);
+    cudaError_t e = LAUNCHED(c);
+    if (e) return e;
+    e = scan_exclusive(c, nseg, base, c.n + 1, tmp, tmp_bytes);
+    if (e) return e;
+    if (items) {
+        k_fill_items<<<(c.n + BLOCK - 1) / BLOCK, BLOCK, 0, c.stream>>>(c.n, offs, base, items);
+        e = LAUNCHED(c);
+    }
+    return e;
+}
+cudaError_t launch_init_registers(Ctx& c) {
+    int64_t words = (int64_t)c.n * (c.J >> 2);
+    k_init_registers<<<grid_for(c, words), BLOCK, 0, c.stream>>>(c.n, c.J, c.seedV, c.seedJ, c.permd,
+                                                                 reinterpret_cast<uint32_t*>(c.M));
+    return LAUNCHED(c);
+}
+
+// bits of the composite key (row << KB) | (h >> B): rows need bits(n-1), the bucket 31-B bits
+void prep_key_bits(const Ctx& c, int& KB, int& end_bit, bool& wide) {
+    KB = 31 - c.B0;
+    int nb = 0;
+    while (nb < 31 && ((int64_t)1 << nb) < (int64_t)c.n) nb++;
+    end_bit = nb + KB;
+    wide = end_bit > 32;
+}
+
+// scratch sizes (bytes) the edge prep needs: [0] src, [1] mark/keys0, [2] keys1, [3] vals, [4] cub temp
+cudaError_t prep_scratch_sizes(Ctx& c, size_t* sz) {
+    const size_t m = (size_t)(c.m ? c.m : 1);
+    int KB, end_bit;
+    bool wide;
+    prep_key_bits(c, KB, end_bit, wide);
+    const size_t ks = wide ? 8 : 4;
+    sz[0] = m * 4;
+    sz[1] = m * (c.sorted_h ? ks : 4);
+    sz[2] = c.sorted_h ? m * ks : 4;
+    sz[3] = c.sorted_h ? m * 8 : 8;
+    size_t t1 = 0, t2 = 0;
+    cudaError_t e = cub::DeviceScan::InclusiveScan(nullptr, t1, (int32_t*)nullptr, (int32_t*)nullptr, MaxOp(), (int)m, c.stream);
+    if (e) return e;
+    if (c.sorted_h) {
+        if (wide)
+            e = cub::DeviceRadixSort::SortPairs(nullptr, t2, (ull*)nullptr, (ull*)nullptr, (uint2*)nullptr, (uint2*)nullptr,
+                                                (int)m, 0, end_bit, c.stream);
+        else
+            e = cub::DeviceRadixSort::SortPairs(nullptr, t2, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint2*)nullptr,
+                                                (uint2*)nullptr, (int)m, 0, end_bit, c.stream);
+    }
+    if (e) return e;
+    size_t t3 = 0;
+    e = cub::DeviceScan::ExclusiveSum(nullptr, t3, (int32_t*)nullptr, (int32_t*)nullptr, c.n + 1, c.stream);
+    size_t t = t1 > t2 ? t1 : t2;
+    sz[4] = (t > t3 ? t : t3) + 256;
+    return e;
+}
+
+template <typename K>
+static cudaError_t prep_sorted(Ctx& c, const int32_t* src, const int32_t* tgt, const float* prob, int32_t* indeg,
+                               void** scr, size_t temp_bytes, int KB, int end_bit) {
+    K* k0 = (K*)scr[1];
+    K* k1 = (K*)scr[2];
+    uint2* vals = (uint2*)scr[3];
+    cudaError_t e;
+    // forward: (u << KB | h >> B) -> rows stay in place, ordered by bucket inside
+    k_edge_prep<K, true><<<grid_for(c, c.m), BLOCK, 0, c.stream>>>(c.m, src, tgt, prob, c.B0, KB, k0, vals, nullptr, indeg);
+    if ((e = LAUNCHED(c))) return e;
+    e = cub::DeviceRadixSort::SortPairs(scr[4], temp_bytes, k0, k1, vals, c.fwd, (int)c.m, 0, end_bit, c.stream);
+    c.launches += (end_bit + 7) / 8 + 1;
+    if (e) return e;
+    // reverse: (v << KB | h >> B) with payload {u, h}: the sort is the transpose
+    k_rev_keys<K><<<grid_for(c, c.m), BLOCK, 0, c.stream>>>(c.m, src, c.fwd, c.B0, KB, k0, vals);
+    if ((e = LAUNCHED(c))) return e;
+    e = cub::DeviceRadixSort::SortPairs(scr[4], temp_bytes, k0, k1, vals, c.rev, (int)c.m, 0, end_bit, c.stream);
+    c.launches += (end_bit + 7) / 8 + 1;
+    return e;
+}
+
+// the whole edge prep after validation: fills c.fwd (+fwdT), c.roff, c.rev (+revT)
+cudaError_t prep_edges(Ctx& c, const int32_t* tgt, const float* prob, int32_t* indeg, int32_t* scan_tmp_i,
+                       void** scr, const size_t* sz) {
+    cudaError_t e;
+    const int64_t m = c.m;
+    int32_t* src = (int32_t*)scr[0];
+    int32_t* mark = (int32_t*)scr[1];
+    size_t tb = sz[4];
+    (void)scan_tmp_i;
+    if ((e = cudaMemsetAsync(indeg, 0, ((size_t)c.n + 1) * sizeof(int32_t), c.stream))) return e;
+    if (m > 0) {
+        if ((e = cudaMemsetAsync(mark, 0, (size_t)m * sizeof(int32_t), c.stream))) return e;
+        k_row_markers<<<grid_for(c, c.n), BLOCK, 0, c.stream>>>(c.n, c.off, mark);
+        if ((e = LAUNCHED(c))) return e;
+        if ((e = cub::DeviceScan::InclusiveScan(scr[4], tb, mark, src, MaxOp(), (int)m, c.stream))) return e;
+        c.launches += 2;
+    }
+    if (c.sorted_h) {
+        int KB, end_bit;
+        bool wide;
+        prep_key_bits(c, KB, end_bit, wide);
+        e = wide ? prep_sorted<ull>(c, src, tgt, prob, indeg, scr, tb, KB, end_bit)
+                 : prep_sorted<uint32_t>(c, src, tgt, prob, indeg, scr, tb, KB, end_bit);
+        if (e) return e;
+        size_t t2 = tb;
+        return scan_exclusive(c, indeg, c.roff, c.n + 1, scr[4], t2);
+    }
+    if (m > 0) {
+        k_edge_prep<uint32_t, false><<<grid_for(c, m), BLOCK, 0, c.stream>>>(m, src, tgt, prob, 0, 0, nullptr, c.fwd, c.fwdT, indeg);
+        if ((e = LAUNCHED(c))) return e;
+    }
+    size_t t2 = tb;
+    if ((e = scan_exclusive(c, indeg, c.roff, c.n + 1, scr[4], t2))) return e;
+    if (m > 0) {
+        if ((e = cudaMemsetAsync(indeg, 0, ((size_t)c.n + 1) * sizeof(int32_t), c.stream))) return e;
+        k_transpose<<<grid_for(c, m), BLOCK, 0, c.stream>>>(m, src, c.fwd, c.fwdT, c.roff, indeg, c.rev, c.revT);
+        e = LAUNCHED(c);
+    }
+    return e;
+}
+
+}  // namespace im
