@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <random>
 #include <string>
@@ -102,8 +103,10 @@ int ensure_device() {
     int bs = 0, bb = 0;
     CK((cudaError_t)occupancy_sweep(&bs));
     CK((cudaError_t)occupancy_bfs(&bb));
+
     g.max_blocks_sweep = std::max(1, bs) * g.num_sms;
     g.max_blocks_bfs = std::max(1, bb) * g.num_sms;
+    g.trace = getenv("IM_TRACE") != nullptr;
     if (!g.own_stream) CK(cudaStreamCreateWithFlags(&g.own_stream, cudaStreamNonBlocking));
     if (!g.stream) g.stream = g.own_stream;
     if (!g.hpin) CK(cudaMallocHost(&g.hpin, 4096));
@@ -132,9 +135,9 @@ void reset_graph_state() {
 
 void release_all() {
     dfree(g.Xs); dfree(g.s12); dfree(g.permd); dfree(g.M); dfree(g.vis);
-    for (int i = 0; i < 2; i++) { dfree(g.items[i]); dfree(g.bits[i]); dfree(g.delta[i]); dfree(g.bitems[i]); dfree(g.bvl[i]); }
-    dfree(g.inS); dfree(g.MS); dfree(g.btag); dfree(g.gain); dfree(g.list); dfree(g.lcount); dfree(g.hist);
-    dfree(g.off); dfree(g.fwd); dfree(g.fwdT); dfree(g.roff); dfree(g.rev); dfree(g.revT); dfree(g.ritems);
+    for (int i = 0; i < 2; i++) { dfree(g.items[i]); dfree(g.bits[i]); dfree(g.cm[i]); dfree(g.delta[i]); dfree(g.bitems[i]); dfree(g.bvl[i]); }
+    dfree(g.inS); dfree(g.MS); dfree(g.btag); dfree(g.nbits); dfree(g.gain); dfree(g.big); dfree(g.list); dfree(g.lcount); dfree(g.hist);
+    dfree(g.off); dfree(g.fwd); dfree(g.fwdT); dfree(g.roff); dfree(g.rev); dfree(g.revT); dfree(g.ritems); dfree(g.fbig);
     dfree(g.ctr); dfree(g.rec); dfree(g.varsigma); dfree(g.key); dfree(g.first); dfree(g.sigma_count);
     dfree(g.t_flags); dfree(g.t_indeg); dfree(g.t_nseg); dfree(g.t_scan); dfree(g.t_off); dfree(g.t_tgt); dfree(g.t_prob);
     dfree(g.t_est); dfree(g.t_rows); dfree(g.t_rowsout);
@@ -218,6 +221,11 @@ int load_common(int32_t n, int64_t m, const int32_t* d_off_src, const int32_t* d
     CK(launch_build_items(g, g.off, nullptr, nseg, tmp, tmp_bytes));
     TRY(readback(nseg + (n + 1) + n, sizeof(int32_t), &total[1]));
     g.n_fitems_cap = total[1];
+    // rows gathered by a whole block in the first sweep
+    TRY(dalloc(g.fbig, (size_t)n));
+    CK(cudaMemsetAsync(g.t_flags + 2, 0, sizeof(int), g.stream));
+    CK(launch_list_big_rows(g, g.fbig, g.t_flags + 2));
+    TRY(readback(g.t_flags + 2, sizeof(int), &g.n_fbig));
     TRY(sync());
     // small per-graph state
     TRY(dalloc(g.ctr, 2));
@@ -247,6 +255,10 @@ int check_csr_args(int32_t n, int64_t m) {
 int alloc_sketch_state(int32_t J) {
     size_t n = (size_t)g.n, W = (size_t)J / 32;
     bool fr = false;
+    if (g.J != J) g.sweep_dirty = true;  // change-mask rows have J/32 words
+    int bf = 0;
+    CK((cudaError_t)setup_first(J, &bf));
+    g.max_blocks_first = std::max(1, bf) * g.num_sms;
     TRY(dalloc(g.Xs, (size_t)J));
     TRY(dalloc(g.s12, 4097));
     TRY(dalloc(g.permd, (size_t)J));
@@ -254,9 +266,11 @@ int alloc_sketch_state(int32_t J) {
     TRY(dalloc(g.vis, n * W));
     for (int i = 0; i < 2; i++) {
         TRY(dalloc(g.items[i], (size_t)g.n_ritems + 4 * n + 1));  // slices add <= 3 partial segments per vertex
-        // a completed build leaves both change-bit buffers zero; fresh ones are cleared here
+        // a completed build leaves the change buffers zero; fresh ones are cleared by simulate()
         TRY(dalloc(g.bits[i], n, &fr));
-        if (fr) CK(cudaMemsetAsync(g.bits[i], 0, n * sizeof(uint32_t), g.stream));
+        if (fr) g.sweep_dirty = true;
+        TRY(dalloc(g.cm[i], n * W, &fr));
+        if (fr) g.sweep_dirty = true;
         TRY(dalloc(g.delta[i], n * W, &fr));
         if (fr || g.J != J) CK(cudaMemsetAsync(g.delta[i], 0, n * W * sizeof(uint32_t), g.stream));
         TRY(dalloc(g.bitems[i], (size_t)g.n_fitems_cap + 4 * n + 1));
@@ -264,12 +278,13 @@ int alloc_sketch_state(int32_t J) {
     }
     TRY(dalloc(g.inS, n));
     TRY(dalloc(g.MS, (size_t)J));
+    TRY(dalloc(g.big, n));
     TRY(dalloc(g.gain, n));
     TRY(dalloc(g.list, n));
     TRY(dalloc(g.lcount, 2));
     TRY(dalloc(g.hist, 4096));
-    TRY(dalloc(g.btag, n, &fr));  // BFS tags only grow (g.bt is never reset)
-    if (fr) CK(cudaMemsetAsync(g.btag, 0, n * sizeof(uint32_t), g.stream));
+    TRY(dalloc(g.nbits, n, &fr));  // zero between levels (consumed by k_bfs_compact)
+    if (fr) CK(cudaMemsetAsync(g.nbits, 0, n * sizeof(uint32_t), g.stream));
     g.J = J;
     return 0;
 }
@@ -306,12 +321,18 @@ int setup_salts(int32_t J, uint64_t seed) {
 // compaction then emits the next items and clears bits[(s-1)&1] for sweep s+1.
 int simulate(bool blocked) {
     auto t0 = clk::now();
-    CK(launch_init_registers(g));
-    CK(cudaMemsetAsync(g.bits[1], 0, (size_t)g.n * sizeof(uint32_t), g.stream));
+    const size_t W = (size_t)g.J / 32;
+    if (g.sweep_dirty)
+        for (int i = 0; i < 2; i++) {
+            CK(cudaMemsetAsync(g.bits[i], 0, (size_t)g.n * sizeof(uint32_t), g.stream));
+            CK(cudaMemsetAsync(g.cm[i], 0, (size_t)g.n * W * sizeof(uint32_t), g.stream));
+        }
+    g.sweep_dirty = true;  // until this build completes
     IterCounters hc;
     int sweeps = 0;
     int64_t edges = 0, wedges = 0, launches = 0;
     float kms = 0.f;
+    int64_t edges_in = g.m;
     const int4* items = g.ritems;
     int n_items = g.n_ritems;
     edges = g.m;
@@ -319,9 +340,12 @@ int simulate(bool blocked) {
         IterCounters* ctr = &g.ctr[s & 1];
         CK(cudaMemsetAsync(ctr, 0, sizeof(IterCounters), g.stream));
         CK(cudaEventRecord(g.ev[0], g.stream));
-        CK(launch_sweep(g, items, n_items, s == 1 ? nullptr : g.bits[(s - 1) & 1], g.bits[s & 1], ctr, blocked));
+        if (s == 1)  // register init fused with the first sweep (every row written)
+            CK(launch_first(g, g.cm[1], g.bits[1], ctr, blocked));
+        else
+            CK(launch_sweep(g, items, n_items, g.cm[(s - 1) & 1], g.cm[s & 1], g.bits[s & 1], ctr, blocked));
         CK(cudaEventRecord(g.ev[1], g.stream));
-        CK(launch_compact(g, g.bits[s & 1], g.bits[(s - 1) & 1], g.items[s & 1], ctr));
+        CK(launch_compact(g, g.bits[s & 1], g.bits[(s - 1) & 1], g.cm[s & 1], g.cm[(s - 1) & 1], g.items[s & 1], ctr));
         TRY(readback(ctr, sizeof hc, &hc));
         float t;
         CK(cudaEventElapsedTime(&t, g.ev[0], g.ev[1]));
@@ -329,11 +353,17 @@ int simulate(bool blocked) {
         sweeps++;
         launches++;
         wedges += (int64_t)hc.win_edges;
+        if (g.trace)
+            fprintf(stderr, "[im] sweep %d items %d edges %lld window_edges %llu -> changed %d next_items %d next_edges %llu big %d  %.3f ms\n",
+                    s, n_items, (long long)(s == 1 ? g.m : (int64_t)edges_in), hc.win_edges, hc.changed, hc.next_items,
+                    hc.next_edges, hc.big, t);
+        edges_in = (int64_t)hc.next_edges;
         if (hc.next_items == 0) break;
         items = g.items[s & 1];
         n_items = hc.next_items;
         edges += (int64_t)hc.next_edges;
     }
+    g.sweep_dirty = false;  // a completed build leaves every change buffer zero
     g.st.builds++;
     g.st.last_build_sweeps = sweeps;
     g.st.last_build_edges = edges;
@@ -511,8 +541,10 @@ int im_select_seeds_ex(int32_t K, double eps_l, double eps_g, int32_t* out_seeds
             CK(cudaMemsetAsync(&g.ctr[cur ^ 1], 0, sizeof(IterCounters), g.stream));
             CK(launch_bfs_level(g, cur, n_items, tag));
             CK(launch_bfs_clear(g, cur, n_v));
-            CK(launch_bfs_items(g, cur ^ 1));
             TRY(readback(&g.ctr[cur ^ 1], sizeof hc, &hc));
+            if (g.trace)
+                fprintf(stderr, "[im] bfs k=%d level items %d frontier %d -> frontier %d next_items %d next_edges %llu big %d new_bits %llu\n",
+                        k, n_items, n_v, hc.changed, hc.next_items, hc.next_edges, hc.big, hc.new_bits);
             cur ^= 1;
             g.st.bfs_levels++;
         }

@@ -144,3 +144,46 @@ __device__ __forceinline__ int slices_for(const uint2* __restrict__ rec, int rb,
     return k;
 }
 }  // namespace im
+
+namespace im {
+// Block-aggregated reservation on the per-iteration counters (one atomic per counter per block
+// iteration instead of one per warp).  Every thread of the block calls it; lane 31 of each warp
+// passes its warp's totals.  Returns the warp's base for items / changed / big.
+struct BlockTotals {
+    int items, changed, big;
+    unsigned long long edges;
+};
+template <int NW>
+__device__ __forceinline__ void block_reserve(BlockTotals wt, int lane, int wib, int* c_items, int* c_changed,
+                                              unsigned long long* c_edges, int* c_big, int& b_items, int& b_changed,
+                                              int& b_big) {
+    __shared__ BlockTotals sT[NW];
+    __shared__ int sB[NW][3];
+    if (lane == 31) sT[wib] = wt;
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        const int t = threadIdx.x;
+        unsigned long long acc = 0;
+        for (int w = 0; w < NW; w++) {
+            unsigned long long x = t == 0 ? sT[w].items : t == 1 ? sT[w].changed : t == 2 ? sT[w].big : sT[w].edges;
+            if (t < 3) sB[w][t] = (int)acc;
+            acc += x;
+        }
+        if (acc) {
+            if (t == 3) {
+                if (c_edges) atomicAdd(c_edges, acc);
+            } else {
+                int* cp = t == 0 ? c_items : t == 1 ? c_changed : c_big;
+                int g0 = cp ? atomicAdd(cp, (int)acc) : 0;
+                for (int w = 0; w < NW; w++) sB[w][t] += g0;
+            }
+        }
+    }
+    __syncthreads();
+    b_items = sB[wib][0];
+    b_changed = sB[wib][1];
+    b_big = sB[wib][2];
+    __syncthreads();
+}
+}  // namespace im
+

@@ -15,6 +15,7 @@ typedef unsigned long long ull;
 constexpr int SEG = 256;        // max edges per work item (a segment of one vertex's edge list)
 constexpr int DENSE_WIN = 32;   // windows wider than this many simulations take the warp-cooperative path
 constexpr int BLOCK = 256;      // threads per block of the persistent work-list kernels
+constexpr int FIRST_BIG = 2048; // first sweep: rows with more out-edges are gathered by a whole block
 
 // device-side counters of one sweep / BFS level (one 32-byte D2H per iteration)
 struct IterCounters {
@@ -22,7 +23,7 @@ struct IterCounters {
     int changed;        // vertices that changed (first change per iteration)
     ull next_edges;     // edges covered by the appended items
     int batch;          // dynamic batch cursor of the persistent kernel
-    int pad;
+    int big;            // long rows queued for per-word slicing (k_slices_big)
     ull new_bits;       // BFS: newly visited (vertex, simulation) pairs
     ull win_edges;      // sweep: edges with a non-empty candidate window (after the change filter)
 };
@@ -57,6 +58,8 @@ struct Ctx {
     int4* ritems = nullptr;     // all reverse segments {v, eb, ee, 0}
     int32_t n_ritems = 0;
     int32_t n_fitems_cap = 0;   // sum_v ceil(outdeg/SEG)
+    int32_t* fbig = nullptr;    // vertices with > FIRST_BIG out-edges
+    int32_t n_fbig = 0;
     // sketches
     int32_t J = 0;
     uint64_t seed = 0;
@@ -71,6 +74,10 @@ struct Ctx {
     // sweep buffers
     int4* items[2] = {nullptr, nullptr};
     uint32_t* bits[2] = {nullptr, nullptr};  // per-vertex 32-simulation-chunk change bits, ping-pong
+    uint32_t* cm[2] = {nullptr, nullptr};    // per-(vertex, simulation) change masks, n x J/32 words, ping-pong
+    int32_t* big = nullptr;                  // long rows awaiting slicing
+    bool sweep_dirty = true;
+    bool trace = false;                      // IM_TRACE: per-sweep / per-level lines on stderr                 // change buffers may hold stale bits (fresh / aborted build)
     IterCounters* ctr = nullptr;   // [2]
     // selection buffers
     uint8_t* inS = nullptr;
@@ -80,6 +87,7 @@ struct Ctx {
     int32_t* bvl[2] = {nullptr, nullptr};
     uint32_t* btag = nullptr;
     uint32_t bt = 0;
+    uint32_t* nbits = nullptr;   // BFS: per-vertex words with new bits in the current level
     StepDev* rec = nullptr;
     double* varsigma = nullptr;
     ull* key = nullptr;
@@ -108,7 +116,7 @@ struct Ctx {
     std::vector<im_step> steps;
     int64_t launches = 0;
     int st_argmax_full = 0, st_argmax_list = 0;
-    int max_blocks_sweep = 0, max_blocks_bfs = 0;
+    int max_blocks_sweep = 0, max_blocks_bfs = 0, max_blocks_first = 0;
     cudaEvent_t ev[2] = {nullptr, nullptr};
 };
 
@@ -122,9 +130,14 @@ inline int grid_for(Ctx& c, int64_t work, int per_block = BLOCK) {
 #define LAUNCHED(c) ((c).launches++, cudaGetLastError())
 
 // ---- launchers (im_kernels.cu, im_sweep.cu); all enqueue on c.stream, return cudaError_t ----
-cudaError_t launch_compact(Ctx& c, const uint32_t* bits_new, uint32_t* bits_clear, int4* items_out, IterCounters* ctr);
+cudaError_t launch_compact(Ctx& c, const uint32_t* bits_new, uint32_t* bits_clear, const uint32_t* cm_new,
+                           uint32_t* cm_clear, int4* items_out, IterCounters* ctr);
 int occupancy_sweep(int* blocks_per_sm);
 int occupancy_bfs(int* blocks_per_sm);
+int setup_first(int J, int* blocks_per_sm);  // smem opt-in + occupancy of the first-sweep kernel for this J
+// register init + first sweep (gather, im_first.cu): writes every row, its change mask and chunk bits
+cudaError_t launch_first(Ctx& c, uint32_t* cm_out, uint32_t* bits_out, IterCounters* ctr, bool blocked);
+cudaError_t launch_list_big_rows(Ctx& c, int32_t* out, int* count);
 cudaError_t launch_validate(Ctx& c, const int32_t* off, const int32_t* tgt, const float* prob, int* flags);
 cudaError_t launch_const_check(Ctx& c, const float* prob, int* flag);
 cudaError_t prep_scratch_sizes(Ctx& c, size_t* sz);  // 5 sizes (bytes) for prep_edges scratch
@@ -134,7 +147,12 @@ cudaError_t launch_build_items(Ctx& c, const int32_t* offs, int4* items, int32_t
 cudaError_t scan_exclusive(Ctx& c, const int32_t* in, int32_t* out, int n, void* tmp, size_t& tmp_bytes);
 cudaError_t launch_salt_tables(Ctx& c);
 cudaError_t launch_init_registers(Ctx& c);
-// one sweep over `items`; bits_in: chunk-change bits of the previous sweep (null: no filter, sweep 1);
+// one sweep over `items`; cm_in: per-simulation change mask of the previous sweep (null: no filter,
+// sweep 1); cm_out / bits_out: this sweep's change mask and chunk summary; counters in *ctr (zeroed)
+cudaError_t launch_sweep(Ctx& c, const int4* items, int n_items, const uint32_t* cm_in, uint32_t* cm_out,
+                         uint32_t* bits_out, IterCounters* ctr, bool blocked);
+cudaError_t launch_slices_big(Ctx& c, const int32_t* big, const uint32_t* mask, const int32_t* offs, const uint2* rec,
+                              int4* items_out, IterCounters* ctr);
 // bits_out: this sweep's chunk-change bits (red.or); counters in *ctr (zeroed by the caller)
 cudaError_t launch_sweep(Ctx& c, const int4* items, int n_items, const uint32_t* bits_in, uint32_t* bits_out,
                          IterCounters* ctr, bool blocked);
@@ -142,6 +160,8 @@ cudaError_t launch_estimate(Ctx& c, double* out);
 cudaError_t launch_argmax_full(Ctx& c, bool pool, int T);
 cudaError_t launch_argmax_list(Ctx& c, int list_len);
 cudaError_t launch_seed_start(Ctx& c, int k);
+// one BFS level from frontier buffer cur (items, Delta) into cur^1, plus the compaction that builds
+// the next frontier's vertex list / items and adds the level's new bits to sigma
 cudaError_t launch_bfs_level(Ctx& c, int cur, int n_items, uint32_t tag);
 cudaError_t launch_bfs_clear(Ctx& c, int cur, int n_v);
 cudaError_t launch_bfs_items(Ctx& c, int buf);

@@ -219,30 +219,27 @@ struct BfsArgs {
     uint32_t* vis;
     const uint32_t* din;
     uint32_t* dout;
-    uint32_t* btag;
-    uint32_t tag;
-    int4* next_items;
-    int32_t* next_vl;
+    uint32_t* nbits;   // per vertex: which 32-simulation words got new bits in this level
 };
 
-// one 32-simulation word of one edge: new = Delta_u & live & ~visited(v); returns popcount of truly new bits
-__device__ __forceinline__ int bfs_word(const BfsArgs& a, const uint32_t* sX, uint32_t u, uint32_t v, int w, uint32_t h,
-                                        uint32_t T, int lo, int hi) {
+// one 32-simulation word w of one edge (u,v): the simulations new at v are Delta_u & live & ~visited(v).
+// All updates are fire-and-forget ORs: a bit that two threads both find new is new either way, and
+// the next frontier / the new-bit count are built afterwards by k_bfs_compact from the OR-ed words.
+__device__ __forceinline__ void bfs_word(const BfsArgs& a, const uint32_t* sX, uint32_t u, uint32_t v, int w, uint32_t h,
+                                         uint32_t T, int lo, int hi) {
     const int W = a.J >> 5;
     uint32_t d = a.din[(size_t)u * W + w];
-    if (!d) return 0;
+    if (!d) return;
     int i0 = max(lo, w << 5), i1 = min(hi, (w << 5) + 32);
     uint32_t live = 0;
     for (int i = i0; i < i1; ++i) live |= ((sX[i] ^ h) < T) ? (1u << (i & 31)) : 0u;
     uint32_t nv = d & live;
-    if (!nv) return 0;
+    if (!nv) return;
     nv &= ~__ldcg(&a.vis[(size_t)v * W + w]);
-    if (!nv) return 0;
-    uint32_t old = atomicOr(&a.vis[(size_t)v * W + w], nv);
-    uint32_t tn = nv & ~old;
-    if (!tn) return 0;
-    atomicOr(&a.dout[(size_t)v * W + w], tn);
-    return __popc(tn);
+    if (!nv) return;
+    atomicOr(&a.vis[(size_t)v * W + w], nv);
+    atomicOr(&a.dout[(size_t)v * W + w], nv);
+    atomicOr(&a.nbits[v], 1u << w);
 }
 
 template <bool CONST_T>
@@ -254,11 +251,16 @@ __global__ void __launch_bounds__(BLOCK) k_bfs_level(BfsArgs a) {
     for (int i = threadIdx.x; i < 4097; i += blockDim.x) sS[i] = a.s12[i];
     __syncthreads();
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    uint32_t newbits = 0;
+    int base = 0, left = 0;  // 128-item grabs (4 batches of 32)
     for (;;) {
-        int base = 0;
-        if (lane == 0) base = atomicAdd(&a.ctr_next->batch, 32);
-        base = __shfl_sync(IM_FULL, base, 0);
+        if (left == 0) {
+            if (lane == 0) base = atomicAdd(&a.ctr_next->batch, 128);
+            base = __shfl_sync(IM_FULL, base, 0);
+            left = 4;
+        } else {
+            base += 32;
+        }
+        --left;
         if (base >= a.n_items) break;
         int it = base + lane;
         int u = 0, eb = 0, cnt = 0;
@@ -286,7 +288,7 @@ __global__ void __launch_bounds__(BLOCK) k_bfs_level(BfsArgs a) {
             int ost = __shfl_sync(IM_FULL, start, owner);
             int idx = e0 + lane;
             uint32_t v = 0, h = 0, T = 0;
-            int lo = 0, hi = 0, got = 0;
+            int lo = 0, hi = 0;
             bool dense = false;
             if (idx < total) {
                 int e = oeb + (idx - ost);
@@ -298,7 +300,7 @@ __global__ void __launch_bounds__(BLOCK) k_bfs_level(BfsArgs a) {
                     edge_window(h, T, sX, sS, a.J, lo, hi);
                     if (hi - lo > DENSE_WIN) dense = true;
                     else if (lo < hi)
-                        for (int w = lo >> 5; w <= (hi - 1) >> 5; ++w) got += bfs_word(a, sX, (uint32_t)ou, v, w, h, T, lo, hi);
+                        for (int w = lo >> 5; w <= (hi - 1) >> 5; ++w) bfs_word(a, sX, (uint32_t)ou, v, w, h, T, lo, hi);
                 }
             }
             uint32_t dmask = __ballot_sync(IM_FULL, dense);
@@ -308,89 +310,88 @@ __global__ void __launch_bounds__(BLOCK) k_bfs_level(BfsArgs a) {
                 uint32_t dv = __shfl_sync(IM_FULL, v, l), dh = __shfl_sync(IM_FULL, h, l), dT = __shfl_sync(IM_FULL, T, l);
                 int dlo = __shfl_sync(IM_FULL, lo, l), dhi = __shfl_sync(IM_FULL, hi, l);
                 uint32_t du = (uint32_t)__shfl_sync(IM_FULL, ou, l);
-                int c = 0;
-                for (int w = (dlo >> 5) + lane; w <= (dhi - 1) >> 5; w += 32) c += bfs_word(a, sX, du, dv, w, dh, dT, dlo, dhi);
-                c = __reduce_add_sync(IM_FULL, (uint32_t)c);
-                if (lane == l) got += c;
-            }
-            newbits += (uint32_t)got;
-            // first new bit of v in this level: v joins the next frontier (its slices are built after the level)
-            bool first = got > 0 && atomicMax(&a.btag[v], a.tag) < a.tag;
-            uint32_t fmask = __ballot_sync(IM_FULL, first);
-            if (fmask) {
-                int vpos = 0;
-                if (lane == 31) vpos = atomicAdd(&a.ctr_next->changed, __popc(fmask));
-                vpos = __shfl_sync(IM_FULL, vpos, 31);
-                if (first) a.next_vl[vpos + __popc(fmask & ((1u << lane) - 1u))] = (int32_t)v;
+                for (int w = (dlo >> 5) + lane; w <= (dhi - 1) >> 5; w += 32) bfs_word(a, sX, du, dv, w, dh, dT, dlo, dhi);
             }
         }
     }
-    newbits = __reduce_add_sync(IM_FULL, newbits);
+}
+
+// Next BFS frontier: every vertex with new bits in this level (nbits != 0).  Counts the new
+// (vertex, simulation) pairs (popcount of the OR-ed Delta words) into sigma, lists the vertex (to
+// clear its Delta after the next level), emits its out-edge items (long rows of a hash-sorted
+// graph go to k_slices_big) and clears nbits for the next level.
+__global__ void k_bfs_compact(int32_t n, int J, bool sorted, uint32_t* __restrict__ nbits, const uint32_t* __restrict__ dout,
+                              const int32_t* __restrict__ off, int32_t* __restrict__ vl, int4* __restrict__ items,
+                              int32_t* __restrict__ big, IterCounters* ctr, ull* sigma_count) {
+    const int lane = threadIdx.x & 31, W = J >> 5;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    ull newbits = 0;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+        int64_t v = base + threadIdx.x;
+        uint32_t b = v < n ? nbits[v] : 0u;
+        if (!__syncthreads_or(b != 0u)) continue;  // block-uniform: nothing new in these 256 vertices
+        int rb = 0, rd = 0, ns = 0;
+        bool isbig = false;
+        if (b) {
+            nbits[v] = 0u;
+            for (uint32_t t = b; t; t &= t - 1) newbits += __popc(dout[(size_t)v * W + (__ffs(t) - 1)]);
+            rb = off[v];
+            rd = off[v + 1] - rb;
+            isbig = sorted && rd > SEG;
+            ns = isbig ? 0 : (rd + SEG - 1) / SEG;
+        }
+        uint32_t fmask = __ballot_sync(IM_FULL, b != 0u);
+        uint32_t bmask = __ballot_sync(IM_FULL, isbig);
+        int ninc = warp_incl_scan(ns, lane);
+        long long esum = isbig ? 0 : rd;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) esum += __shfl_xor_sync(IM_FULL, esum, o);
+        BlockTotals wt{ninc, __popc(fmask), __popc(bmask), (unsigned long long)esum};
+        int pos, cpos, bpos;
+        block_reserve<BLOCK / 32>(wt, lane, threadIdx.x >> 5, &ctr->next_items, &ctr->changed, &ctr->next_edges, &ctr->big,
+                                  pos, cpos, bpos);
+        if (b) vl[cpos + __popc(fmask & ((1u << lane) - 1u))] = (int32_t)v;
+        int p = pos + ninc - ns;
+        for (int s0 = rb; s0 < rb + rd && ns; s0 += SEG) items[p++] = make_int4((int)v, s0, min(s0 + SEG, rb + rd), 0);
+        if (isbig) big[bpos + __popc(bmask & ((1u << lane) - 1u))] = (int32_t)v;
+    }
+    newbits = __reduce_add_sync(IM_FULL, (uint32_t)newbits);
     if (lane == 0 && newbits) {
-        atomicAdd(&a.ctr_next->new_bits, (ull)newbits);
-        atomicAdd(a.sigma_count, (ull)newbits);
+        atomicAdd(&ctr->new_bits, newbits);
+        atomicAdd(sigma_count, newbits);
     }
 }
 
-// Work items of a BFS frontier: for every vertex v of vl, the out-edges whose candidate window can
-// meet a simulation in Delta_v (<= 4 hash-sorted slices of its row for a constant threshold, the
-// whole row otherwise).
-__global__ void k_bfs_items(int J, int B, bool sorted, const uint32_t* __restrict__ Xs, const int32_t* __restrict__ vl,
-                            const uint32_t* __restrict__ delta, const int32_t* __restrict__ off, const uint2* __restrict__ fwd,
-                            int4* __restrict__ items, IterCounters* ctr) {
-    const int lane = threadIdx.x & 31, W = J >> 5, NQ = W < 4 ? W : 4;
+// Work items of a BFS frontier: for every vertex v of vl, its out-edges; a long row of a
+// hash-sorted graph is queued for k_slices_big (im_sweep.cu), which emits only the slices whose
+// candidate windows can meet a simulation of Delta_v.
+__global__ void k_bfs_items(bool sorted, const int32_t* __restrict__ vl, const int32_t* __restrict__ off,
+                            int4* __restrict__ items, int32_t* __restrict__ big, IterCounters* ctr) {
+    const int lane = threadIdx.x & 31;
     const int nv = ctr->changed;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < nv; base += stride) {
         int64_t i = base + threadIdx.x;
-        bool in = i < nv;
-        int eb[4], ee[4], k = 0, ns = 0, es = 0;
-        int v = in ? vl[i] : 0;
-        if (in) {
-            int rb = off[v], re = off[v + 1];
-            if (sorted) {
-                int sa[4], sb[4];
-#pragma unroll
-                for (int q = 0; q < 4; q++) {
-                    sa[q] = sb[q] = -1;
-                    if (q < NQ)
-                        for (int w = q * W / NQ; w < (q + 1) * W / NQ; w++) {
-                            uint32_t d = delta[(size_t)v * W + w];
-                            if (!d) continue;
-                            if (sa[q] < 0) sa[q] = 32 * w + __ffs(d) - 1;
-                            sb[q] = 32 * w + 31 - __clz(d);
-                        }
-                }
-                k = slices_for(fwd, rb, re, Xs, B, sa, sb, eb, ee);
-            } else if (rb < re) {
-                eb[0] = rb;
-                ee[0] = re;
-                k = 1;
-            }
-#pragma unroll
-            for (int t = 0; t < 4; t++)
-                if (t < k) {
-                    ns += (ee[t] - eb[t] + SEG - 1) / SEG;
-                    es += ee[t] - eb[t];
-                }
+        int v = i < nv ? vl[i] : 0, rb = 0, rd = 0, ns = 0;
+        bool isbig = false;
+        if (i < nv) {
+            rb = off[v];
+            rd = off[v + 1] - rb;
+            isbig = sorted && rd > SEG;
+            ns = isbig ? 0 : (rd + SEG - 1) / SEG;
         }
+        uint32_t bmask = __ballot_sync(IM_FULL, isbig);
         int ninc = warp_incl_scan(ns, lane);
-        int ntot = __shfl_sync(IM_FULL, ninc, 31);
-        if (!ntot) continue;
-        long long esum = es;
+        long long esum = isbig ? 0 : rd;
 #pragma unroll
         for (int o = 16; o; o >>= 1) esum += __shfl_xor_sync(IM_FULL, esum, o);
-        int pos = 0;
-        if (lane == 31) {
-            pos = atomicAdd(&ctr->next_items, ntot);
-            atomicAdd(&ctr->next_edges, (ull)esum);
-        }
-        pos = __shfl_sync(IM_FULL, pos, 31);
+        BlockTotals wt{ninc, 0, __popc(bmask), (unsigned long long)esum};
+        int pos, cpos, bpos;
+        block_reserve<BLOCK / 32>(wt, lane, threadIdx.x >> 5, &ctr->next_items, nullptr, &ctr->next_edges, &ctr->big, pos,
+                                  cpos, bpos);
         int p = pos + ninc - ns;
-#pragma unroll
-        for (int t = 0; t < 4; t++)
-            if (t < k)
-                for (int s0 = eb[t]; s0 < ee[t]; s0 += SEG) items[p++] = make_int4(v, s0, min(s0 + SEG, ee[t]), 0);
+        for (int s0 = rb; s0 < rb + rd && ns; s0 += SEG) items[p++] = make_int4(v, s0, min(s0 + SEG, rb + rd), 0);
+        if (isbig) big[bpos + __popc(bmask & ((1u << lane) - 1u))] = v;
     }
 }
 
@@ -500,6 +501,7 @@ cudaError_t launch_seed_start(Ctx& c, int k) {
     return LAUNCHED(c);
 }
 cudaError_t launch_bfs_level(Ctx& c, int cur, int n_items, uint32_t tag) {
+    (void)tag;
     BfsArgs a;
     a.items = c.bitems[cur];
     a.n_items = n_items;
@@ -515,20 +517,25 @@ cudaError_t launch_bfs_level(Ctx& c, int cur, int n_items, uint32_t tag) {
     a.vis = c.vis;
     a.din = c.delta[cur];
     a.dout = c.delta[cur ^ 1];
-    a.btag = c.btag;
-    a.tag = tag;
-    a.next_items = c.bitems[cur ^ 1];
-    a.next_vl = c.bvl[cur ^ 1];
+    a.nbits = c.nbits;
     int64_t want = ((int64_t)n_items + 32 * (BLOCK / 32) - 1) / (32 * (BLOCK / 32));
     int grid = (int)(want < 1 ? 1 : (want > c.max_blocks_bfs ? c.max_blocks_bfs : want));
     if (c.constT) k_bfs_level<true><<<grid, BLOCK, 0, c.stream>>>(a);
     else k_bfs_level<false><<<grid, BLOCK, 0, c.stream>>>(a);
-    return LAUNCHED(c);
+    cudaError_t e = LAUNCHED(c);
+    if (e) return e;
+    const int nxt = cur ^ 1;
+    k_bfs_compact<<<grid_for(c, c.n), BLOCK, 0, c.stream>>>(c.n, c.J, c.sorted_h, c.nbits, c.delta[nxt], c.off, c.bvl[nxt],
+                                                            c.bitems[nxt], c.big, &c.ctr[nxt], c.sigma_count);
+    if ((e = LAUNCHED(c))) return e;
+    if (!c.sorted_h) return e;
+    return launch_slices_big(c, c.big, c.delta[nxt], c.off, c.fwd, c.bitems[nxt], &c.ctr[nxt]);
 }
 cudaError_t launch_bfs_items(Ctx& c, int buf) {
-    k_bfs_items<<<c.num_sms * 4, BLOCK, 0, c.stream>>>(c.J, c.B0, c.sorted_h, c.Xs, c.bvl[buf], c.delta[buf], c.off, c.fwd,
-                                                        c.bitems[buf], &c.ctr[buf]);
-    return LAUNCHED(c);
+    k_bfs_items<<<c.num_sms * 4, BLOCK, 0, c.stream>>>(c.sorted_h, c.bvl[buf], c.off, c.bitems[buf], c.big, &c.ctr[buf]);
+    cudaError_t e = LAUNCHED(c);
+    if (e || !c.sorted_h) return e;
+    return launch_slices_big(c, c.big, c.delta[buf], c.off, c.fwd, c.bitems[buf], &c.ctr[buf]);
 }
 cudaError_t launch_bfs_clear(Ctx& c, int cur, int n_v) {
     int W = c.J >> 5;

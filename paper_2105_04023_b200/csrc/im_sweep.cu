@@ -1,13 +1,14 @@
 // im_sweep.cu -- Simulate (Alg. 2) on sm_100a: the sweep kernel and the
-// per-sweep frontier compaction.  DESIGN.md "Kernels / k_sweep".
+// per-sweep frontier compaction.  DESIGN.md §6 "k_sweep".
 //
 // One sweep is an edge-parallel, in-place pass over the in-edges (u,v) of every vertex v whose
 // registers changed in the previous sweep (all vertices in sweep 1).  For such an edge and every
 // simulation j with (X_j xor h_uv) < T_uv and u not in R_S[j], M_u[j] <- max(M_u[j], M_v[j])
 // (Alg. 2 'update', pull direction, reading R9).  Alg. 2 processes u in Gamma^-(L) with all its
-// out-edges; the edges into unchanged vertices are no-ops (u already holds their values), so they
-// are skipped, and edges whose candidate window misses every 32-simulation chunk of v that changed
-// are skipped too.  The fixpoint is unique, hence equal to the oracle's synchronous schedule.
+// out-edges; the edges into unchanged vertices are no-ops (u already holds their values) and so are
+// the simulations in which v did not change, so an edge is only worked on when its candidate window
+// holds a simulation in which v changed (exact per-simulation change masks).  The fixpoint is
+// unique, hence equal to the oracle's synchronous schedule.
 //
 // Simulations are stored in ascending-salt order, so the simulations where an edge can be live
 // form one contiguous window [lo, hi) (im_device.cuh).  A lane owns one edge; it touches only the
@@ -30,14 +31,20 @@ struct SweepArgs {
     int J;
     ull* M64;
     const uint32_t* vis;
-    const uint32_t* bits_in;
-    uint32_t* bits_out;
+    const uint32_t* cm_in;   // per-simulation change mask of the previous sweep, n x J/32 words (FILTER)
+    uint32_t* cm_out;        // this sweep's per-simulation change mask
+    uint32_t* bits_out;      // this sweep's per-vertex 32-simulation-chunk summary
 };
 
 __device__ __forceinline__ ull vmax8(ull a, ull b) {
     return (ull)__vmaxu4((uint32_t)a, (uint32_t)b) | ((ull)__vmaxu4((uint32_t)(a >> 32), (uint32_t)(b >> 32)) << 32);
 }
 __device__ __forceinline__ ull expand8(uint32_t b) { return (ull)expand4(b & 0xFu) | ((ull)expand4(b >> 4) << 32); }
+// one bit per byte that differs between a and b
+__device__ __forceinline__ uint32_t diff_bits8(ull a, ull b) {
+    uint32_t lo = ~__vcmpeq4((uint32_t)a, (uint32_t)b) & 0x01010101u, hi = ~__vcmpeq4((uint32_t)(a >> 32), (uint32_t)(b >> 32)) & 0x01010101u;
+    return (((lo * 0x00204081u) >> 21) & 0xFu) | ((((hi * 0x00204081u) >> 21) & 0xFu) << 4);
+}
 
 // byte mask of the simulations of 8-byte word w that are live for (h, T) inside [lo, hi), minus blocked ones
 template <bool BLOCKED>
@@ -57,16 +64,24 @@ __device__ __forceinline__ ull live8(const SweepArgs& a, const uint32_t* sX, uin
     return live;
 }
 
-// bytewise max of `cand` into *p given a first observed value; returns true if this thread raised a register
-__device__ __forceinline__ bool vmax_cas8(ull* p, ull cur, ull cand) {
+// bytewise max of `cand` into *p starting from an observed value `cur`; returns the bits of the
+// registers this thread raised (0 if none: someone else already holds values >= cand)
+__device__ __forceinline__ uint32_t vmax_cas8(ull* p, ull cur, ull cand) {
     ull nw = vmax8(cur, cand);
     while (nw != cur) {
         ull prev = atomicCAS(p, cur, nw);
-        if (prev == cur) return true;
+        if (prev == cur) return diff_bits8(cur, nw);
         cur = prev;
         nw = vmax8(cur, cand);
     }
-    return false;
+    return 0u;
+}
+
+// record raised registers of word w of u: per-simulation mask word + returns the chunk bit
+__device__ __forceinline__ uint32_t record8(const SweepArgs& a, uint32_t u, int w, uint32_t raised) {
+    if (!raised) return 0u;
+    atomicOr(&a.cm_out[(size_t)u * (a.J >> 5) + (w >> 2)], raised << ((w & 3) << 3));
+    return 1u << (w >> 2);
 }
 
 template <bool BLOCKED>
@@ -78,7 +93,19 @@ __device__ __forceinline__ uint32_t pull_word8(const SweepArgs& a, const uint32_
     ull cand = a.M64[v * J8 + w] & live;
     if (!cand) return 0u;
     ull* p = &a.M64[u * J8 + w];
-    return vmax_cas8(p, __ldcg(p), cand) ? (1u << (w >> 2)) : 0u;
+    return record8(a, u, w, vmax_cas8(p, __ldcg(p), cand));
+}
+
+// does v's previous-sweep change mask hold a simulation of [lo, hi)?
+__device__ __forceinline__ bool window_changed(const uint32_t* __restrict__ cm, uint32_t v, int W, int lo, int hi) {
+    const uint32_t* row = cm + (size_t)v * W;
+    int w0 = lo >> 5, w1 = (hi - 1) >> 5;
+    for (int w = w0; w <= w1; ++w) {
+        uint32_t m = __ldg(&row[w]);
+        int a = w == w0 ? (lo & 31) : 0, b = w == w1 ? ((hi - 1) & 31) : 31;
+        if (m & bit_range(a, b)) return true;
+    }
+    return false;
 }
 
 constexpr int NS = 2;  // edges in flight per lane
@@ -92,31 +119,35 @@ __global__ void __launch_bounds__(BLOCK, 4) k_sweep(SweepArgs a) {
     for (int i = threadIdx.x; i < 4097; i += blockDim.x) sS[i] = a.s12[i];
     __syncthreads();
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int J = a.J;
+    const int J = a.J, W = J >> 5;
     const size_t J8 = (size_t)(J >> 3);
     uint32_t wcount = 0;
 
+    int base = 0, left = 0;  // 128-item grabs (4 batches of 32) keep the cursor atomic off the critical path
     for (;;) {
-        int base = 0;
-        if (lane == 0) base = atomicAdd(&a.ctr->batch, 32);
-        base = __shfl_sync(IM_FULL, base, 0);
+        if (left == 0) {
+            if (lane == 0) base = atomicAdd(&a.ctr->batch, 128);
+            base = __shfl_sync(IM_FULL, base, 0);
+            left = 4;
+        } else {
+            base += 32;
+        }
+        --left;
         if (base >= a.n_items) break;
         int it = base + lane;
         int v = 0, eb = 0, cnt = 0;
-        uint32_t vbits = IM_FULL;
         if (it < a.n_items) {
             int4 I = a.items[it];
             v = I.x;
             eb = I.y;
             cnt = I.z - I.y;
-            if (FILTER) vbits = a.bits_in[v];
         }
         int incl = warp_incl_scan(cnt, lane);
         const int total = __shfl_sync(IM_FULL, incl, 31);
         const int start = incl - cnt;
         int carry = 0;
         for (int e0 = 0; e0 < total; e0 += 32 * NS) {
-            uint32_t u[NS], h[NS], T[NS], vv[NS], ob[NS];
+            uint32_t u[NS], h[NS], T[NS], vv[NS];
             int lo[NS], hi[NS];
             // owner item of each edge slot: the last non-empty item starting at or before it
 #pragma unroll
@@ -136,7 +167,6 @@ __global__ void __launch_bounds__(BLOCK, 4) k_sweep(SweepArgs a) {
                 vv[s] = (uint32_t)__shfl_sync(IM_FULL, v, owner);
                 int oeb = __shfl_sync(IM_FULL, eb, owner);
                 int ost = __shfl_sync(IM_FULL, start, owner);
-                ob[s] = __shfl_sync(IM_FULL, vbits, owner);
                 int idx = w0 + lane;
                 T[s] = 0u;
                 u[s] = h[s] = 0u;
@@ -155,7 +185,7 @@ __global__ void __launch_bounds__(BLOCK, 4) k_sweep(SweepArgs a) {
                 lo[s] = hi[s] = 0;
                 if (T[s]) {
                     edge_window(h[s], T[s], sX, sS, J, lo[s], hi[s]);
-                    if (FILTER && lo[s] < hi[s] && !(ob[s] & bit_range(lo[s] >> 5, (hi[s] - 1) >> 5))) hi[s] = lo[s];
+                    if (FILTER && lo[s] < hi[s] && !window_changed(a.cm_in, vv[s], W, lo[s], hi[s])) hi[s] = lo[s];
                 }
                 sparse[s] = lo[s] < hi[s] && hi[s] - lo[s] <= DENSE_WIN;
                 if (sparse[s]) {  // first word of the window: both loads in flight before any use
@@ -185,8 +215,9 @@ __global__ void __launch_bounds__(BLOCK, 4) k_sweep(SweepArgs a) {
                 chg[s] = 0u;
                 if (need[s]) {
                     int w = lo[s] >> 3;
-                    bool up = prev[s] == mu[s] || vmax_cas8(&a.M64[u[s] * J8 + w], prev[s], cand[s]);
-                    if (up) chg[s] = 1u << (w >> 2);
+                    uint32_t raised = prev[s] == mu[s] ? diff_bits8(mu[s], nw[s])
+                                                       : vmax_cas8(&a.M64[u[s] * J8 + w], prev[s], cand[s]);
+                    chg[s] |= record8(a, u[s], w, raised);
                 }
                 if (sparse[s])  // remaining words of a multi-word window
                     for (int w = (lo[s] >> 3) + 1; w <= (hi[s] - 1) >> 3; ++w)
@@ -209,7 +240,7 @@ __global__ void __launch_bounds__(BLOCK, 4) k_sweep(SweepArgs a) {
                     if (lane == l) chg[s] |= c;
                 }
             }
-            // record which 32-simulation chunks of u rose (fire-and-forget; the compaction builds the next frontier)
+            // which 32-simulation chunks of u rose (fire-and-forget; the compaction builds the next frontier)
 #pragma unroll
             for (int s = 0; s < NS; s++)
                 if (chg[s]) atomicOr(&a.bits_out[u[s]], chg[s]);
@@ -218,70 +249,99 @@ __global__ void __launch_bounds__(BLOCK, 4) k_sweep(SweepArgs a) {
     if (lane == 0 && wcount) atomicAdd(&a.ctr->win_edges, (ull)wcount);
 }
 
-// Next frontier: every vertex whose change bits are set.  Its in-edges whose candidate window can
-// meet a changed 32-simulation chunk are emitted as work items (<= 4 hash-sorted slices of its
-// in-edge row when every edge has the same threshold, the whole row otherwise); the other bit
-// buffer is cleared for the following sweep.
-__global__ void k_compact(int32_t n, int J, int B, bool sorted, const uint32_t* __restrict__ Xs,
-                          const uint32_t* __restrict__ bits_new, uint32_t* __restrict__ bits_clear,
-                          const int32_t* __restrict__ roff, const uint2* __restrict__ rev, int4* __restrict__ items,
-                          IterCounters* ctr) {
-    const int lane = threadIdx.x & 31;
-    const int NC = J >> 5, NQ = NC < 4 ? NC : 4;
+// ------------------------------------------------------------------ frontier compaction
+// Next frontier: every vertex v whose chunk bits are set.  A short in-edge row (<= SEG) is emitted
+// whole (the sweep's exact filter skips edges whose window holds no changed simulation); a long
+// row of a hash-sorted graph is queued for k_slices_big, which emits, per 32-simulation word of
+// v's change mask, the slice of the row whose windows can meet those simulations.  The buffers
+// of the sweep before are cleared here for the next sweep's writes.
+__global__ void k_compact(int32_t n, int J, bool sorted, const uint32_t* __restrict__ bits_new, uint32_t* __restrict__ bits_clear,
+                          uint32_t* __restrict__ cm_clear, const int32_t* __restrict__ roff, int4* __restrict__ items,
+                          int32_t* __restrict__ big, IterCounters* ctr) {
+    const int lane = threadIdx.x & 31, W = J >> 5;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
         int64_t v = base + threadIdx.x;
         bool in = v < n;
         uint32_t b = in ? bits_new[v] : 0u;
-        if (in && bits_clear && bits_clear[v]) bits_clear[v] = 0u;
-        int eb[4], ee[4], k = 0, ns = 0, es = 0;
-        if (b) {
-            int rb = roff[v], re = roff[v + 1];
-            if (sorted) {
-                int sa[4], sb[4];
-#pragma unroll
-                for (int q = 0; q < 4; q++) {
-                    sa[q] = sb[q] = -1;
-                    if (q < NQ) {
-                        uint32_t qb = b & bit_range(q * NC / NQ, (q + 1) * NC / NQ - 1);
-                        if (qb) {
-                            sa[q] = 32 * (__ffs(qb) - 1);
-                            sb[q] = 32 * (31 - __clz(qb)) + 31;
-                        }
-                    }
-                }
-                k = slices_for(rev, rb, re, Xs, B, sa, sb, eb, ee);
-            } else if (rb < re) {
-                eb[0] = rb;
-                ee[0] = re;
-                k = 1;
+        if (in && bits_clear) {
+            uint32_t bc = bits_clear[v];
+            if (bc) {
+                bits_clear[v] = 0u;
+                for (; bc; bc &= bc - 1) cm_clear[(size_t)v * W + (__ffs(bc) - 1)] = 0u;
             }
-#pragma unroll
-            for (int i = 0; i < 4; i++)
-                if (i < k) {
-                    ns += (ee[i] - eb[i] + SEG - 1) / SEG;
-                    es += ee[i] - eb[i];
-                }
+        }
+        if (!__syncthreads_or(b != 0u)) continue;  // block-uniform: no changed vertex among these 256
+        int rb = 0, rd = 0, ns = 0;
+        bool isbig = false;
+        if (b) {
+            rb = roff[v];
+            rd = roff[v + 1] - rb;
+            isbig = sorted && rd > SEG;
+            ns = isbig ? 0 : (rd > 0 ? (rd + SEG - 1) / SEG : 0);
         }
         uint32_t fmask = __ballot_sync(IM_FULL, b != 0u);
-        if (!fmask) continue;
+        uint32_t bmask = __ballot_sync(IM_FULL, isbig);
         int ninc = warp_incl_scan(ns, lane);
-        int ntot = __shfl_sync(IM_FULL, ninc, 31);
-        long long esum = es;
+        long long esum = isbig ? 0 : rd;
 #pragma unroll
         for (int o = 16; o; o >>= 1) esum += __shfl_xor_sync(IM_FULL, esum, o);
-        int pos = 0;
-        if (lane == 31) {
-            if (ntot) pos = atomicAdd(&ctr->next_items, ntot);
-            atomicAdd(&ctr->changed, __popc(fmask));
-            if (esum) atomicAdd(&ctr->next_edges, (ull)esum);
-        }
-        pos = __shfl_sync(IM_FULL, pos, 31);
+        BlockTotals wt{ninc, __popc(fmask), __popc(bmask), (unsigned long long)esum};
+        int pos, cpos, bpos;
+        block_reserve<BLOCK / 32>(wt, lane, threadIdx.x >> 5, &ctr->next_items, &ctr->changed, &ctr->next_edges, &ctr->big,
+                                  pos, cpos, bpos);
         int p = pos + ninc - ns;
+        for (int s0 = rb; s0 < rb + rd && ns; s0 += SEG) items[p++] = make_int4((int)v, s0, min(s0 + SEG, rb + rd), 0);
+        if (isbig) big[bpos + __popc(bmask & ((1u << lane) - 1u))] = (int32_t)v;
+    }
+}
+
+// warp per long row: one slice per non-zero 32-simulation word of the vertex's mask (change mask
+// for sweeps, Delta for BFS levels), trimmed so slices do not overlap, cut into <= SEG items
+__global__ void k_slices_big(int J, int B, const uint32_t* __restrict__ Xs, const int32_t* __restrict__ big,
+                             const uint32_t* __restrict__ mask, const int32_t* __restrict__ offs, const uint2* __restrict__ rec,
+                             int4* __restrict__ items, IterCounters* ctr) {
+    const int lane = threadIdx.x & 31, W = J >> 5;
+    const int nb = ctr->big;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < nb; i += nwarps) {
+        const int v = big[i];
+        const int rb = offs[v], re = offs[v + 1];
+        int b0 = re, e0 = re;
+        if (lane < W) {
+            uint32_t m = mask[(size_t)v * W + lane];
+            if (m) {
+                int sa = 32 * lane + __ffs(m) - 1, sb = 32 * lane + 31 - __clz(m);
+                uint32_t klo = (__ldg(&Xs[sa]) >> B) << B, khi = ((__ldg(&Xs[sb]) >> B) + 1u) << B;
+                b0 = lower_bound_h(rec, rb, re, klo);
+                e0 = lower_bound_h(rec, b0, re, khi);
+            }
+        }
+        // trim against the furthest end of the lanes before (slice bounds grow with the word index)
+        int pe = b0 < e0 ? e0 : rb;
 #pragma unroll
-        for (int i = 0; i < 4; i++)
-            if (i < k)
-                for (int s0 = eb[i]; s0 < ee[i]; s0 += SEG) items[p++] = make_int4((int)v, s0, min(s0 + SEG, ee[i]), 0);
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(IM_FULL, pe, o);
+            if (lane >= o) pe = max(pe, y);
+        }
+        int prev_end = __shfl_up_sync(IM_FULL, pe, 1);
+        if (lane == 0) prev_end = rb;
+        if (b0 < prev_end) b0 = prev_end;
+        int len = b0 < e0 ? e0 - b0 : 0;
+        int ns = (len + SEG - 1) / SEG;
+        int ninc = warp_incl_scan(ns, lane);
+        int ntot = __shfl_sync(IM_FULL, ninc, 31);
+        int es = len;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) es += __shfl_xor_sync(IM_FULL, es, o);
+        int pos = 0;
+        if (lane == 0 && ntot) {
+            pos = atomicAdd(&ctr->next_items, ntot);
+            atomicAdd(&ctr->next_edges, (ull)es);
+        }
+        pos = __shfl_sync(IM_FULL, pos, 0);
+        int p = pos + ninc - ns;
+        for (int s0 = b0; s0 < b0 + len; s0 += SEG) items[p++] = make_int4(v, s0, min(s0 + SEG, b0 + len), 0);
     }
 }
 
@@ -290,8 +350,8 @@ static void sweep_inst(int grid, cudaStream_t s, const SweepArgs& a) {
     k_sweep<C, B, F><<<grid, BLOCK, 0, s>>>(a);
 }
 
-cudaError_t launch_sweep(Ctx& c, const int4* items, int n_items, const uint32_t* bits_in, uint32_t* bits_out,
-                         IterCounters* ctr, bool blocked) {
+cudaError_t launch_sweep(Ctx& c, const int4* items, int n_items, const uint32_t* cm_in, uint32_t* cm_out,
+                         uint32_t* bits_out, IterCounters* ctr, bool blocked) {
     SweepArgs a;
     a.items = items;
     a.n_items = n_items;
@@ -304,11 +364,12 @@ cudaError_t launch_sweep(Ctx& c, const int4* items, int n_items, const uint32_t*
     a.J = c.J;
     a.M64 = reinterpret_cast<ull*>(c.M);
     a.vis = c.vis;
-    a.bits_in = bits_in;
+    a.cm_in = cm_in;
+    a.cm_out = cm_out;
     a.bits_out = bits_out;
     int64_t want = ((int64_t)n_items + 32 * (BLOCK / 32) - 1) / (32 * (BLOCK / 32));
     int grid = (int)(want < 1 ? 1 : (want > c.max_blocks_sweep ? c.max_blocks_sweep : want));
-    const bool ct = c.constT, f = bits_in != nullptr;
+    const bool ct = c.constT, f = cm_in != nullptr;
     if (!f) {
         if (ct) { if (blocked) sweep_inst<true, true, false>(grid, c.stream, a); else sweep_inst<true, false, false>(grid, c.stream, a); }
         else { if (blocked) sweep_inst<false, true, false>(grid, c.stream, a); else sweep_inst<false, false, false>(grid, c.stream, a); }
@@ -319,9 +380,18 @@ cudaError_t launch_sweep(Ctx& c, const int4* items, int n_items, const uint32_t*
     return LAUNCHED(c);
 }
 
-cudaError_t launch_compact(Ctx& c, const uint32_t* bits_new, uint32_t* bits_clear, int4* items_out, IterCounters* ctr) {
-    k_compact<<<grid_for(c, c.n), BLOCK, 0, c.stream>>>(c.n, c.J, c.B0, c.sorted_h, c.Xs, bits_new, bits_clear, c.roff,
-                                                        c.rev, items_out, ctr);
+cudaError_t launch_compact(Ctx& c, const uint32_t* bits_new, uint32_t* bits_clear, const uint32_t* cm_new,
+                           uint32_t* cm_clear, int4* items_out, IterCounters* ctr) {
+    k_compact<<<grid_for(c, c.n), BLOCK, 0, c.stream>>>(c.n, c.J, c.sorted_h, bits_new, bits_clear, cm_clear, c.roff,
+                                                        items_out, c.big, ctr);
+    cudaError_t e = LAUNCHED(c);
+    if (e || !c.sorted_h) return e;
+    return launch_slices_big(c, c.big, cm_new, c.roff, c.rev, items_out, ctr);
+}
+
+cudaError_t launch_slices_big(Ctx& c, const int32_t* big, const uint32_t* mask, const int32_t* offs, const uint2* rec,
+                              int4* items_out, IterCounters* ctr) {
+    k_slices_big<<<c.num_sms * 4, BLOCK, 0, c.stream>>>(c.J, c.B0, c.Xs, big, mask, offs, rec, items_out, ctr);
     return LAUNCHED(c);
 }
 
