@@ -69,6 +69,7 @@ def _load():
             "or_reach_register": (ctypes.c_int, [i32, vp, vp, vp, i32, u64, i64, vp, vp, vp]),
             "or_seed_sigma": (ctypes.c_int, [i32, vp, vp, vp, i32, u64, i32, vp, vp]),
             "or_first_sweep_sample": (i64, [i32, vp, vp, vp, i32, u64, i32, i32, vp, vp]),
+            "or_seed_reach_per_sim": (ctypes.c_int, [i32, vp, vp, vp, i32, u64, i32, vp, i32, vp, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -196,6 +197,19 @@ def seed_sigma(n, offsets, targets, probs, J, seed, seeds) -> np.ndarray:
     seeds = np.ascontiguousarray(seeds, dtype=np.int32)
     out = np.zeros(len(seeds), dtype=np.int64)
     rc = _load().or_seed_sigma(n, _p(offsets), _p(targets), _p(probs), J, seed, len(seeds), _p(seeds), _p(out))
+    if rc != 0:
+        raise MemoryError(rc)
+    return out
+
+
+def seed_reach_per_sim(n, offsets, targets, probs, J, seed, sims, seeds) -> np.ndarray:
+    """int64 [len(sims), K]: |R_{G_j}(first k+1 seeds)| for each listed simulation j."""
+    offsets, targets, probs = _csr(offsets, targets, probs)
+    sims = np.ascontiguousarray(sims, dtype=np.int32)
+    seeds = np.ascontiguousarray(seeds, dtype=np.int32)
+    out = np.zeros((len(sims), len(seeds)), dtype=np.int64)
+    rc = _load().or_seed_reach_per_sim(n, _p(offsets), _p(targets), _p(probs), J, seed, len(sims), _p(sims), len(seeds),
+                                       _p(seeds), _p(out))
     if rc != 0:
         raise MemoryError(rc)
     return out

@@ -532,3 +532,42 @@ int64_t or_first_sweep_sample(int32_t n, const int32_t *offsets, const int32_t *
     free(X);
     return processed;
 }
+
+/*
+ * Per-simulation form of or_seed_sigma for a subset of simulations (sampled parity at full size):
+ * out[s*K + k] = |R_{G_j}({seeds_0..seeds_k})| for j = sims[s] (Alg. 1 lines 13-14, R13).
+ */
+int or_seed_reach_per_sim(int32_t n, const int32_t *offsets, const int32_t *targets, const float *probs, int32_t J,
+                          uint64_t seed, int32_t nsims, const int32_t *sims, int32_t K, const int32_t *seeds, int64_t *out) {
+    uint32_t seed_v, seed_j;
+    uint32_t *X = (uint32_t *)malloc((size_t)J * sizeof(uint32_t));
+    or_salts(seed, J, &seed_v, &seed_j, X);
+    uint8_t *seen = (uint8_t *)calloc((size_t)n, 1);
+    int32_t *queue = (int32_t *)malloc((size_t)n * sizeof(int32_t));
+    if (!X || !seen || !queue) return -3;
+    for (int32_t si = 0; si < nsims; si++) {
+        int32_t j = sims[si];
+        int64_t qt = 0, qh = 0;
+        for (int32_t k = 0; k < K; k++) {
+            int32_t s = seeds[k];
+            if (!seen[s]) {
+                seen[s] = 1;
+                queue[qt++] = s;
+            }
+            while (qh < qt) {
+                int32_t x = queue[qh++];
+                for (int64_t e = offsets[x]; e < offsets[x + 1]; e++) {
+                    int32_t y = targets[e];
+                    if (!seen[y] && or_live(X[j], or_edge_hash(x, y), probs[e])) {
+                        seen[y] = 1;
+                        queue[qt++] = y;
+                    }
+                }
+            }
+            out[(int64_t)si * K + k] = qt;
+        }
+        for (int64_t q = 0; q < qt; q++) seen[queue[q]] = 0;
+    }
+    free(X); free(seen); free(queue);
+    return 0;
+}

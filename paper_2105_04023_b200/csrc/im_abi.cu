@@ -107,6 +107,7 @@ int ensure_device() {
     g.max_blocks_sweep = std::max(1, bs) * g.num_sms;
     g.max_blocks_bfs = std::max(1, bb) * g.num_sms;
     g.trace = getenv("IM_TRACE") != nullptr;
+    if (const char* pf = getenv("IM_PULL_FRAC")) g.pull_frac = atof(pf);
     if (!g.own_stream) CK(cudaStreamCreateWithFlags(&g.own_stream, cudaStreamNonBlocking));
     if (!g.stream) g.stream = g.own_stream;
     if (!g.hpin) CK(cudaMallocHost(&g.hpin, 4096));
@@ -340,8 +341,13 @@ int simulate(bool blocked) {
         IterCounters* ctr = &g.ctr[s & 1];
         CK(cudaMemsetAsync(ctr, 0, sizeof(IterCounters), g.stream));
         CK(cudaEventRecord(g.ev[0], g.stream));
+        // direction-optimised: a frontier whose in-edges cover most of the graph is swept by a full
+        // in-place gather (every row owned by one warp, no atomics); sparse frontiers are pushed
+        const bool gather = s > 1 && (double)edges_in > g.pull_frac * (double)g.m;
         if (s == 1)  // register init fused with the first sweep (every row written)
-            CK(launch_first(g, g.cm[1], g.bits[1], ctr, blocked));
+            CK(launch_first(g, g.cm[1], g.bits[1], ctr, blocked, false));
+        else if (gather)
+            CK(launch_first(g, g.cm[s & 1], g.bits[s & 1], ctr, blocked, true));
         else
             CK(launch_sweep(g, items, n_items, g.cm[(s - 1) & 1], g.cm[s & 1], g.bits[s & 1], ctr, blocked));
         CK(cudaEventRecord(g.ev[1], g.stream));
@@ -354,14 +360,14 @@ int simulate(bool blocked) {
         launches++;
         wedges += (int64_t)hc.win_edges;
         if (g.trace)
-            fprintf(stderr, "[im] sweep %d items %d edges %lld window_edges %llu -> changed %d next_items %d next_edges %llu big %d  %.3f ms\n",
-                    s, n_items, (long long)(s == 1 ? g.m : (int64_t)edges_in), hc.win_edges, hc.changed, hc.next_items,
-                    hc.next_edges, hc.big, t);
+            fprintf(stderr, "[im] sweep %d %s items %d edges %lld window_edges %llu -> changed %d next_items %d next_edges %llu big %d  %.3f ms\n",
+                    s, s == 1 ? "init+gather" : gather ? "gather" : "push", n_items, (long long)(s == 1 || gather ? g.m : (int64_t)edges_in),
+                    hc.win_edges, hc.changed, hc.next_items, hc.next_edges, hc.big, t);
         edges_in = (int64_t)hc.next_edges;
         if (hc.next_items == 0) break;
         items = g.items[s & 1];
         n_items = hc.next_items;
-        edges += (int64_t)hc.next_edges;
+        edges += (double)hc.next_edges > g.pull_frac * (double)g.m ? g.m : (int64_t)hc.next_edges;
     }
     g.sweep_dirty = false;  // a completed build leaves every change buffer zero
     g.st.builds++;

@@ -1,12 +1,20 @@
-// im_first.cu -- register init (Alg. 1 lines 2-5) fused with the first sweep of Alg. 2.
+// im_first.cu -- register init (Alg. 1 lines 2-5) fused with the first sweep of Alg. 2, and the
+// same gather as a full in-place sweep for dense frontiers (direction-optimised Simulate).
 //
 // In the first sweep every vertex is live and every register still holds its init value
 // M_v[j] = clz(hash(v) xor hash(j)), which is a pure function of (v, j).  So the
-// first sweep is computed here as a gather, one warp per vertex u over its out-edges (pull, reading
-// R9): row(u) = max(init(u), max over live (u,v), u not blocked, of init(v)) -- exactly the
-// synchronous first iteration -- with init(v) recomputed from the hashes instead of read from HBM.
-// The warp owns the row, so it is written once, with no atomics, together with u's exact
+// first sweep is computed as a gather, one warp per vertex u over its out-edges (pull, reading R9):
+// row(u) = max(init(u), max over live (u,v), u not blocked, of init(v)) -- exactly the synchronous
+// first iteration -- with init(v) recomputed from the hashes instead of read from HBM.  The warp
+// owns the row, so it is written once, without global atomics, together with u's exact
 // per-simulation change mask (row != init) that drives the second sweep (im_sweep.cu).
+// With MEM = true the same kernel is a full gather sweep reading the current registers (used when
+// the next push frontier would cover nearly every edge): rows are read and written sequentially,
+// only the window words of the out-neighbours are random reads; in place (Gauss-Seidel), and the
+// fixpoint is unique.
+//
+// The working row lives in shared memory as packed 4-register words; an edge merges the live
+// registers of its window word by word with a shared-memory bytewise-max CAS.
 // Vertices with more than FIRST_BIG out-edges are done by a whole block (k_first_big).
 #include "im_device.cuh"
 #include "im_internal.h"
@@ -29,89 +37,118 @@ struct FirstArgs {
     uint32_t* cm_out;
     uint32_t* bits_out;
     IterCounters* ctr;
-    const int32_t* big;   // vertices with > FIRST_BIG out-edges (k_first_big)
+    const int32_t* big;  // vertices with > FIRST_BIG out-edges (k_first_big)
     int n_big;
 };
 
-// shared-memory working row: one u32 per simulation (native smem atomicMax).  `e` is this lane's
-// edge (or -1); the loop around it must be warp-uniform.  Windows wider than DENSE_WIN simulations
-// (w close to 1) are walked by the whole warp, one candidate per lane.
-template <bool CONST_T, bool BLOCKED>
+// init registers of simulations 4w..4w+3 of a vertex with hash hv, packed
+__device__ __forceinline__ uint32_t init_word(uint32_t hv, const uint32_t* sHJ, int w) {
+    const uint4 h = reinterpret_cast<const uint4*>(sHJ)[w];
+    return (uint32_t)__clz(hv ^ h.x) | ((uint32_t)__clz(hv ^ h.y) << 8) | ((uint32_t)__clz(hv ^ h.z) << 16) |
+           ((uint32_t)__clz(hv ^ h.w) << 24);
+}
+
+// shared-memory bytewise max
+__device__ __forceinline__ void smem_vmax(uint32_t* p, uint32_t val) {
+    uint32_t cur = *p;
+    uint32_t nw = __vmaxu4(cur, val);
+    while (nw != cur) {
+        uint32_t prev = atomicCAS(p, cur, nw);
+        if (prev == cur) return;
+        cur = prev;
+        nw = __vmaxu4(cur, val);
+    }
+}
+
+// merge word w of edge (u -> v, h, T) restricted to [lo, hi) into the smem row
+template <bool BLOCKED, bool MEM>
+__device__ __forceinline__ void merge_word(const FirstArgs& a, const uint32_t* sX, const uint32_t* sHJ, const uint32_t* sVis,
+                                           uint32_t* row, uint32_t v, uint32_t hv, uint32_t h, uint32_t T, int lo, int hi, int w) {
+    uint32_t live = 0;
+#pragma unroll
+    for (int b = 0; b < 4; b++) {
+        int i = 4 * w + b;
+        bool ok = (i >= lo) & (i < hi) & ((sX[i] ^ h) < T);
+        live |= ok ? (0xFFu << (8 * b)) : 0u;
+    }
+    if (BLOCKED && live) live &= ~expand4((sVis[w >> 3] >> ((w & 7) << 2)) & 0xFu);
+    if (!live) return;
+    uint32_t val = MEM ? reinterpret_cast<const uint32_t*>(a.M)[(size_t)v * (a.J >> 2) + w] : init_word(hv, sHJ, w);
+    val &= live;
+    if (__vmaxu4(row[w], val) != row[w]) smem_vmax(&row[w], val);
+}
+
+// `e` is this lane's edge (or -1); the loop around it must be warp-uniform.  Windows wider than
+// DENSE_WIN simulations (w close to 1) are walked by the whole warp, one word per lane.
+template <bool CONST_T, bool BLOCKED, bool MEM>
 __device__ __forceinline__ void gather_edge(const FirstArgs& a, const uint32_t* sX, const uint16_t* sS, const uint32_t* sHJ,
                                             const uint32_t* sVis, uint32_t* row, int e, uint32_t& wcount) {
     const int lane = threadIdx.x & 31;
-    uint32_t h = 0, T = 0, hv = 0;
+    uint32_t h = 0, T = 0, hv = 0, v = 0;
     int lo = 0, hi = 0;
     if (e >= 0) {
         uint2 f = a.fwd[e];
         T = CONST_T ? a.T0 : a.fwdT[e];
         h = f.y;
+        v = f.x;
         if (T) {
             edge_window(h, T, sX, sS, a.J, lo, hi);
             if (lo < hi) {
                 wcount++;
-                hv = murmur_word(f.x, a.seedV);
+                if (!MEM) hv = murmur_word(v, a.seedV);
             }
         }
     }
     const bool dense = hi - lo > DENSE_WIN;
-    if (!dense)
-        for (int i = lo; i < hi; ++i) {
-            if ((sX[i] ^ h) >= T) continue;
-            if (BLOCKED && ((sVis[i >> 5] >> (i & 31)) & 1u)) continue;
-            uint32_t val = __clz(hv ^ sHJ[i]);
-            if (val > row[i]) atomicMax(&row[i], val);
-        }
+    if (!dense && lo < hi)
+        for (int w = lo >> 2; w <= (hi - 1) >> 2; ++w) merge_word<BLOCKED, MEM>(a, sX, sHJ, sVis, row, v, hv, h, T, lo, hi, w);
     uint32_t dmask = __ballot_sync(IM_FULL, dense);
     while (dmask) {
         int l = __ffs(dmask) - 1;
         dmask &= dmask - 1;
         uint32_t dh = __shfl_sync(IM_FULL, h, l), dT = __shfl_sync(IM_FULL, T, l), dhv = __shfl_sync(IM_FULL, hv, l);
+        uint32_t dv = __shfl_sync(IM_FULL, v, l);
         int dlo = __shfl_sync(IM_FULL, lo, l), dhi = __shfl_sync(IM_FULL, hi, l);
-        for (int i = dlo + lane; i < dhi; i += 32) {
-            if ((sX[i] ^ dh) >= dT) continue;
-            if (BLOCKED && ((sVis[i >> 5] >> (i & 31)) & 1u)) continue;
-            uint32_t val = __clz(dhv ^ sHJ[i]);
-            if (val > row[i]) atomicMax(&row[i], val);
-        }
+        for (int w = (dlo >> 2) + lane; w <= (dhi - 1) >> 2; w += 32)
+            merge_word<BLOCKED, MEM>(a, sX, sHJ, sVis, row, dv, dhv, dh, dT, dlo, dhi, w);
     }
 }
 
-// write the row of u, its per-simulation change mask and chunk summary
-__device__ __forceinline__ void write_row(const FirstArgs& a, const uint32_t* sHJ, const uint32_t* row, uint32_t hu, uint32_t u,
-                                          int tid, int nthreads, uint32_t* sMask) {
-    const int J = a.J;
-    uint32_t* M32 = reinterpret_cast<uint32_t*>(a.M) + (size_t)u * (J >> 2);
-    for (int w = tid; w < (J >> 2); w += nthreads) {
-        uint32_t x = 0, ch = 0;
-#pragma unroll
-        for (int b = 0; b < 4; b++) {
-            uint32_t r = row[4 * w + b];
-            x |= r << (8 * b);
-            ch |= (r != (uint32_t)__clz(hu ^ sHJ[4 * w + b]) ? 1u : 0u) << b;
-        }
-        M32[w] = x;
-        if (ch) atomicOr(&sMask[w >> 3], ch << ((w & 7) << 2));
-    }
+constexpr int FW = 8;  // max words per lane of the warp kernel (J/4/32 <= 8)
+
+template <bool MEM>
+__device__ __forceinline__ uint32_t start_word(const FirstArgs& a, const uint32_t* sHJ, uint32_t hu, uint32_t u, int w) {
+    return MEM ? reinterpret_cast<const uint32_t*>(a.M)[(size_t)u * (a.J >> 2) + w] : init_word(hu, sHJ, w);
 }
 
-template <bool CONST_T, bool BLOCKED>
+// final smem word vs its start value: write it back if it rose (always for the first sweep, which
+// also writes the init registers) and return the 4 change bits (one per simulation) of word w
+__device__ __forceinline__ uint32_t finish_word(const FirstArgs& a, const uint32_t* row, uint32_t u, int w, uint32_t old,
+                                                bool always_write) {
+    uint32_t x = row[w];
+    if (always_write || x != old) reinterpret_cast<uint32_t*>(a.M)[(size_t)u * (a.J >> 2) + w] = x;
+    uint32_t eq = __vcmpeq4(x, old);
+    return ((((~eq) & 0x01010101u) * 0x00204081u) >> 21) & 0xFu;
+}
+
+template <bool CONST_T, bool BLOCKED, bool MEM>
 __global__ void __launch_bounds__(BLOCK) k_first(FirstArgs a) {
     __shared__ uint32_t sX[1024];
     __shared__ uint16_t sS[4098];
-    __shared__ uint32_t sHJ[1024];
-    extern __shared__ uint32_t sRows[];  // BLOCK/32 working rows of J u32 (dynamic: 8*J*4 bytes)
+    __shared__ __align__(16) uint32_t sHJ[1024];
+    __shared__ uint32_t sRow[BLOCK / 32][256];
+    __shared__ uint32_t sOldRow[BLOCK / 32][256];
     __shared__ uint32_t sVis[BLOCK / 32][32];
-    __shared__ uint32_t sMask[BLOCK / 32][32];
-    const int J = a.J, W = J >> 5;
+    const int J = a.J, W = J >> 5, NW = J >> 2;
     for (int i = threadIdx.x; i < J; i += blockDim.x) {
         sX[i] = a.Xs[i];
-        sHJ[i] = murmur_word((uint32_t)a.perm[i], a.seedJ);
+        sHJ[i] = MEM ? 0u : murmur_word((uint32_t)a.perm[i], a.seedJ);
     }
     for (int i = threadIdx.x; i < 4097; i += blockDim.x) sS[i] = a.s12[i];
     __syncthreads();
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    uint32_t* row = sRows + wib * J;
+    uint32_t* row = sRow[wib];
+    uint32_t* old = sOldRow[wib];
     uint32_t wcount = 0;
     for (;;) {
         int base = 0;
@@ -122,21 +159,39 @@ __global__ void __launch_bounds__(BLOCK) k_first(FirstArgs a) {
         for (int u = base; u < end; ++u) {
             const int eb = a.off[u], ee = a.off[u + 1];
             if (ee - eb > FIRST_BIG) continue;  // done by k_first_big
-            const uint32_t hu = murmur_word((uint32_t)u, a.seedV);
-            for (int i = lane; i < J; i += 32) row[i] = __clz(hu ^ sHJ[i]);
-            if (lane < W) {
-                sMask[wib][lane] = 0u;
-                if (BLOCKED) sVis[wib][lane] = a.vis[(size_t)u * W + lane];
+            if (MEM && ee == eb) {             // nothing to pull: the row cannot change
+                if (lane < W) a.cm_out[(size_t)u * W + lane] = 0u;
+                if (lane == 0) a.bits_out[u] = 0u;
+                continue;
             }
+            const uint32_t hu = MEM ? 0u : murmur_word((uint32_t)u, a.seedV);
+            for (int w = lane; w < NW; w += 32) {
+                uint32_t x = start_word<MEM>(a, sHJ, hu, (uint32_t)u, w);
+                row[w] = x;
+                old[w] = x;
+            }
+            if (BLOCKED && lane < W) sVis[wib][lane] = a.vis[(size_t)u * W + lane];
             __syncwarp();
             for (int e0 = eb; e0 < ee; e0 += 32)
-                gather_edge<CONST_T, BLOCKED>(a, sX, sS, sHJ, sVis[wib], row, e0 + lane < ee ? e0 + lane : -1, wcount);
+                gather_edge<CONST_T, BLOCKED, MEM>(a, sX, sS, sHJ, sVis[wib], row, e0 + lane < ee ? e0 + lane : -1, wcount);
             __syncwarp();
-            write_row(a, sHJ, row, hu, (uint32_t)u, lane, 32, sMask[wib]);
-            __syncwarp();
-            uint32_t m = lane < W ? sMask[wib][lane] : 0u;
-            if (lane < W) a.cm_out[(size_t)u * W + lane] = m;
-            uint32_t chunks = __ballot_sync(IM_FULL, m != 0u);
+            uint32_t chunks = 0;
+#pragma unroll
+            for (int k = 0; k < FW; k++) {
+                if (32 * k < NW) {  // warp-uniform
+                    const int w = lane + 32 * k;
+                    uint32_t nib = w < NW ? finish_word(a, row, (uint32_t)u, w, old[w], !MEM) : 0u;
+                    // change-mask word (w >> 3) = 4k + lane/8 from the nibbles of 8 consecutive lanes
+                    uint32_t x = nib << ((lane & 7) << 2);
+                    x |= __shfl_xor_sync(IM_FULL, x, 1);
+                    x |= __shfl_xor_sync(IM_FULL, x, 2);
+                    x |= __shfl_xor_sync(IM_FULL, x, 4);
+                    if ((lane & 7) == 0 && w < NW) a.cm_out[(size_t)u * W + (w >> 3)] = x;
+                    const uint32_t bl = __ballot_sync(IM_FULL, (lane & 7) == 0 && x != 0u);
+#pragma unroll
+                    for (int c = 0; c < 4; c++) chunks |= ((bl >> (8 * c)) & 1u) << (4 * k + c);
+                }
+            }
             if (lane == 0) a.bits_out[u] = chunks;
             __syncwarp();
         }
@@ -146,26 +201,31 @@ __global__ void __launch_bounds__(BLOCK) k_first(FirstArgs a) {
 }
 
 // one block per vertex with more than FIRST_BIG out-edges
-template <bool CONST_T, bool BLOCKED>
+template <bool CONST_T, bool BLOCKED, bool MEM>
 __global__ void __launch_bounds__(BLOCK) k_first_big(FirstArgs a) {
     __shared__ uint32_t sX[1024];
     __shared__ uint16_t sS[4098];
-    __shared__ uint32_t sHJ[1024];
-    __shared__ uint32_t row[1024];
+    __shared__ __align__(16) uint32_t sHJ[1024];
+    __shared__ uint32_t row[256];
+    __shared__ uint32_t sOld[256];
     __shared__ uint32_t sVis[32];
     __shared__ uint32_t sMask[32];
-    const int J = a.J, W = J >> 5;
+    const int J = a.J, W = J >> 5, NW = J >> 2;
     for (int i = threadIdx.x; i < J; i += blockDim.x) {
         sX[i] = a.Xs[i];
-        sHJ[i] = murmur_word((uint32_t)a.perm[i], a.seedJ);
+        sHJ[i] = MEM ? 0u : murmur_word((uint32_t)a.perm[i], a.seedJ);
     }
     for (int i = threadIdx.x; i < 4097; i += blockDim.x) sS[i] = a.s12[i];
     uint32_t wcount = 0;
     for (int bi = blockIdx.x; bi < a.n_big; bi += gridDim.x) {
         const uint32_t u = (uint32_t)a.big[bi];
         __syncthreads();
-        const uint32_t hu = murmur_word(u, a.seedV);
-        for (int i = threadIdx.x; i < J; i += blockDim.x) row[i] = __clz(hu ^ sHJ[i]);
+        const uint32_t hu = MEM ? 0u : murmur_word(u, a.seedV);
+        for (int w = threadIdx.x; w < NW; w += blockDim.x) {
+            uint32_t x = start_word<MEM>(a, sHJ, hu, u, w);
+            row[w] = x;
+            sOld[w] = x;
+        }
         if (threadIdx.x < W) {
             sMask[threadIdx.x] = 0u;
             if (BLOCKED) sVis[threadIdx.x] = a.vis[(size_t)u * W + threadIdx.x];
@@ -173,9 +233,12 @@ __global__ void __launch_bounds__(BLOCK) k_first_big(FirstArgs a) {
         __syncthreads();
         const int eb = a.off[u], ee = a.off[u + 1];
         for (int e0 = eb + (threadIdx.x & ~31); e0 < ee; e0 += blockDim.x)  // warp-uniform trip count
-            gather_edge<CONST_T, BLOCKED>(a, sX, sS, sHJ, sVis, row, e0 + (threadIdx.x & 31) < ee ? e0 + (threadIdx.x & 31) : -1, wcount);
+            gather_edge<CONST_T, BLOCKED, MEM>(a, sX, sS, sHJ, sVis, row, e0 + (threadIdx.x & 31) < ee ? e0 + (threadIdx.x & 31) : -1, wcount);
         __syncthreads();
-        write_row(a, sHJ, row, hu, u, threadIdx.x, blockDim.x, sMask);
+        for (int w = threadIdx.x; w < NW; w += blockDim.x) {
+            uint32_t nib = finish_word(a, row, u, w, sOld[w], !MEM);
+            if (nib) atomicOr(&sMask[w >> 3], nib << ((w & 7) << 2));
+        }
         __syncthreads();
         if (threadIdx.x < 32) {
             uint32_t m = threadIdx.x < W ? sMask[threadIdx.x] : 0u;
@@ -189,16 +252,16 @@ __global__ void __launch_bounds__(BLOCK) k_first_big(FirstArgs a) {
     if (lane == 0 && wcount) atomicAdd(&a.ctr->win_edges, (ull)wcount);
 }
 
-template <bool C, bool B>
+template <bool C, bool B, bool MEM>
 static cudaError_t first_inst(Ctx& c, const FirstArgs& a) {
-    k_first<C, B><<<c.max_blocks_first, BLOCK, (BLOCK / 32) * c.J * sizeof(uint32_t), c.stream>>>(a);
+    k_first<C, B, MEM><<<c.max_blocks_first, BLOCK, 0, c.stream>>>(a);
     cudaError_t e = LAUNCHED(c);
     if (e || a.n_big == 0) return e;
-    k_first_big<C, B><<<a.n_big < c.num_sms * 4 ? a.n_big : c.num_sms * 4, BLOCK, 0, c.stream>>>(a);
+    k_first_big<C, B, MEM><<<a.n_big < c.num_sms * 4 ? a.n_big : c.num_sms * 4, BLOCK, 0, c.stream>>>(a);
     return LAUNCHED(c);
 }
 
-cudaError_t launch_first(Ctx& c, uint32_t* cm_out, uint32_t* bits_out, IterCounters* ctr, bool blocked) {
+cudaError_t launch_first(Ctx& c, uint32_t* cm_out, uint32_t* bits_out, IterCounters* ctr, bool blocked, bool from_memory) {
     FirstArgs a;
     a.n = c.n;
     a.J = c.J;
@@ -218,11 +281,15 @@ cudaError_t launch_first(Ctx& c, uint32_t* cm_out, uint32_t* bits_out, IterCount
     a.ctr = ctr;
     a.big = c.fbig;
     a.n_big = c.n_fbig;
-    if (c.constT) return blocked ? first_inst<true, true>(c, a) : first_inst<true, false>(c, a);
-    return blocked ? first_inst<false, true>(c, a) : first_inst<false, false>(c, a);
+    if (from_memory) {
+        if (c.constT) return blocked ? first_inst<true, true, true>(c, a) : first_inst<true, false, true>(c, a);
+        return blocked ? first_inst<false, true, true>(c, a) : first_inst<false, false, true>(c, a);
+    }
+    if (c.constT) return blocked ? first_inst<true, true, false>(c, a) : first_inst<true, false, false>(c, a);
+    return blocked ? first_inst<false, true, false>(c, a) : first_inst<false, false, false>(c, a);
 }
 
-// vertices with more than FIRST_BIG out-edges, ascending (once per graph)
+// vertices with more than FIRST_BIG out-edges (once per graph)
 __global__ void k_list_big_rows(int32_t n, const int32_t* __restrict__ off, int32_t* __restrict__ out, int* count) {
     int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += stride)
@@ -234,16 +301,9 @@ cudaError_t launch_list_big_rows(Ctx& c, int32_t* out, int* count) {
     return LAUNCHED(c);
 }
 
-// opt in to the dynamic shared memory of the largest J (8 rows x 1024 x 4 B = 32 KB + 17 KB static)
 int setup_first(int J, int* blocks_per_sm) {
-    const int dyn = (BLOCK / 32) * 1024 * (int)sizeof(uint32_t);
-    cudaError_t e;
-    if ((e = cudaFuncSetAttribute(k_first<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn))) return (int)e;
-    if ((e = cudaFuncSetAttribute(k_first<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn))) return (int)e;
-    if ((e = cudaFuncSetAttribute(k_first<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn))) return (int)e;
-    if ((e = cudaFuncSetAttribute(k_first<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn))) return (int)e;
-    return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_first<true, true>, BLOCK,
-                                                              (BLOCK / 32) * J * sizeof(uint32_t));
+    (void)J;
+    return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_first<true, true, false>, BLOCK, 0);
 }
 
 }  // namespace im

@@ -76,8 +76,9 @@ struct Ctx {
     uint32_t* bits[2] = {nullptr, nullptr};  // per-vertex 32-simulation-chunk change bits, ping-pong
     uint32_t* cm[2] = {nullptr, nullptr};    // per-(vertex, simulation) change masks, n x J/32 words, ping-pong
     int32_t* big = nullptr;                  // long rows awaiting slicing
-    bool sweep_dirty = true;
-    bool trace = false;                      // IM_TRACE: per-sweep / per-level lines on stderr                 // change buffers may hold stale bits (fresh / aborted build)
+    bool sweep_dirty = true;   // change buffers may hold stale bits (fresh / aborted build)
+    bool trace = false;        // IM_TRACE: per-sweep / per-level lines on stderr
+    double pull_frac = 0.97;   // gather sweep when the push frontier's in-edges exceed this share of m (IM_PULL_FRAC)
     IterCounters* ctr = nullptr;   // [2]
     // selection buffers
     uint8_t* inS = nullptr;
@@ -136,7 +137,7 @@ int occupancy_sweep(int* blocks_per_sm);
 int occupancy_bfs(int* blocks_per_sm);
 int setup_first(int J, int* blocks_per_sm);  // smem opt-in + occupancy of the first-sweep kernel for this J
 // register init + first sweep (gather, im_first.cu): writes every row, its change mask and chunk bits
-cudaError_t launch_first(Ctx& c, uint32_t* cm_out, uint32_t* bits_out, IterCounters* ctr, bool blocked);
+cudaError_t launch_first(Ctx& c, uint32_t* cm_out, uint32_t* bits_out, IterCounters* ctr, bool blocked, bool from_memory);
 cudaError_t launch_list_big_rows(Ctx& c, int32_t* out, int* count);
 cudaError_t launch_validate(Ctx& c, const int32_t* off, const int32_t* tgt, const float* prob, int* flags);
 cudaError_t launch_const_check(Ctx& c, const float* prob, int* flag);

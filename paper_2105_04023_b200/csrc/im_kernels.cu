@@ -43,6 +43,7 @@ __device__ __forceinline__ uint32_t gain16(uint4 x, uint4 m) {
 }
 
 constexpr int HIST_BINS = 4096;
+constexpr int AG = 4;  // vertex groups in flight per warp in k_argmax
 
 // LIST = false: every vertex (full pass: stores gains + histogram); LIST = true: the vertices in list[0..*count)
 template <bool POOL, bool LIST>
@@ -70,12 +71,12 @@ __global__ void __launch_bounds__(BLOCK) k_argmax(int32_t n, int32_t J, int L, i
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     ull best = 0;
-    for (int64_t g0 = gw; g0 < groups; g0 += 2 * nwarps) {
-        uint4 x[2][2];
-        int64_t vv[2];
-        bool ok[2];
+    for (int64_t g0 = gw; g0 < groups; g0 += AG * nwarps) {
+        uint4 x[AG][2];
+        int64_t vv[AG];
+        bool ok[AG];
 #pragma unroll
-        for (int u = 0; u < 2; u++) {
+        for (int u = 0; u < AG; u++) {
             int64_t idx = (g0 + u * nwarps) * VPW + sub;
             ok[u] = (g0 + u * nwarps) < groups && idx < nv;
             vv[u] = ok[u] ? (LIST ? (int64_t)list[idx] : idx) : 0;
@@ -86,7 +87,7 @@ __global__ void __launch_bounds__(BLOCK) k_argmax(int32_t n, int32_t J, int L, i
             }
         }
 #pragma unroll
-        for (int u = 0; u < 2; u++) {
+        for (int u = 0; u < AG; u++) {
             uint32_t gn = gain16(x[u][0], ms[0]) + gain16(x[u][1], ms[1]);
             int full = 1;
             if (POOL && ok[u])
@@ -303,6 +304,8 @@ __global__ void __launch_bounds__(BLOCK) k_bfs_level(BfsArgs a) {
                         for (int w = lo >> 5; w <= (hi - 1) >> 5; ++w) bfs_word(a, sX, (uint32_t)ou, v, w, h, T, lo, hi);
                 }
             }
+            // wide windows: one simulation per lane, the 32-bit live words come from ballots, then
+            // lane (w & 31) applies word w (a window spans <= J/32 <= 32 words)
             uint32_t dmask = __ballot_sync(IM_FULL, dense);
             while (dmask) {
                 int l = __ffs(dmask) - 1;
@@ -310,7 +313,26 @@ __global__ void __launch_bounds__(BLOCK) k_bfs_level(BfsArgs a) {
                 uint32_t dv = __shfl_sync(IM_FULL, v, l), dh = __shfl_sync(IM_FULL, h, l), dT = __shfl_sync(IM_FULL, T, l);
                 int dlo = __shfl_sync(IM_FULL, lo, l), dhi = __shfl_sync(IM_FULL, hi, l);
                 uint32_t du = (uint32_t)__shfl_sync(IM_FULL, ou, l);
-                for (int w = (dlo >> 5) + lane; w <= (dhi - 1) >> 5; w += 32) bfs_word(a, sX, du, dv, w, dh, dT, dlo, dhi);
+                const int w0 = dlo >> 5, w1 = (dhi - 1) >> 5, W = a.J >> 5;
+                uint32_t mylive = 0;
+                int myw = -1;
+                for (int w = w0; w <= w1; ++w) {
+                    int i = 32 * w + lane;
+                    uint32_t lv = __ballot_sync(IM_FULL, i >= dlo && i < dhi && (sX[i] ^ dh) < dT);
+                    if ((w & 31) == lane) {
+                        mylive = lv;
+                        myw = w;
+                    }
+                }
+                if (myw >= 0 && mylive) {
+                    uint32_t nv = a.din[(size_t)du * W + myw] & mylive;
+                    if (nv) nv &= ~__ldcg(&a.vis[(size_t)dv * W + myw]);
+                    if (nv) {
+                        atomicOr(&a.vis[(size_t)dv * W + myw], nv);
+                        atomicOr(&a.dout[(size_t)dv * W + myw], nv);
+                        atomicOr(&a.nbits[dv], 1u << myw);
+                    }
+                }
             }
         }
     }

@@ -28,6 +28,15 @@ def sha(*arrs):
     return h.hexdigest()
 
 
+_graphs = {}
+
+
+def cached_graph(name):
+    if name not in _graphs:
+        _graphs[name] = gen.graph(name)
+    return _graphs[name]
+
+
 def golden(tag):
     p = os.path.join(GOLDEN, f"{tag}_oracle.json")
     return json.load(open(p)) if os.path.exists(p) else None
@@ -90,3 +99,68 @@ def test_c2_parity():
         assert list(s) == g["select"]["seeds"]
         assert [x["rebuilt"] for x in im.im_get_step_log(cfg.K)] == g["select"]["rebuilt"]
         assert sha(reach_words_abi(n, cfg.J)) == g["select"]["reach_sha256"]
+
+
+def sampled_seed_reach_check(n, off, tgt, pr, J, seed, seeds, sims):
+    """Per-simulation |R_G(S)| of the GPU's seed set vs the oracle's BFS definition, for a few simulations."""
+    vis = im.reach_bits_to_bool(im.im_get_reach(n, J), J)
+    want = oracle.seed_reach_per_sim(n, off, tgt, pr, J, seed, sims, seeds)
+    assert [int(vis[:, j].sum()) for j in sims] == list(want[:, -1])
+
+
+def test_c3_parity():
+    """C3 (Chung-Lu, 4M / 67.9M, p = 0.01, J = 256): first-build registers vs the oracle's digest,
+    sampled registers vs the reach-max definition, K = 50 selection: sigma of every step vs the
+    step log, per-simulation reach of the seed set vs the oracle's BFS."""
+    cfg = gen.CONFIGS["c3"]
+    n, off, tgt = cached_graph(cfg.graph)
+    pr = np.full(len(tgt), cfg.p, np.float32)
+    im.im_load_csr(n, off, tgt, pr)
+    im.im_build_sketches(cfg.J, cfg.salt_seed)
+    g = golden("c3")
+    if g is not None:
+        assert g["graph_sha256"] == sha(off, tgt, pr)
+        M = im.im_get_registers(n, cfg.J)
+        assert sha(M) == g["first_build"]["registers_sha256"]
+        del M
+    sampled_register_check(n, off, tgt, pr, cfg.J, cfg.salt_seed, 300, rng_seed=3)
+    s, sc = im.im_select_seeds(cfg.K, cfg.t)
+    assert len(set(s.tolist())) == cfg.K and all(np.diff(sc) >= 0)
+    log = im.im_get_step_log(cfg.K)
+    assert [x["sigma_count"] / cfg.J for x in log] == list(sc)
+    sampled_seed_reach_check(n, off, tgt, pr, cfg.J, cfg.salt_seed, s, [0, 97, 255])
+
+
+def test_c4_parity():
+    """C4 (RMAT-24, 16.8M / 520.8M, p = 0.005, J = 512): sampled registers of the first build vs
+    the reach-max definition (and the oracle's digest when tests/golden/c4_oracle.json exists),
+    K = 50 selection, per-simulation reach of the seed set vs the oracle's BFS."""
+    cfg = gen.CONFIGS["c4"]
+    n, off, tgt, pr = gen.workload(cfg)
+    im.im_load_csr(n, off, tgt, pr)
+    im.im_build_sketches(cfg.J, cfg.salt_seed)
+    g = golden("c4")
+    if g is not None and "first_build" in g:
+        assert g["graph_sha256"] == sha(off, tgt, pr)
+        sr = g["first_build"]["sample_rows"]
+        assert np.array_equal(im.im_get_register_rows(np.array(sr["vertices"], np.int32), cfg.J), np.array(sr["rows"], np.uint8))
+        assert sha(im.im_get_registers(n, cfg.J)) == g["first_build"]["registers_sha256"]
+    sampled_register_check(n, off, tgt, pr, cfg.J, cfg.salt_seed, 200, rng_seed=4)
+    s, sc = im.im_select_seeds(cfg.K, cfg.t)
+    assert len(set(s.tolist())) == cfg.K and all(np.diff(sc) >= 0)
+    sampled_seed_reach_check(n, off, tgt, pr, cfg.J, cfg.salt_seed, s, [5, 300])
+
+
+@pytest.mark.parametrize("J,p,t", [(64, 0.005, 0.01), (1024, 0.1, 0.3), (128, 0.01, 0.05), (512, 0.1, 0.01)])
+def test_c5_grid_points(J, p, t):
+    """C5 grid corners on the C3 graph (J x p x t, K = 100): sampled registers of the first build,
+    the selection's invariants and the per-simulation reach of its seeds (J = 1024 / p = 0.1 drives
+    128-simulation windows through the warp-cooperative paths)."""
+    n, off, tgt = cached_graph("cl4m")
+    pr = np.full(len(tgt), p, np.float32)
+    im.im_load_csr(n, off, tgt, pr)
+    im.im_build_sketches(J, 1)
+    sampled_register_check(n, off, tgt, pr, J, 1, 100, rng_seed=J)
+    s, sc = im.im_select_seeds(100, t)
+    assert len(set(s.tolist())) == 100 and all(np.diff(sc) >= 0)
+    sampled_seed_reach_check(n, off, tgt, pr, J, 1, s, [0, J - 1])

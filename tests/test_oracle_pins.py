@@ -239,8 +239,12 @@ def test_reach_register_and_seed_sigma_vs_bruteforce():
         assert np.array_equal(oracle.reach_register(n, off, tgt, pr, J, seed, us, js), R[us, js])
         seeds = rng.choice(n, min(n, 5), replace=False)
         cnt = oracle.seed_sigma(n, off, tgt, pr, J, seed, seeds)
+        sims = rng.choice(J, 4, replace=False)
+        per = oracle.seed_reach_per_sim(n, off, tgt, pr, J, seed, sims, seeds)
         for k in range(len(seeds)):
-            assert cnt[k] == brute.reach_masks(n, off, tgt, pr, J, seed, seeds[: k + 1]).sum()
+            vis = brute.reach_masks(n, off, tgt, pr, J, seed, seeds[: k + 1])
+            assert cnt[k] == vis.sum()
+            assert list(per[:, k]) == [int(vis[:, j].sum()) for j in sims]
 
 
 # ---------------------------------------------------------------- Alg. 1
