@@ -221,7 +221,7 @@ def main():
 
     for _ in range(args.warmup):
         step_device()
-    times, edges, wedges, sweep_ms, sweeps, launches_sweep, rebuilds, launches = [], [], [], [], [], [], [], []
+    times, edges, wedges, sweep_ms, sweeps, launches_sweep, rebuilds, launches, algb = [], [], [], [], [], [], [], [], []
     first_build = {}
     clocks = Clocks(int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[0]) if os.environ.get("CUDA_VISIBLE_DEVICES", "").strip().isdigit() else local)
     for i in range(args.steps):
@@ -238,6 +238,7 @@ def main():
         times.append(ev0.elapsed_time(ev1))
         edges.append(sb["total_edges"] + ss["total_edges"])
         wedges.append(sb["window_edges"] + ss["window_edges"])
+        algb.append(sb["sweep_alg_bytes"] + ss["sweep_alg_bytes"])
         sweep_ms.append(sb["sweep_kernel_ms"] + ss["sweep_kernel_ms"])
         sweeps.append(sb["total_sweeps"] + ss["total_sweeps"])
         launches_sweep.append(sb["sweep_launches"] + ss["sweep_launches"])
@@ -268,8 +269,7 @@ def main():
     work = statistics.mean(edges) * J  # edge x sim updates per step (deterministic count up to in-place order)
     value = world * work / (ms / 1e3) / 1e9
     hbm_peak, peak_kind, _ = load_peaks()
-    const_t = 1 if cfg.p is not None else 0
-    alg_bytes = statistics.mean(edges) * (8 + 4 * (1 - const_t)) + statistics.mean(wedges) * 32
+    alg_bytes = statistics.mean(algb)
     sweep_s = statistics.mean(sweep_ms) / 1e3
     achieved = alg_bytes / sweep_s / 1e9 if sweep_s > 0 else None
     roof = {"bound": "hbm", "kernel": "k_sweep (Simulate sweeps, all builds of the step)",
@@ -277,8 +277,9 @@ def main():
             "peak_kind": peak_kind, "traffic": None,
             "alg_bytes_per_step": alg_bytes, "sweep_kernel_ms_per_step": statistics.mean(sweep_ms),
             "sweep_share_of_step": statistics.mean(sweep_ms) / ms,
-            "unit_def": "per enumerated in-edge: 8 B record (+4 B threshold when w varies) + 32 B sector of the puller's "
-                        "register row when the edge's candidate window is non-empty after the change filter"}
+            "unit_def": "DESIGN.md section 6: per enumerated edge 8 B record (+4 B threshold when w varies) + one 32 B register "
+                        "sector per worked candidate window; + n*J row write (first sweep), + 2*n*J row read/write (gather sweeps), "
+                        "+ change masks"}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/u32",
             "data": "synthetic", "config": config_dict(cfg, n, m, args), "clocks": clk,

@@ -76,7 +76,8 @@ typedef struct {
     int32_t argmax_full;       /* full argmax passes in the last selection (exact lazy argmax) */
     int32_t argmax_lazy;       /* candidate-list argmax evaluations in the last selection */
     int32_t sorted_rows;       /* 1 if adjacency rows are sorted by edge hash (constant threshold) */
-    int32_t pad2;
+    int32_t gather_sweeps;     /* sweeps in the window run as full gathers (direction-optimised) */
+    double sweep_alg_bytes;    /* algorithmic bytes of all sweeps in the window */
 } im_stats;
 
 /*

@@ -44,7 +44,8 @@ class im_stats(ctypes.Structure):
         ("prep_ms", ctypes.c_double), ("last_build_ms", ctypes.c_double), ("last_select_ms", ctypes.c_double),
         ("sweep_kernel_ms", ctypes.c_double), ("sweep_launches", ctypes.c_int64), ("window_edges", ctypes.c_int64),
         ("kernel_launches", ctypes.c_int64),
-        ("argmax_full", ctypes.c_int32), ("argmax_lazy", ctypes.c_int32), ("sorted_rows", ctypes.c_int32), ("pad2", ctypes.c_int32),
+        ("argmax_full", ctypes.c_int32), ("argmax_lazy", ctypes.c_int32), ("sorted_rows", ctypes.c_int32), ("gather_sweeps", ctypes.c_int32),
+        ("sweep_alg_bytes", ctypes.c_double),
     ]
 
 

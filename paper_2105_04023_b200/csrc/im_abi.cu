@@ -334,6 +334,8 @@ int simulate(bool blocked) {
     int64_t edges = 0, wedges = 0, launches = 0;
     float kms = 0.f;
     int64_t edges_in = g.m;
+    double alg = 0.0;
+    int ngather = 0;
     const int4* items = g.ritems;
     int n_items = g.n_ritems;
     edges = g.m;
@@ -359,6 +361,14 @@ int simulate(bool blocked) {
         sweeps++;
         launches++;
         wedges += (int64_t)hc.win_edges;
+        {   // algorithmic bytes: records + one 32-B sector per worked window
+            const double nJ = (double)g.n * g.J, rec = 8.0 + (g.constT ? 0.0 : 4.0);
+            const double cmb = (double)g.n * ((double)g.J / 8.0 + 4.0);  // change mask + chunk word per vertex
+            if (s == 1) alg += rec * (double)g.m + nJ + cmb;               // + every row written once
+            else if (gather) alg += rec * (double)g.m + 2.0 * nJ + cmb + 32.0 * (double)hc.win_edges;
+            else alg += rec * (double)edges_in + 32.0 * (double)hc.win_edges;
+            if (gather) ngather++;
+        }
         if (g.trace)
             fprintf(stderr, "[im] sweep %d %s items %d edges %lld window_edges %llu -> changed %d next_items %d next_edges %llu big %d  %.3f ms\n",
                     s, s == 1 ? "init+gather" : gather ? "gather" : "push", n_items, (long long)(s == 1 || gather ? g.m : (int64_t)edges_in),
@@ -378,6 +388,8 @@ int simulate(bool blocked) {
     g.st.sweep_kernel_ms += kms;
     g.st.sweep_launches += launches;
     g.st.window_edges += wedges;
+    g.st.sweep_alg_bytes += alg;
+    g.st.gather_sweeps += ngather;
     g.st.last_build_ms = ms_since(t0);
     g.built = true;
     g.fresh = !blocked;
@@ -458,6 +470,8 @@ int im_build_sketches(int32_t J, uint64_t seed) {
     g.st.sweep_kernel_ms = 0;
     g.st.sweep_launches = 0;
     g.st.window_edges = 0;
+    g.st.sweep_alg_bytes = 0;
+    g.st.gather_sweeps = 0;
     int64_t l0 = g.launches;
     TRY(alloc_sketch_state(J));
     TRY(setup_salts(J, seed));
@@ -496,6 +510,8 @@ int im_select_seeds_ex(int32_t K, double eps_l, double eps_g, int32_t* out_seeds
     g.st.sweep_kernel_ms = 0;
     g.st.sweep_launches = 0;
     g.st.window_edges = 0;
+    g.st.sweep_alg_bytes = 0;
+    g.st.gather_sweeps = 0;
     g.st.rebuilds = 0;
     g.st.bfs_levels = 0;
     g.st.bfs_edges = 0;
