@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libim_b200.so")
+LIB_PATH = os.environ.get("IM_LIB") or os.path.join(_HERE, "libim_b200.so")  # IM_LIB: experiment builds
 
 IM_OK, IM_EINVAL, IM_ESTATE, IM_ENOMEM, IM_ECUDA = 0, -1, -2, -3, -4
 

@@ -103,6 +103,7 @@ int ensure_device() {
     int bs = 0, bb = 0;
     CK((cudaError_t)occupancy_sweep(&bs));
     CK((cudaError_t)occupancy_bfs(&bb));
+    CK((cudaError_t)setup_argmax_tma());
 
     g.max_blocks_sweep = std::max(1, bs) * g.num_sms;
     g.max_blocks_bfs = std::max(1, bb) * g.num_sms;
@@ -263,8 +264,8 @@ int alloc_sketch_state(int32_t J) {
     TRY(dalloc(g.Xs, (size_t)J));
     TRY(dalloc(g.s12, 4097));
     TRY(dalloc(g.permd, (size_t)J));
-    TRY(dalloc(g.M, n * (size_t)J));
-    TRY(dalloc(g.vis, n * W));
+    TRY(dalloc(g.M, n * (size_t)J + 65536));  // + tail padding read by the TMA argmax tiles
+    TRY(dalloc(g.vis, n * W + 16384));
     for (int i = 0; i < 2; i++) {
         TRY(dalloc(g.items[i], (size_t)g.n_ritems + 4 * n + 1));  // slices add <= 3 partial segments per vertex
         // a completed build leaves the change buffers zero; fresh ones are cleared by simulate()

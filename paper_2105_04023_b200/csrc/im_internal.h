@@ -159,6 +159,8 @@ cudaError_t launch_sweep(Ctx& c, const int4* items, int n_items, const uint32_t*
                          IterCounters* ctr, bool blocked);
 cudaError_t launch_estimate(Ctx& c, double* out);
 cudaError_t launch_argmax_full(Ctx& c, bool pool, int T);
+cudaError_t launch_argmax_tma(Ctx& c, bool pool, int L, int C, int shift);
+int setup_argmax_tma();
 cudaError_t launch_argmax_list(Ctx& c, int list_len);
 cudaError_t launch_seed_start(Ctx& c, int k);
 // one BFS level from frontier buffer cur (items, Delta) into cur^1, plus the compaction that builds

@@ -37,9 +37,14 @@ __global__ void k_estimate(int32_t n, int32_t J, const uint32_t* __restrict__ M3
 // result is exact whenever its best current gain is >= theta (every vertex outside the list has
 // current gain <= stored gain < theta).  Otherwise the host runs a new full pass.
 // A row is read as 16-byte chunks by L lanes, 32/L vertices per warp, two groups in flight.
-__device__ __forceinline__ uint32_t gain16(uint4 x, uint4 m) {
-    return __vsadu4(__vsubus4(x.x, m.x), 0u) + __vsadu4(__vsubus4(x.y, m.y), 0u) + __vsadu4(__vsubus4(x.z, m.z), 0u) +
-           __vsadu4(__vsubus4(x.w, m.w), 0u);
+// 2 * sum (x - m)^+ = sum |x - m| + sum x - sum m over the 16 bytes; the |.| sums are single
+// VABSDIFF4 instructions.  The caller subtracts sum m (a per-lane constant) and halves at the end.
+__device__ __forceinline__ uint32_t gain16x2(uint4 x, uint4 m) {
+    return __vsadu4(x.x, m.x) + __vsadu4(x.y, m.y) + __vsadu4(x.z, m.z) + __vsadu4(x.w, m.w) + __vsadu4(x.x, 0u) +
+           __vsadu4(x.y, 0u) + __vsadu4(x.z, 0u) + __vsadu4(x.w, 0u);
+}
+__device__ __forceinline__ uint32_t sum16(uint4 m) {
+    return __vsadu4(m.x, 0u) + __vsadu4(m.y, 0u) + __vsadu4(m.z, 0u) + __vsadu4(m.w, 0u);
 }
 
 constexpr int HIST_BINS = 4096;
@@ -62,10 +67,12 @@ __global__ void __launch_bounds__(BLOCK) k_argmax(int32_t n, int32_t J, int L, i
     const int nv = LIST ? *list_count : n;
     const int lane = threadIdx.x & 31, q = lane & (L - 1), sub = lane / L, VPW = 32 / L;
     uint4 ms[2];
+    uint32_t msum = 0;  // sum of this lane's M_S' bytes (only over chunks the lane actually loads)
 #pragma unroll
     for (int c = 0; c < 2; c++) {
         int ci = q * C + c;
         ms[c] = (c < C && ci < nch) ? sMS[ci] : make_uint4(0, 0, 0, 0);
+        msum += sum16(ms[c]);
     }
     const int64_t groups = ((int64_t)nv + VPW - 1) / VPW;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -88,7 +95,7 @@ __global__ void __launch_bounds__(BLOCK) k_argmax(int32_t n, int32_t J, int L, i
         }
 #pragma unroll
         for (int u = 0; u < AG; u++) {
-            uint32_t gn = gain16(x[u][0], ms[0]) + gain16(x[u][1], ms[1]);
+            uint32_t gn = gain16x2(x[u][0], ms[0]) + gain16x2(x[u][1], ms[1]) - msum;
             int full = 1;
             if (POOL && ok[u])
                 for (int w = q; w < W; w += L) full &= __ldcs(&vis[vv[u] * W + w]) == IM_FULL;
@@ -96,6 +103,7 @@ __global__ void __launch_bounds__(BLOCK) k_argmax(int32_t n, int32_t J, int L, i
                 gn += __shfl_xor_sync(IM_FULL, gn, o);
                 if (POOL) full &= __shfl_xor_sync(IM_FULL, full, o);
             }
+            gn >>= 1;
             bool inpool = ok[u] && (!POOL || !full);
             if (ok[u] && q == 0) {
                 if (inpool) {
@@ -494,11 +502,7 @@ cudaError_t launch_argmax_full(Ctx& c, bool pool, int T) {
     if (!e) e = cudaMemsetAsync(c.hist, 0, HIST_BINS * sizeof(uint32_t), c.stream);
     if (!e) e = cudaMemsetAsync(c.lcount, 0, 2 * sizeof(int), c.stream);
     if (e) return e;
-    int g = grid_for(c, (int64_t)c.n * L / 2);
-    const uint4* M16 = reinterpret_cast<const uint4*>(c.M);
-    if (pool) k_argmax<true, false><<<g, BLOCK, 0, c.stream>>>(c.n, c.J, L, C, M16, c.MS, c.vis, c.key, c.gain, c.hist, sh, nullptr, nullptr);
-    else k_argmax<false, false><<<g, BLOCK, 0, c.stream>>>(c.n, c.J, L, C, M16, c.MS, c.vis, c.key, c.gain, c.hist, sh, nullptr, nullptr);
-    if ((e = LAUNCHED(c))) return e;
+    if ((e = launch_argmax_tma(c, pool, L, C, sh))) return e;  // TMA-bulk streaming pass (im_stream.cu)
     k_theta<<<1, 32, 0, c.stream>>>(c.hist, sh, T, c.lcount + 1);
     if ((e = LAUNCHED(c))) return e;
     k_list_build<<<grid_for(c, c.n), BLOCK, 0, c.stream>>>(c.n, c.gain, c.lcount + 1, c.list, c.lcount);

@@ -18,6 +18,9 @@
 #include "im_internal.h"
 
 namespace im {
+#ifndef IM_NS
+#define IM_NS 2
+#endif
 
 struct SweepArgs {
     const int4* items;
@@ -108,7 +111,7 @@ __device__ __forceinline__ bool window_changed(const uint32_t* __restrict__ cm, 
     return false;
 }
 
-constexpr int NS = 2;  // edges in flight per lane
+constexpr int NS = IM_NS;  // edges in flight per lane
 
 template <bool CONST_T, bool BLOCKED, bool FILTER>
 __global__ void __launch_bounds__(BLOCK, 4) k_sweep(SweepArgs a) {
