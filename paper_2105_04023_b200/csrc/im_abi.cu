@@ -347,8 +347,12 @@ int simulate(bool blocked) {
         // direction-optimised: a frontier whose in-edges cover most of the graph is swept by a full
         // in-place gather (every row owned by one warp, no atomics); sparse frontiers are pushed
         const bool gather = s > 1 && (double)edges_in > g.pull_frac * (double)g.m;
-        if (s == 1)  // register init fused with the first sweep (every row written)
+        if (s == 1) {  // streaming register init, then the first sweep as a gather from init values
+            CK(launch_init_registers(g));
+            CK(cudaMemsetAsync(g.cm[1], 0, (size_t)g.n * W * sizeof(uint32_t), g.stream));
+            CK(cudaMemsetAsync(g.bits[1], 0, (size_t)g.n * sizeof(uint32_t), g.stream));
             CK(launch_first(g, g.cm[1], g.bits[1], ctr, blocked, false));
+        }
         else if (gather)
             CK(launch_first(g, g.cm[s & 1], g.bits[s & 1], ctr, blocked, true));
         else

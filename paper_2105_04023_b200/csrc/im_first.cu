@@ -81,14 +81,30 @@ __device__ __forceinline__ void merge_word(const FirstArgs& a, const uint32_t* s
 // `e` is this lane's edge (or -1); the loop around it must be warp-uniform.  Windows wider than
 // DENSE_WIN simulations (w close to 1) are walked by the whole warp, one word per lane.
 template <bool CONST_T, bool BLOCKED, bool MEM>
+__device__ __forceinline__ void gather_rec(const FirstArgs& a, const uint32_t* sX, const uint16_t* sS, const uint32_t* sHJ,
+                                           const uint32_t* sVis, uint32_t* row, bool have, uint2 f, uint32_t Tin, uint32_t& wcount);
+
+template <bool CONST_T, bool BLOCKED, bool MEM>
 __device__ __forceinline__ void gather_edge(const FirstArgs& a, const uint32_t* sX, const uint16_t* sS, const uint32_t* sHJ,
                                             const uint32_t* sVis, uint32_t* row, int e, uint32_t& wcount) {
+    uint2 f = make_uint2(0, 0);
+    uint32_t T = 0;
+    if (e >= 0) {
+        f = a.fwd[e];
+        T = CONST_T ? a.T0 : a.fwdT[e];
+    }
+    gather_rec<CONST_T, BLOCKED, MEM>(a, sX, sS, sHJ, sVis, row, e >= 0, f, T, wcount);
+}
+
+// the edge's record is already loaded (prefetched by the caller)
+template <bool CONST_T, bool BLOCKED, bool MEM>
+__device__ __forceinline__ void gather_rec(const FirstArgs& a, const uint32_t* sX, const uint16_t* sS, const uint32_t* sHJ,
+                                           const uint32_t* sVis, uint32_t* row, bool have, uint2 f, uint32_t Tin, uint32_t& wcount) {
     const int lane = threadIdx.x & 31;
     uint32_t h = 0, T = 0, hv = 0, v = 0;
     int lo = 0, hi = 0;
-    if (e >= 0) {
-        uint2 f = a.fwd[e];
-        T = CONST_T ? a.T0 : a.fwdT[e];
+    if (have) {
+        T = Tin;
         h = f.y;
         v = f.x;
         if (T) {
@@ -121,14 +137,64 @@ __device__ __forceinline__ uint32_t start_word(const FirstArgs& a, const uint32_
     return MEM ? reinterpret_cast<const uint32_t*>(a.M)[(size_t)u * (a.J >> 2) + w] : init_word(hu, sHJ, w);
 }
 
-// final smem word vs its start value: write it back if it rose (always for the first sweep, which
-// also writes the init registers) and return the 4 change bits (one per simulation) of word w
+// final smem word vs its start value: write it back if it rose (the first sweep runs after
+// k_init_registers wrote every row) and return the 4 change bits (one per simulation) of word w
 __device__ __forceinline__ uint32_t finish_word(const FirstArgs& a, const uint32_t* row, uint32_t u, int w, uint32_t old,
                                                 bool always_write) {
     uint32_t x = row[w];
     if (always_write || x != old) reinterpret_cast<uint32_t*>(a.M)[(size_t)u * (a.J >> 2) + w] = x;
     uint32_t eq = __vcmpeq4(x, old);
     return ((((~eq) & 0x01010101u) * 0x00204081u) >> 21) & 0xFu;
+}
+
+
+// A vertex with at most 32 out-edges: one edge per lane, and only the row words inside the edges'
+// candidate windows are touched (marked in a per-warp bitmap, started from init / current values,
+// merged, then compared and written back) instead of the whole J-register row.
+template <bool CONST_T, bool BLOCKED, bool MEM>
+__device__ __forceinline__ void first_small(const FirstArgs& a, const uint32_t* sX, const uint16_t* sS, const uint32_t* sHJ,
+                                            const uint32_t* sVis, uint32_t* row, uint32_t* bm, uint32_t u, bool have, uint2 f,
+                                            uint32_t Tin, uint32_t& wcount) {
+    const int lane = threadIdx.x & 31, J = a.J, W = J >> 5, NW = J >> 2, NB = (NW + 31) >> 5;
+    uint32_t h = 0, T = 0, hv = 0, v = 0;
+    int lo = 0, hi = 0;
+    if (have && Tin) {
+        T = Tin;
+        h = f.y;
+        v = f.x;
+        edge_window(h, T, sX, sS, J, lo, hi);
+        if (lo < hi) {
+            wcount++;
+            if (!MEM) hv = murmur_word(v, a.seedV);
+        }
+    }
+    const uint32_t hu = MEM ? 0u : murmur_word(u, a.seedV);
+    if (lane < NB) bm[lane] = 0u;
+    __syncwarp();
+    const int w0 = lo >> 2, w1 = lo < hi ? (hi - 1) >> 2 : w0 - 1;
+    for (int w = w0; w <= w1; ++w) atomicOr(&bm[w >> 5], 1u << (w & 31));
+    for (int w = w0; w <= w1; ++w) row[w] = start_word<MEM>(a, sHJ, hu, u, w);  // same value from every writer
+    __syncwarp();
+    for (int w = w0; w <= w1; ++w) merge_word<BLOCKED, MEM>(a, sX, sHJ, sVis, row, v, hv, h, T, lo, hi, w);
+    __syncwarp();
+    uint32_t chunks = 0;
+    for (int k = 0; k < NB; k++) {
+        const uint32_t m = bm[k];
+        if (!m) continue;  // warp-uniform
+        const int w = 32 * k + lane;
+        uint32_t nib = 0;
+        if ((m >> lane) & 1u) nib = finish_word(a, row, u, w, start_word<MEM>(a, sHJ, hu, u, w), false);
+        uint32_t x = nib << ((lane & 7) << 2);
+        x |= __shfl_xor_sync(IM_FULL, x, 1);
+        x |= __shfl_xor_sync(IM_FULL, x, 2);
+        x |= __shfl_xor_sync(IM_FULL, x, 4);
+        if ((lane & 7) == 0 && w < NW && x) a.cm_out[(size_t)u * W + (w >> 3)] = x;  // the buffer starts zeroed
+        const uint32_t bl = __ballot_sync(IM_FULL, (lane & 7) == 0 && x != 0u);
+#pragma unroll
+        for (int c = 0; c < 4; c++) chunks |= ((bl >> (8 * c)) & 1u) << (4 * k + c);
+    }
+    if (lane == 0 && chunks) a.bits_out[u] = chunks;
+    __syncwarp();
 }
 
 template <bool CONST_T, bool BLOCKED, bool MEM>
@@ -139,6 +205,8 @@ __global__ void __launch_bounds__(BLOCK) k_first(FirstArgs a) {
     __shared__ uint32_t sRow[BLOCK / 32][256];
     __shared__ uint32_t sOldRow[BLOCK / 32][256];
     __shared__ uint32_t sVis[BLOCK / 32][32];
+    __shared__ int sOff[BLOCK / 32][258];
+    __shared__ uint32_t sBm[BLOCK / 32][8];
     const int J = a.J, W = J >> 5, NW = J >> 2;
     for (int i = threadIdx.x; i < J; i += blockDim.x) {
         sX[i] = a.Xs[i];
@@ -150,18 +218,51 @@ __global__ void __launch_bounds__(BLOCK) k_first(FirstArgs a) {
     uint32_t* row = sRow[wib];
     uint32_t* old = sOldRow[wib];
     uint32_t wcount = 0;
+    int* off_w = sOff[wib];
     for (;;) {
         int base = 0;
         if (lane == 0) base = atomicAdd(&a.ctr->batch, 256);
         base = __shfl_sync(IM_FULL, base, 0);
         if (base >= a.n) break;
         const int end = min(base + 256, a.n);
+        for (int i = lane; i <= end - base; i += 32) off_w[i] = a.off[base + i];  // the batch's offsets, one coalesced read
+        __syncwarp();
+        // first 32 records of the next vertex are prefetched while the current one is processed
+        uint2 nf = make_uint2(0, 0);
+        uint32_t nT = 0;
+        {
+            const int eb0 = off_w[0], ee0 = off_w[1];
+            if (ee0 - eb0 <= FIRST_BIG && eb0 + lane < ee0) {
+                nf = a.fwd[eb0 + lane];
+                nT = CONST_T ? a.T0 : a.fwdT[eb0 + lane];
+            }
+        }
         for (int u = base; u < end; ++u) {
-            const int eb = a.off[u], ee = a.off[u + 1];
+            const int eb = off_w[u - base], ee = off_w[u - base + 1];
+            const uint2 cf = nf;
+            const uint32_t cT = nT;
+            nf = make_uint2(0, 0);
+            nT = 0;
+            if (u + 1 < end) {
+                const int eb1 = off_w[u + 1 - base], ee1 = off_w[u + 2 - base];
+                if (ee1 - eb1 <= FIRST_BIG && eb1 + lane < ee1) {
+                    nf = a.fwd[eb1 + lane];
+                    nT = CONST_T ? a.T0 : a.fwdT[eb1 + lane];
+                }
+            }
             if (ee - eb > FIRST_BIG) continue;  // done by k_first_big
-            if (MEM && ee == eb) {             // nothing to pull: the row cannot change
-                if (lane < W) a.cm_out[(size_t)u * W + lane] = 0u;
-                if (lane == 0) a.bits_out[u] = 0u;
+            if (ee == eb) {  // no out-edge: the row keeps its value (init rows and zeroed masks are written before)
+                if (MEM) {
+                    if (lane < W) a.cm_out[(size_t)u * W + lane] = 0u;
+                    if (lane == 0) a.bits_out[u] = 0u;
+                }
+                continue;
+            }
+            if (ee - eb <= 32) {  // sparse path: touch only the window words
+                if (BLOCKED && lane < W) sVis[wib][lane] = a.vis[(size_t)u * W + lane];
+                __syncwarp();
+                first_small<CONST_T, BLOCKED, MEM>(a, sX, sS, sHJ, sVis[wib], row, sBm[wib], (uint32_t)u, eb + lane < ee, cf, cT,
+                                                   wcount);
                 continue;
             }
             const uint32_t hu = MEM ? 0u : murmur_word((uint32_t)u, a.seedV);
@@ -172,7 +273,8 @@ __global__ void __launch_bounds__(BLOCK) k_first(FirstArgs a) {
             }
             if (BLOCKED && lane < W) sVis[wib][lane] = a.vis[(size_t)u * W + lane];
             __syncwarp();
-            for (int e0 = eb; e0 < ee; e0 += 32)
+            if (eb < ee) gather_rec<CONST_T, BLOCKED, MEM>(a, sX, sS, sHJ, sVis[wib], row, eb + lane < ee, cf, cT, wcount);
+            for (int e0 = eb + 32; e0 < ee; e0 += 32)
                 gather_edge<CONST_T, BLOCKED, MEM>(a, sX, sS, sHJ, sVis[wib], row, e0 + lane < ee ? e0 + lane : -1, wcount);
             __syncwarp();
             uint32_t chunks = 0;
@@ -180,7 +282,7 @@ __global__ void __launch_bounds__(BLOCK) k_first(FirstArgs a) {
             for (int k = 0; k < FW; k++) {
                 if (32 * k < NW) {  // warp-uniform
                     const int w = lane + 32 * k;
-                    uint32_t nib = w < NW ? finish_word(a, row, (uint32_t)u, w, old[w], !MEM) : 0u;
+                    uint32_t nib = w < NW ? finish_word(a, row, (uint32_t)u, w, old[w], false) : 0u;
                     // change-mask word (w >> 3) = 4k + lane/8 from the nibbles of 8 consecutive lanes
                     uint32_t x = nib << ((lane & 7) << 2);
                     x |= __shfl_xor_sync(IM_FULL, x, 1);
@@ -236,7 +338,7 @@ __global__ void __launch_bounds__(BLOCK) k_first_big(FirstArgs a) {
             gather_edge<CONST_T, BLOCKED, MEM>(a, sX, sS, sHJ, sVis, row, e0 + (threadIdx.x & 31) < ee ? e0 + (threadIdx.x & 31) : -1, wcount);
         __syncthreads();
         for (int w = threadIdx.x; w < NW; w += blockDim.x) {
-            uint32_t nib = finish_word(a, row, u, w, sOld[w], !MEM);
+            uint32_t nib = finish_word(a, row, u, w, sOld[w], false);
             if (nib) atomicOr(&sMask[w >> 3], nib << ((w & 7) << 2));
         }
         __syncthreads();

@@ -112,22 +112,34 @@ __global__ void k_fill_items(int32_t n, const int32_t* __restrict__ offs, const 
 
 // ------------------------------------------------------------------ a2: register init
 // M_v[jj] = clz(Murmur3(v, seed_V) xor Murmur3(perm[jj], seed_J)), clz(0) = 32 (Alg. 1 lines 2-5; R5, R6).
-// One thread per 4-register word; hash(j) of the 4 simulations is read as one 16-byte shared load.
+// One thread per 16 bytes (16 simulations) of a row: one Murmur3 per thread, one 16-byte store.
+// hash(j) is kept in shared memory transposed by word (HJ4T[q][c] = sims 16c+4q .. 16c+4q+3) so the
+// 16-byte shared loads of consecutive lanes are conflict-free.
 __global__ void k_init_registers(int32_t n, int32_t J, uint32_t seedV, uint32_t seedJ, const int32_t* __restrict__ perm,
-                                 uint32_t* __restrict__ M32) {
-    __shared__ uint4 HJ4[256];
-    uint32_t* HJ = reinterpret_cast<uint32_t*>(HJ4);
-    for (int j = threadIdx.x; j < J; j += blockDim.x) HJ[j] = murmur_word((uint32_t)perm[j], seedJ);
+                                 uint4* __restrict__ M16) {
+    __shared__ uint4 HJ4T[256];
+    const int cpr = J >> 4;  // 16-byte chunks per row
+    for (int c = threadIdx.x; c < cpr; c += blockDim.x)
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const int j0 = 16 * c + 4 * q;
+            HJ4T[q * cpr + c] = make_uint4(murmur_word((uint32_t)perm[j0], seedJ), murmur_word((uint32_t)perm[j0 + 1], seedJ),
+                                           murmur_word((uint32_t)perm[j0 + 2], seedJ), murmur_word((uint32_t)perm[j0 + 3], seedJ));
+        }
     __syncthreads();
-    const int wpr = J >> 2;  // words per row
-    const int64_t total = (int64_t)n * wpr, stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t total = (int64_t)n * cpr, stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += stride) {
-        uint32_t v = (uint32_t)(idx / wpr);
-        int w = (int)(idx - (int64_t)v * wpr);
-        uint32_t hv = murmur_word(v, seedV);
-        uint4 hj = HJ4[w];
-        M32[idx] = (uint32_t)__clz(hv ^ hj.x) | ((uint32_t)__clz(hv ^ hj.y) << 8) | ((uint32_t)__clz(hv ^ hj.z) << 16) |
-                   ((uint32_t)__clz(hv ^ hj.w) << 24);
+        const uint32_t v = (uint32_t)(idx / cpr);
+        const int c = (int)(idx - (int64_t)v * cpr);
+        const uint32_t hv = murmur_word(v, seedV);
+        uint32_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const uint4 h = HJ4T[q * cpr + c];
+            w[q] = (uint32_t)__clz(hv ^ h.x) | ((uint32_t)__clz(hv ^ h.y) << 8) | ((uint32_t)__clz(hv ^ h.z) << 16) |
+                   ((uint32_t)__clz(hv ^ h.w) << 24);
+        }
+        M16[idx] = make_uint4(w[0], w[1], w[2], w[3]);
     }
 }
 
@@ -159,9 +171,9 @@ cudaError_t launch_build_items(Ctx& c, const int32_t* offs, int4* items, int32_t
     return e;
 }
 cudaError_t launch_init_registers(Ctx& c) {
-    int64_t words = (int64_t)c.n * (c.J >> 2);
-    k_init_registers<<<grid_for(c, words), BLOCK, 0, c.stream>>>(c.n, c.J, c.seedV, c.seedJ, c.permd,
-                                                                 reinterpret_cast<uint32_t*>(c.M));
+    int64_t chunks = (int64_t)c.n * (c.J >> 4);
+    k_init_registers<<<grid_for(c, chunks), BLOCK, 0, c.stream>>>(c.n, c.J, c.seedV, c.seedJ, c.permd,
+                                                                  reinterpret_cast<uint4*>(c.M));
     return LAUNCHED(c);
 }
 
