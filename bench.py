@@ -16,7 +16,12 @@ roofline : the sweep kernel (dominant), algorithmic bytes
 cpu_baseline : the oracle (oracle/, plain single-threaded C) on a bounded sample of the same
         workload: the first Alg. 2 sweep over a vertex range, on the host.
 
-    python bench.py [--config c4] [--steps 3] [--warmup 3] [--gpus N] [--impl ours|reference]
+multi-GPU (torchrun, N > 1): --mode shard (default) splits the J simulations of the one job over
+        the ranks (im_build_sketches_shard + an NCCL allreduce hook at the three
+        exchange points of each greedy step; strong scaling, value = all ranks' updates / max time);
+        --mode replicas runs N independent copies of the job (weak scaling).
+
+    python bench.py [--config c4] [--steps 3] [--warmup 3] [--gpus N] [--impl ours|reference] [--mode shard|replicas]
 """
 from __future__ import annotations
 
@@ -138,7 +143,8 @@ def run_reference(args, rank):
 def config_dict(cfg, n, m, args):
     return {"workload": f"{cfg.name}: {cfg.note}", "n": int(n), "m": int(m), "J": cfg.J, "K": cfg.K, "t": cfg.t,
             "p": cfg.p if cfg.p is not None else "weighted-cascade 1/indeg", "salt_seed": cfg.salt_seed,
-            "parallelism": "replicas" if args.gpus > 1 else "single-gpu",
+            "parallelism": (f"simulation-sharded x{args.gpus} (NCCL allreduce hook)" if args.mode == "shard" else f"replicas x{args.gpus}")
+            if args.gpus > 1 else "single-gpu",
             "l2": "inputs (CSR+hash records) larger than L2" if m * 16 > 126e6 else "L2 flushed (256 MB write) between steps"}
 
 
@@ -152,8 +158,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--mode", default="shard", choices=["shard", "replicas"])
     args = ap.parse_args()
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    args.gpus = world if world > 1 else args.gpus
     if args.impl == "reference":
         return run_reference(args, rank)
 
@@ -161,12 +169,19 @@ def main():
 
     import paper_2105_04023_b200 as im
 
+    # IM_BENCH_BACKEND=gloo: plumbing check of the sharded path with several ranks on one GPU (the
+    # ranks then only wait for each other on the host); the measured configuration is NCCL
+    backend = os.environ.get("IM_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     cfg = gen.CONFIGS[args.config]
     t0 = time.time()
     n, off, tgt, pr = gen.workload(cfg)
@@ -175,6 +190,17 @@ def main():
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
     im.im_set_stream(stream)
+    shard = dist is not None and args.mode == "shard"
+    if shard:
+        from paper_2105_04023_b200.shard import shard_range, torch_allreduce_hook
+
+        j0, j1 = shard_range(cfg.J, rank, world)
+        im.im_set_allreduce(torch_allreduce_hook())
+    else:
+        j0, j1 = 0, cfg.J
+
+    def build():
+        im.im_build_sketches_shard(cfg.J, cfg.salt_seed, j0, j1)
     d_off = torch.from_numpy(off).to(dev)
     d_tgt = torch.from_numpy(tgt).to(dev)
     d_pr = torch.from_numpy(pr).to(dev)
@@ -198,7 +224,7 @@ def main():
         t = time.perf_counter()
         im.im_load_csr_device(n, m, d_off, d_tgt, d_pr)
         t1 = time.perf_counter()
-        im.im_build_sketches(cfg.J, cfg.salt_seed)
+        build()
         sb = im.im_get_stats()
         t2 = time.perf_counter()
         im.im_estimate_device(d_est)
@@ -212,7 +238,7 @@ def main():
 
     def step_e2e():
         im.lib().im_load_csr(n, h_off.data_ptr(), h_tgt.data_ptr(), h_pr.data_ptr())
-        im.im_build_sketches(cfg.J, cfg.salt_seed)
+        build()
         sb = im.im_get_stats()
         im.lib().im_estimate(h_est.data_ptr())
         im.im_select_seeds_into(cfg.K, cfg.t, h_seeds.numpy(), h_scores.numpy())
@@ -262,12 +288,20 @@ def main():
     if dist is not None:
         tt = torch.tensor([ms, statistics.mean(e2e_times) if e2e_times else 0.0], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms, e2e_ms = float(tt[0]), float(tt[1])
+        ms, e2e_ms = float(tt[0]), (float(tt[1]) if e2e_times else None)
     else:
         e2e_ms = statistics.mean(e2e_times) if e2e_times else None
     J = cfg.J
-    work = statistics.mean(edges) * J  # edge x sim updates per step (deterministic count up to in-place order)
-    value = world * work / (ms / 1e3) / 1e9
+    work = statistics.mean(edges) * (j1 - j0)  # this rank's edge x sim updates per step
+    if dist is None:
+        total_work = work
+    elif shard:
+        tw = torch.tensor([work], device=dev, dtype=torch.float64)
+        dist.all_reduce(tw)
+        total_work = float(tw[0])
+    else:
+        total_work = world * work
+    value = total_work / (ms / 1e3) / 1e9
     hbm_peak, peak_kind, _ = load_peaks()
     alg_bytes = statistics.mean(algb)
     sweep_s = statistics.mean(sweep_ms) / 1e3
@@ -281,21 +315,21 @@ def main():
                         "sector per worked candidate window; + n*J row write (first sweep), + 2*n*J row read/write (gather sweeps), "
                         "+ change masks"}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/u32",
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong" if shard else "weak", "vs_baseline": None, "dtype": "u8/u32",
             "data": "synthetic", "config": config_dict(cfg, n, m, args), "clocks": clk,
             "gpu_launches": int(statistics.mean(launches)), "roofline": roof,
             "im_time_s": ms / 1e3,
             "sketch_build": {"first_build_ms": first_build.get("ms"), "first_build_sweeps": first_build.get("sweeps"),
-                             "first_build_gedge_sims_per_s": first_build.get("edges", 0) * J / max(first_build.get("sweep_kernel_ms", 1e-9), 1e-9) / 1e6,
+                             "first_build_gedge_sims_per_s": first_build.get("edges", 0) * (j1 - j0) / max(first_build.get("sweep_kernel_ms", 1e-9), 1e-9) / 1e6,
                              "prep_ms": first_build.get("prep_ms"), "sweeps_per_step": statistics.mean(sweeps),
                              "sweep_launches_per_step": statistics.mean(launches_sweep), "rebuilds_per_step": statistics.mean(rebuilds)},
             "phase_ms": {k: statistics.mean(v[-args.steps:]) for k, v in phase_ms.items()}, "step_ms_all": times,
             "bfs": {"levels": ss["bfs_levels"], "edges": ss["bfs_edges"]},
             "argmax": {"full_passes": ss["argmax_full"], "lazy_passes": ss["argmax_lazy"], "sorted_rows": ss["sorted_rows"]},
             "seeds_head": [int(x) for x in seeds[:5]], "sigma_final": float(scores[-1]) if len(scores) else None,
-            "gen_seconds": gen_s}
+            "gen_seconds": gen_s, "sims_per_rank": j1 - j0}
     if e2e_ms is not None:
-        line["e2e"] = {"value": world * work / (e2e_ms / 1e3) / 1e9, "unit": UNIT,
+        line["e2e"] = {"value": total_work / (e2e_ms / 1e3) / 1e9, "unit": UNIT,
                        "h2d_bytes_per_step": int((n + 1) * 4 + m * 8), "d2h_bytes_per_step": int(n * 8 + cfg.K * 12),
                        "ms_per_step": e2e_ms}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -36,6 +36,11 @@ extern "C" {
 #define IM_ESTATE (-2) /* wrong call order (e.g. im_estimate before im_build_sketches) */
 #define IM_ENOMEM (-3) /* device or host allocation failed */
 #define IM_ECUDA (-4)  /* CUDA error, or no sm_100 device */
+#define IM_ECOMM (-5)  /* the allreduce hook (im_set_allreduce) returned non-zero */
+
+#define IM_DTYPE_I32 0 /* allreduce element types */
+#define IM_DTYPE_I64 1
+#define IM_MAX_J_TOTAL 65536 /* simulations of one (possibly sharded) job */
 
 /* One greedy step of Alg. 1. */
 typedef struct {
@@ -78,6 +83,8 @@ typedef struct {
     int32_t sorted_rows;       /* 1 if adjacency rows are sorted by edge hash (constant threshold) */
     int32_t gather_sweeps;     /* sweeps in the window run as full gathers (direction-optimised) */
     double sweep_alg_bytes;    /* algorithmic bytes of all sweeps in the window */
+    int32_t J_total;           /* simulations of the whole job (== J unless sharded) */
+    int32_t j0;                /* global index of this context's first simulation (0 unless sharded) */
 } im_stats;
 
 /*
@@ -105,6 +112,41 @@ int im_load_csr_device(int32_t n, int64_t m, const int32_t *d_offsets, const int
  * Requires a loaded graph (IM_ESTATE otherwise).
  */
 int im_build_sketches(int32_t J, uint64_t seed);
+
+/*
+ * Simulation sharding.  The J simulations of
+ * Alg. 1 are independent samples (simulation j only reads salt
+ * X_j and the hash of j), so a job of J_total simulations can be split over ranks (one
+ * process and one GPU each), rank r holding simulations [j0, j1).  Every rank loads the
+ * same graph, calls im_set_allreduce with a hook over all ranks, then
+ * im_build_sketches_shard with its range; im_estimate and im_select_seeds* are then
+ * collective calls that every rank must make with the same arguments, and all ranks
+ * return the same seeds, scores, step log and estimates as one unsharded context with
+ * J = J_total would.  Per-rank outputs (im_get_registers / rows / reach) cover the
+ * rank's own simulations, columns j - j0.
+ *
+ * Exchanged per greedy step (all in-place SUMs): the packed per-vertex argmax values
+ * (gain + (not fully visited) << 24, n int32 for a full pass, list-length int32 for a
+ * lazy one), the integer score of the chosen vertex (1 int64) and the sigma count
+ * (1 int64); im_estimate exchanges n int32 register sums.
+ *
+ * J_total  : multiple of 32 in [32, IM_MAX_J_TOTAL]; salts X_0..X_{J_total-1} are drawn
+ *            as in im_build_sketches(J_total, seed) and this context keeps [j0, j1).
+ * j0, j1   : 0 <= j0 < j1 <= J_total, j1 - j0 a multiple of 32 in [32, 1024].
+ * im_build_sketches(J, seed) == im_build_sketches_shard(J, seed, 0, J).
+ */
+int im_build_sketches_shard(int32_t J_total, uint64_t seed, int32_t j0, int32_t j1);
+
+/*
+ * Allreduce hook of a sharded job: fn(buf, count, dtype, user) must replace the
+ * `count` elements (IM_DTYPE_I32 / IM_DTYPE_I64) at DEVICE pointer buf (on the
+ * library's device) by their sum over all ranks and return 0 once the result is in
+ * buf.  The library's stream is synchronised before each call.  Non-zero -> IM_ECOMM.
+ * fn = NULL (the default) turns sharding off: single-context behaviour, no calls.
+ * A sharded context must run with the hook set during im_estimate / im_select_seeds*.
+ */
+typedef int (*im_allreduce_fn)(void *buf, int64_t count, int32_t dtype, void *user);
+int im_set_allreduce(im_allreduce_fn fn, void *user);
 
 /* e_v = 2^{mean_j M_v[j]} / 0.77351 for every vertex (Eq. 2, R8).  out: HOST double[n]. */
 int im_estimate(double *out);
@@ -141,7 +183,7 @@ int im_set_stream(void *cuda_stream);
 int64_t im_kernel_launch_count(void);
 void im_free(void);
 const char *im_last_error(void);
-/* ABI version (major*100 + minor) */
+/* ABI version (major*100 + minor): 101 adds sharding (im_build_sketches_shard, im_set_allreduce) */
 int32_t im_version(void);
 
 #ifdef __cplusplus

@@ -45,7 +45,7 @@ class im_stats(ctypes.Structure):
         ("sweep_kernel_ms", ctypes.c_double), ("sweep_launches", ctypes.c_int64), ("window_edges", ctypes.c_int64),
         ("kernel_launches", ctypes.c_int64),
         ("argmax_full", ctypes.c_int32), ("argmax_lazy", ctypes.c_int32), ("sorted_rows", ctypes.c_int32), ("gather_sweeps", ctypes.c_int32),
-        ("sweep_alg_bytes", ctypes.c_double),
+        ("sweep_alg_bytes", ctypes.c_double), ("J_total", ctypes.c_int32), ("j0", ctypes.c_int32),
     ]
 
 
@@ -71,28 +71,163 @@ SIGNATURES = {
     "im_version": (_i32, []),
 }
 
-_lib = None
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p)
+SIGNATURES["im_build_sketches_shard"] = (ctypes.c_int, [_i32, _u64, _i32, _i32])
+SIGNATURES["im_set_allreduce"] = (ctypes.c_int, [ALLREDUCE_FN, _vp])
+IM_ECOMM = -5
+IM_DTYPE_I32, IM_DTYPE_I64 = 0, 1
+
+
+class Library:
+    """One loaded copy of the C library (= one context of include/im.h).
+
+    The module-level functions below use the default copy at LIB_PATH.  A second Library on
+    a copy of the .so file gets its own context (tests drive two simulation shards this way
+    in one process)."""
+
+    def __init__(self, path: str | None = None):
+        self.path = path or LIB_PATH
+        self._L = None
+        self._hook = None  # keeps the ctypes callback alive while registered
+
+    @property
+    def L(self):
+        if self._L is None:
+            if not os.path.exists(self.path):
+                raise ImportError(f"{self.path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+            L = ctypes.CDLL(self.path)
+            for name, (res, args) in SIGNATURES.items():
+                f = getattr(L, name)
+                f.restype = res
+                f.argtypes = args
+            self._L = L
+        return self._L
+
+    def _check(self, rc: int) -> int:
+        if rc < 0:
+            raise IMError(rc, self.L.im_last_error().decode(errors="replace"))
+        return rc
+
+    def im_load_csr(self, n: int, offsets, targets, probs) -> None:
+        """Host arrays (copied to the device inside the call)."""
+        o, po = _host(offsets, np.int32)
+        t, pt = _host(targets, np.int32)
+        p, pp = _host(probs, np.float32)
+        if len(o) != n + 1 or len(t) != int(o[-1]) or len(p) != len(t):
+            raise IMError(IM_EINVAL, "array lengths do not match n / offsets[n]")
+        self._check(self.L.im_load_csr(n, po, pt or None, pp or None))
+
+    def im_load_csr_device(self, n: int, m: int, d_offsets, d_targets, d_probs) -> None:
+        """Device arrays (torch CUDA tensors or raw pointers), already resident in HBM."""
+        self._check(self.L.im_load_csr_device(n, m, _dptr(d_offsets), _dptr(d_targets) or None, _dptr(d_probs) or None))
+
+    def im_build_sketches(self, J: int, seed: int) -> None:
+        self._check(self.L.im_build_sketches(J, seed & 0xFFFFFFFFFFFFFFFF))
+
+    def im_build_sketches_shard(self, J_total: int, seed: int, j0: int, j1: int) -> None:
+        self._check(self.L.im_build_sketches_shard(J_total, seed & 0xFFFFFFFFFFFFFFFF, j0, j1))
+
+    def im_set_allreduce(self, fn) -> None:
+        """fn(ptr: int, count: int, dtype: int) -> None sums `count` IM_DTYPE_* elements at device
+        pointer ptr over all ranks in place (see shard.py); None turns sharding off."""
+        if fn is None:
+            self._hook = None
+            self._check(self.L.im_set_allreduce(ALLREDUCE_FN(), None))
+            return
+
+        def tramp(ptr, count, dtype, user):
+            try:
+                fn(int(ptr), int(count), int(dtype))
+                return 0
+            except Exception as e:  # reported as IM_ECOMM by the library
+                import sys
+                print(f"[im] allreduce hook failed: {e!r}", file=sys.stderr)
+                return 1
+
+        self._hook = ALLREDUCE_FN(tramp)
+        self._check(self.L.im_set_allreduce(self._hook, None))
+
+    def im_estimate(self, n: int) -> np.ndarray:
+        out = np.empty(n, dtype=np.float64)
+        self._check(self.L.im_estimate(out.ctypes.data))
+        return out
+
+    def im_estimate_device(self, d_out) -> None:
+        self._check(self.L.im_estimate_device(_dptr(d_out)))
+
+    def im_select_seeds(self, K: int, err_threshold: float, eps_g: float | None = None):
+        """Returns (seeds int32[K], scores float64[K]).  eps_g given -> im_select_seeds_ex(K, eps_l, eps_g)."""
+        seeds = np.zeros(max(K, 1), dtype=np.int32)
+        scores = np.zeros(max(K, 1), dtype=np.float64)
+        if eps_g is None:
+            self._check(self.L.im_select_seeds(K, float(err_threshold), seeds.ctypes.data, scores.ctypes.data))
+        else:
+            self._check(self.L.im_select_seeds_ex(K, float(err_threshold), float(eps_g), seeds.ctypes.data, scores.ctypes.data))
+        return seeds[:K].copy(), scores[:K].copy()
+
+    def im_select_seeds_into(self, K: int, err_threshold: float, seeds: np.ndarray, scores: np.ndarray) -> None:
+        """Allocation-free variant writing into caller arrays (e.g. pinned host buffers)."""
+        self._check(self.L.im_select_seeds(K, float(err_threshold), seeds.ctypes.data, scores.ctypes.data))
+
+    def im_get_registers(self, n: int, J: int) -> np.ndarray:
+        """J = the simulations this context holds (j1 - j0 when sharded)."""
+        out = np.empty((n, J), dtype=np.uint8)
+        self._check(self.L.im_get_registers(out.ctypes.data))
+        return out
+
+    def im_get_register_rows(self, rows, J: int) -> np.ndarray:
+        r, pr = _host(rows, np.int32)
+        out = np.empty((len(r), J), dtype=np.uint8)
+        self._check(self.L.im_get_register_rows(len(r), pr, out.ctypes.data))
+        return out
+
+    def im_get_reach(self, n: int, J: int) -> np.ndarray:
+        out = np.empty((n, J // 32), dtype=np.uint32)
+        self._check(self.L.im_get_reach(out.ctypes.data))
+        return out
+
+    def im_get_step_log(self, K: int) -> list[dict]:
+        arr = (im_step * max(K, 1))()
+        k = self._check(self.L.im_get_step_log(ctypes.cast(arr, ctypes.c_void_p), K))
+        return [{f: getattr(arr[i], f) for f, _ in im_step._fields_ if f != "pad"} for i in range(k)]
+
+    def im_get_stats(self) -> dict:
+        s = im_stats()
+        self._check(self.L.im_get_stats(ctypes.byref(s)))
+        return {f: getattr(s, f) for f, _ in im_stats._fields_}
+
+    def im_set_stream(self, stream) -> None:
+        """torch.cuda.Stream, raw cudaStream_t int, or None (library stream)."""
+        h = 0 if stream is None else (stream if isinstance(stream, int) else int(stream.cuda_stream))
+        self._check(self.L.im_set_stream(h or None))
+
+    def im_kernel_launch_count(self) -> int:
+        return int(self.L.im_kernel_launch_count())
+
+    def im_free(self) -> None:
+        self.L.im_free()
+
+    def im_version(self) -> int:
+        return int(self.L.im_version())
+
+
+_default = None
+
+
+def default() -> Library:
+    global _default
+    if _default is None:
+        _default = Library(LIB_PATH)
+    return _default
 
 
 def lib():
-    """Load libim_b200.so (raises if it was not built: there is no fallback)."""
-    global _lib
-    if _lib is None:
-        if not os.path.exists(LIB_PATH):
-            raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
-        L = ctypes.CDLL(LIB_PATH)
-        for name, (res, args) in SIGNATURES.items():
-            f = getattr(L, name)
-            f.restype = res
-            f.argtypes = args
-        _lib = L
-    return _lib
+    """The default ctypes library (raises if it was not built: there is no fallback)."""
+    return default().L
 
 
 def _check(rc: int) -> int:
-    if rc < 0:
-        raise IMError(rc, lib().im_last_error().decode(errors="replace"))
-    return rc
+    return default()._check(rc)
 
 
 def _host(a, dtype):
@@ -109,98 +244,17 @@ def _dptr(x) -> int:
     return int(x.data_ptr())
 
 
-def im_load_csr(n: int, offsets, targets, probs) -> None:
-    """Host arrays (copied to the device inside the call)."""
-    o, po = _host(offsets, np.int32)
-    t, pt = _host(targets, np.int32)
-    p, pp = _host(probs, np.float32)
-    if len(o) != n + 1 or len(t) != int(o[-1]) or len(p) != len(t):
-        raise IMError(IM_EINVAL, "array lengths do not match n / offsets[n]")
-    _check(lib().im_load_csr(n, po, pt or None, pp or None))
+def _bind(name):
+    def f(*args, **kw):
+        return getattr(default(), name)(*args, **kw)
+    f.__name__ = name
+    f.__doc__ = getattr(Library, name).__doc__
+    return f
 
 
-def im_load_csr_device(n: int, m: int, d_offsets, d_targets, d_probs) -> None:
-    """Device arrays (torch CUDA tensors or raw pointers), already resident in HBM."""
-    _check(lib().im_load_csr_device(n, m, _dptr(d_offsets), _dptr(d_targets) or None, _dptr(d_probs) or None))
-
-
-def im_build_sketches(J: int, seed: int) -> None:
-    _check(lib().im_build_sketches(J, seed & 0xFFFFFFFFFFFFFFFF))
-
-
-def im_estimate(n: int) -> np.ndarray:
-    out = np.empty(n, dtype=np.float64)
-    _check(lib().im_estimate(out.ctypes.data))
-    return out
-
-
-def im_estimate_device(d_out) -> None:
-    _check(lib().im_estimate_device(_dptr(d_out)))
-
-
-def im_select_seeds(K: int, err_threshold: float, eps_g: float | None = None):
-    """Returns (seeds int32[K], scores float64[K]).  eps_g given -> im_select_seeds_ex(K, eps_l, eps_g)."""
-    seeds = np.zeros(max(K, 1), dtype=np.int32)
-    scores = np.zeros(max(K, 1), dtype=np.float64)
-    if eps_g is None:
-        _check(lib().im_select_seeds(K, float(err_threshold), seeds.ctypes.data, scores.ctypes.data))
-    else:
-        _check(lib().im_select_seeds_ex(K, float(err_threshold), float(eps_g), seeds.ctypes.data, scores.ctypes.data))
-    return seeds[:K].copy(), scores[:K].copy()
-
-
-def im_select_seeds_into(K: int, err_threshold: float, seeds: np.ndarray, scores: np.ndarray) -> None:
-    """Allocation-free variant writing into caller arrays (e.g. pinned host buffers)."""
-    _check(lib().im_select_seeds(K, float(err_threshold), seeds.ctypes.data, scores.ctypes.data))
-
-
-def im_get_registers(n: int, J: int) -> np.ndarray:
-    out = np.empty((n, J), dtype=np.uint8)
-    _check(lib().im_get_registers(out.ctypes.data))
-    return out
-
-
-def im_get_register_rows(rows, J: int) -> np.ndarray:
-    r, pr = _host(rows, np.int32)
-    out = np.empty((len(r), J), dtype=np.uint8)
-    _check(lib().im_get_register_rows(len(r), pr, out.ctypes.data))
-    return out
-
-
-def im_get_reach(n: int, J: int) -> np.ndarray:
-    out = np.empty((n, J // 32), dtype=np.uint32)
-    _check(lib().im_get_reach(out.ctypes.data))
-    return out
-
-
-def im_get_step_log(K: int) -> list[dict]:
-    arr = (im_step * max(K, 1))()
-    k = _check(lib().im_get_step_log(ctypes.cast(arr, ctypes.c_void_p), K))
-    return [{f: getattr(arr[i], f) for f, _ in im_step._fields_ if f != "pad"} for i in range(k)]
-
-
-def im_get_stats() -> dict:
-    s = im_stats()
-    _check(lib().im_get_stats(ctypes.byref(s)))
-    return {f: getattr(s, f) for f, _ in im_stats._fields_}
-
-
-def im_set_stream(stream) -> None:
-    """torch.cuda.Stream, raw cudaStream_t int, or None (library stream)."""
-    h = 0 if stream is None else (stream if isinstance(stream, int) else int(stream.cuda_stream))
-    _check(lib().im_set_stream(h or None))
-
-
-def im_kernel_launch_count() -> int:
-    return int(lib().im_kernel_launch_count())
-
-
-def im_free() -> None:
-    lib().im_free()
-
-
-def im_version() -> int:
-    return int(lib().im_version())
+for _name in [k for k in vars(Library) if k.startswith("im_")]:
+    globals()[_name] = _bind(_name)
+del _name
 
 
 def reach_bits_to_bool(words: np.ndarray, J: int) -> np.ndarray:

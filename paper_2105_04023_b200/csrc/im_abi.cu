@@ -120,7 +120,7 @@ int ensure_device() {
 }
 
 void reset_sketch_state() {
-    g.J = 0;
+    g.J = g.Jt = g.j0 = 0;
     g.built = g.fresh = g.any_blocked = false;
     g.perm.clear();
 }
@@ -141,6 +141,7 @@ void release_all() {
     dfree(g.inS); dfree(g.MS); dfree(g.btag); dfree(g.nbits); dfree(g.gain); dfree(g.big); dfree(g.list); dfree(g.lcount); dfree(g.hist);
     dfree(g.off); dfree(g.fwd); dfree(g.fwdT); dfree(g.roff); dfree(g.rev); dfree(g.revT); dfree(g.ritems); dfree(g.fbig);
     dfree(g.ctr); dfree(g.rec); dfree(g.varsigma); dfree(g.key); dfree(g.first); dfree(g.sigma_count);
+    dfree(g.lval); dfree(g.sigma_g); dfree(g.bcount);
     dfree(g.t_flags); dfree(g.t_indeg); dfree(g.t_nseg); dfree(g.t_scan); dfree(g.t_off); dfree(g.t_tgt); dfree(g.t_prob);
     dfree(g.t_est); dfree(g.t_rows); dfree(g.t_rowsout);
     for (int i = 0; i < 5; i++) dfree(g.t_prep[i]);
@@ -149,6 +150,17 @@ void release_all() {
 
 int sync() {
     CK(cudaStreamSynchronize(g.stream));
+    return 0;
+}
+
+// Simulation sharding: in-place SUM over all ranks of `count` elements at the
+// device pointer `buf`, through the caller's hook (im_set_allreduce).  The stream is drained first;
+// the hook returns after the reduced values are in `buf`.  No-op when unsharded.
+int allreduce(void* buf, int64_t count, int32_t dtype) {
+    if (!g.ar) return 0;
+    TRY(sync());
+    int r = g.ar(buf, count, dtype, g.ar_user);
+    if (r) return fail(IM_ECOMM, "allreduce hook failed (%d) on %lld elements", r, (long long)count);
     return 0;
 }
 
@@ -236,6 +248,7 @@ int load_common(int32_t n, int64_t m, const int32_t* d_off_src, const int32_t* d
     TRY(dalloc(g.key, 1));
     TRY(dalloc(g.first, 1));
     TRY(dalloc(g.sigma_count, 1));
+    TRY(dalloc(g.sigma_g, 1));
     g.loaded = true;
     g.st = im_stats{};
     g.st.n = n;
@@ -283,7 +296,9 @@ int alloc_sketch_state(int32_t J) {
     TRY(dalloc(g.big, n));
     TRY(dalloc(g.gain, n));
     TRY(dalloc(g.list, n));
+    TRY(dalloc(g.lval, n));
     TRY(dalloc(g.lcount, 2));
+    TRY(dalloc(g.bcount, (size_t)g.num_sms * 8));
     TRY(dalloc(g.hist, 4096));
     TRY(dalloc(g.nbits, n, &fr));  // zero between levels (consumed by k_bfs_compact)
     if (fr) CK(cudaMemsetAsync(g.nbits, 0, n * sizeof(uint32_t), g.stream));
@@ -291,14 +306,18 @@ int alloc_sketch_state(int32_t J) {
     return 0;
 }
 
-// Alg. 1 salts (R2, R3): mt19937(low 32 bits of seed): seed_V, seed_J, X_j = draw & (2^31-1).
+// Alg. 1 salts (R2, R3): mt19937(low 32 bits of seed): seed_V, seed_J, X_j = draw & (2^31-1) for
+// j < Jt; this context holds simulations [j0, j0 + J) of them (all of them unless sharded).
 // Internally simulations are ordered by ascending salt.
-int setup_salts(int32_t J, uint64_t seed) {
+int setup_salts(int32_t Jt, int32_t j0, int32_t J, uint64_t seed) {
     std::mt19937 gen((uint32_t)seed);
     g.seedV = gen();
     g.seedJ = gen();
     std::vector<uint32_t> X(J);
-    for (int j = 0; j < J; j++) X[j] = gen() & 0x7FFFFFFFu;
+    for (int j = 0; j < j0 + J; j++) {
+        uint32_t x = gen() & 0x7FFFFFFFu;
+        if (j >= j0) X[j - j0] = x;
+    }
     g.perm.resize(J);
     for (int j = 0; j < J; j++) g.perm[j] = j;
     std::stable_sort(g.perm.begin(), g.perm.end(), [&](int a, int b) { return X[a] < X[b]; });
@@ -311,9 +330,13 @@ int setup_salts(int32_t J, uint64_t seed) {
     }
     CK(cudaMemcpyAsync(g.Xs, Xs.data(), J * sizeof(uint32_t), cudaMemcpyHostToDevice, g.stream));
     CK(cudaMemcpyAsync(g.s12, s12.data(), 4097 * sizeof(uint16_t), cudaMemcpyHostToDevice, g.stream));
-    CK(cudaMemcpyAsync(g.permd, g.perm.data(), J * sizeof(int32_t), cudaMemcpyHostToDevice, g.stream));
+    std::vector<int32_t> gj(J);
+    for (int i = 0; i < J; i++) gj[i] = g.perm[i] + j0;
+    CK(cudaMemcpyAsync(g.permd, gj.data(), J * sizeof(int32_t), cudaMemcpyHostToDevice, g.stream));
     TRY(sync());  // host vectors go out of scope
     g.seed = seed;
+    g.Jt = Jt;
+    g.j0 = j0;
     return 0;
 }
 
@@ -412,7 +435,7 @@ int build_fresh() {
 // =========================================================== C ABI
 extern "C" {
 
-int32_t im_version(void) { return 100; }
+int32_t im_version(void) { return 101; }
 
 const char* im_last_error(void) { return g_err.c_str(); }
 
@@ -467,9 +490,13 @@ int im_load_csr_device(int32_t n, int64_t m, const int32_t* d_offsets, const int
     return r;
 }
 
-int im_build_sketches(int32_t J, uint64_t seed) {
+int im_build_sketches_shard(int32_t J_total, uint64_t seed, int32_t j0, int32_t j1) {
     if (!g.loaded) return fail(IM_ESTATE, "im_build_sketches: no graph loaded");
-    if (J < 32 || J > 1024 || J % 32) return fail(IM_EINVAL, "J must be a multiple of 32 in [32, 1024] (got %d)", J);
+    if (J_total < 32 || J_total > IM_MAX_J_TOTAL || J_total % 32)
+        return fail(IM_EINVAL, "J_total must be a multiple of 32 in [32, %d] (got %d)", IM_MAX_J_TOTAL, J_total);
+    if (j0 < 0 || j1 > J_total || j0 >= j1) return fail(IM_EINVAL, "shard [%d, %d) not inside [0, %d)", j0, j1, J_total);
+    const int32_t J = j1 - j0;
+    if (J < 32 || J > 1024 || J % 32) return fail(IM_EINVAL, "shard size j1 - j0 must be a multiple of 32 in [32, 1024] (got %d)", J);
     g.st.total_sweeps = 0;
     g.st.total_edges = 0;
     g.st.sweep_kernel_ms = 0;
@@ -479,17 +506,48 @@ int im_build_sketches(int32_t J, uint64_t seed) {
     g.st.gather_sweeps = 0;
     int64_t l0 = g.launches;
     TRY(alloc_sketch_state(J));
-    TRY(setup_salts(J, seed));
+    TRY(setup_salts(J_total, j0, J, seed));
     TRY(build_fresh());
     g.st.J = J;
+    g.st.J_total = J_total;
+    g.st.j0 = j0;
     g.st.kernel_launches = g.launches - l0;
+    return 0;
+}
+
+int im_build_sketches(int32_t J, uint64_t seed) {
+    if (J < 32 || J > 1024 || J % 32) return fail(IM_EINVAL, "J must be a multiple of 32 in [32, 1024] (got %d)", J);
+    return im_build_sketches_shard(J, seed, 0, J);
+}
+
+int im_set_allreduce(im_allreduce_fn fn, void* user) {
+    g.ar = fn;
+    g.ar_user = fn ? user : nullptr;
+    return 0;
+}
+
+static int shard_check(const char* what) {
+    if (g.J != g.Jt && !g.ar) return fail(IM_ESTATE, "%s: sharded sketches (%d of %d simulations) need im_set_allreduce", what, g.J, g.Jt);
+    return 0;
+}
+
+// Eq. 2 into device memory; sharded: register sums of this rank, allreduced, then Eq. 2 over J_total
+static int estimate_into(double* d) {
+    TRY(shard_check("im_estimate"));
+    if (!g.ar) {
+        CK(launch_estimate(g, d));
+        return 0;
+    }
+    CK(launch_estimate_sums(g, g.gain));
+    TRY(allreduce(g.gain, g.n, IM_DTYPE_I32));
+    CK(launch_estimate_fin(g, g.gain, d));
     return 0;
 }
 
 int im_estimate_device(double* d_out) {
     if (!g.built) return fail(IM_ESTATE, "im_estimate: sketches not built");
     if (!d_out) return fail(IM_EINVAL, "null output");
-    CK(launch_estimate(g, d_out));
+    TRY(estimate_into(d_out));
     return sync();
 }
 
@@ -498,7 +556,7 @@ int im_estimate(double* out) {
     if (!out) return fail(IM_EINVAL, "null output");
     double*& d = g.t_est;
     TRY(dalloc(d, (size_t)g.n));
-    CK(launch_estimate(g, d));
+    TRY(estimate_into(d));
     CK(cudaMemcpyAsync(out, d, (size_t)g.n * sizeof(double), cudaMemcpyDeviceToHost, g.stream));
     return sync();
 }
@@ -508,6 +566,7 @@ int im_select_seeds_ex(int32_t K, double eps_l, double eps_g, int32_t* out_seeds
     if (K < 0 || K > g.n) return fail(IM_EINVAL, "K must be in [0, n] (got %d, n = %d)", K, g.n);
     if (std::isnan(eps_l) || std::isnan(eps_g) || eps_l < 0 || eps_g < 0) return fail(IM_EINVAL, "thresholds must be >= 0 and not NaN");
     if (K > 0 && (!out_seeds || !out_scores)) return fail(IM_EINVAL, "null output");
+    TRY(shard_check("im_select_seeds"));
     auto t0 = clk::now();
     int64_t l0 = g.launches;
     g.st.total_sweeps = 0;
@@ -540,13 +599,19 @@ int im_select_seeds_ex(int32_t K, double eps_l, double eps_g, int32_t* out_seeds
         // line 10: argmax over the pool (exact lazy evaluation, im_kernels.cu "a6")
         if (!need_full) {
             CK(launch_argmax_list(g, list_len));
+            if (g.ar) {  // sharded: sum the packed local values, then decode (im_kernels.cu)
+                TRY(allreduce(g.lval, list_len, IM_DTYPE_I32));
+                CK(launch_argmax_list_finish(g, list_len));
+            }
             ull hk;
             TRY(readback(g.key, sizeof hk, &hk));
             if (hk == 0 || (int64_t)(hk >> 32) < theta) need_full = true;
             g.st_argmax_list++;
         }
         if (need_full) {
-            CK(launch_argmax_full(g, pool_check, T));
+            CK(launch_argmax_full(g, pool_check));
+            TRY(allreduce(g.gain, g.n, IM_DTYPE_I32));
+            CK(launch_argmax_full_finish(g, T));
             int lc[2];
             TRY(readback(g.lcount, sizeof lc, lc));
             list_len = lc[0];
@@ -557,6 +622,7 @@ int im_select_seeds_ex(int32_t K, double eps_l, double eps_g, int32_t* out_seeds
         // lines 11, 13-14: S <- S + s, BFS for R_G(S), sigma
         CK(cudaMemsetAsync(&g.ctr[0], 0, sizeof(IterCounters), g.stream));
         CK(launch_seed_start(g, k));
+        TRY(allreduce(&g.rec->score, 1, IM_DTYPE_I64));  // sharded: score summed over all simulations
         CK(launch_bfs_items(g, 0));
         IterCounters hc;
         TRY(readback(&g.ctr[0], sizeof hc, &hc));
@@ -578,7 +644,12 @@ int im_select_seeds_ex(int32_t K, double eps_l, double eps_g, int32_t* out_seeds
         if (hc.changed > 0) CK(launch_bfs_clear(g, cur, hc.changed));  // frontier without work items
         pool_check = true;
         g.any_blocked = true;
-        // lines 12, 15-27: error test, M_S' merge or rebuild decision
+        // lines 12, 15-27: error test, M_S' merge or rebuild decision (sharded: on the summed sigma count,
+        // so every rank takes the same decision)
+        if (g.ar) {
+            CK(cudaMemcpyAsync(g.sigma_g, g.sigma_count, sizeof(ull), cudaMemcpyDeviceToDevice, g.stream));
+            TRY(allreduce(g.sigma_g, 1, IM_DTYPE_I64));
+        }
         CK(launch_error_check(g, k, K, eps_l, eps_g));
         StepDev rec;
         TRY(readback(g.rec, sizeof rec, &rec));

@@ -16,6 +16,7 @@ constexpr int SEG = 256;        // max edges per work item (a segment of one ver
 constexpr int DENSE_WIN = 32;   // windows wider than this many simulations take the warp-cooperative path
 constexpr int BLOCK = 256;      // threads per block of the persistent work-list kernels
 constexpr int FIRST_BIG = 2048; // first sweep: rows with more out-edges are gathered by a whole block
+constexpr uint32_t SHARD_POOL_ONE = 1u << 24;  // sharded argmax: gain + (in local pool) << 24, summed over ranks
 
 // device-side counters of one sweep / BFS level (one 32-byte D2H per iteration)
 struct IterCounters {
@@ -61,13 +62,14 @@ struct Ctx {
     int32_t* fbig = nullptr;    // vertices with > FIRST_BIG out-edges
     int32_t n_fbig = 0;
     // sketches
-    int32_t J = 0;
+    int32_t J = 0;              // simulations held here (this rank's shard)
+    int32_t Jt = 0, j0 = 0;     // all simulations of the job / global index of the first one held here
     uint64_t seed = 0;
     uint32_t seedV = 0, seedJ = 0;
-    std::vector<int32_t> perm;  // internal (ascending salt) index -> simulation j
+    std::vector<int32_t> perm;  // internal (ascending salt) index -> local simulation column j - j0
     uint32_t* Xs = nullptr;     // sorted salts [J]
     uint16_t* s12 = nullptr;    // [4097]
-    int32_t* permd = nullptr;   // [J]
+    int32_t* permd = nullptr;   // [J] internal index -> global simulation j (hash input of Eq. 1)
     uint8_t* M = nullptr;       // n*J registers, row-major, internal simulation order
     uint32_t* vis = nullptr;    // n*(J/32) R_G(S) bits, internal order
     bool built = false, fresh = false, any_blocked = false;
@@ -96,8 +98,14 @@ struct Ctx {
     int32_t* gain = nullptr;     // stored gains of the last full argmax pass (-1: not in the pool)
     int32_t* list = nullptr;     // candidate list of the lazy argmax
     int* lcount = nullptr;       // [0] list length, [1] theta
+    int* bcount = nullptr;       // per-block match counts of the ordered list build [num_sms * 8]
     uint32_t* hist = nullptr;    // gain histogram of the full pass
     ull* sigma_count = nullptr;
+    // simulation sharding: in-place SUM over ranks, null when unsharded
+    im_allreduce_fn ar = nullptr;
+    void* ar_user = nullptr;
+    int32_t* lval = nullptr;     // packed local values of the lazy-list argmax [list capacity]
+    ull* sigma_g = nullptr;      // sigma count summed over ranks
     // reused temporaries (edge prep, host-pointer loads, diagnostics)
     int* t_flags = nullptr;
     int32_t* t_indeg = nullptr;
@@ -158,7 +166,11 @@ cudaError_t launch_slices_big(Ctx& c, const int32_t* big, const uint32_t* mask, 
 cudaError_t launch_sweep(Ctx& c, const int4* items, int n_items, const uint32_t* bits_in, uint32_t* bits_out,
                          IterCounters* ctr, bool blocked);
 cudaError_t launch_estimate(Ctx& c, double* out);
-cudaError_t launch_argmax_full(Ctx& c, bool pool, int T);
+cudaError_t launch_estimate_sums(Ctx& c, int32_t* sums);
+cudaError_t launch_estimate_fin(Ctx& c, const int32_t* sums, double* out);
+cudaError_t launch_argmax_full(Ctx& c, bool pool);
+cudaError_t launch_argmax_full_finish(Ctx& c, int T);
+cudaError_t launch_argmax_list_finish(Ctx& c, int list_len);
 cudaError_t launch_argmax_tma(Ctx& c, bool pool, int L, int C, int shift);
 int setup_argmax_tma();
 cudaError_t launch_argmax_list(Ctx& c, int list_len);

@@ -15,7 +15,8 @@
 namespace im {
 
 // ============================================================ a5: Eq. 2 estimate
-__global__ void k_estimate(int32_t n, int32_t J, const uint32_t* __restrict__ M32, double* __restrict__ out) {
+template <bool SUMS>
+__global__ void k_estimate(int32_t n, int32_t J, const uint32_t* __restrict__ M32, double* __restrict__ out, int32_t* sums) {
     const int lane = threadIdx.x & 31, Jw = J >> 2;
     const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < n; v += warps) {
@@ -23,8 +24,18 @@ __global__ void k_estimate(int32_t n, int32_t J, const uint32_t* __restrict__ M3
         for (int w = lane; w < Jw; w += 32) s += __vsadu4(__ldcs(&M32[v * Jw + w]), 0u);
 #pragma unroll
         for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(IM_FULL, s, o);
-        if (lane == 0) out[v] = exp2((double)s / (double)J) / 0.77351;
+        if (lane == 0) {
+            if (SUMS) sums[v] = (int32_t)s;
+            else out[v] = exp2((double)s / (double)J) / 0.77351;
+        }
     }
+}
+
+// sharded (Sec. 8(e) of SURVEY.md): Eq. 2 from the register sums allreduced over all J_total simulations
+__global__ void k_estimate_fin(int32_t n, int32_t Jt, const int32_t* __restrict__ sums, double* __restrict__ out) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += stride)
+        out[v] = exp2((double)sums[v] / (double)Jt) / 0.77351;
 }
 
 // ============================================================ a6: greedy argmax
@@ -51,7 +62,8 @@ constexpr int HIST_BINS = 4096;
 constexpr int AG = 4;  // vertex groups in flight per warp in k_argmax
 
 // LIST = false: every vertex (full pass: stores gains + histogram); LIST = true: the vertices in list[0..*count)
-template <bool POOL, bool LIST>
+// SHARD (list only): writes the packed local value gain + (in local pool) << 24 to gain_out[i] for list entry i
+template <bool POOL, bool LIST, bool SHARD = false>
 __global__ void __launch_bounds__(BLOCK) k_argmax(int32_t n, int32_t J, int L, int C, const uint4* __restrict__ M16,
                                                   const uint8_t* __restrict__ MS, const uint32_t* __restrict__ vis,
                                                   ull* key, int32_t* gain_out, uint32_t* hist, int shift,
@@ -105,6 +117,10 @@ __global__ void __launch_bounds__(BLOCK) k_argmax(int32_t n, int32_t J, int L, i
             }
             gn >>= 1;
             bool inpool = ok[u] && (!POOL || !full);
+            if (SHARD) {
+                if (ok[u] && q == 0) gain_out[(g0 + u * nwarps) * VPW + sub] = (int32_t)(gn + (inpool ? SHARD_POOL_ONE : 0u));
+                continue;
+            }
             if (ok[u] && q == 0) {
                 if (inpool) {
                     ull k = ((ull)gn << 32) | (ull)(0xFFFFFFFFu - (uint32_t)vv[u]);
@@ -147,18 +163,102 @@ __global__ void k_theta(const uint32_t* __restrict__ hist, int shift, int T, int
     }
 }
 
-__global__ void k_list_build(int32_t n, const int32_t* __restrict__ gain, const int* theta, int32_t* list, int* count) {
-    const int th = *theta, lane = threadIdx.x & 31;
+// Candidate list = the vertices with stored gain >= theta, in ascending vertex order (the order is
+// deterministic, so every rank of a sharded job indexes the same list).  Block b owns a contiguous
+// vertex range: k_list_count counts its matches, k_list_write places them after the matches of
+// blocks 0..b-1 with a block-wide scan per 256-vertex tile.
+__device__ __forceinline__ void list_range(int32_t n, int b, int nb, int64_t& v0, int64_t& v1) {
+    const int64_t chunk = (((int64_t)n + nb - 1) / nb + BLOCK - 1) / BLOCK * BLOCK;
+    v0 = min((int64_t)n, b * chunk);
+    v1 = min((int64_t)n, v0 + chunk);
+}
+
+__global__ void k_list_count(int32_t n, const int32_t* __restrict__ gain, const int* theta, int* bcount) {
+    __shared__ int sW[BLOCK / 32];
+    const int th = *theta;
+    int64_t v0, v1;
+    list_range(n, blockIdx.x, gridDim.x, v0, v1);
+    int cnt = 0;
+    for (int64_t v = v0 + threadIdx.x; v < v1; v += BLOCK) cnt += gain[v] >= th;
+    cnt = __reduce_add_sync(IM_FULL, cnt);
+    if ((threadIdx.x & 31) == 0) sW[threadIdx.x >> 5] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int i = 0; i < BLOCK / 32; i++) t += sW[i];
+        bcount[blockIdx.x] = t;
+    }
+}
+
+__global__ void k_list_write(int32_t n, const int32_t* __restrict__ gain, const int* theta, const int* __restrict__ bcount,
+                             int32_t* list, int* count) {
+    __shared__ int sW[BLOCK / 32];
+    __shared__ int sBase;
+    const int th = *theta, lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    int part = 0;
+    for (int i = threadIdx.x; i < (int)blockIdx.x; i += BLOCK) part += bcount[i];
+    part = __reduce_add_sync(IM_FULL, part);
+    if (lane == 0) sW[wib] = part;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int i = 0; i < BLOCK / 32; i++) t += sW[i];
+        sBase = t;
+        if (blockIdx.x == gridDim.x - 1) *count = t + bcount[blockIdx.x];
+    }
+    __syncthreads();
+    int base = sBase;
+    int64_t v0, v1;
+    list_range(n, blockIdx.x, gridDim.x, v0, v1);
+    for (int64_t t0 = v0; t0 < v1; t0 += BLOCK) {
+        const int64_t v = t0 + threadIdx.x;
+        const bool take = v < v1 && gain[v] >= th;
+        const uint32_t m = __ballot_sync(IM_FULL, take);
+        __syncthreads();  // sW reuse
+        if (lane == 0) sW[wib] = __popc(m);
+        __syncthreads();
+        int before = 0, total = 0;
+        for (int i = 0; i < BLOCK / 32; i++) {
+            before += i < wib ? sW[i] : 0;
+            total += sW[i];
+        }
+        if (take) list[base + before + __popc(m & ((1u << lane) - 1u))] = (int32_t)v;
+        base += total;
+    }
+}
+
+// sharded argmax: vals[i] = sum over ranks of (local gain + local pool flag << 24),
+// after the allreduce.  A vertex is in the global pool iff some rank still has an unvisited simulation
+// of it (R14); its global gain is the low 24 bits.  Writes the key (and, for the full pass, the stored
+// gains and histogram) exactly as the unsharded kernels do.
+__global__ void k_argmax_decode(int nv, const int32_t* __restrict__ list, const int* list_count, const int32_t* __restrict__ vals,
+                                int32_t* gain_out, ull* key, uint32_t* hist, int shift) {
+    __shared__ ull sKey[BLOCK / 32];
+    if (list) nv = *list_count;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
-        int64_t v = base + threadIdx.x;
-        bool take = v < n && gain[v] >= th;
-        uint32_t m = __ballot_sync(IM_FULL, take);
-        if (!m) continue;
-        int pos = 0;
-        if (lane == 0) pos = atomicAdd(count, __popc(m));
-        pos = __shfl_sync(IM_FULL, pos, 0);
-        if (take) list[pos + __popc(m & ((1u << lane) - 1u))] = (int32_t)v;
+    ull best = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv; i += stride) {
+        const uint32_t x = (uint32_t)vals[i];
+        const uint32_t gn = x & (SHARD_POOL_ONE - 1u), v = list ? (uint32_t)list[i] : (uint32_t)i;
+        const bool inpool = (x >> 24) != 0u;
+        if (inpool) {
+            ull k = ((ull)gn << 32) | (ull)(0xFFFFFFFFu - v);
+            best = k > best ? k : best;
+            if (hist) atomicAdd(&hist[min((int)(gn >> shift), HIST_BINS - 1)], 1u);
+        }
+        if (gain_out) gain_out[i] = inpool ? (int32_t)gn : -1;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        ull ob = __shfl_xor_sync(IM_FULL, best, o);
+        best = ob > best ? ob : best;
+    }
+    if ((threadIdx.x & 31) == 0) sKey[threadIdx.x >> 5] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        ull b = 0;
+        for (int i = 0; i < BLOCK / 32; i++) b = sKey[i] > b ? sKey[i] : b;
+        if (b) atomicMax(key, b);
     }
 }
 
@@ -432,16 +532,17 @@ __global__ void k_bfs_clear(int n_v, int W, const int32_t* __restrict__ vl, uint
 }
 
 // ============================================================ a8: error check (Alg. 1 lines 12, 15-27)
-__global__ void k_error_check(int32_t J, int k, int K, double eps_l, double eps_g, const uint32_t* __restrict__ M32,
+// J: this rank's simulations (M_S' merge); Jt: all simulations (Eq. 2 and sigma; == J unless sharded)
+__global__ void k_error_check(int32_t J, int32_t Jt, int k, int K, double eps_l, double eps_g, const uint32_t* __restrict__ M32,
                               uint8_t* MS, const IterCounters* ctr_unused, const ull* sigma_count, double* varsigma,
                               StepDev* rec) {
     (void)ctr_unused;
     const int lane = threadIdx.x, Jw = J >> 2;
     __shared__ int sRebuild;
     if (lane == 0) {
-        double e = exp2((double)rec->score / (double)J) / 0.77351;
+        double e = exp2((double)rec->score / (double)Jt) / 0.77351;
         ull cnt = *sigma_count;
-        double sigma = (double)cnt / (double)J;
+        double sigma = (double)cnt / (double)Jt;
         double delta = sigma - *varsigma;
         double err_l = delta != 0.0 ? fabs((e - delta) / delta) : (double)INFINITY;
         double err_g = fabs((e - delta) / sigma);
@@ -478,7 +579,15 @@ __global__ void k_gather_rows(int64_t nrows, int32_t J, const int32_t* __restric
 
 
 cudaError_t launch_estimate(Ctx& c, double* out) {
-    k_estimate<<<grid_for(c, (int64_t)c.n * 32), BLOCK, 0, c.stream>>>(c.n, c.J, reinterpret_cast<const uint32_t*>(c.M), out);
+    k_estimate<false><<<grid_for(c, (int64_t)c.n * 32), BLOCK, 0, c.stream>>>(c.n, c.J, reinterpret_cast<const uint32_t*>(c.M), out, nullptr);
+    return LAUNCHED(c);
+}
+cudaError_t launch_estimate_sums(Ctx& c, int32_t* sums) {
+    k_estimate<true><<<grid_for(c, (int64_t)c.n * 32), BLOCK, 0, c.stream>>>(c.n, c.J, reinterpret_cast<const uint32_t*>(c.M), nullptr, sums);
+    return LAUNCHED(c);
+}
+cudaError_t launch_estimate_fin(Ctx& c, const int32_t* sums, double* out) {
+    k_estimate_fin<<<grid_for(c, c.n), BLOCK, 0, c.stream>>>(c.n, c.Jt, sums, out);
     return LAUNCHED(c);
 }
 static void argmax_geometry(const Ctx& c, int& L, int& C) {
@@ -489,12 +598,14 @@ static void argmax_geometry(const Ctx& c, int& L, int& C) {
 }
 static int hist_shift(const Ctx& c) {
     int sh = 0;
-    while (((32 * c.J) >> sh) >= HIST_BINS) sh++;
+    while (((32 * c.Jt) >> sh) >= HIST_BINS) sh++;  // gains of all J_total simulations
     return sh;
 }
 
-// full pass: exact argmax into c.key (zeroed here) + stored gains + candidate list for later steps
-cudaError_t launch_argmax_full(Ctx& c, bool pool, int T) {
+// full pass: exact argmax into c.key (zeroed here) + stored gains + candidate list for later steps.
+// Sharded: the pass leaves packed local values in c.gain; the caller allreduces them and calls
+// launch_argmax_full_finish, which decodes them (k_argmax_decode) before theta / list.
+cudaError_t launch_argmax_full(Ctx& c, bool pool) {
     int L, C;
     argmax_geometry(c, L, C);
     const int sh = hist_shift(c);
@@ -502,14 +613,26 @@ cudaError_t launch_argmax_full(Ctx& c, bool pool, int T) {
     if (!e) e = cudaMemsetAsync(c.hist, 0, HIST_BINS * sizeof(uint32_t), c.stream);
     if (!e) e = cudaMemsetAsync(c.lcount, 0, 2 * sizeof(int), c.stream);
     if (e) return e;
-    if ((e = launch_argmax_tma(c, pool, L, C, sh))) return e;  // TMA-bulk streaming pass (im_stream.cu)
+    return launch_argmax_tma(c, pool, L, C, sh);  // TMA-bulk streaming pass (im_stream.cu)
+}
+cudaError_t launch_argmax_full_finish(Ctx& c, int T) {
+    const int sh = hist_shift(c);
+    cudaError_t e;
+    if (c.ar) {
+        k_argmax_decode<<<grid_for(c, c.n), BLOCK, 0, c.stream>>>(c.n, nullptr, nullptr, c.gain, c.gain, c.key, c.hist, sh);
+        if ((e = LAUNCHED(c))) return e;
+    }
     k_theta<<<1, 32, 0, c.stream>>>(c.hist, sh, T, c.lcount + 1);
     if ((e = LAUNCHED(c))) return e;
-    k_list_build<<<grid_for(c, c.n), BLOCK, 0, c.stream>>>(c.n, c.gain, c.lcount + 1, c.list, c.lcount);
+    const int nb = grid_for(c, c.n);  // <= LIST_BLOCKS(c)
+    k_list_count<<<nb, BLOCK, 0, c.stream>>>(c.n, c.gain, c.lcount + 1, c.bcount);
+    if ((e = LAUNCHED(c))) return e;
+    k_list_write<<<nb, BLOCK, 0, c.stream>>>(c.n, c.gain, c.lcount + 1, c.bcount, c.list, c.lcount);
     return LAUNCHED(c);
 }
 
-// lazy step: exact gains over the candidate list only; valid iff best gain >= theta (checked by the host)
+// lazy step: exact gains over the candidate list only; valid iff best gain >= theta (checked by the host).
+// Sharded: packed local values go to c.lval; the caller allreduces them and calls launch_argmax_list_finish.
 cudaError_t launch_argmax_list(Ctx& c, int list_len) {
     int L, C;
     argmax_geometry(c, L, C);
@@ -517,7 +640,15 @@ cudaError_t launch_argmax_list(Ctx& c, int list_len) {
     if (e) return e;
     int g = grid_for(c, (int64_t)list_len * L / 2);
     const uint4* M16 = reinterpret_cast<const uint4*>(c.M);
-    k_argmax<true, true><<<g, BLOCK, 0, c.stream>>>(c.n, c.J, L, C, M16, c.MS, c.vis, c.key, nullptr, nullptr, 0, c.list, c.lcount);
+    if (c.ar)
+        k_argmax<true, true, true><<<g, BLOCK, 0, c.stream>>>(c.n, c.J, L, C, M16, c.MS, c.vis, c.key, c.lval, nullptr, 0, c.list, c.lcount);
+    else
+        k_argmax<true, true><<<g, BLOCK, 0, c.stream>>>(c.n, c.J, L, C, M16, c.MS, c.vis, c.key, nullptr, nullptr, 0, c.list, c.lcount);
+    return LAUNCHED(c);
+}
+cudaError_t launch_argmax_list_finish(Ctx& c, int list_len) {
+    if (!c.ar) return cudaSuccess;
+    k_argmax_decode<<<grid_for(c, list_len), BLOCK, 0, c.stream>>>(list_len, c.list, c.lcount, c.lval, nullptr, c.key, nullptr, 0);
     return LAUNCHED(c);
 }
 cudaError_t launch_seed_start(Ctx& c, int k) {
@@ -569,8 +700,8 @@ cudaError_t launch_bfs_clear(Ctx& c, int cur, int n_v) {
     return LAUNCHED(c);
 }
 cudaError_t launch_error_check(Ctx& c, int k, int K, double eps_l, double eps_g) {
-    k_error_check<<<1, 32, 0, c.stream>>>(c.J, k, K, eps_l, eps_g, reinterpret_cast<const uint32_t*>(c.M), c.MS, nullptr,
-                                          c.sigma_count, c.varsigma, c.rec);
+    k_error_check<<<1, 32, 0, c.stream>>>(c.J, c.Jt, k, K, eps_l, eps_g, reinterpret_cast<const uint32_t*>(c.M), c.MS, nullptr,
+                                          c.ar ? c.sigma_g : c.sigma_count, c.varsigma, c.rec);
     return LAUNCHED(c);
 }
 cudaError_t launch_gather_rows(Ctx& c, const int32_t* rows, int64_t nrows, uint8_t* out) {

@@ -48,7 +48,9 @@ __device__ __forceinline__ uint32_t gain16x2_s(uint4 x, uint4 m) {
 // rows of tile t: vertices [t*TV, min(n, (t+1)*TV)); M and vis carry 64 KB of padding so the last
 // tile may read past row n; TV is a multiple of 8 * (vertices per warp), so every bulk copy is a
 // whole multiple of 16 bytes at a 16-byte aligned address and the per-warp loop is uniform
-template <bool POOL>
+// SHARD: this rank holds only its simulations; gain_out[v] = local gain + (not fully visited) << 24
+// for every v (the allreduce SUM over ranks then k_argmax_decode give the global gains / pool)
+template <bool POOL, bool SHARD>
 __global__ void __launch_bounds__(BLOCK) k_argmax_tma(int32_t n, int32_t J, int L, int C, const uint8_t* __restrict__ M,
                                                       const uint8_t* __restrict__ MS, const uint32_t* __restrict__ vis,
                                                       ull* key, int32_t* gain_out, uint32_t* hist, int shift, int TV) {
@@ -116,6 +118,10 @@ __global__ void __launch_bounds__(BLOCK) k_argmax_tma(int32_t n, int32_t J, int 
             }
             gn >>= 1;
             const bool inpool = ok && (!POOL || !fullrow);
+            if (SHARD) {
+                if (ok && q == 0) gain_out[v] = (int32_t)(gn + (inpool ? SHARD_POOL_ONE : 0u));
+                continue;
+            }
             if (ok && q == 0) {
                 if (inpool) {
                     ull k = ((ull)gn << 32) | (ull)(0xFFFFFFFFu - (uint32_t)v);
@@ -165,16 +171,20 @@ static size_t tma_smem(int J, int TV, bool pool) {
 int setup_argmax_tma() {
     const int dyn = 3 * (TILE_M + 4096 + 128) + 128;  // >= tma_smem for every J
     cudaError_t e;
-    if ((e = cudaFuncSetAttribute(k_argmax_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn))) return (int)e;
-    return (int)cudaFuncSetAttribute(k_argmax_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+    if ((e = cudaFuncSetAttribute(k_argmax_tma<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn))) return (int)e;
+    if ((e = cudaFuncSetAttribute(k_argmax_tma<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn))) return (int)e;
+    if ((e = cudaFuncSetAttribute(k_argmax_tma<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn))) return (int)e;
+    return (int)cudaFuncSetAttribute(k_argmax_tma<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
 }
 
 cudaError_t launch_argmax_tma(Ctx& c, bool pool, int L, int C, int shift) {
     const int TV = tma_tv(c.J, L), ntiles = (c.n + TV - 1) / TV;
     const int grid = ntiles < c.num_sms * 2 ? ntiles : c.num_sms * 2;
     const size_t smem = tma_smem(c.J, TV, pool);
-    if (pool) k_argmax_tma<true><<<grid, BLOCK, smem, c.stream>>>(c.n, c.J, L, C, c.M, c.MS, c.vis, c.key, c.gain, c.hist, shift, TV);
-    else k_argmax_tma<false><<<grid, BLOCK, smem, c.stream>>>(c.n, c.J, L, C, c.M, c.MS, c.vis, c.key, c.gain, c.hist, shift, TV);
+    const bool sh = c.ar != nullptr;
+    auto kf = pool ? (sh ? k_argmax_tma<true, true> : k_argmax_tma<true, false>)
+                   : (sh ? k_argmax_tma<false, true> : k_argmax_tma<false, false>);
+    kf<<<grid, BLOCK, smem, c.stream>>>(c.n, c.J, L, C, c.M, c.MS, c.vis, c.key, c.gain, c.hist, shift, TV);
     return LAUNCHED(c);
 }
 

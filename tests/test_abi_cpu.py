@@ -35,7 +35,7 @@ def test_library_loads_and_binds():
     L = im.lib()
     for name in declared_symbols():
         assert hasattr(L, name)
-    assert im.im_version() == 100
+    assert im.im_version() == 101
 
 
 def test_call_order_errors_without_gpu():
@@ -61,3 +61,26 @@ def test_no_oracle_in_product_path():
                 assert "import oracle" not in txt and "liboracle" not in txt and "from oracle" not in txt, f
     out = subprocess.run(["ldd", im.LIB_PATH], capture_output=True, text=True).stdout
     assert "oracle" not in out
+
+
+def test_binding_struct_layouts_match_header(tmp_path):
+    """ctypes mirrors of im_stats / im_step have the C sizes and field offsets (gcc on include/im.h)."""
+    import ctypes
+
+    fields = {"im_stats": im.im_stats, "im_step": im.im_step}
+    src = ['#include <stdio.h>', '#include <stddef.h>', '#include "im.h"', "int main(void) {"]
+    for cname, cls in fields.items():
+        src.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
+        for f, _ in cls._fields_:
+            src.append(f'printf("{cname} {f} %zu\\n", offsetof({cname}, {f}));')
+    src.append("return 0; }")
+    c = tmp_path / "layout.c"
+    c.write_text("\n".join(src))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(c), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n")
+    for line in filter(None, out):
+        cname, f, v = line.split()
+        cls = fields[cname]
+        want = ctypes.sizeof(cls) if f == "size" else getattr(cls, f).offset
+        assert int(v) == want, (cname, f, v, want)
