@@ -64,8 +64,8 @@ def _load():
             "or_init_rows": (None, [i32, u64, i64, vp, vp]),
             "or_estimate_row": (f64, [vp, i32]),
             "or_estimate": (None, [i32, i32, vp, vp]),
-            "or_simulate": (ctypes.c_int, [i32, vp, vp, vp, i32, vp, vp, vp, vp, vp, i32]),
-            "or_select_seeds": (ctypes.c_int, [i32, vp, vp, vp, i32, u64, i32, f64, f64, vp, vp, vp, vp, vp, vp]),
+            "or_simulate": (ctypes.c_int, [i32, vp, vp, vp, i32, vp, vp, vp, vp, vp, i32, f64]),
+            "or_select_seeds": (ctypes.c_int, [i32, vp, vp, vp, i32, u64, i32, f64, f64, f64, vp, vp, vp, vp, vp, vp]),
             "or_reach_register": (ctypes.c_int, [i32, vp, vp, vp, i32, u64, i64, vp, vp, vp]),
             "or_seed_sigma": (ctypes.c_int, [i32, vp, vp, vp, i32, u64, i32, vp, vp]),
             "or_first_sweep_sample": (i64, [i32, vp, vp, vp, i32, u64, i32, i32, vp, vp]),
@@ -134,8 +134,9 @@ def estimate(M: np.ndarray) -> np.ndarray:
     return out
 
 
-def simulate(n, offsets, targets, probs, J, seed, blocked=None, M=None):
-    """Alg. 2 to the fixpoint.  Returns (M, stats dict incl. per-sweep changed counts)."""
+def simulate(n, offsets, targets, probs, J, seed, blocked=None, M=None, eps_c=0.0):
+    """Alg. 2 (synchronous sweeps) while |L|/|V| > eps_c; eps_c = 0: to the fixpoint.
+    Returns (M, stats dict incl. per-sweep changed counts)."""
     offsets, targets, probs = _csr(offsets, targets, probs)
     sv, sj, X = salts(seed, J)
     if M is None:
@@ -147,14 +148,14 @@ def simulate(n, offsets, targets, probs, J, seed, blocked=None, M=None):
     st = SimStats()
     cap = 100000
     log = np.zeros(cap, dtype=np.int32)
-    rc = _load().or_simulate(n, _p(offsets), _p(targets), _p(probs), J, _p(X), _p(blocked), _p(M), ctypes.byref(st), _p(log), cap)
+    rc = _load().or_simulate(n, _p(offsets), _p(targets), _p(probs), J, _p(X), _p(blocked), _p(M), ctypes.byref(st), _p(log), cap, float(eps_c))
     if rc != 0:
         raise MemoryError(rc)
     return M, {"sweeps": st.sweeps, "processed_edges": st.processed_edges,
                "processed_vertices": st.processed_vertices, "changed": log[: min(st.sweeps, cap)].tolist()}
 
 
-def select_seeds(n, offsets, targets, probs, J, seed, K, eps_l, eps_g=None, want_vis=False, want_final=False):
+def select_seeds(n, offsets, targets, probs, J, seed, K, eps_l, eps_g=None, want_vis=False, want_final=False, eps_c=0.0):
     """Alg. 1.  Returns dict(seeds, scores, steps[list of dict], stats, vis?, M_final?)."""
     if eps_g is None:
         eps_g = eps_l
@@ -165,7 +166,7 @@ def select_seeds(n, offsets, targets, probs, J, seed, K, eps_l, eps_g=None, want
     vis = np.zeros((n, J), dtype=np.uint8) if want_vis else None
     Mf = np.zeros((n, J), dtype=np.uint8) if want_final else None
     st = SelectStats()
-    rc = _load().or_select_seeds(n, _p(offsets), _p(targets), _p(probs), J, seed, K, float(eps_l), float(eps_g),
+    rc = _load().or_select_seeds(n, _p(offsets), _p(targets), _p(probs), J, seed, K, float(eps_l), float(eps_g), float(eps_c),
                                  _p(seeds), _p(scores), ctypes.cast(log, ctypes.c_void_p), _p(vis), _p(Mf), ctypes.byref(st))
     if rc != 0:
         raise MemoryError(rc)

@@ -8,7 +8,7 @@
  *
  * Every function follows the paper's definition or algorithm step by step, in
  * the paper's order and notation, with the readings of DESIGN.md "Readings"
- * (R1..R21) where the paper is silent or garbled.  No blocking, fusion or
+ * (R1..R22) where the paper is silent or garbled.  No blocking, fusion or
  * reordering: registers are u8 per (vertex, simulation), blocked/visited flags
  * are one byte per (vertex, simulation), the live test is the double-precision
  * division of Eq. 5 evaluated per (edge, simulation).
@@ -20,7 +20,10 @@
  *   or_live        <- closed forms (w=0, w=1), binomial rate, 1-(1-w)^J
  *   or_init        <- sklearn murmur + Python bit_length (independent clz)
  *   or_simulate    <- brute force: per-simulation BFS on explicitly sampled subgraphs
- *                     (register = max init register over the reach set), Fig. 5 shape
+ *                     (register = max init register over the reach set), Fig. 5 shape;
+ *                     eps_c > 0: after s synchronous sweeps the register is the max init
+ *                     register within s hops (hop distances by scipy's shortest_path), and the
+ *                     run stops at the first s with |changed_s| <= eps_c * n
  *   or_estimate    <- closed forms of Eq. 2 (all-0 -> 1.29281, all-10 -> 1323.84)
  *   or_select      <- star / two-star / K=1 reductions, t=0 / t=inf variants,
  *                     sigma vs brute-force BFS, invariants (monotone sigma, ...)
@@ -193,10 +196,12 @@ typedef struct {
 } or_sim_stats;
 
 /*
- * Alg. 2 Simulate(G, M, J, R_S) with eps_c = 0 (R11) and the
- * synchronous reading of Fig. 5: every sweep reads the
- * registers as they were when the sweep started.
- *   L <- V; while L != {}:
+ * Alg. 2 Simulate(G, M, J, R_S) with the early-exit threshold eps_c
+ * (the loop runs while |L|/|V| > eps_c; eps_c = 0 is the exact fixpoint,
+ * R11) and the synchronous reading of Fig. 5: every sweep reads the
+ * registers as they were when the sweep started (R22: with eps_c > 0 the result depends on
+ * the schedule, and this one is the paper's figure's).
+ *   L <- V; while |L| / |V| > eps_c:
  *     for u in Gamma^-(L) (R10: in-neighbours of L; the first sweep processes all of V):
  *       for e_{u,v} in A(u): for j: if P(u,v)_j < w_uv and u not in R_S[j]:
  *           M_u[j] <- max(M_u[j], M_v[j])        (R9: pull into u from out-neighbour v)
@@ -207,7 +212,7 @@ typedef struct {
  */
 int or_simulate(int32_t n, const int32_t *offsets, const int32_t *targets, const float *probs, int32_t J,
                 const uint32_t *X, const uint8_t *blocked, uint8_t *M, or_sim_stats *stats,
-                int32_t *change_log, int32_t change_cap) {
+                int32_t *change_log, int32_t change_cap, double eps_c) {
     int64_t m = offsets[n];
     uint32_t *h = (uint32_t *)malloc((size_t)(m ? m : 1) * sizeof(uint32_t));
     uint8_t *Mold = (uint8_t *)malloc((size_t)n * (size_t)J);
@@ -221,7 +226,7 @@ int or_simulate(int32_t n, const int32_t *offsets, const int32_t *targets, const
     int64_t Lsize = n;
     or_sim_stats st = {0, 0, 0};
     int first = 1;
-    while (Lsize > 0) { /* eps_c = 0: while |L| / |V| > 0 */
+    while ((double)Lsize / (double)n > eps_c) { /* Alg. 2 line 3 */
         memcpy(Mold, M, (size_t)n * (size_t)J);
         memset(inLnext, 0, (size_t)n);
         int64_t next = 0;
@@ -319,7 +324,7 @@ typedef struct {
  * at return (after the last executed rebuild, or the first build if none ran).
  */
 int or_select_seeds(int32_t n, const int32_t *offsets, const int32_t *targets, const float *probs, int32_t J,
-                    uint64_t seed, int32_t K, double eps_l, double eps_g, int32_t *out_seeds, double *out_scores,
+                    uint64_t seed, int32_t K, double eps_l, double eps_g, double eps_c, int32_t *out_seeds, double *out_scores,
                     or_step *log, uint8_t *vis_out, uint8_t *M_final, or_select_stats *sstats) {
     int64_t m = offsets[n];
     uint32_t seed_v, seed_j;
@@ -339,7 +344,7 @@ int or_select_seeds(int32_t n, const int32_t *offsets, const int32_t *targets, c
 
     /* lines 2-6: init + Simulate(G, M, J, {}) */
     or_init_registers(n, J, seed_v, seed_j, M);
-    or_simulate(n, offsets, targets, probs, J, X, NULL, M, &st, NULL, 0);
+    or_simulate(n, offsets, targets, probs, J, X, NULL, M, &st, NULL, 0, eps_c);
     ss.builds++;
     ss.total_sweeps += st.sweeps;
     ss.total_processed_edges += st.processed_edges;
@@ -393,7 +398,7 @@ int or_select_seeds(int32_t n, const int32_t *offsets, const int32_t *targets, c
         } else if (k < K - 1) {
             /* lines 21-27 (R18: skipped after the last pick, it cannot change the output) */
             or_init_registers(n, J, seed_v, seed_j, M);
-            or_simulate(n, offsets, targets, probs, J, X, vis, M, &st, NULL, 0);
+            or_simulate(n, offsets, targets, probs, J, X, vis, M, &st, NULL, 0, eps_c);
             ss.builds++;
             ss.total_sweeps += st.sweeps;
             ss.total_processed_edges += st.processed_edges;

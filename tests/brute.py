@@ -106,6 +106,23 @@ def registers(n, offsets, targets, probs, J, seed, blocked=None) -> np.ndarray:
     return out
 
 
+def khop_registers(n, offsets, targets, probs, J, seed, hops, blocked=None) -> np.ndarray:
+    """Registers after `hops` synchronous sweeps, in closed form: M[u][j] = max init register over
+    the vertices within `hops` hops of u in the sampled subgraph G_j (hop distances from scipy)."""
+    from scipy.sparse import csr_matrix
+    from scipy.sparse.csgraph import shortest_path
+
+    _, _, X = salts(seed, J)
+    L = live_matrix(offsets, targets, probs, X)
+    init = init_registers(n, J, seed).astype(np.int64)
+    out = np.zeros((n, J), dtype=np.uint8)
+    for j in range(J):
+        A = sample_adjacency(n, offsets, targets, L, j, blocked)
+        D = shortest_path(csr_matrix(A.astype(np.float64)), unweighted=True, directed=True)
+        out[:, j] = np.max(np.where(D <= hops, init[None, :, j], 0), axis=1)
+    return out
+
+
 def reach_masks(n, offsets, targets, probs, J, seed, seeds) -> np.ndarray:
     """bool [n, J]: v reachable from the seed set in sample j (no blocking)."""
     _, _, X = salts(seed, J)

@@ -186,6 +186,60 @@ def test_simulate_with_blocked_equals_bruteforce():
         assert np.array_equal(M, brute.registers(n, off, tgt, pr, J, seed, blocked=blocked.astype(bool)))
 
 
+@pytest.mark.parametrize("eps_c", [0.02, 0.05, 0.15, 0.4])
+def test_simulate_early_exit_equals_khop_closed_form(eps_c):
+    """Alg. 2 with the early exit eps_c (reading R22, synchronous sweeps): the run
+    stops after the first sweep s with |changed_s| / n <= eps_c, and the registers are then the max
+    init register within s hops in each sampled subgraph (closed form via hop distances)."""
+    rng = np.random.default_rng(int(eps_c * 1000))
+    hit_early = 0
+    for g in range(12):
+        n = int(rng.integers(20, 90))
+        off, tgt, pr = brute.random_graph(rng, n, int(rng.integers(n, 4 * n)), float(rng.choice([0.2, 0.5, 1.0])))
+        J, seed = 32, int(rng.integers(0, 2**32))
+        blocked = (rng.random((n, J)) < 0.2).astype(np.uint8) if g % 3 == 2 else None
+        M, st = oracle.simulate(n, off, tgt, pr, J, seed, blocked=blocked, eps_c=eps_c)
+        bl = None if blocked is None else blocked.astype(bool)
+        prev = brute.init_registers(n, J, seed)
+        changed = []
+        for s in range(1, n + 2):
+            cur = brute.khop_registers(n, off, tgt, pr, J, seed, s, blocked=bl)
+            changed.append(int(np.any(cur != prev, axis=1).sum()))
+            prev = cur
+            if changed[-1] / n <= eps_c:
+                break
+        assert st["sweeps"] == s and st["changed"] == changed, (g, st, changed)
+        assert np.array_equal(M, cur), g
+        hit_early += changed[-1] > 0
+    assert hit_early > 0  # some runs stopped before the fixpoint
+
+
+def test_simulate_early_exit_limits():
+    """eps_c >= 1: the loop condition |V|/|V| > eps_c fails at once, registers stay at init; eps_c = 0
+    is the fixpoint (the ordinary build)."""
+    rng = np.random.default_rng(77)
+    n = 40
+    off, tgt, pr = brute.random_graph(rng, n, 120, 0.5)
+    M, st = oracle.simulate(n, off, tgt, pr, 32, 3, eps_c=1.0)
+    assert st["sweeps"] == 0 and np.array_equal(M, oracle.init_registers(n, 32, 3))
+    M0, _ = oracle.simulate(n, off, tgt, pr, 32, 3)
+    Me, _ = oracle.simulate(n, off, tgt, pr, 32, 3, eps_c=0.0)
+    assert np.array_equal(M0, Me) and np.array_equal(M0, brute.registers(n, off, tgt, pr, 32, 3))
+
+
+def test_select_with_early_exit_reduction():
+    """K = 1, t = inf with eps_c > 0: the seed is the argmax row sum of the early-exit registers."""
+    rng = np.random.default_rng(78)
+    for g in range(5):
+        n = int(rng.integers(30, 80))
+        off, tgt, pr = brute.random_graph(rng, n, 3 * n, 0.5)
+        J, seed = 32, int(rng.integers(0, 2**32))
+        M, _ = oracle.simulate(n, off, tgt, pr, J, seed, eps_c=0.1)
+        r = oracle.select_seeds(n, off, tgt, pr, J, seed, 1, math.inf, eps_c=0.1)
+        rows = M.astype(np.int64).sum(axis=1)
+        assert r["seeds"][0] == int(np.argmax(rows)) and r["steps"][0]["score"] == rows.max()
+
+
 def test_simulate_special_cases():
     """No edges -> M unchanged after one sweep; path a->b->c with w = 1 -> pairwise max."""
     n, J, seed = 5, 64, 3
