@@ -85,6 +85,7 @@ typedef struct {
     double sweep_alg_bytes;    /* algorithmic bytes of all sweeps in the window */
     int32_t J_total;           /* simulations of the whole job (== J unless sharded) */
     int32_t j0;                /* global index of this context's first simulation (0 unless sharded) */
+    double eps_c;              /* early-exit threshold the current sketches were built with (im_set_policy) */
 } im_stats;
 
 /*
@@ -167,6 +168,23 @@ int im_select_seeds(int32_t K, double err_threshold, int32_t *out_seeds, double 
 /* Same with separate local / global thresholds. */
 int im_select_seeds_ex(int32_t K, double eps_l, double eps_g, int32_t *out_seeds, double *out_scores);
 
+/*
+ * Selection policy.  Persists across calls and loads; the default
+ * (NaN, NaN, 0) is the behaviour described above.
+ * eps_l, eps_g : local / global error thresholds of the keep test (Alg. 1 line 18, PAPER.md:288-290,
+ *                413) used by im_select_seeds instead of its err_threshold; NaN = use err_threshold.
+ *                Must be >= 0 or NaN.  im_select_seeds_ex always uses its own arguments.
+ * eps_c        : early-exit threshold of Simulate (Alg. 2 line 3): sweeps run while
+ *                |L|/|V| > eps_c, L = vertices changed by the last sweep.  0 = to the fixpoint
+ *                (reading R11).  eps_c > 0 switches to synchronous sweeps (every sweep reads the
+ *                registers as they were when it started, Fig. 5, reading R22; +n*J bytes of device
+ *                memory) so the early-exit state is well defined; it applies to im_build_sketches*
+ *                and to every rebuild, and im_select_seeds* rebuilds first when the held sketches
+ *                were built with another eps_c.  In [0, 1]; 1 runs no sweep (registers = init).
+ * IM_EINVAL on out-of-range values (policy unchanged).
+ */
+int im_set_policy(double eps_l, double eps_g, double eps_c);
+
 /* ---- test / diagnostic extras ---- */
 /* registers after the most recent Simulate, HOST uint8[n*J] row-major, simulation order j = 0..J-1 */
 int im_get_registers(uint8_t *out);
@@ -183,7 +201,7 @@ int im_set_stream(void *cuda_stream);
 int64_t im_kernel_launch_count(void);
 void im_free(void);
 const char *im_last_error(void);
-/* ABI version (major*100 + minor): 101 adds sharding (im_build_sketches_shard, im_set_allreduce) */
+/* ABI version (major*100 + minor): 101 adds sharding (im_build_sketches_shard, im_set_allreduce), 102 im_set_policy */
 int32_t im_version(void);
 
 #ifdef __cplusplus

@@ -68,6 +68,7 @@ def _load():
             "or_select_seeds": (ctypes.c_int, [i32, vp, vp, vp, i32, u64, i32, f64, f64, f64, vp, vp, vp, vp, vp, vp]),
             "or_reach_register": (ctypes.c_int, [i32, vp, vp, vp, i32, u64, i64, vp, vp, vp]),
             "or_seed_sigma": (ctypes.c_int, [i32, vp, vp, vp, i32, u64, i32, vp, vp]),
+            "or_khop_register": (ctypes.c_int, [i32, vp, vp, vp, i32, u64, i32, i64, vp, vp, vp]),
             "or_first_sweep_sample": (i64, [i32, vp, vp, vp, i32, u64, i32, i32, vp, vp]),
             "or_seed_reach_per_sim": (ctypes.c_int, [i32, vp, vp, vp, i32, u64, i32, vp, i32, vp, vp]),
         }
@@ -187,6 +188,18 @@ def reach_register(n, offsets, targets, probs, J, seed, us, js) -> np.ndarray:
     js = np.ascontiguousarray(js, dtype=np.int32)
     out = np.empty(len(us), dtype=np.uint8)
     rc = _load().or_reach_register(n, _p(offsets), _p(targets), _p(probs), J, seed, len(us), _p(us), _p(js), _p(out))
+    if rc != 0:
+        raise MemoryError(rc)
+    return out
+
+
+def khop_register(n, offsets, targets, probs, J, seed, hops, us, js) -> np.ndarray:
+    """Definition of a first-build register after `hops` synchronous sweeps (eps_c > 0, R22)."""
+    offsets, targets, probs = _csr(offsets, targets, probs)
+    us = np.ascontiguousarray(us, dtype=np.int32)
+    js = np.ascontiguousarray(js, dtype=np.int32)
+    out = np.empty(len(us), dtype=np.uint8)
+    rc = _load().or_khop_register(n, _p(offsets), _p(targets), _p(probs), J, seed, int(hops), len(us), _p(us), _p(js), _p(out))
     if rc != 0:
         raise MemoryError(rc)
     return out

@@ -27,7 +27,7 @@
  *   or_estimate    <- closed forms of Eq. 2 (all-0 -> 1.29281, all-10 -> 1323.84)
  *   or_select      <- star / two-star / K=1 reductions, t=0 / t=inf variants,
  *                     sigma vs brute-force BFS, invariants (monotone sigma, ...)
- *   or_reach_register, or_seed_sigma <- brute force on small graphs
+ *   or_reach_register, or_khop_register, or_seed_sigma <- brute force on small graphs
  * The full greedy K-loop beyond these is "pinned by construction + invariants"
  * (the method is a heuristic with no closed form); see DESIGN.md "Parity".
  */
@@ -465,6 +465,50 @@ int or_reach_register(int32_t n, const int32_t *offsets, const int32_t *targets,
         out[p] = (uint8_t)best;
     }
     free(X); free(seen); free(queue);
+    return 0;
+}
+
+/*
+ * The plain definition of a register after `hops` synchronous sweeps of the first build (eps_c > 0,
+ * reading R22): the FM union over the vertices within `hops` hops of u in G_j,
+ *   M_u[j] = max_{w : dist_{G_j}(u, w) <= hops} clz(hash(w) xor hash(j)).
+ * Level-synchronous BFS for npairs (u, j) pairs.
+ */
+int or_khop_register(int32_t n, const int32_t *offsets, const int32_t *targets, const float *probs, int32_t J,
+                     uint64_t seed, int32_t hops, int64_t npairs, const int32_t *us, const int32_t *js, uint8_t *out) {
+    uint32_t seed_v, seed_j;
+    uint32_t *X = (uint32_t *)malloc((size_t)J * sizeof(uint32_t));
+    or_salts(seed, J, &seed_v, &seed_j, X);
+    uint8_t *seen = (uint8_t *)calloc((size_t)n, 1);
+    int32_t *queue = (int32_t *)malloc((size_t)n * sizeof(int32_t));
+    int32_t *depth = (int32_t *)malloc((size_t)n * sizeof(int32_t));
+    if (!X || !seen || !queue || !depth) return -3;
+    for (int64_t p = 0; p < npairs; p++) {
+        int32_t u = us[p], j = js[p];
+        uint32_t hj = hash_index((uint32_t)j, seed_j);
+        int64_t qh = 0, qt = 0;
+        int best = 0;
+        seen[u] = 1;
+        depth[u] = 0;
+        queue[qt++] = u;
+        while (qh < qt) {
+            int32_t x = queue[qh++];
+            int r = clz32(hash_index((uint32_t)x, seed_v) ^ hj);
+            if (r > best) best = r;
+            if (depth[x] == hops) continue;
+            for (int64_t e = offsets[x]; e < offsets[x + 1]; e++) {
+                int32_t y = targets[e];
+                if (!seen[y] && or_live(X[j], or_edge_hash(x, y), probs[e])) {
+                    seen[y] = 1;
+                    depth[y] = depth[x] + 1;
+                    queue[qt++] = y;
+                }
+            }
+        }
+        for (int64_t q = 0; q < qt; q++) seen[queue[q]] = 0;
+        out[p] = (uint8_t)best;
+    }
+    free(X); free(seen); free(queue); free(depth);
     return 0;
 }
 

@@ -46,6 +46,7 @@ class im_stats(ctypes.Structure):
         ("kernel_launches", ctypes.c_int64),
         ("argmax_full", ctypes.c_int32), ("argmax_lazy", ctypes.c_int32), ("sorted_rows", ctypes.c_int32), ("gather_sweeps", ctypes.c_int32),
         ("sweep_alg_bytes", ctypes.c_double), ("J_total", ctypes.c_int32), ("j0", ctypes.c_int32),
+        ("eps_c", ctypes.c_double),
     ]
 
 
@@ -74,6 +75,7 @@ SIGNATURES = {
 ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p)
 SIGNATURES["im_build_sketches_shard"] = (ctypes.c_int, [_i32, _u64, _i32, _i32])
 SIGNATURES["im_set_allreduce"] = (ctypes.c_int, [ALLREDUCE_FN, _vp])
+SIGNATURES["im_set_policy"] = (ctypes.c_int, [_f64, _f64, _f64])
 IM_ECOMM = -5
 IM_DTYPE_I32, IM_DTYPE_I64 = 0, 1
 
@@ -146,6 +148,10 @@ class Library:
 
         self._hook = ALLREDUCE_FN(tramp)
         self._check(self.L.im_set_allreduce(self._hook, None))
+
+    def im_set_policy(self, eps_l: float = float("nan"), eps_g: float = float("nan"), eps_c: float = 0.0) -> None:
+        """Alg. 1 thresholds used by im_select_seeds (NaN: its err_threshold) and Alg. 2's early exit."""
+        self._check(self.L.im_set_policy(float(eps_l), float(eps_g), float(eps_c)))
 
     def im_estimate(self, n: int) -> np.ndarray:
         out = np.empty(n, dtype=np.float64)

@@ -340,13 +340,31 @@ int setup_salts(int32_t Jt, int32_t j0, int32_t J, uint64_t seed) {
     return 0;
 }
 
-// Alg. 1 lines 2-5 / 21-25 + Alg. 2 to the fixpoint (eps_c = 0).  blocked: R_S = current visited bits.
+// Alg. 1 lines 2-5 / 21-25 + Alg. 2 (eps_c = 0: to the fixpoint).  blocked: R_S = current visited bits.
 // Sweep s consumes the items of the vertices changed in sweep s-1 (all in-edge segments for s = 1),
 // filters by their chunk-change bits bits[(s-1)&1], records its own changes in bits[s&1]; the
 // compaction then emits the next items and clears bits[(s-1)&1] for sweep s+1.
+// eps_c > 0 (R22): synchronous sweeps -- the first sweep gathers from init values (already
+// synchronous), later push sweeps read M_v from the pre-sweep copy Mold and k_commit refreshes it;
+// the loop stops once a sweep changed <= eps_c * n vertices (Alg. 2 line 3).
 int simulate(bool blocked) {
     auto t0 = clk::now();
     const size_t W = (size_t)g.J / 32;
+    const double eps_c = g.eps_c;
+    g.sync_sweeps = eps_c > 0.0;
+    if (g.sync_sweeps) TRY(dalloc(g.Mold, (size_t)g.n * g.J));
+    g.built_eps_c = eps_c;
+    if (!(1.0 > eps_c)) {  // |V|/|V| > eps_c fails: no sweep, registers stay at their init values
+        CK(launch_init_registers(g));
+        TRY(sync());
+        g.st.builds++;
+        g.st.last_build_sweeps = 0;
+        g.st.last_build_edges = 0;
+        g.st.last_build_ms = ms_since(t0);
+        g.built = true;
+        g.fresh = !blocked;
+        return 0;
+    }
     if (g.sweep_dirty)
         for (int i = 0; i < 2; i++) {
             CK(cudaMemsetAsync(g.bits[i], 0, (size_t)g.n * sizeof(uint32_t), g.stream));
@@ -360,6 +378,7 @@ int simulate(bool blocked) {
     int64_t edges_in = g.m;
     double alg = 0.0;
     int ngather = 0;
+    bool dirty = true;  // the last sweep left change bits set (early exit, or changed vertices without in-edges)
     const int4* items = g.ritems;
     int n_items = g.n_ritems;
     edges = g.m;
@@ -369,7 +388,7 @@ int simulate(bool blocked) {
         CK(cudaEventRecord(g.ev[0], g.stream));
         // direction-optimised: a frontier whose in-edges cover most of the graph is swept by a full
         // in-place gather (every row owned by one warp, no atomics); sparse frontiers are pushed
-        const bool gather = s > 1 && (double)edges_in > g.pull_frac * (double)g.m;
+        const bool gather = s > 1 && !g.sync_sweeps && (double)edges_in > g.pull_frac * (double)g.m;
         if (s == 1) {  // streaming register init, then the first sweep as a gather from init values
             CK(launch_init_registers(g));
             CK(cudaMemsetAsync(g.cm[1], 0, (size_t)g.n * W * sizeof(uint32_t), g.stream));
@@ -382,6 +401,10 @@ int simulate(bool blocked) {
             CK(launch_sweep(g, items, n_items, g.cm[(s - 1) & 1], g.cm[s & 1], g.bits[s & 1], ctr, blocked));
         CK(cudaEventRecord(g.ev[1], g.stream));
         CK(launch_compact(g, g.bits[s & 1], g.bits[(s - 1) & 1], g.cm[s & 1], g.cm[(s - 1) & 1], g.items[s & 1], ctr));
+        if (g.sync_sweeps) {  // Mold <- M (all rows after the first sweep, changed chunks after later ones)
+            if (s == 1) CK(cudaMemcpyAsync(g.Mold, g.M, (size_t)g.n * g.J, cudaMemcpyDeviceToDevice, g.stream));
+            else CK(launch_commit(g, g.bits[s & 1]));
+        }
         TRY(readback(ctr, sizeof hc, &hc));
         float t;
         CK(cudaEventElapsedTime(&t, g.ev[0], g.ev[1]));
@@ -402,12 +425,14 @@ int simulate(bool blocked) {
                     s, s == 1 ? "init+gather" : gather ? "gather" : "push", n_items, (long long)(s == 1 || gather ? g.m : (int64_t)edges_in),
                     hc.win_edges, hc.changed, hc.next_items, hc.next_edges, hc.big, t);
         edges_in = (int64_t)hc.next_edges;
-        if (hc.next_items == 0) break;
+        dirty = hc.changed > 0;  // this sweep's change bits stay set until the next sweep consumes them
+        if (!((double)hc.changed / (double)g.n > eps_c)) break;  // Alg. 2 line 3 (eps_c = 0: nothing changed)
+        if (hc.next_items == 0) break;                            // changed vertices without in-edges
         items = g.items[s & 1];
         n_items = hc.next_items;
         edges += (double)hc.next_edges > g.pull_frac * (double)g.m ? g.m : (int64_t)hc.next_edges;
     }
-    g.sweep_dirty = false;  // a completed build leaves every change buffer zero
+    g.sweep_dirty = dirty;  // a last sweep without changes leaves every change buffer zero
     g.st.builds++;
     g.st.last_build_sweeps = sweeps;
     g.st.last_build_edges = edges;
@@ -435,7 +460,7 @@ int build_fresh() {
 // =========================================================== C ABI
 extern "C" {
 
-int32_t im_version(void) { return 101; }
+int32_t im_version(void) { return 102; }
 
 const char* im_last_error(void) { return g_err.c_str(); }
 
@@ -582,8 +607,8 @@ int im_select_seeds_ex(int32_t K, double eps_l, double eps_g, int32_t* out_seeds
     g.st_argmax_full = g.st_argmax_list = 0;
     g.steps.clear();
     if (K == 0) return 0;
-    // start from S = {}, varsigma = 0, M_S' = 0 and freshly built sketches
-    if (!g.fresh) TRY(build_fresh());
+    // start from S = {}, varsigma = 0, M_S' = 0 and freshly built sketches (under the current eps_c)
+    if (!g.fresh || g.built_eps_c != g.eps_c) TRY(build_fresh());
     const size_t n = (size_t)g.n, W = (size_t)g.J / 32;
     CK(cudaMemsetAsync(g.vis, 0, n * W * sizeof(uint32_t), g.stream));
     CK(cudaMemsetAsync(g.inS, 0, n, g.stream));
@@ -673,7 +698,18 @@ int im_select_seeds_ex(int32_t K, double eps_l, double eps_g, int32_t* out_seeds
 }
 
 int im_select_seeds(int32_t K, double err_threshold, int32_t* out_seeds, double* out_scores) {
-    return im_select_seeds_ex(K, err_threshold, err_threshold, out_seeds, out_scores);
+    const double l = std::isnan(g.pol_l) ? err_threshold : g.pol_l, gg = std::isnan(g.pol_g) ? err_threshold : g.pol_g;
+    return im_select_seeds_ex(K, l, gg, out_seeds, out_scores);
+}
+
+int im_set_policy(double eps_l, double eps_g, double eps_c) {
+    if ((!std::isnan(eps_l) && eps_l < 0) || (!std::isnan(eps_g) && eps_g < 0))
+        return fail(IM_EINVAL, "eps_l / eps_g must be >= 0 or NaN (got %g, %g)", eps_l, eps_g);
+    if (std::isnan(eps_c) || eps_c < 0 || eps_c > 1) return fail(IM_EINVAL, "eps_c must be in [0, 1] (got %g)", eps_c);
+    g.pol_l = eps_l;
+    g.pol_g = eps_g;
+    g.eps_c = eps_c;
+    return 0;
 }
 
 static void unpermute_rows(const uint8_t* in, uint8_t* out, int64_t nrows) {
@@ -746,6 +782,7 @@ int im_get_stats(im_stats* out) {
     out->n = g.n;
     out->J = g.J;
     out->m = g.m;
+    out->eps_c = g.built ? g.built_eps_c : g.eps_c;
     return 0;
 }
 

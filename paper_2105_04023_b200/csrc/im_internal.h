@@ -71,6 +71,11 @@ struct Ctx {
     uint16_t* s12 = nullptr;    // [4097]
     int32_t* permd = nullptr;   // [J] internal index -> global simulation j (hash input of Eq. 1)
     uint8_t* M = nullptr;       // n*J registers, row-major, internal simulation order
+    uint8_t* Mold = nullptr;    // pre-sweep copy read by synchronous sweeps (eps_c > 0, R22), n*J
+    bool sync_sweeps = false;   // the running Simulate uses synchronous sweeps
+    // policy (im_set_policy): NaN eps_l / eps_g = the threshold of the select call
+    double pol_l = __builtin_nan(""), pol_g = __builtin_nan(""), eps_c = 0.0;
+    double built_eps_c = 0.0;   // eps_c of the sketches currently held
     uint32_t* vis = nullptr;    // n*(J/32) R_G(S) bits, internal order
     bool built = false, fresh = false, any_blocked = false;
     // sweep buffers
@@ -160,6 +165,7 @@ cudaError_t launch_init_registers(Ctx& c);
 // sweep 1); cm_out / bits_out: this sweep's change mask and chunk summary; counters in *ctr (zeroed)
 cudaError_t launch_sweep(Ctx& c, const int4* items, int n_items, const uint32_t* cm_in, uint32_t* cm_out,
                          uint32_t* bits_out, IterCounters* ctr, bool blocked);
+cudaError_t launch_commit(Ctx& c, const uint32_t* bits_new);
 cudaError_t launch_slices_big(Ctx& c, const int32_t* big, const uint32_t* mask, const int32_t* offs, const uint2* rec,
                               int4* items_out, IterCounters* ctr);
 // bits_out: this sweep's chunk-change bits (red.or); counters in *ctr (zeroed by the caller)

@@ -32,7 +32,8 @@ struct SweepArgs {
     const uint32_t* Xs;
     const uint16_t* s12;
     int J;
-    ull* M64;
+    ull* M64;                // registers written (M_u, bytewise-max CAS)
+    const ull* Mr64;         // registers read (M_v): == M64 (in place), or the pre-sweep copy (synchronous sweeps, R22)
     const uint32_t* vis;
     const uint32_t* cm_in;   // per-simulation change mask of the previous sweep, n x J/32 words (FILTER)
     uint32_t* cm_out;        // this sweep's per-simulation change mask
@@ -93,7 +94,7 @@ __device__ __forceinline__ uint32_t pull_word8(const SweepArgs& a, const uint32_
     ull live = live8<BLOCKED>(a, sX, u, w, h, T, lo, hi);
     if (!live) return 0u;
     const size_t J8 = (size_t)(a.J >> 3);
-    ull cand = a.M64[v * J8 + w] & live;
+    ull cand = a.Mr64[v * J8 + w] & live;
     if (!cand) return 0u;
     ull* p = &a.M64[u * J8 + w];
     return record8(a, u, w, vmax_cas8(p, __ldcg(p), cand));
@@ -193,7 +194,7 @@ __global__ void __launch_bounds__(BLOCK, 4) k_sweep(SweepArgs a) {
                 sparse[s] = lo[s] < hi[s] && hi[s] - lo[s] <= DENSE_WIN;
                 if (sparse[s]) {  // first word of the window: both loads in flight before any use
                     int w = lo[s] >> 3;
-                    mv[s] = a.M64[vv[s] * J8 + w];
+                    mv[s] = a.Mr64[vv[s] * J8 + w];
                     mu[s] = __ldcg(&a.M64[u[s] * J8 + w]);
                 }
             }
@@ -366,6 +367,7 @@ cudaError_t launch_sweep(Ctx& c, const int4* items, int n_items, const uint32_t*
     a.s12 = c.s12;
     a.J = c.J;
     a.M64 = reinterpret_cast<ull*>(c.M);
+    a.Mr64 = reinterpret_cast<const ull*>(c.sync_sweeps ? c.Mold : c.M);
     a.vis = c.vis;
     a.cm_in = cm_in;
     a.cm_out = cm_out;
@@ -380,6 +382,27 @@ cudaError_t launch_sweep(Ctx& c, const int4* items, int n_items, const uint32_t*
         if (ct) { if (blocked) sweep_inst<true, true, true>(grid, c.stream, a); else sweep_inst<true, false, true>(grid, c.stream, a); }
         else { if (blocked) sweep_inst<false, true, true>(grid, c.stream, a); else sweep_inst<false, false, true>(grid, c.stream, a); }
     }
+    return LAUNCHED(c);
+}
+
+// synchronous sweeps (R22): after a sweep, bring the read copy up to date -- copy every 32-simulation
+// chunk whose change bit is set (bits_new) from M to Mold, so Mold == M again for the next sweep
+__global__ void k_commit(int32_t n, int J, const uint32_t* __restrict__ bits_new, const uint4* __restrict__ M, uint4* Mold) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int C = J >> 4;  // 16-byte chunks per row
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += stride) {
+        for (uint32_t b = bits_new[v]; b; b &= b - 1) {
+            const int w = __ffs(b) - 1;
+            const int64_t i = v * C + 2 * w;
+            Mold[i] = M[i];
+            Mold[i + 1] = M[i + 1];
+        }
+    }
+}
+
+cudaError_t launch_commit(Ctx& c, const uint32_t* bits_new) {
+    k_commit<<<grid_for(c, c.n), BLOCK, 0, c.stream>>>(c.n, c.J, bits_new, reinterpret_cast<const uint4*>(c.M),
+                                                       reinterpret_cast<uint4*>(c.Mold));
     return LAUNCHED(c);
 }
 

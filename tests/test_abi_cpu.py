@@ -35,7 +35,7 @@ def test_library_loads_and_binds():
     L = im.lib()
     for name in declared_symbols():
         assert hasattr(L, name)
-    assert im.im_version() == 101
+    assert im.im_version() == 102
 
 
 def test_call_order_errors_without_gpu():

@@ -214,6 +214,21 @@ def test_simulate_early_exit_equals_khop_closed_form(eps_c):
     assert hit_early > 0  # some runs stopped before the fixpoint
 
 
+def test_khop_register_vs_closed_form():
+    """or_khop_register (sampled definition used at full size) vs the hop-distance closed form."""
+    rng = np.random.default_rng(79)
+    for g in range(6):
+        n = int(rng.integers(20, 70))
+        off, tgt, pr = brute.random_graph(rng, n, 3 * n, float(rng.choice([0.3, 0.7])))
+        J, seed = 32, int(rng.integers(0, 2**32))
+        for hops in (0, 1, 2, 4, n):
+            want = brute.khop_registers(n, off, tgt, pr, J, seed, hops)
+            us = np.repeat(np.arange(n), J)
+            js = np.tile(np.arange(J), n)
+            got = oracle.khop_register(n, off, tgt, pr, J, seed, hops, us, js).reshape(n, J)
+            assert np.array_equal(got, want), (g, hops)
+
+
 def test_simulate_early_exit_limits():
     """eps_c >= 1: the loop condition |V|/|V| > eps_c fails at once, registers stay at init; eps_c = 0
     is the fixpoint (the ordinary build)."""
