@@ -68,6 +68,9 @@ def _load():
             "or_select_seeds": (ctypes.c_int, [i32, vp, vp, vp, i32, u64, i32, f64, f64, f64, vp, vp, vp, vp, vp, vp]),
             "or_reach_register": (ctypes.c_int, [i32, vp, vp, vp, i32, u64, i64, vp, vp, vp]),
             "or_seed_sigma": (ctypes.c_int, [i32, vp, vp, vp, i32, u64, i32, vp, vp]),
+            "or_mix64": (u64, [u64]),
+            "or_mc_draw": (u32, [u64, i64, i32, i32]),
+            "or_mc_influence": (ctypes.c_int, [i32, vp, vp, vp, i32, vp, u64, i64, i64, vp]),
             "or_khop_register": (ctypes.c_int, [i32, vp, vp, vp, i32, u64, i32, i64, vp, vp, vp]),
             "or_first_sweep_sample": (i64, [i32, vp, vp, vp, i32, u64, i32, i32, vp, vp]),
             "or_seed_reach_per_sim": (ctypes.c_int, [i32, vp, vp, vp, i32, u64, i32, vp, i32, vp, vp]),
@@ -200,6 +203,27 @@ def khop_register(n, offsets, targets, probs, J, seed, hops, us, js) -> np.ndarr
     js = np.ascontiguousarray(js, dtype=np.int32)
     out = np.empty(len(us), dtype=np.uint8)
     rc = _load().or_khop_register(n, _p(offsets), _p(targets), _p(probs), J, seed, int(hops), len(us), _p(us), _p(js), _p(out))
+    if rc != 0:
+        raise MemoryError(rc)
+    return out
+
+
+def mix64(z: int) -> int:
+    return int(_load().or_mix64(z & 0xFFFFFFFFFFFFFFFF))
+
+
+def mc_draw(seed: int, r: int, u: int, v: int) -> int:
+    """31-bit fresh draw of edge (u,v) in evaluation sample r (reading R23)."""
+    return int(_load().or_mc_draw(seed & 0xFFFFFFFFFFFFFFFF, r, u, v))
+
+
+def mc_influence(n, offsets, targets, probs, seeds, seed, r0, R) -> np.ndarray:
+    """int64[K]: sum over samples r0..r0+R-1 of |R_{G_r}(first k+1 seeds)| with fresh randomness (R23)."""
+    offsets, targets, probs = _csr(offsets, targets, probs)
+    seeds = np.ascontiguousarray(seeds, dtype=np.int32)
+    out = np.zeros(len(seeds), dtype=np.int64)
+    rc = _load().or_mc_influence(n, _p(offsets), _p(targets), _p(probs), len(seeds), _p(seeds), seed & 0xFFFFFFFFFFFFFFFF,
+                                 int(r0), int(R), _p(out))
     if rc != 0:
         raise MemoryError(rc)
     return out

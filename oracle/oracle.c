@@ -8,7 +8,7 @@
  *
  * Every function follows the paper's definition or algorithm step by step, in
  * the paper's order and notation, with the readings of DESIGN.md "Readings"
- * (R1..R22) where the paper is silent or garbled.  No blocking, fusion or
+ * (R1..R23) where the paper is silent or garbled.  No blocking, fusion or
  * reordering: registers are u8 per (vertex, simulation), blocked/visited flags
  * are one byte per (vertex, simulation), the live test is the double-precision
  * division of Eq. 5 evaluated per (edge, simulation).
@@ -28,6 +28,9 @@
  *   or_select      <- star / two-star / K=1 reductions, t=0 / t=inf variants,
  *                     sigma vs brute-force BFS, invariants (monotone sigma, ...)
  *   or_reach_register, or_khop_register, or_seed_sigma <- brute force on small graphs
+ *   or_mix64       <- SplitMix64 published reference outputs (seed 0)
+ *   or_mc_influence<- closed forms (w = 0, w = 1 -> BFS reach, star 1 + L w, chain sum w^i within
+ *                     CLT bounds), draw uniformity / independence
  * The full greedy K-loop beyond these is "pinned by construction + invariants"
  * (the method is a heuristic with no closed form); see DESIGN.md "Parity".
  */
@@ -618,5 +621,67 @@ int or_seed_reach_per_sim(int32_t n, const int32_t *offsets, const int32_t *targ
         for (int64_t q = 0; q < qt; q++) seen[queue[q]] = 0;
     }
     free(X); free(seen); free(queue);
+    return 0;
+}
+
+/* ------------------------------------------------------------------ */
+/* Independent Monte-Carlo influence evaluator.     */
+/* ------------------------------------------------------------------ */
+
+/*
+ * The paper scores every seed set with an independent sample-then-diffuse oracle using fresh
+ * randomness.  Reading R23: the fresh value of edge (u,v) in sample r is a
+ * counter-based SplitMix64 draw (Steele, Lea, Flood 2014; restated) instead of an mt19937 stream,
+ * so that any sample can be evaluated independently:
+ *   z_e   = mix64(seed xor (u << 32 | v))
+ *   P_r   = (mix64(z_e + (r + 1) * 0x9E3779B97F4A7C15) >> 33) / h_max        (31-bit draw)
+ * and (u,v) is live in sample r iff P_r < w_uv -- the live test of Eq. 5 with the
+ * draw in place of X_r xor h(u,v).
+ */
+uint64_t or_mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+uint32_t or_mc_draw(uint64_t seed, int64_t r, int32_t u, int32_t v) {
+    uint64_t ze = or_mix64(seed ^ (((uint64_t)(uint32_t)u << 32) | (uint64_t)(uint32_t)v));
+    return (uint32_t)(or_mix64(ze + (uint64_t)(r + 1) * 0x9E3779B97F4A7C15ULL) >> 33);
+}
+
+/*
+ * out_counts[k] = sum over samples r = r0 .. r0+R-1 of |R_{G_r}({seeds_0 .. seeds_k})|: the
+ * influence of every prefix of the seed sequence, times R (mean = count / R).  One BFS per
+ * sample and seed, incremental over k (R_G(S) is closed under reachability).
+ */
+int or_mc_influence(int32_t n, const int32_t *offsets, const int32_t *targets, const float *probs, int32_t K,
+                    const int32_t *seeds, uint64_t seed, int64_t r0, int64_t R, int64_t *out_counts) {
+    uint8_t *seen = (uint8_t *)calloc((size_t)n, 1);
+    int32_t *queue = (int32_t *)malloc((size_t)n * sizeof(int32_t));
+    if (!seen || !queue) return -3;
+    for (int32_t k = 0; k < K; k++) out_counts[k] = 0;
+    for (int64_t r = r0; r < r0 + R; r++) {
+        int64_t qt = 0, qh = 0;
+        for (int32_t k = 0; k < K; k++) {
+            int32_t s = seeds[k];
+            if (!seen[s]) {
+                seen[s] = 1;
+                queue[qt++] = s;
+            }
+            while (qh < qt) {
+                int32_t x = queue[qh++];
+                for (int64_t e = offsets[x]; e < offsets[x + 1]; e++) {
+                    int32_t y = targets[e];
+                    if (!seen[y] && or_live(or_mc_draw(seed, r, x, y), 0u, probs[e])) {
+                        seen[y] = 1;
+                        queue[qt++] = y;
+                    }
+                }
+            }
+            out_counts[k] += qt;
+        }
+        for (int64_t q = 0; q < qt; q++) seen[queue[q]] = 0;
+    }
+    free(seen); free(queue);
     return 0;
 }

@@ -400,3 +400,71 @@ def test_rebuilt_registers_vs_bruteforce():
         assert np.array_equal(r["M_final"], brute.registers(n, off, tgt, pr, J, seed, blocked=blocked))
         M1, _ = oracle.simulate(n, off, tgt, pr, J, seed)
         assert (r["M_final"] <= M1).all()
+
+
+# ---------------------------------------------------------------- Monte-Carlo evaluator (f2, R23)
+def test_mix64_reference_outputs():
+    """SplitMix64 (Steele et al. 2014) seeded with 0: outputs mix64(k * golden gamma), k = 1, 2, 3."""
+    gamma = 0x9E3779B97F4A7C15
+    want = [0xE220A8397B1DCDAF, 0x6E789E6AA1B965F4, 0x06C45D188009454F]
+    assert [oracle.mix64(k * gamma) for k in (1, 2, 3)] == want
+
+
+def test_mc_draw_uniform_and_independent():
+    rng = np.random.default_rng(90)
+    N = 40000
+    us = rng.integers(0, 1 << 24, N)
+    vs = rng.integers(0, 1 << 24, N)
+    rs = rng.integers(0, 1 << 20, N)
+    d = np.array([oracle.mc_draw(7, int(r), int(u), int(v)) for r, u, v in zip(rs, us, vs)], np.float64)
+    assert d.max() < 2**31
+    x = d / 2**31
+    assert abs(x.mean() - 0.5) < 5 * math.sqrt(1 / 12 / N)
+    counts = np.histogram(x, bins=16, range=(0, 1))[0]
+    chi2 = ((counts - N / 16) ** 2 / (N / 16)).sum()
+    assert chi2 < 60  # 15 dof, p ~ 1e-6
+    d2 = np.array([oracle.mc_draw(7, int(r) + 1, int(u), int(v)) for r, u, v in zip(rs, us, vs)], np.float64) / 2**31
+    assert abs(np.corrcoef(x, d2)[0, 1]) < 5 / math.sqrt(N)
+    d3 = np.array([oracle.mc_draw(8, int(r), int(u), int(v)) for r, u, v in zip(rs, us, vs)], np.float64) / 2**31
+    assert abs(np.corrcoef(x, d3)[0, 1]) < 5 / math.sqrt(N)
+
+
+def test_mc_influence_closed_forms():
+    """w = 0: only the seeds; w = 1: the full BFS reach in every sample (a draw equal to h_max, the
+    only dead case, has probability 2^-31); star centre: E = 1 + L w; chain: E = sum_i w^i."""
+    rng = np.random.default_rng(91)
+    n = 60
+    off, tgt, _ = brute.random_graph(rng, n, 150, 1.0, allow_dups=False, allow_loops=False)
+    seeds = np.array([3, 17, 3 + 1, 40], np.int32)
+    R = 64
+    c0 = oracle.mc_influence(n, off, tgt, np.zeros(len(tgt), np.float32), seeds, 5, 0, R)
+    assert list(c0) == [R * (k + 1) for k in range(4)]
+    c1 = oracle.mc_influence(n, off, tgt, np.ones(len(tgt), np.float32), seeds, 5, 0, R)
+    A = np.zeros((n, n), bool)
+    for u in range(n):
+        A[u, tgt[off[u]:off[u + 1]]] = True
+    C = brute.closure(A)
+    assert list(c1) == [R * int(C[seeds[: k + 1]].any(axis=0).sum()) for k in range(4)]
+    L, w, R = 200, 0.1, 4000
+    off_s, tgt_s, pr_s = csr_from_edges(L + 1, star(L))
+    pr_s = np.full(len(tgt_s), w, np.float32)
+    mean = oracle.mc_influence(L + 1, off_s, tgt_s, pr_s, [0], 11, 0, R)[0] / R
+    assert abs(mean - (1 + L * w)) < 5 * math.sqrt(L * w * (1 - w) / R)
+    d, w = 8, 0.7
+    off_c = np.arange(d + 2, dtype=np.int32).clip(max=d)
+    tgt_c = np.arange(1, d + 1, dtype=np.int32)
+    mean = oracle.mc_influence(d + 1, off_c, tgt_c, np.full(d, w, np.float32), [0], 12, 0, R)[0] / R
+    want = sum(w**i for i in range(d + 1))
+    var = sum((2 * i + 1) * w**i for i in range(d + 1)) - want**2  # E[X^2] for X = 1 + number of live prefix edges
+    assert abs(mean - want) < 5 * math.sqrt(var / R)
+
+
+def test_mc_influence_sample_ranges_add_up():
+    """Counter-based samples: [0, R) = [0, a) + [a, R); counts are non-decreasing in k."""
+    rng = np.random.default_rng(92)
+    n = 80
+    off, tgt, pr = brute.random_graph(rng, n, 300, 0.3)
+    seeds = np.array([1, 5, 9], np.int32)
+    full = oracle.mc_influence(n, off, tgt, pr, seeds, 3, 0, 96)
+    parts = oracle.mc_influence(n, off, tgt, pr, seeds, 3, 0, 40) + oracle.mc_influence(n, off, tgt, pr, seeds, 3, 40, 56)
+    assert np.array_equal(full, parts) and all(np.diff(full) >= 0)
