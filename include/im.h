@@ -185,6 +185,21 @@ int im_select_seeds_ex(int32_t K, double eps_l, double eps_g, int32_t *out_seeds
  */
 int im_set_policy(double eps_l, double eps_g, double eps_c);
 
+/*
+ * Independent Monte-Carlo influence of a seed sequence: the paper scores every
+ * method with a sample-then-diffuse oracle on fresh randomness.  Sample r of
+ * edge (u,v) is live iff its counter-based SplitMix64 draw (reading R23) / h_max < w_uv,
+ * independent of the sketch salts; samples r0 .. r0+R-1 are evaluated (any range: ranks can split
+ * the samples and add the counts).
+ * K          : 0 <= K <= n; seeds: HOST int32[K] in [0, n) (repeats allowed).
+ * seed       : evaluation seed (use one unrelated to the sketch seed).
+ * r0, R      : r0 >= 0; R a positive multiple of 32 (run in batches of up to 512 samples).
+ * out_counts : HOST int64[K]; out_counts[k] = sum_r |R_{G_r}({seeds_0..seeds_k})|; the expected
+ *              influence estimate of the first k+1 seeds is out_counts[k] / R.
+ * Needs a loaded graph only (no sketches).  IM_EINVAL / IM_ESTATE / IM_ENOMEM / IM_ECUDA.
+ */
+int im_evaluate(int32_t K, const int32_t *seeds, uint64_t seed, int64_t r0, int64_t R, int64_t *out_counts);
+
 /* ---- test / diagnostic extras ---- */
 /* registers after the most recent Simulate, HOST uint8[n*J] row-major, simulation order j = 0..J-1 */
 int im_get_registers(uint8_t *out);

@@ -76,6 +76,7 @@ ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, c
 SIGNATURES["im_build_sketches_shard"] = (ctypes.c_int, [_i32, _u64, _i32, _i32])
 SIGNATURES["im_set_allreduce"] = (ctypes.c_int, [ALLREDUCE_FN, _vp])
 SIGNATURES["im_set_policy"] = (ctypes.c_int, [_f64, _f64, _f64])
+SIGNATURES["im_evaluate"] = (ctypes.c_int, [_i32, _vp, _u64, _i64, _i64, _vp])
 IM_ECOMM = -5
 IM_DTYPE_I32, IM_DTYPE_I64 = 0, 1
 
@@ -152,6 +153,13 @@ class Library:
     def im_set_policy(self, eps_l: float = float("nan"), eps_g: float = float("nan"), eps_c: float = 0.0) -> None:
         """Alg. 1 thresholds used by im_select_seeds (NaN: its err_threshold) and Alg. 2's early exit."""
         self._check(self.L.im_set_policy(float(eps_l), float(eps_g), float(eps_c)))
+
+    def im_evaluate(self, seeds, seed: int, R: int, r0: int = 0) -> np.ndarray:
+        """int64[K]: sum over samples r0..r0+R-1 of the reach of each seed prefix (fresh randomness)."""
+        s, ps = _host(seeds, np.int32)
+        out = np.zeros(max(len(s), 1), dtype=np.int64)
+        self._check(self.L.im_evaluate(len(s), ps if len(s) else None, seed & 0xFFFFFFFFFFFFFFFF, int(r0), int(R), out.ctypes.data))
+        return out[: len(s)].copy()
 
     def im_estimate(self, n: int) -> np.ndarray:
         out = np.empty(n, dtype=np.float64)

@@ -141,7 +141,9 @@ void release_all() {
     dfree(g.inS); dfree(g.MS); dfree(g.btag); dfree(g.nbits); dfree(g.gain); dfree(g.big); dfree(g.list); dfree(g.lcount); dfree(g.hist);
     dfree(g.off); dfree(g.fwd); dfree(g.fwdT); dfree(g.roff); dfree(g.rev); dfree(g.revT); dfree(g.ritems); dfree(g.fbig);
     dfree(g.ctr); dfree(g.rec); dfree(g.varsigma); dfree(g.key); dfree(g.first); dfree(g.sigma_count);
-    dfree(g.lval); dfree(g.sigma_g); dfree(g.bcount);
+    dfree(g.lval); dfree(g.sigma_g); dfree(g.bcount); dfree(g.Mold);
+    dfree(g.ev_vis); dfree(g.ev_nbits); dfree(g.ev_ctr); dfree(g.ev_count);
+    for (int i = 0; i < 2; i++) { dfree(g.ev_delta[i]); dfree(g.ev_items[i]); dfree(g.ev_vl[i]); }
     dfree(g.t_flags); dfree(g.t_indeg); dfree(g.t_nseg); dfree(g.t_scan); dfree(g.t_off); dfree(g.t_tgt); dfree(g.t_prob);
     dfree(g.t_est); dfree(g.t_rows); dfree(g.t_rowsout);
     for (int i = 0; i < 5; i++) dfree(g.t_prep[i]);
@@ -763,6 +765,61 @@ int im_get_reach(uint32_t* out) {
                 o[j >> 5] |= 1u << (j & 31);
             }
     }
+    return 0;
+}
+
+int im_evaluate(int32_t K, const int32_t* seeds, uint64_t seed, int64_t r0, int64_t R, int64_t* out_counts) {
+    if (!g.loaded) return fail(IM_ESTATE, "im_evaluate: no graph loaded");
+    if (K < 0 || K > g.n) return fail(IM_EINVAL, "K must be in [0, n] (got %d)", K);
+    if (r0 < 0 || R < 32 || R % 32) return fail(IM_EINVAL, "r0 >= 0 and R a positive multiple of 32 required (got %lld, %lld)",
+                                               (long long)r0, (long long)R);
+    if (K > 0 && (!seeds || !out_counts)) return fail(IM_EINVAL, "null pointer argument");
+    for (int k = 0; k < K; k++)
+        if (seeds[k] < 0 || seeds[k] >= g.n) return fail(IM_EINVAL, "seed %d out of range", k);
+    if (K == 0) return 0;
+    const int64_t l0 = g.launches;
+    const int B = (int)std::min<int64_t>(R, 512), Wb = B / 32;
+    const size_t n = (size_t)g.n;
+    bool fr = false;
+    TRY(dalloc(g.ev_vis, n * Wb));
+    for (int i = 0; i < 2; i++) {
+        TRY(dalloc(g.ev_delta[i], n * Wb, &fr));
+        if (fr) CK(cudaMemsetAsync(g.ev_delta[i], 0, n * Wb * sizeof(uint32_t), g.stream));
+        TRY(dalloc(g.ev_items[i], (size_t)g.n_fitems_cap + 1));
+        TRY(dalloc(g.ev_vl[i], n));
+    }
+    TRY(dalloc(g.ev_ctr, 2));
+    TRY(dalloc(g.ev_count, 1));
+    TRY(dalloc(g.ev_nbits, n, &fr));
+    if (fr) CK(cudaMemsetAsync(g.ev_nbits, 0, n * sizeof(uint32_t), g.stream));
+    std::vector<int64_t> acc(K, 0);
+    for (int64_t b0 = r0; b0 < r0 + R; b0 += B) {
+        const int Bb = (int)std::min<int64_t>(B, r0 + R - b0), W = Bb / 32;
+        CK(cudaMemsetAsync(g.ev_vis, 0, n * W * sizeof(uint32_t), g.stream));
+        CK(cudaMemsetAsync(g.ev_count, 0, sizeof(ull), g.stream));
+        for (int k = 0; k < K; k++) {
+            CK(cudaMemsetAsync(&g.ev_ctr[0], 0, sizeof(IterCounters), g.stream));
+            CK(launch_mc_start(g, seeds[k], W, g.ev_count));
+            CK(launch_bfs_items_raw(g, g.ev_vl[0], g.ev_items[0], &g.ev_ctr[0]));
+            IterCounters hc;
+            TRY(readback(&g.ev_ctr[0], sizeof hc, &hc));
+            int cur = 0;
+            while (hc.next_items > 0) {
+                const int n_items = hc.next_items, n_v = hc.changed;
+                CK(cudaMemsetAsync(&g.ev_ctr[cur ^ 1], 0, sizeof(IterCounters), g.stream));
+                CK(launch_mc_level(g, cur, n_items, W, seed, (ull)b0, g.ev_count));
+                CK(launch_bfs_clear_raw(g, n_v, W, g.ev_vl[cur], g.ev_delta[cur]));
+                TRY(readback(&g.ev_ctr[cur ^ 1], sizeof hc, &hc));
+                cur ^= 1;
+            }
+            if (hc.changed > 0) CK(launch_bfs_clear_raw(g, hc.changed, W, g.ev_vl[cur], g.ev_delta[cur]));
+            ull cnt;
+            TRY(readback(g.ev_count, sizeof cnt, &cnt));
+            acc[k] += (int64_t)cnt;  // cumulative over the prefix within this batch
+        }
+    }
+    memcpy(out_counts, acc.data(), K * sizeof(int64_t));
+    g.st.kernel_launches = g.launches - l0;
     return 0;
 }
 

@@ -111,6 +111,14 @@ struct Ctx {
     void* ar_user = nullptr;
     int32_t* lval = nullptr;     // packed local values of the lazy-list argmax [list capacity]
     ull* sigma_g = nullptr;      // sigma count summed over ranks
+    // Monte-Carlo evaluator (im_eval.cu): B-sample masks, frontier buffers
+    uint32_t* ev_vis = nullptr;
+    uint32_t* ev_delta[2] = {nullptr, nullptr};
+    int4* ev_items[2] = {nullptr, nullptr};
+    int32_t* ev_vl[2] = {nullptr, nullptr};
+    IterCounters* ev_ctr = nullptr;  // [2]
+    uint32_t* ev_nbits = nullptr;
+    ull* ev_count = nullptr;
     // reused temporaries (edge prep, host-pointer loads, diagnostics)
     int* t_flags = nullptr;
     int32_t* t_indeg = nullptr;
@@ -187,6 +195,13 @@ cudaError_t launch_bfs_level(Ctx& c, int cur, int n_items, uint32_t tag);
 cudaError_t launch_bfs_clear(Ctx& c, int cur, int n_v);
 cudaError_t launch_bfs_items(Ctx& c, int buf);
 cudaError_t launch_error_check(Ctx& c, int k, int K, double eps_l, double eps_g);
+cudaError_t launch_bfs_compact_raw(Ctx& c, int J, uint32_t* nbits, const uint32_t* dout, int32_t* vl, int4* items,
+                                   IterCounters* ctr, ull* count);
+cudaError_t launch_bfs_items_raw(Ctx& c, const int32_t* vl, int4* items, IterCounters* ctr);
+cudaError_t launch_bfs_clear_raw(Ctx& c, int n_v, int W, const int32_t* vl, uint32_t* delta);
+// Monte-Carlo evaluator (im_eval.cu)
+cudaError_t launch_mc_start(Ctx& c, int32_t s, int W, ull* count);
+cudaError_t launch_mc_level(Ctx& c, int cur, int n_items, int W, ull seed, ull r0, ull* count);
 cudaError_t launch_gather_rows(Ctx& c, const int32_t* rows, int64_t nrows, uint8_t* out);
 
 }  // namespace im

@@ -694,6 +694,21 @@ cudaError_t launch_bfs_items(Ctx& c, int buf) {
     if (e || !c.sorted_h) return e;
     return launch_slices_big(c, c.big, c.delta[buf], c.off, c.fwd, c.bitems[buf], &c.ctr[buf]);
 }
+// the same compaction / item / clear kernels on caller-chosen buffers, unsorted rows (evaluator, im_eval.cu)
+cudaError_t launch_bfs_compact_raw(Ctx& c, int J, uint32_t* nbits, const uint32_t* dout, int32_t* vl, int4* items,
+                                   IterCounters* ctr, ull* count) {
+    k_bfs_compact<<<grid_for(c, c.n), BLOCK, 0, c.stream>>>(c.n, J, false, nbits, dout, c.off, vl, items, nullptr, ctr, count);
+    return LAUNCHED(c);
+}
+cudaError_t launch_bfs_items_raw(Ctx& c, const int32_t* vl, int4* items, IterCounters* ctr) {
+    k_bfs_items<<<c.num_sms * 4, BLOCK, 0, c.stream>>>(false, vl, c.off, items, nullptr, ctr);
+    return LAUNCHED(c);
+}
+cudaError_t launch_bfs_clear_raw(Ctx& c, int n_v, int W, const int32_t* vl, uint32_t* delta) {
+    k_bfs_clear<<<grid_for(c, (int64_t)n_v * W), BLOCK, 0, c.stream>>>(n_v, W, vl, delta);
+    return LAUNCHED(c);
+}
+
 cudaError_t launch_bfs_clear(Ctx& c, int cur, int n_v) {
     int W = c.J >> 5;
     k_bfs_clear<<<grid_for(c, (int64_t)n_v * W), BLOCK, 0, c.stream>>>(n_v, W, c.bvl[cur], c.delta[cur]);
