@@ -109,6 +109,7 @@ int ensure_device() {
     g.max_blocks_bfs = std::max(1, bb) * g.num_sms;
     g.trace = getenv("IM_TRACE") != nullptr;
     if (const char* pf = getenv("IM_PULL_FRAC")) g.pull_frac = atof(pf);
+    if (const char* b = getenv("IM_BFS")) g.bfs2 = atoi(b) != 1;
     if (!g.own_stream) CK(cudaStreamCreateWithFlags(&g.own_stream, cudaStreamNonBlocking));
     if (!g.stream) g.stream = g.own_stream;
     if (!g.hpin) CK(cudaMallocHost(&g.hpin, 4096));
@@ -276,6 +277,9 @@ int alloc_sketch_state(int32_t J) {
     int bf = 0;
     CK((cudaError_t)setup_first(J, &bf));
     g.max_blocks_first = std::max(1, bf) * g.num_sms;
+    int b2 = 0;
+    CK((cudaError_t)occupancy_bfs2(J, &b2));
+    g.max_blocks_bfs2 = std::max(1, b2) * g.num_sms;
     TRY(dalloc(g.Xs, (size_t)J));
     TRY(dalloc(g.s12, 4097));
     TRY(dalloc(g.permd, (size_t)J));

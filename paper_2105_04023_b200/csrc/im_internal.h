@@ -138,7 +138,8 @@ struct Ctx {
     std::vector<im_step> steps;
     int64_t launches = 0;
     int st_argmax_full = 0, st_argmax_list = 0;
-    int max_blocks_sweep = 0, max_blocks_bfs = 0, max_blocks_first = 0;
+    int max_blocks_sweep = 0, max_blocks_bfs = 0, max_blocks_first = 0, max_blocks_bfs2 = 0;
+    bool bfs2 = true;  // k_bfs_level2 (IM_BFS=1: the original level kernel)
     cudaEvent_t ev[2] = {nullptr, nullptr};
 };
 
@@ -156,6 +157,7 @@ cudaError_t launch_compact(Ctx& c, const uint32_t* bits_new, uint32_t* bits_clea
                            uint32_t* cm_clear, int4* items_out, IterCounters* ctr);
 int occupancy_sweep(int* blocks_per_sm);
 int occupancy_bfs(int* blocks_per_sm);
+int occupancy_bfs2(int J, int* blocks_per_sm);
 int setup_first(int J, int* blocks_per_sm);  // smem opt-in + occupancy of the first-sweep kernel for this J
 // register init + first sweep (gather, im_first.cu): writes every row, its change mask and chunk bits
 cudaError_t launch_first(Ctx& c, uint32_t* cm_out, uint32_t* bits_out, IterCounters* ctr, bool blocked, bool from_memory);

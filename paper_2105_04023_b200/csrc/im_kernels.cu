@@ -446,6 +446,160 @@ __global__ void __launch_bounds__(BLOCK) k_bfs_level(BfsArgs a) {
     }
 }
 
+// Same level, reworked for memory-level parallelism (the level is bound by dependent random loads):
+// the Delta rows of a warp's 32 items are staged in shared memory once (coalesced), so an edge's
+// chain is record -> visited word only; edges are taken two per lane (e0, e0 + 32) and both visited
+// words are loaded before either is used.  Windows wider than DENSE_WIN go through the warp path.
+__device__ __forceinline__ void bfs_sparse(const uint32_t* sX, const uint32_t* dRow, uint32_t h, uint32_t T, int lo, int hi,
+                                           int& w0, uint32_t& nv0, uint32_t& nv1) {
+    w0 = lo >> 5;
+    const int w1 = (hi - 1) >> 5;
+    const uint32_t d0 = dRow[w0], d1 = w1 != w0 ? dRow[w1] : 0u;
+    nv0 = nv1 = 0u;
+    if (!(d0 | d1)) return;
+    for (int i = lo; i < hi; ++i) {
+        const uint32_t ok = (sX[i] ^ h) < T ? 1u : 0u;
+        if ((i >> 5) == w0) nv0 |= ok << (i & 31);
+        else nv1 |= ok << (i & 31);
+    }
+    nv0 &= d0;
+    nv1 &= d1;
+}
+
+template <bool CONST_T>
+__global__ void __launch_bounds__(BLOCK) k_bfs_level2(BfsArgs a) {
+    extern __shared__ uint32_t sDyn[];
+    __shared__ uint32_t sX[1024];
+    __shared__ uint16_t sS[4098];
+    __shared__ int sSlot[BLOCK / 32][32];
+    for (int i = threadIdx.x; i < a.J; i += blockDim.x) sX[i] = a.Xs[i];
+    for (int i = threadIdx.x; i < 4097; i += blockDim.x) sS[i] = a.s12[i];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, W = a.J >> 5;
+    uint32_t* sD = sDyn + (size_t)wib * 32 * W;  // Delta rows of this warp's 32 items
+    int base = 0, left = 0;  // 128-item grabs (4 batches of 32)
+    for (;;) {
+        if (left == 0) {
+            if (lane == 0) base = atomicAdd(&a.ctr_next->batch, 128);
+            base = __shfl_sync(IM_FULL, base, 0);
+            left = 4;
+        } else {
+            base += 32;
+        }
+        --left;
+        if (base >= a.n_items) break;
+        const int it = base + lane;
+        int u = 0, eb = 0, cnt = 0;
+        if (it < a.n_items) {
+            const int4 I = a.items[it];
+            u = I.x;
+            eb = I.y;
+            cnt = I.z - I.y;
+        }
+        __syncwarp();
+        for (int idx = lane; idx < 32 * W; idx += 32) {
+            const int i = idx / W, w = idx - i * W;
+            const int ui = __shfl_sync(IM_FULL, u, i);
+            sD[idx] = base + i < a.n_items ? a.din[(size_t)ui * W + w] : 0u;
+        }
+        __syncwarp();
+        const int incl = warp_incl_scan(cnt, lane);
+        const int total = __shfl_sync(IM_FULL, incl, 31);
+        const int start = incl - cnt;
+        int carry = 0;
+        for (int e0 = 0; e0 < total; e0 += 64) {
+            int own[2], ed[2];
+#pragma unroll
+            for (int s = 0; s < 2; s++) {  // owner item of edge e0 + 32 s + lane
+                const int b0 = e0 + 32 * s;
+                const bool starts = cnt > 0 && start >= b0 && start < b0 + 32;
+                if (starts) sSlot[wib][start - b0] = lane;
+                const uint32_t smask = __reduce_or_sync(IM_FULL, starts ? (1u << (start - b0)) : 0u);
+                __syncwarp();
+                const uint32_t below = smask & ((2u << lane) - 1u);
+                const int owner = below ? sSlot[wib][31 - __clz(below)] : carry;
+                __syncwarp();
+                carry = __shfl_sync(IM_FULL, owner, 31);
+                const int oeb = __shfl_sync(IM_FULL, eb, owner), ost = __shfl_sync(IM_FULL, start, owner);
+                own[s] = owner;
+                ed[s] = b0 + lane < total ? oeb + (b0 + lane - ost) : -1;
+            }
+            uint2 f[2];
+            uint32_t T[2];
+#pragma unroll
+            for (int s = 0; s < 2; s++) {
+                f[s] = ed[s] >= 0 ? a.fwd[ed[s]] : make_uint2(0, 0);
+                T[s] = ed[s] >= 0 ? (CONST_T ? a.T0 : a.fwdT[ed[s]]) : 0u;
+            }
+            int lo[2], hi[2], w0[2];
+            uint32_t nv0[2], nv1[2], x0[2], x1[2];
+            bool dense[2];
+#pragma unroll
+            for (int s = 0; s < 2; s++) {
+                lo[s] = hi[s] = 0;
+                nv0[s] = nv1[s] = 0u;
+                w0[s] = 0;
+                if (T[s]) edge_window(f[s].y, T[s], sX, sS, a.J, lo[s], hi[s]);
+                dense[s] = hi[s] - lo[s] > DENSE_WIN;
+                if (!dense[s] && lo[s] < hi[s]) bfs_sparse(sX, sD + own[s] * W, f[s].y, T[s], lo[s], hi[s], w0[s], nv0[s], nv1[s]);
+            }
+#pragma unroll
+            for (int s = 0; s < 2; s++) {  // both edges' visited words in flight
+                const size_t r = (size_t)f[s].x * W + w0[s];
+                x0[s] = nv0[s] ? __ldcg(&a.vis[r]) : 0u;
+                x1[s] = nv1[s] ? __ldcg(&a.vis[r + 1]) : 0u;
+            }
+#pragma unroll
+            for (int s = 0; s < 2; s++) {
+                const size_t r = (size_t)f[s].x * W + w0[s];
+                const uint32_t n0 = nv0[s] & ~x0[s], n1 = nv1[s] & ~x1[s];
+                if (n0) {
+                    atomicOr(&a.vis[r], n0);
+                    atomicOr(&a.dout[r], n0);
+                }
+                if (n1) {
+                    atomicOr(&a.vis[r + 1], n1);
+                    atomicOr(&a.dout[r + 1], n1);
+                }
+                if (n0 | n1) atomicOr(&a.nbits[f[s].x], (n0 ? 1u << w0[s] : 0u) | (n1 ? 2u << w0[s] : 0u));
+            }
+            // wide windows: one simulation per lane (as in k_bfs_level)
+#pragma unroll
+            for (int s = 0; s < 2; s++) {
+                uint32_t dmask = __ballot_sync(IM_FULL, dense[s]);
+                while (dmask) {
+                    const int l = __ffs(dmask) - 1;
+                    dmask &= dmask - 1;
+                    const uint32_t dv = __shfl_sync(IM_FULL, f[s].x, l), dh = __shfl_sync(IM_FULL, f[s].y, l);
+                    const uint32_t dT = __shfl_sync(IM_FULL, T[s], l);
+                    const int dlo = __shfl_sync(IM_FULL, lo[s], l), dhi = __shfl_sync(IM_FULL, hi[s], l);
+                    const int downer = __shfl_sync(IM_FULL, own[s], l);
+                    const int ww0 = dlo >> 5, ww1 = (dhi - 1) >> 5;
+                    uint32_t mylive = 0;
+                    int myw = -1;
+                    for (int w = ww0; w <= ww1; ++w) {
+                        const int i = 32 * w + lane;
+                        const uint32_t lv = __ballot_sync(IM_FULL, i >= dlo && i < dhi && (sX[i] ^ dh) < dT);
+                        if ((w & 31) == lane) {
+                            mylive = lv;
+                            myw = w;
+                        }
+                    }
+                    if (myw >= 0 && mylive) {
+                        uint32_t nv = sD[downer * W + myw] & mylive;
+                        if (nv) nv &= ~__ldcg(&a.vis[(size_t)dv * W + myw]);
+                        if (nv) {
+                            atomicOr(&a.vis[(size_t)dv * W + myw], nv);
+                            atomicOr(&a.dout[(size_t)dv * W + myw], nv);
+                            atomicOr(&a.nbits[dv], 1u << myw);
+                        }
+                    }
+                }
+            }
+        }
+    }
+}
+
 // Next BFS frontier: every vertex with new bits in this level (nbits != 0).  Counts the new
 // (vertex, simulation) pairs (popcount of the OR-ed Delta words) into sigma, lists the vertex (to
 // clear its Delta after the next level), emits its out-edge items (long rows of a hash-sorted
@@ -676,9 +830,16 @@ cudaError_t launch_bfs_level(Ctx& c, int cur, int n_items, uint32_t tag) {
     a.dout = c.delta[cur ^ 1];
     a.nbits = c.nbits;
     int64_t want = ((int64_t)n_items + 32 * (BLOCK / 32) - 1) / (32 * (BLOCK / 32));
-    int grid = (int)(want < 1 ? 1 : (want > c.max_blocks_bfs ? c.max_blocks_bfs : want));
-    if (c.constT) k_bfs_level<true><<<grid, BLOCK, 0, c.stream>>>(a);
-    else k_bfs_level<false><<<grid, BLOCK, 0, c.stream>>>(a);
+    if (c.bfs2) {
+        const size_t smem = (size_t)BLOCK * (c.J >> 5) * sizeof(uint32_t);
+        int grid = (int)(want < 1 ? 1 : (want > c.max_blocks_bfs2 ? c.max_blocks_bfs2 : want));
+        if (c.constT) k_bfs_level2<true><<<grid, BLOCK, smem, c.stream>>>(a);
+        else k_bfs_level2<false><<<grid, BLOCK, smem, c.stream>>>(a);
+    } else {
+        int grid = (int)(want < 1 ? 1 : (want > c.max_blocks_bfs ? c.max_blocks_bfs : want));
+        if (c.constT) k_bfs_level<true><<<grid, BLOCK, 0, c.stream>>>(a);
+        else k_bfs_level<false><<<grid, BLOCK, 0, c.stream>>>(a);
+    }
     cudaError_t e = LAUNCHED(c);
     if (e) return e;
     const int nxt = cur ^ 1;
@@ -726,6 +887,14 @@ cudaError_t launch_gather_rows(Ctx& c, const int32_t* rows, int64_t nrows, uint8
 
 int occupancy_bfs(int* blocks_per_sm) {
     return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_bfs_level<true>, BLOCK, 0);
+}
+// k_bfs_level2 for this J (dynamic shared memory: the Delta rows of every warp's 32 items)
+int occupancy_bfs2(int J, int* blocks_per_sm) {
+    const int smem = BLOCK * (J >> 5) * (int)sizeof(uint32_t);
+    cudaError_t e = cudaFuncSetAttribute(k_bfs_level2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (!e) e = cudaFuncSetAttribute(k_bfs_level2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e) return (int)e;
+    return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_bfs_level2<true>, BLOCK, smem);
 }
 
 }  // namespace im
