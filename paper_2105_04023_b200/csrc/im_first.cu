@@ -354,12 +354,19 @@ __global__ void __launch_bounds__(BLOCK) k_first_big(FirstArgs a) {
     if (lane == 0 && wcount) atomicAdd(&a.ctr->win_edges, (ull)wcount);
 }
 
+// In a gather sweep from memory (in place), the long rows go first: their vertices are the hubs most
+// other rows read, so the rest of the sweep already sees their new values (Gauss-Seidel order).
 template <bool C, bool B, bool MEM>
 static cudaError_t first_inst(Ctx& c, const FirstArgs& a) {
+    cudaError_t e;
+    const int gb = a.n_big < c.num_sms * 4 ? a.n_big : c.num_sms * 4;
+    if (MEM && a.n_big) {
+        k_first_big<C, B, MEM><<<gb, BLOCK, 0, c.stream>>>(a);
+        if ((e = LAUNCHED(c))) return e;
+    }
     k_first<C, B, MEM><<<c.max_blocks_first, BLOCK, 0, c.stream>>>(a);
-    cudaError_t e = LAUNCHED(c);
-    if (e || a.n_big == 0) return e;
-    k_first_big<C, B, MEM><<<a.n_big < c.num_sms * 4 ? a.n_big : c.num_sms * 4, BLOCK, 0, c.stream>>>(a);
+    if ((e = LAUNCHED(c)) || a.n_big == 0 || MEM) return e;
+    k_first_big<C, B, MEM><<<gb, BLOCK, 0, c.stream>>>(a);
     return LAUNCHED(c);
 }
 
