@@ -306,9 +306,16 @@ def main():
     alg_bytes = statistics.mean(algb)
     sweep_s = statistics.mean(sweep_ms) / 1e3
     achieved = alg_bytes / sweep_s / 1e9 if sweep_s > 0 else None
+    traffic, traffic_src = None, None
+    tfiles = sorted(f for f in os.listdir(os.path.join(ROOT, "profiles")) if f.endswith(f"_traffic_{args.config}.json")) \
+        if os.path.isdir(os.path.join(ROOT, "profiles")) else []
+    if tfiles:  # DRAM bytes of the same kernels per step, from the committed ncu capture (tools/ncu_summary.py traffic)
+        tj = json.load(open(os.path.join(ROOT, "profiles", tfiles[-1])))
+        traffic, traffic_src = tj["sweep"]["dram_bytes_per_step"], "profiles/" + tfiles[-1]
     roof = {"bound": "hbm", "kernel": "k_sweep (Simulate sweeps, all builds of the step)",
             "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak if achieved else None,
-            "peak_kind": peak_kind, "traffic": None,
+            "peak_kind": peak_kind, "traffic": traffic, "traffic_unit": "bytes per step (ncu dram__bytes_read.sum + dram__bytes_write.sum)",
+            "traffic_source": traffic_src,
             "alg_bytes_per_step": alg_bytes, "sweep_kernel_ms_per_step": statistics.mean(sweep_ms),
             "sweep_share_of_step": statistics.mean(sweep_ms) / ms,
             "unit_def": "DESIGN.md section 6: per enumerated edge 8 B record (+4 B threshold when w varies) + one 32 B register "

@@ -110,6 +110,197 @@ __global__ void k_fill_items(int32_t n, const int32_t* __restrict__ offs, const 
     for (int32_t s = b; s < e; s += SEG) items[p++] = make_int4(v, s, min(s + SEG, e), 0);
 }
 
+// ------------------------------------------------------------------ bucket-ordered rows (constant T)
+// With one threshold T (2^(B-1) < T <= 2^B) a row only has to be grouped by bucket b = h >> B
+// (KB = 31 - B bits); the order inside a bucket is immaterial (every consumer takes the slice of
+// a bucket range, im_device.cuh "hash-sorted adjacency ranges").  For KB <= 8 the forward rows
+// are ordered in place by a row-local counting sort instead of a full-width radix sort of m keys:
+//   k_rows       forward row u: h = Murmur3(u||v) mod 2^31 (Eq. 4), records {v, h} written in
+//                bucket order; at the edge's input position, the reverse sort key (v << KB) | b
+//                and payload {u, h} (coalesced; the radix sort of these is the transpose)
+//   radix sort   reverse records grouped by v, bucket-ordered inside (one LSD sort)
+//   k_row_bounds reverse offsets from the sorted keys (no in-degree atomics)
+// Rows of at most 32 edges are ranked inside one warp by a radix ballot; rows up to PREP_BIG by a
+// warp with a shared-memory histogram; longer rows by a whole block (k_rows_big).
+constexpr int PREP_BIG = 2048;
+constexpr int PREP_KB_MAX = 8;
+
+__global__ void k_list_long(int32_t n, const int32_t* __restrict__ off, int32_t* __restrict__ lf, int* count) {
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += stride)
+        if (off[u + 1] - off[u] > PREP_BIG) lf[atomicAdd(count, 1)] = (int32_t)u;
+}
+
+template <typename K>
+struct RowSortArgs {
+    int32_t n;
+    int B, KB;
+    const int32_t* off;     // forward row offsets
+    const int32_t* tgt;     // input targets (CSR order)
+    uint2* out;             // bucket-ordered forward records {v, h}
+    K* rkey;                // reverse sort keys (v << KB) | b, input order
+    uint2* rval;            // reverse payload {u, h}, input order
+    const int32_t* lst;     // k_rows_big: rows longer than PREP_BIG
+    const int* lcount;
+    int* batch;             // dynamic row-batch cursor (zeroed)
+};
+
+// record {v, h(u,v)} of input edge e of row u (+ its reverse key and payload on the first visit)
+template <typename K>
+__device__ __forceinline__ uint2 row_rec(const RowSortArgs<K>& a, int64_t e, uint32_t u, bool first) {
+    const uint32_t v = (uint32_t)a.tgt[e];
+    const uint32_t h = edge_hash(u, v);
+    if (first) {
+        a.rkey[e] = ((K)v << a.KB) | (K)(h >> a.B);
+        a.rval[e] = make_uint2(u, h);
+    }
+    return make_uint2(v, h);
+}
+
+// rank of this lane's key among the lanes of `act` (keys < mine, then equal keys of lower lanes)
+__device__ __forceinline__ int ballot_rank(uint32_t b, int KB, uint32_t act, int lane) {
+    uint32_t eq = act;
+    int less = 0;
+    for (int k = KB - 1; k >= 0; --k) {
+        const uint32_t bit = (b >> k) & 1u;
+        const uint32_t bk = __ballot_sync(IM_FULL, bit);
+        if (bit) {
+            less += __popc(eq & ~bk);
+            eq &= bk;
+        } else {
+            eq &= ~bk;
+        }
+    }
+    return less + __popc(eq & ((1u << lane) - 1u));
+}
+
+// exclusive scan of NB <= 256 shared counters by one warp (lane owns NB/32 consecutive bins)
+__device__ __forceinline__ void warp_scan_bins(int* hist, int NB, int lane) {
+    const int per = (NB + 31) >> 5;
+    int loc[8], s = 0;
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+        loc[q] = q < per && lane * per + q < NB ? hist[lane * per + q] : 0;
+        s += loc[q];
+    }
+    int run = warp_incl_scan(s, lane) - s;
+#pragma unroll
+    for (int q = 0; q < 8; q++)
+        if (q < per && lane * per + q < NB) {
+            hist[lane * per + q] = run;
+            run += loc[q];
+        }
+}
+
+template <typename K>
+__global__ void __launch_bounds__(BLOCK) k_rows(RowSortArgs<K> a) {
+    __shared__ int sH[BLOCK / 32][1 << PREP_KB_MAX];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    int* hist = sH[wib];
+    const int NB = 1 << a.KB;
+    for (;;) {
+        int base = 0;
+        if (lane == 0) base = atomicAdd(a.batch, 63);
+        base = __shfl_sync(IM_FULL, base, 0);
+        if (base >= a.n) break;
+        const int end = min(base + 63, a.n);  // 63 rows: their 64 offsets fit two lane registers
+        const int myoff = base + lane <= end ? a.off[base + lane] : 0;
+        const int myoff2 = base + 32 + lane <= end ? a.off[base + 32 + lane] : 0;
+        for (int u = base; u < end; ++u) {
+            const int i = u - base;
+            const int eb = i < 32 ? __shfl_sync(IM_FULL, myoff, i) : __shfl_sync(IM_FULL, myoff2, i - 32);
+            const int ee = i + 1 < 32 ? __shfl_sync(IM_FULL, myoff, i + 1) : __shfl_sync(IM_FULL, myoff2, i + 1 - 32);
+            const int d = ee - eb;
+            if (d == 0 || d > PREP_BIG) continue;  // warp-uniform
+            if (d <= 32) {
+                const bool have = lane < d;
+                uint2 r = make_uint2(0, 0);
+                if (have) r = row_rec(a, eb + lane, (uint32_t)u, true);
+                const int pos = ballot_rank(r.y >> a.B, a.KB, (d == 32 ? IM_FULL : (1u << d) - 1u), lane);
+                if (have) a.out[eb + pos] = r;
+                continue;
+            }
+            for (int q = lane; q < NB; q += 32) hist[q] = 0;
+            __syncwarp();
+            for (int e0 = eb; e0 < ee; e0 += 32) {  // pass 1: bucket counts
+                const bool have = e0 + lane < ee;
+                uint32_t b = 0xFFFFFFFFu;
+                if (have) b = row_rec(a, e0 + lane, (uint32_t)u, true).y >> a.B;
+                const uint32_t peers = __match_any_sync(IM_FULL, b);
+                if (have && lane == __ffs(peers) - 1) hist[b] += __popc(peers);
+                __syncwarp();
+            }
+            warp_scan_bins(hist, NB, lane);
+            __syncwarp();
+            for (int e0 = eb; e0 < ee; e0 += 32) {  // pass 2: place (stable)
+                const bool have = e0 + lane < ee;
+                uint2 r = make_uint2(0, 0);
+                uint32_t b = 0xFFFFFFFFu;
+                if (have) {
+                    r = row_rec(a, e0 + lane, (uint32_t)u, false);
+                    b = r.y >> a.B;
+                }
+                const uint32_t peers = __match_any_sync(IM_FULL, b);
+                if (have) a.out[eb + hist[b] + __popc(peers & ((1u << lane) - 1u))] = r;
+                __syncwarp();
+                if (have && lane == __ffs(peers) - 1) hist[b] += __popc(peers);
+                __syncwarp();
+            }
+        }
+    }
+}
+
+// rows longer than PREP_BIG: one block per row, shared-memory histogram, atomic placement
+template <typename K>
+__global__ void __launch_bounds__(BLOCK) k_rows_big(RowSortArgs<K> a) {
+    __shared__ int hist[1 << PREP_KB_MAX];
+    const int NB = 1 << a.KB;
+    const int cnt = *a.lcount;
+    for (int bi = blockIdx.x; bi < cnt; bi += gridDim.x) {
+        const uint32_t u = (uint32_t)a.lst[bi];
+        const int eb = a.off[u], ee = a.off[u + 1];
+        __syncthreads();
+        for (int i = threadIdx.x; i < NB; i += blockDim.x) hist[i] = 0;
+        __syncthreads();
+        for (int e0 = eb; e0 < ee; e0 += blockDim.x) {  // block-uniform trip count
+            const bool have = e0 + (int)threadIdx.x < ee;
+            uint32_t b = 0xFFFFFFFFu;
+            if (have) b = row_rec(a, e0 + threadIdx.x, u, true).y >> a.B;
+            const uint32_t peers = __match_any_sync(IM_FULL, b);
+            if (have && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[b], __popc(peers));
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) warp_scan_bins(hist, NB, threadIdx.x);
+        __syncthreads();
+        for (int e0 = eb; e0 < ee; e0 += blockDim.x) {
+            const bool have = e0 + (int)threadIdx.x < ee;
+            uint2 r = make_uint2(0, 0);
+            uint32_t b = 0xFFFFFFFFu;
+            if (have) {
+                r = row_rec(a, e0 + threadIdx.x, u, false);
+                b = r.y >> a.B;
+            }
+            const uint32_t peers = __match_any_sync(IM_FULL, b);
+            const int lane = threadIdx.x & 31, leader = __ffs(peers) - 1;
+            int p = 0;
+            if (have && lane == leader) p = atomicAdd(&hist[b], __popc(peers));
+            p = __shfl_sync(IM_FULL, p, leader);
+            if (have) a.out[eb + p + __popc(peers & ((1u << lane) - 1u))] = r;
+        }
+    }
+}
+
+// reverse offsets from the sorted keys (row = key >> KB): roff[v] = first position with row >= v
+template <typename K>
+__global__ void k_row_bounds(int64_t m, int32_t n, const K* __restrict__ keys, int KB, int32_t* __restrict__ roff) {
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= m; i += stride) {
+        const int64_t r = i < m ? (int64_t)(keys[i] >> KB) : (int64_t)n;
+        const int64_t p = i > 0 ? (int64_t)(keys[i - 1] >> KB) : -1;
+        for (int64_t v = p + 1; v <= r; ++v) roff[v] = (int32_t)i;
+    }
+}
+
 // ------------------------------------------------------------------ a2: register init
 // M_v[jj] = clz(Murmur3(v, seed_V) xor Murmur3(perm[jj], seed_J)), clz(0) = 32 (Alg. 1 lines 2-5; R5, R6).
 // One thread per 16 bytes (16 simulations) of a row: one Murmur3 per thread, one 16-byte store.
@@ -186,6 +377,41 @@ void prep_key_bits(const Ctx& c, int& KB, int& end_bit, bool& wide) {
     wide = end_bit > 32;
 }
 
+// the row-local bucket ordering applies (constant threshold, at most 2^PREP_KB_MAX buckets)
+static bool rows_path(const Ctx& c) { return c.sorted_h && 31 - c.B0 <= PREP_KB_MAX; }
+
+template <typename K>
+static cudaError_t prep_rows(Ctx& c, const int32_t* tgt, void** scr, size_t tb, int KB, int end_bit) {
+    cudaError_t e;
+    const int n = c.n;
+    int32_t* lf = (int32_t*)scr[0];
+    int* cnt = (int*)(lf + n);  // [0] long-row count, [1] batch cursor
+    if ((e = cudaMemsetAsync(cnt, 0, 2 * sizeof(int), c.stream))) return e;
+    k_list_long<<<grid_for(c, n), BLOCK, 0, c.stream>>>(n, c.off, lf, cnt);
+    if ((e = LAUNCHED(c))) return e;
+    RowSortArgs<K> a{};
+    a.n = n;
+    a.B = c.B0;
+    a.KB = KB;
+    a.off = c.off;
+    a.tgt = tgt;
+    a.out = c.fwd;
+    a.rkey = (K*)scr[1];
+    a.rval = (uint2*)scr[3];
+    a.lst = lf;
+    a.lcount = cnt;
+    a.batch = cnt + 1;
+    k_rows<K><<<c.num_sms * 8, BLOCK, 0, c.stream>>>(a);
+    if ((e = LAUNCHED(c))) return e;
+    k_rows_big<K><<<c.num_sms * 4, BLOCK, 0, c.stream>>>(a);
+    if ((e = LAUNCHED(c))) return e;
+    e = cub::DeviceRadixSort::SortPairs(scr[4], tb, (K*)scr[1], (K*)scr[2], (uint2*)scr[3], c.rev, (int)c.m, 0, end_bit, c.stream);
+    c.launches += (end_bit + 7) / 8 + 1;
+    if (e) return e;
+    k_row_bounds<K><<<grid_for(c, c.m + 1), BLOCK, 0, c.stream>>>(c.m, n, (const K*)scr[2], KB, c.roff);
+    return LAUNCHED(c);
+}
+
 // scratch sizes (bytes) the edge prep needs: [0] src, [1] mark/keys0, [2] keys1, [3] vals, [4] cub temp
 cudaError_t prep_scratch_sizes(Ctx& c, size_t* sz) {
     const size_t m = (size_t)(c.m ? c.m : 1);
@@ -193,7 +419,7 @@ cudaError_t prep_scratch_sizes(Ctx& c, size_t* sz) {
     bool wide;
     prep_key_bits(c, KB, end_bit, wide);
     const size_t ks = wide ? 8 : 4;
-    sz[0] = m * 4;
+    sz[0] = rows_path(c) ? ((size_t)c.n + 8) * 4 : m * 4;  // long-row list + counters, or the edge sources
     sz[1] = m * (c.sorted_h ? ks : 4);
     sz[2] = c.sorted_h ? m * ks : 4;
     sz[3] = c.sorted_h ? m * 8 : 8;
@@ -247,6 +473,12 @@ cudaError_t prep_edges(Ctx& c, const int32_t* tgt, const float* prob, int32_t* i
     size_t tb = sz[4];
     (void)scan_tmp_i;
     if ((e = cudaMemsetAsync(indeg, 0, ((size_t)c.n + 1) * sizeof(int32_t), c.stream))) return e;
+    if (rows_path(c) && c.m > 0) {
+        int KB, end_bit;
+        bool wide;
+        prep_key_bits(c, KB, end_bit, wide);
+        return wide ? prep_rows<ull>(c, tgt, scr, tb, KB, end_bit) : prep_rows<uint32_t>(c, tgt, scr, tb, KB, end_bit);
+    }
     if (m > 0) {
         if ((e = cudaMemsetAsync(mark, 0, (size_t)m * sizeof(int32_t), c.stream))) return e;
         k_row_markers<<<grid_for(c, c.n), BLOCK, 0, c.stream>>>(c.n, c.off, mark);

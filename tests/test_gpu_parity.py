@@ -85,10 +85,11 @@ def test_degenerate_graphs():
 @pytest.mark.parametrize("J", [32, 64, 96, 128, 256, 512, 1024])
 def test_registers_random_graphs(J):
     rng = np.random.default_rng(100 + J)
-    for g in range(6):
+    for g in range(7):
         n = int(rng.integers(2, 3000 if J <= 256 else 800))
         m = int(rng.integers(0, 6 * n))
-        p = [None, 0.005, 0.05, 0.3, 1.0, 0.01][g]
+        # 0.001: more than 2^8 hash buckets per row, the radix-sort edge prep (im_prep.cu)
+        p = [None, 0.005, 0.05, 0.3, 1.0, 0.01, 0.001][g]
         off, tgt, pr = brute.random_graph(rng, n, m, p)
         seed = int(rng.integers(0, 2**63))
         M = run_build(n, off, tgt, pr, J, seed)
@@ -118,7 +119,7 @@ def test_hub_and_wide_windows():
     off = np.cumsum(off).astype(np.int32)
     tgt = dst.astype(np.int32)
     indeg = np.bincount(tgt, minlength=n)
-    for pr in (np.full(len(tgt), 0.02, np.float32), (1.0 / indeg[tgt]).astype(np.float32)):
+    for pr in (np.full(len(tgt), 0.02, np.float32), np.full(len(tgt), 0.001, np.float32), (1.0 / indeg[tgt]).astype(np.float32)):
         for J in (64, 512):
             M = run_build(n, off, tgt, pr, J, 11)
             Mo, _ = oracle.simulate(n, off, tgt, pr, J, 11)

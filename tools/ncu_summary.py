@@ -61,5 +61,36 @@ def report(path):
             pass
 
 
+BYTES = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+# kernels inside the sweep kernel's CUDA-event window (im_abi.cu simulate(): init + first/gather/push sweeps)
+SWEEP_KERNELS = ("k_init_registers", "k_first", "k_first_big", "k_sweep")
+
+
+def traffic(path, config="c4"):
+    """DRAM bytes per kernel from an `ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,
+    gpu__time_duration.sum --csv` log of ONE hot-path step (tools/profile_step.py --what step); prints
+    the JSON bench.py reads for roofline.traffic (the sweep kernels' bytes per step)."""
+    import json
+    rows = [r for r in csv.reader(open(path)) if len(r) > 5]
+    hdr = rows[0]
+    ik, iid, im_, iv, iu = (hdr.index(x) for x in ("Kernel Name", "ID", "Metric Name", "Metric Value", "Metric Unit"))
+    per = collections.defaultdict(lambda: {"launches": set(), "dram_bytes": 0.0, "ms": 0.0})
+    for r in rows[1:]:
+        name = r[ik].split("(")[0].replace("void ", "").split("<")[0].replace("im::", "")
+        v = float(r[iv].replace(",", ""))
+        d = per[name]
+        d["launches"].add(r[iid])
+        if r[im_].startswith("dram__bytes_"):
+            d["dram_bytes"] += v * BYTES[r[iu]]
+        elif r[im_] == "gpu__time_duration.sum":
+            d["ms"] += v * UNIT[r[iu]]
+    out = {k: {"launches": len(d["launches"]), "dram_bytes": d["dram_bytes"], "ms": d["ms"]} for k, d in per.items()}
+    sw = [out[k] for k in SWEEP_KERNELS if k in out]
+    res = {"source": path, "config": config, "kernels": out,
+           "sweep": {"kernels": list(SWEEP_KERNELS), "dram_bytes_per_step": sum(x["dram_bytes"] for x in sw),
+                     "ms_per_step": sum(x["ms"] for x in sw), "launches": sum(x["launches"] for x in sw)}}
+    print(json.dumps(res, indent=1))
+
+
 if __name__ == "__main__":
-    {"launches": launches, "report": report}[sys.argv[1]](sys.argv[2])
+    {"launches": launches, "report": report, "traffic": traffic}[sys.argv[1]](*sys.argv[2:])
