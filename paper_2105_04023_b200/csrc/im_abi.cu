@@ -110,6 +110,7 @@ int ensure_device() {
     g.trace = getenv("IM_TRACE") != nullptr;
     if (const char* pf = getenv("IM_PULL_FRAC")) g.pull_frac = atof(pf);
     if (const char* b = getenv("IM_BFS")) g.bfs2 = atoi(b) != 1;
+    if (const char* lm = getenv("IM_LIST_MAX")) g.list_max = atoll(lm);
     if (!g.own_stream) CK(cudaStreamCreateWithFlags(&g.own_stream, cudaStreamNonBlocking));
     if (!g.stream) g.stream = g.own_stream;
     if (!g.hpin) CK(cudaMallocHost(&g.hpin, 4096));
@@ -624,7 +625,7 @@ int im_select_seeds_ex(int32_t K, double eps_l, double eps_g, int32_t* out_seeds
     std::vector<int32_t> seeds(K);
     std::vector<double> scores(K);
     bool pool_check = false, need_full = true;
-    const int T = (int)std::min<int64_t>(g.n, std::max<int64_t>(1024, std::min<int64_t>(65536, g.n / 256)));
+    const int T = (int)std::min<int64_t>(g.n, std::max<int64_t>(1024, std::min<int64_t>(g.list_max, g.n / 64)));
     int list_len = 0, theta = 0;
     for (int k = 0; k < K; k++) {
         // line 10: argmax over the pool (exact lazy evaluation, im_kernels.cu "a6")

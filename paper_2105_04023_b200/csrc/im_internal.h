@@ -85,6 +85,7 @@ struct Ctx {
     int32_t* big = nullptr;                  // long rows awaiting slicing
     bool sweep_dirty = true;   // change buffers may hold stale bits (fresh / aborted build)
     bool trace = false;        // IM_TRACE: per-sweep / per-level lines on stderr
+    int64_t list_max = 65536;  // cap of the lazy argmax candidate list length (IM_LIST_MAX)
     double pull_frac = 0.97;   // gather sweep when the push frontier's in-edges exceed this share of m (IM_PULL_FRAC)
     IterCounters* ctr = nullptr;   // [2]
     // selection buffers

@@ -59,6 +59,7 @@ __device__ __forceinline__ uint32_t sum16(uint4 m) {
 }
 
 constexpr int HIST_BINS = 4096;
+constexpr int CU = 8;  // vertex groups of BLOCK per block iteration of the frontier compactions
 constexpr int AG = 4;  // vertex groups in flight per warp in k_argmax
 
 // LIST = false: every vertex (full pass: stores gains + histogram); LIST = true: the vertices in list[0..*count)
@@ -610,9 +611,23 @@ __global__ void k_bfs_compact(int32_t n, int J, bool sorted, uint32_t* __restric
     const int lane = threadIdx.x & 31, W = J >> 5;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     ull newbits = 0;
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+    // CU vertex groups per block iteration, loaded up front (independent loads in flight): a level
+    // with few new vertices costs one pass over nbits, not a dependent load per 256 vertices
+    for (int64_t base0 = (int64_t)blockIdx.x * blockDim.x * CU; base0 < n; base0 += stride * CU) {
+      uint32_t bb[CU];
+      bool anyb = false;
+#pragma unroll
+      for (int k = 0; k < CU; k++) {
+          const int64_t v = base0 + (int64_t)k * blockDim.x + threadIdx.x;
+          bb[k] = v < n ? nbits[v] : 0u;
+          anyb |= bb[k] != 0u;
+      }
+      if (!__syncthreads_or(anyb)) continue;
+#pragma unroll 1
+      for (int k = 0; k < CU; k++) {
+        const int64_t base = base0 + (int64_t)k * blockDim.x;
         int64_t v = base + threadIdx.x;
-        uint32_t b = v < n ? nbits[v] : 0u;
+        uint32_t b = bb[k];
         if (!__syncthreads_or(b != 0u)) continue;  // block-uniform: nothing new in these 256 vertices
         int rb = 0, rd = 0, ns = 0;
         bool isbig = false;
@@ -638,6 +653,7 @@ __global__ void k_bfs_compact(int32_t n, int J, bool sorted, uint32_t* __restric
         int p = pos + ninc - ns;
         for (int s0 = rb; s0 < rb + rd && ns; s0 += SEG) items[p++] = make_int4((int)v, s0, min(s0 + SEG, rb + rd), 0);
         if (isbig) big[bpos + __popc(bmask & ((1u << lane) - 1u))] = (int32_t)v;
+      }
     }
     newbits = __reduce_add_sync(IM_FULL, (uint32_t)newbits);
     if (lane == 0 && newbits) {

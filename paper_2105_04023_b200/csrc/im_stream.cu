@@ -12,6 +12,7 @@ namespace im {
 constexpr int TS = 3;                 // pipeline stages
 constexpr int TILE_M = 24576;         // register bytes per tile (TV ~ TILE_M / J vertices; 2 blocks per SM fit)
 constexpr int HBINS = 4096;           // == HIST_BINS (im_kernels.cu)
+constexpr int TC = 8;                 // max 16-byte chunks per lane (J <= 1024, L = 8)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -82,12 +83,14 @@ __global__ void __launch_bounds__(BLOCK) k_argmax_tma(int32_t n, int32_t J, int 
             int t = blockIdx.x + s * gridDim.x;
             if (t < ntiles) issue(t, s);
         }
+    // L lanes per vertex (<= 8), chunk c of lane q = 16-byte chunk c*L + q of the row: the L lanes of a
+    // vertex read one contiguous 16*L-byte run per c (conflict-free), C <= TC chunks per lane
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, q = lane & (L - 1), sub = lane / L, VPW = 32 / L;
-    uint4 ms[2];
+    uint4 ms[TC];
     uint32_t msum = 0;
 #pragma unroll
-    for (int c = 0; c < 2; c++) {
-        int ci = q * C + c;
+    for (int c = 0; c < TC; c++) {
+        const int ci = c * L + q;
         ms[c] = (c < C && ci < nch) ? sMS[ci] : make_uint4(0, 0, 0, 0);
         msum += __vsadu4(ms[c].x, 0u) + __vsadu4(ms[c].y, 0u) + __vsadu4(ms[c].z, 0u) + __vsadu4(ms[c].w, 0u);
     }
@@ -104,8 +107,8 @@ __global__ void __launch_bounds__(BLOCK) k_argmax_tma(int32_t n, int32_t J, int 
             const bool ok = v < n;
             uint32_t gn = 0;
 #pragma unroll
-            for (int c = 0; c < 2; c++) {
-                int ci = q * C + c;
+            for (int c = 0; c < TC; c++) {
+                const int ci = c * L + q;
                 if (c < C && ci < nch) gn += gain16x2_s(reinterpret_cast<const uint4*>(tileM + (size_t)r * J)[ci], ms[c]);
             }
             gn -= msum;
@@ -156,10 +159,19 @@ __global__ void __launch_bounds__(BLOCK) k_argmax_tma(int32_t n, int32_t J, int 
         if (sHist[i]) atomicAdd(&hist[i], sHist[i]);
 }
 
+// a multiple of the vertices per warp (uniform warp loop) and of 16 (16-byte aligned bulk copies of
+// the TV*J register bytes and TV*J/8 visited bytes)
 static int tma_tv(int J, int L) {
-    const int step = 8 * (32 / L);
+    const int vpw = 32 / L, step = vpw > 16 ? vpw : 16;
     int tv = (TILE_M / J) / step * step;
     return tv < step ? step : tv;
+}
+// lanes per vertex and chunks per lane of the TMA pass: L = min(8, pow2 >= J/16), C = ceil(J/16 / L)
+static void tma_geometry(int J, int& L, int& C) {
+    const int nch = J >> 4;
+    L = 1;
+    while (L < 8 && L < nch) L <<= 1;
+    C = (nch + L - 1) / L;
 }
 
 static size_t tma_smem(int J, int TV, bool pool) {
@@ -178,6 +190,7 @@ int setup_argmax_tma() {
 }
 
 cudaError_t launch_argmax_tma(Ctx& c, bool pool, int L, int C, int shift) {
+    tma_geometry(c.J, L, C);
     const int TV = tma_tv(c.J, L), ntiles = (c.n + TV - 1) / TV;
     const int grid = ntiles < c.num_sms * 2 ? ntiles : c.num_sms * 2;
     const size_t smem = tma_smem(c.J, TV, pool);

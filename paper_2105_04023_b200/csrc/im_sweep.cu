@@ -264,17 +264,32 @@ __global__ void k_compact(int32_t n, int J, bool sorted, const uint32_t* __restr
                           int32_t* __restrict__ big, IterCounters* ctr) {
     const int lane = threadIdx.x & 31, W = J >> 5;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+    constexpr int CU = 8;  // vertex groups of BLOCK per block iteration, loaded up front
+    for (int64_t base0 = (int64_t)blockIdx.x * blockDim.x * CU; base0 < n; base0 += stride * CU) {
+      uint32_t bn[CU], bcl[CU];
+      bool anyn = false;
+#pragma unroll
+      for (int k = 0; k < CU; k++) {
+          const int64_t v = base0 + (int64_t)k * blockDim.x + threadIdx.x;
+          bn[k] = v < n ? bits_new[v] : 0u;
+          bcl[k] = v < n && bits_clear ? bits_clear[v] : 0u;
+          anyn |= bn[k] != 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < CU; k++) {
+          const int64_t v = base0 + (int64_t)k * blockDim.x + threadIdx.x;
+          uint32_t bc = bcl[k];
+          if (bc) {
+              bits_clear[v] = 0u;
+              for (; bc; bc &= bc - 1) cm_clear[(size_t)v * W + (__ffs(bc) - 1)] = 0u;
+          }
+      }
+      if (!__syncthreads_or(anyn)) continue;
+#pragma unroll 1
+      for (int k = 0; k < CU; k++) {
+        const int64_t base = base0 + (int64_t)k * blockDim.x;
         int64_t v = base + threadIdx.x;
-        bool in = v < n;
-        uint32_t b = in ? bits_new[v] : 0u;
-        if (in && bits_clear) {
-            uint32_t bc = bits_clear[v];
-            if (bc) {
-                bits_clear[v] = 0u;
-                for (; bc; bc &= bc - 1) cm_clear[(size_t)v * W + (__ffs(bc) - 1)] = 0u;
-            }
-        }
+        uint32_t b = bn[k];
         if (!__syncthreads_or(b != 0u)) continue;  // block-uniform: no changed vertex among these 256
         int rb = 0, rd = 0, ns = 0;
         bool isbig = false;
@@ -297,6 +312,7 @@ __global__ void k_compact(int32_t n, int J, bool sorted, const uint32_t* __restr
         int p = pos + ninc - ns;
         for (int s0 = rb; s0 < rb + rd && ns; s0 += SEG) items[p++] = make_int4((int)v, s0, min(s0 + SEG, rb + rd), 0);
         if (isbig) big[bpos + __popc(bmask & ((1u << lane) - 1u))] = (int32_t)v;
+      }
     }
 }
 
