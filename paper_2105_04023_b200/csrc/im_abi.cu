@@ -638,6 +638,9 @@ int im_select_seeds_ex(int32_t K, double eps_l, double eps_g, int32_t* out_seeds
             ull hk;
             TRY(readback(g.key, sizeof hk, &hk));
             if (hk == 0 || (int64_t)(hk >> 32) < theta) need_full = true;
+            if (g.trace && need_full)
+                fprintf(stderr, "[im] argmax k=%d lazy list %d: best gain %lld < theta %d -> full pass\n", k, list_len,
+                        hk ? (long long)(hk >> 32) : -1LL, theta);
             g.st_argmax_list++;
         }
         if (need_full) {

@@ -63,7 +63,8 @@ __device__ __forceinline__ void smem_vmax(uint32_t* p, uint32_t val) {
 // merge word w of edge (u -> v, h, T) restricted to [lo, hi) into the smem row
 template <bool BLOCKED, bool MEM>
 __device__ __forceinline__ void merge_word(const FirstArgs& a, const uint32_t* sX, const uint32_t* sHJ, const uint32_t* sVis,
-                                           uint32_t* row, uint32_t v, uint32_t hv, uint32_t h, uint32_t T, int lo, int hi, int w) {
+                                           uint32_t* row, uint32_t v, uint32_t hv, uint32_t h, uint32_t T, int lo, int hi, int w,
+                                           bool have_pre = false, uint32_t pre = 0u) {
     uint32_t live = 0;
 #pragma unroll
     for (int b = 0; b < 4; b++) {
@@ -73,7 +74,7 @@ __device__ __forceinline__ void merge_word(const FirstArgs& a, const uint32_t* s
     }
     if (BLOCKED && live) live &= ~expand4((sVis[w >> 3] >> ((w & 7) << 2)) & 0xFu);
     if (!live) return;
-    uint32_t val = MEM ? reinterpret_cast<const uint32_t*>(a.M)[(size_t)v * (a.J >> 2) + w] : init_word(hv, sHJ, w);
+    uint32_t val = MEM ? (have_pre ? pre : reinterpret_cast<const uint32_t*>(a.M)[(size_t)v * (a.J >> 2) + w]) : init_word(hv, sHJ, w);
     val &= live;
     if (__vmaxu4(row[w], val) != row[w]) smem_vmax(&row[w], val);
 }
@@ -130,7 +131,59 @@ __device__ __forceinline__ void gather_rec(const FirstArgs& a, const uint32_t* s
     }
 }
 
+// U edges per lane, e0 + lane + k * stride (k < U): all records are loaded, then every window and
+// (MEM) the first window word of every edge, before any is merged -- the gather is bound by these
+// dependent random loads, so U of them are kept in flight per lane.  Warp-uniform like gather_rec.
+template <bool CONST_T, bool BLOCKED, bool MEM, int U>
+__device__ __forceinline__ void gather_multi(const FirstArgs& a, const uint32_t* sX, const uint16_t* sS, const uint32_t* sHJ,
+                                             const uint32_t* sVis, uint32_t* row, int e0, int ee, int stride, uint32_t& wcount) {
+    const int lane = threadIdx.x & 31;
+    uint2 f[U];
+    uint32_t T[U];
+#pragma unroll
+    for (int k = 0; k < U; k++) {
+        const int e = e0 + lane + k * stride;
+        f[k] = make_uint2(0, 0);
+        T[k] = 0u;
+        if (e < ee) {
+            f[k] = a.fwd[e];
+            T[k] = CONST_T ? a.T0 : a.fwdT[e];
+        }
+    }
+    int lo[U], hi[U];
+    uint32_t pre[U], hv[U];
+#pragma unroll
+    for (int k = 0; k < U; k++) {
+        lo[k] = hi[k] = 0;
+        hv[k] = pre[k] = 0u;
+        if (T[k]) edge_window(f[k].y, T[k], sX, sS, a.J, lo[k], hi[k]);
+        if (lo[k] < hi[k]) {
+            wcount++;
+            if (!MEM) hv[k] = murmur_word(f[k].x, a.seedV);
+            else if (hi[k] - lo[k] <= DENSE_WIN) pre[k] = reinterpret_cast<const uint32_t*>(a.M)[(size_t)f[k].x * (a.J >> 2) + (lo[k] >> 2)];
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < U; k++) {
+        if (lo[k] < hi[k] && hi[k] - lo[k] <= DENSE_WIN)
+            for (int w = lo[k] >> 2; w <= (hi[k] - 1) >> 2; ++w)
+                merge_word<BLOCKED, MEM>(a, sX, sHJ, sVis, row, f[k].x, hv[k], f[k].y, T[k], lo[k], hi[k], w, w == (lo[k] >> 2), pre[k]);
+        uint32_t dmask = __ballot_sync(IM_FULL, hi[k] - lo[k] > DENSE_WIN);
+        while (dmask) {
+            const int l = __ffs(dmask) - 1;
+            dmask &= dmask - 1;
+            const uint32_t dh = __shfl_sync(IM_FULL, f[k].y, l), dT = __shfl_sync(IM_FULL, T[k], l), dhv = __shfl_sync(IM_FULL, hv[k], l);
+            const uint32_t dv = __shfl_sync(IM_FULL, f[k].x, l);
+            const int dlo = __shfl_sync(IM_FULL, lo[k], l), dhi = __shfl_sync(IM_FULL, hi[k], l);
+            for (int w = (dlo >> 2) + lane; w <= (dhi - 1) >> 2; w += 32)
+                merge_word<BLOCKED, MEM>(a, sX, sHJ, sVis, row, dv, dhv, dh, dT, dlo, dhi, w);
+        }
+    }
+}
+
 constexpr int FW = 8;  // max words per lane of the warp kernel (J/4/32 <= 8)
+constexpr int UW = 2;  // edges in flight per lane, rows of the warp kernel
+constexpr int UB = 1;  // edges per lane per iteration, rows of the block kernel (more was slower: tail waste on 2k-10k rows)
 
 template <bool MEM>
 __device__ __forceinline__ uint32_t start_word(const FirstArgs& a, const uint32_t* sHJ, uint32_t hu, uint32_t u, int w) {
@@ -153,7 +206,7 @@ __device__ __forceinline__ uint32_t finish_word(const FirstArgs& a, const uint32
 // merged, then compared and written back) instead of the whole J-register row.
 template <bool CONST_T, bool BLOCKED, bool MEM>
 __device__ __forceinline__ void first_small(const FirstArgs& a, const uint32_t* sX, const uint16_t* sS, const uint32_t* sHJ,
-                                            const uint32_t* sVis, uint32_t* row, uint32_t* bm, uint32_t u, bool have, uint2 f,
+                                            const uint32_t* sVis, uint32_t* row, uint32_t* bm, uint32_t* scm, uint32_t u, bool have, uint2 f,
                                             uint32_t Tin, uint32_t& wcount) {
     const int lane = threadIdx.x & 31, J = a.J, W = J >> 5, NW = J >> 2, NB = (NW + 31) >> 5;
     uint32_t h = 0, T = 0, hv = 0, v = 0;
@@ -170,6 +223,7 @@ __device__ __forceinline__ void first_small(const FirstArgs& a, const uint32_t* 
     }
     const uint32_t hu = MEM ? 0u : murmur_word(u, a.seedV);
     if (lane < NB) bm[lane] = 0u;
+    if (lane < W) scm[lane] = 0u;
     __syncwarp();
     const int w0 = lo >> 2, w1 = lo < hi ? (hi - 1) >> 2 : w0 - 1;
     for (int w = w0; w <= w1; ++w) atomicOr(&bm[w >> 5], 1u << (w & 31));
@@ -177,28 +231,25 @@ __device__ __forceinline__ void first_small(const FirstArgs& a, const uint32_t* 
     __syncwarp();
     for (int w = w0; w <= w1; ++w) merge_word<BLOCKED, MEM>(a, sX, sHJ, sVis, row, v, hv, h, T, lo, hi, w);
     __syncwarp();
-    uint32_t chunks = 0;
-    for (int k = 0; k < NB; k++) {
-        const uint32_t m = bm[k];
-        if (!m) continue;  // warp-uniform
-        const int w = 32 * k + lane;
-        uint32_t nib = 0;
-        if ((m >> lane) & 1u) nib = finish_word(a, row, u, w, start_word<MEM>(a, sHJ, hu, u, w), false);
-        uint32_t x = nib << ((lane & 7) << 2);
-        x |= __shfl_xor_sync(IM_FULL, x, 1);
-        x |= __shfl_xor_sync(IM_FULL, x, 2);
-        x |= __shfl_xor_sync(IM_FULL, x, 4);
-        if ((lane & 7) == 0 && w < NW && x) a.cm_out[(size_t)u * W + (w >> 3)] = x;  // the buffer starts zeroed
-        const uint32_t bl = __ballot_sync(IM_FULL, (lane & 7) == 0 && x != 0u);
-#pragma unroll
-        for (int c = 0; c < 4; c++) chunks |= ((bl >> (8 * c)) & 1u) << (4 * k + c);
+    // every touched word is finished once, by the lane that clears its bitmap bit first; its change
+    // nibble goes to the warp's change-mask words (word w >> 3 of the row's J/32)
+    for (int w = w0; w <= w1; ++w) {
+        const uint32_t bit = 1u << (w & 31);
+        if (atomicAnd(&bm[w >> 5], ~bit) & bit) {
+            const uint32_t nib = finish_word(a, row, u, w, start_word<MEM>(a, sHJ, hu, u, w), false);
+            if (nib) atomicOr(&scm[w >> 3], nib << ((w & 7) << 2));
+        }
     }
+    __syncwarp();
+    const uint32_t x = lane < W ? scm[lane] : 0u;
+    if (x) a.cm_out[(size_t)u * W + lane] = x;  // the buffer starts zeroed
+    const uint32_t chunks = __ballot_sync(IM_FULL, x != 0u);
     if (lane == 0 && chunks) a.bits_out[u] = chunks;
     __syncwarp();
 }
 
 template <bool CONST_T, bool BLOCKED, bool MEM>
-__global__ void __launch_bounds__(BLOCK) k_first(FirstArgs a) {
+__global__ void __launch_bounds__(BLOCK, 5) k_first(FirstArgs a) {
     __shared__ uint32_t sX[1024];
     __shared__ uint16_t sS[4098];
     __shared__ __align__(16) uint32_t sHJ[1024];
@@ -207,6 +258,7 @@ __global__ void __launch_bounds__(BLOCK) k_first(FirstArgs a) {
     __shared__ uint32_t sVis[BLOCK / 32][32];
     __shared__ int sOff[BLOCK / 32][258];
     __shared__ uint32_t sBm[BLOCK / 32][8];
+    __shared__ uint32_t sCm[BLOCK / 32][32];
     const int J = a.J, W = J >> 5, NW = J >> 2;
     for (int i = threadIdx.x; i < J; i += blockDim.x) {
         sX[i] = a.Xs[i];
@@ -261,7 +313,7 @@ __global__ void __launch_bounds__(BLOCK) k_first(FirstArgs a) {
             if (ee - eb <= 32) {  // sparse path: touch only the window words
                 if (BLOCKED && lane < W) sVis[wib][lane] = a.vis[(size_t)u * W + lane];
                 __syncwarp();
-                first_small<CONST_T, BLOCKED, MEM>(a, sX, sS, sHJ, sVis[wib], row, sBm[wib], (uint32_t)u, eb + lane < ee, cf, cT,
+                first_small<CONST_T, BLOCKED, MEM>(a, sX, sS, sHJ, sVis[wib], row, sBm[wib], sCm[wib], (uint32_t)u, eb + lane < ee, cf, cT,
                                                    wcount);
                 continue;
             }
@@ -274,8 +326,8 @@ __global__ void __launch_bounds__(BLOCK) k_first(FirstArgs a) {
             if (BLOCKED && lane < W) sVis[wib][lane] = a.vis[(size_t)u * W + lane];
             __syncwarp();
             if (eb < ee) gather_rec<CONST_T, BLOCKED, MEM>(a, sX, sS, sHJ, sVis[wib], row, eb + lane < ee, cf, cT, wcount);
-            for (int e0 = eb + 32; e0 < ee; e0 += 32)
-                gather_edge<CONST_T, BLOCKED, MEM>(a, sX, sS, sHJ, sVis[wib], row, e0 + lane < ee ? e0 + lane : -1, wcount);
+            for (int e0 = eb + 32; e0 < ee; e0 += 32 * (MEM ? UW : 1))  // from init values: ALU-bound, one edge per lane
+                gather_multi<CONST_T, BLOCKED, MEM, MEM ? UW : 1>(a, sX, sS, sHJ, sVis[wib], row, e0, ee, 32, wcount);
             __syncwarp();
             uint32_t chunks = 0;
 #pragma unroll
@@ -334,8 +386,8 @@ __global__ void __launch_bounds__(BLOCK) k_first_big(FirstArgs a) {
         }
         __syncthreads();
         const int eb = a.off[u], ee = a.off[u + 1];
-        for (int e0 = eb + (threadIdx.x & ~31); e0 < ee; e0 += blockDim.x)  // warp-uniform trip count
-            gather_edge<CONST_T, BLOCKED, MEM>(a, sX, sS, sHJ, sVis, row, e0 + (threadIdx.x & 31) < ee ? e0 + (threadIdx.x & 31) : -1, wcount);
+        for (int e0 = eb + (threadIdx.x & ~31); e0 < ee; e0 += UB * blockDim.x)  // warp-uniform trip count
+            gather_multi<CONST_T, BLOCKED, MEM, UB>(a, sX, sS, sHJ, sVis, row, e0, ee, blockDim.x, wcount);
         __syncthreads();
         for (int w = threadIdx.x; w < NW; w += blockDim.x) {
             uint32_t nib = finish_word(a, row, u, w, sOld[w], false);

@@ -59,6 +59,12 @@ __device__ __forceinline__ uint32_t sum16(uint4 m) {
 }
 
 constexpr int HIST_BINS = 4096;
+#ifndef BFS_EP
+#define BFS_EP 2  // edges in flight per lane of k_bfs_level2 (3 and 4 measured slower on C4)
+#endif
+#ifndef BFS_MINB
+#define BFS_MINB 1  // min resident blocks per SM k_bfs_level2 is compiled for
+#endif
 constexpr int CU = 8;  // vertex groups of BLOCK per block iteration of the frontier compactions
 constexpr int AG = 4;  // vertex groups in flight per warp in k_argmax
 
@@ -468,7 +474,8 @@ __device__ __forceinline__ void bfs_sparse(const uint32_t* sX, const uint32_t* d
 }
 
 template <bool CONST_T>
-__global__ void __launch_bounds__(BLOCK) k_bfs_level2(BfsArgs a) {
+__global__ void __launch_bounds__(BLOCK, BFS_MINB) k_bfs_level2(BfsArgs a) {
+    constexpr int EP = BFS_EP;  // edges in flight per lane
     extern __shared__ uint32_t sDyn[];
     __shared__ uint32_t sX[1024];
     __shared__ uint16_t sS[4098];
@@ -508,10 +515,10 @@ __global__ void __launch_bounds__(BLOCK) k_bfs_level2(BfsArgs a) {
         const int total = __shfl_sync(IM_FULL, incl, 31);
         const int start = incl - cnt;
         int carry = 0;
-        for (int e0 = 0; e0 < total; e0 += 64) {
-            int own[2], ed[2];
+        for (int e0 = 0; e0 < total; e0 += 32 * EP) {
+            int own[EP], ed[EP];
 #pragma unroll
-            for (int s = 0; s < 2; s++) {  // owner item of edge e0 + 32 s + lane
+            for (int s = 0; s < EP; s++) {  // owner item of edge e0 + 32 s + lane
                 const int b0 = e0 + 32 * s;
                 const bool starts = cnt > 0 && start >= b0 && start < b0 + 32;
                 if (starts) sSlot[wib][start - b0] = lane;
@@ -525,18 +532,18 @@ __global__ void __launch_bounds__(BLOCK) k_bfs_level2(BfsArgs a) {
                 own[s] = owner;
                 ed[s] = b0 + lane < total ? oeb + (b0 + lane - ost) : -1;
             }
-            uint2 f[2];
-            uint32_t T[2];
+            uint2 f[EP];
+            uint32_t T[EP];
 #pragma unroll
-            for (int s = 0; s < 2; s++) {
+            for (int s = 0; s < EP; s++) {
                 f[s] = ed[s] >= 0 ? a.fwd[ed[s]] : make_uint2(0, 0);
                 T[s] = ed[s] >= 0 ? (CONST_T ? a.T0 : a.fwdT[ed[s]]) : 0u;
             }
-            int lo[2], hi[2], w0[2];
-            uint32_t nv0[2], nv1[2], x0[2], x1[2];
-            bool dense[2];
+            int lo[EP], hi[EP], w0[EP];
+            uint32_t nv0[EP], nv1[EP], x0[EP], x1[EP];
+            bool dense[EP];
 #pragma unroll
-            for (int s = 0; s < 2; s++) {
+            for (int s = 0; s < EP; s++) {
                 lo[s] = hi[s] = 0;
                 nv0[s] = nv1[s] = 0u;
                 w0[s] = 0;
@@ -545,13 +552,13 @@ __global__ void __launch_bounds__(BLOCK) k_bfs_level2(BfsArgs a) {
                 if (!dense[s] && lo[s] < hi[s]) bfs_sparse(sX, sD + own[s] * W, f[s].y, T[s], lo[s], hi[s], w0[s], nv0[s], nv1[s]);
             }
 #pragma unroll
-            for (int s = 0; s < 2; s++) {  // both edges' visited words in flight
+            for (int s = 0; s < EP; s++) {  // every edge's visited words in flight
                 const size_t r = (size_t)f[s].x * W + w0[s];
                 x0[s] = nv0[s] ? __ldcg(&a.vis[r]) : 0u;
                 x1[s] = nv1[s] ? __ldcg(&a.vis[r + 1]) : 0u;
             }
 #pragma unroll
-            for (int s = 0; s < 2; s++) {
+            for (int s = 0; s < EP; s++) {
                 const size_t r = (size_t)f[s].x * W + w0[s];
                 const uint32_t n0 = nv0[s] & ~x0[s], n1 = nv1[s] & ~x1[s];
                 if (n0) {
@@ -566,7 +573,7 @@ __global__ void __launch_bounds__(BLOCK) k_bfs_level2(BfsArgs a) {
             }
             // wide windows: one simulation per lane (as in k_bfs_level)
 #pragma unroll
-            for (int s = 0; s < 2; s++) {
+            for (int s = 0; s < EP; s++) {
                 uint32_t dmask = __ballot_sync(IM_FULL, dense[s]);
                 while (dmask) {
                     const int l = __ffs(dmask) - 1;

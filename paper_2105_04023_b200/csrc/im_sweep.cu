@@ -112,6 +112,22 @@ __device__ __forceinline__ bool window_changed(const uint32_t* __restrict__ cm, 
     return false;
 }
 
+// does v's previous-sweep change mask hold a simulation of [lo, hi) (<= DENSE_WIN wide, so at most two
+// mask words) in which the edge is live?  Only those simulations can raise M_u (Alg. 2:
+// a simulation in which v did not change was already pulled, a dead one is never pulled).
+__device__ __forceinline__ bool live_changed(const uint32_t* __restrict__ cm, uint32_t v, int W, const uint32_t* sX, uint32_t h,
+                                             uint32_t T, int lo, int hi) {
+    const uint32_t* row = cm + (size_t)v * W;
+    const int w0 = lo >> 5, w1 = (hi - 1) >> 5;
+    const uint32_t m0 = __ldg(&row[w0]), m1 = w1 != w0 ? __ldg(&row[w1]) : 0u;
+    if (!(m0 | m1)) return false;
+    for (int i = lo; i < hi; ++i) {
+        const uint32_t m = (i >> 5) == w0 ? m0 : m1;
+        if (((m >> (i & 31)) & 1u) && (sX[i] ^ h) < T) return true;
+    }
+    return false;
+}
+
 constexpr int NS = IM_NS;  // edges in flight per lane
 
 template <bool CONST_T, bool BLOCKED, bool FILTER>
@@ -189,7 +205,10 @@ __global__ void __launch_bounds__(BLOCK, 4) k_sweep(SweepArgs a) {
                 lo[s] = hi[s] = 0;
                 if (T[s]) {
                     edge_window(h[s], T[s], sX, sS, J, lo[s], hi[s]);
-                    if (FILTER && lo[s] < hi[s] && !window_changed(a.cm_in, vv[s], W, lo[s], hi[s])) hi[s] = lo[s];
+                    if (FILTER && lo[s] < hi[s] &&
+                        !(hi[s] - lo[s] <= DENSE_WIN ? live_changed(a.cm_in, vv[s], W, sX, h[s], T[s], lo[s], hi[s])
+                                                     : window_changed(a.cm_in, vv[s], W, lo[s], hi[s])))
+                        hi[s] = lo[s];
                 }
                 sparse[s] = lo[s] < hi[s] && hi[s] - lo[s] <= DENSE_WIN;
                 if (sparse[s]) {  // first word of the window: both loads in flight before any use
