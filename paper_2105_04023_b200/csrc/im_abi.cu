@@ -109,7 +109,6 @@ int ensure_device() {
     g.max_blocks_bfs = std::max(1, bb) * g.num_sms;
     g.trace = getenv("IM_TRACE") != nullptr;
     if (const char* pf = getenv("IM_PULL_FRAC")) g.pull_frac = atof(pf);
-    if (const char* b = getenv("IM_BFS")) g.bfs2 = atoi(b) != 1;
     if (const char* lm = getenv("IM_LIST_MAX")) g.list_max = atoll(lm);
     if (!g.own_stream) CK(cudaStreamCreateWithFlags(&g.own_stream, cudaStreamNonBlocking));
     if (!g.stream) g.stream = g.own_stream;
@@ -138,7 +137,7 @@ void reset_graph_state() {
 }
 
 void release_all() {
-    dfree(g.Xs); dfree(g.s12); dfree(g.permd); dfree(g.M); dfree(g.vis);
+    dfree(g.Xs); dfree(g.s12); dfree(g.permd); dfree(g.M); dfree(g.vis); dfree(g.vd);
     for (int i = 0; i < 2; i++) { dfree(g.items[i]); dfree(g.bits[i]); dfree(g.cm[i]); dfree(g.delta[i]); dfree(g.bitems[i]); dfree(g.bvl[i]); }
     dfree(g.inS); dfree(g.MS); dfree(g.btag); dfree(g.nbits); dfree(g.gain); dfree(g.big); dfree(g.list); dfree(g.lcount); dfree(g.hist);
     dfree(g.off); dfree(g.fwd); dfree(g.fwdT); dfree(g.roff); dfree(g.rev); dfree(g.revT); dfree(g.ritems); dfree(g.fbig);
@@ -286,6 +285,7 @@ int alloc_sketch_state(int32_t J) {
     TRY(dalloc(g.permd, (size_t)J));
     TRY(dalloc(g.M, n * (size_t)J + 65536));  // + tail padding read by the TMA argmax tiles
     TRY(dalloc(g.vis, n * W + 16384));
+    TRY(dalloc(g.vd, n * W));
     for (int i = 0; i < 2; i++) {
         TRY(dalloc(g.items[i], (size_t)g.n_ritems + 4 * n + 1));  // slices add <= 3 partial segments per vertex
         // a completed build leaves the change buffers zero; fresh ones are cleared by simulate()
@@ -458,6 +458,7 @@ int simulate(bool blocked) {
 
 int build_fresh() {
     CK(cudaMemsetAsync(g.vis, 0, (size_t)g.n * (g.J / 32) * sizeof(uint32_t), g.stream));
+    CK(cudaMemsetAsync(g.vd, 0, (size_t)g.n * (g.J / 32) * sizeof(uint2), g.stream));
     g.any_blocked = false;
     return simulate(false);
 }
@@ -618,6 +619,7 @@ int im_select_seeds_ex(int32_t K, double eps_l, double eps_g, int32_t* out_seeds
     if (!g.fresh || g.built_eps_c != g.eps_c) TRY(build_fresh());
     const size_t n = (size_t)g.n, W = (size_t)g.J / 32;
     CK(cudaMemsetAsync(g.vis, 0, n * W * sizeof(uint32_t), g.stream));
+    CK(cudaMemsetAsync(g.vd, 0, n * W * sizeof(uint2), g.stream));
     CK(cudaMemsetAsync(g.inS, 0, n, g.stream));
     CK(cudaMemsetAsync(g.MS, 0, (size_t)g.J, g.stream));
     CK(cudaMemsetAsync(g.varsigma, 0, sizeof(double), g.stream));

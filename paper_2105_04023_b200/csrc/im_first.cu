@@ -183,7 +183,10 @@ __device__ __forceinline__ void gather_multi(const FirstArgs& a, const uint32_t*
 
 constexpr int FW = 8;  // max words per lane of the warp kernel (J/4/32 <= 8)
 constexpr int UW = 2;  // edges in flight per lane, rows of the warp kernel
-constexpr int UB = 1;  // edges per lane per iteration, rows of the block kernel (more was slower: tail waste on 2k-10k rows)
+#ifndef FIRST_UB
+#define FIRST_UB 1
+#endif
+constexpr int UB = FIRST_UB;  // edges per lane per iteration in gather sweeps, rows of the block kernel (4 measured slower)
 
 template <bool MEM>
 __device__ __forceinline__ uint32_t start_word(const FirstArgs& a, const uint32_t* sHJ, uint32_t hu, uint32_t u, int w) {
@@ -222,14 +225,16 @@ __device__ __forceinline__ void first_small(const FirstArgs& a, const uint32_t* 
         }
     }
     const uint32_t hu = MEM ? 0u : murmur_word(u, a.seedV);
+    const int w0 = lo >> 2, w1 = lo < hi ? (hi - 1) >> 2 : w0 - 1;
+    // MEM: the out-neighbour's first window word is loaded now, in flight with the row words below
+    const uint32_t pre = MEM && lo < hi ? reinterpret_cast<const uint32_t*>(a.M)[(size_t)v * (J >> 2) + w0] : 0u;
     if (lane < NB) bm[lane] = 0u;
     if (lane < W) scm[lane] = 0u;
     __syncwarp();
-    const int w0 = lo >> 2, w1 = lo < hi ? (hi - 1) >> 2 : w0 - 1;
     for (int w = w0; w <= w1; ++w) atomicOr(&bm[w >> 5], 1u << (w & 31));
     for (int w = w0; w <= w1; ++w) row[w] = start_word<MEM>(a, sHJ, hu, u, w);  // same value from every writer
     __syncwarp();
-    for (int w = w0; w <= w1; ++w) merge_word<BLOCKED, MEM>(a, sX, sHJ, sVis, row, v, hv, h, T, lo, hi, w);
+    for (int w = w0; w <= w1; ++w) merge_word<BLOCKED, MEM>(a, sX, sHJ, sVis, row, v, hv, h, T, lo, hi, w, w == w0, pre);
     __syncwarp();
     // every touched word is finished once, by the lane that clears its bitmap bit first; its change
     // nibble goes to the warp's change-mask words (word w >> 3 of the row's J/32)
@@ -386,8 +391,8 @@ __global__ void __launch_bounds__(BLOCK) k_first_big(FirstArgs a) {
         }
         __syncthreads();
         const int eb = a.off[u], ee = a.off[u + 1];
-        for (int e0 = eb + (threadIdx.x & ~31); e0 < ee; e0 += UB * blockDim.x)  // warp-uniform trip count
-            gather_multi<CONST_T, BLOCKED, MEM, UB>(a, sX, sS, sHJ, sVis, row, e0, ee, blockDim.x, wcount);
+        for (int e0 = eb + (threadIdx.x & ~31); e0 < ee; e0 += (MEM ? UB : 1) * blockDim.x)  // warp-uniform trip count
+            gather_multi<CONST_T, BLOCKED, MEM, MEM ? UB : 1>(a, sX, sS, sHJ, sVis, row, e0, ee, blockDim.x, wcount);
         __syncthreads();
         for (int w = threadIdx.x; w < NW; w += blockDim.x) {
             uint32_t nib = finish_word(a, row, u, w, sOld[w], false);

@@ -77,6 +77,7 @@ struct Ctx {
     double pol_l = __builtin_nan(""), pol_g = __builtin_nan(""), eps_c = 0.0;
     double built_eps_c = 0.0;   // eps_c of the sketches currently held
     uint32_t* vis = nullptr;    // n*(J/32) R_G(S) bits, internal order
+    uint2* vd = nullptr;        // BFS-internal {visited, new in this level} pairs, n*(J/32); .x == vis between levels
     bool built = false, fresh = false, any_blocked = false;
     // sweep buffers
     int4* items[2] = {nullptr, nullptr};
@@ -140,7 +141,6 @@ struct Ctx {
     int64_t launches = 0;
     int st_argmax_full = 0, st_argmax_list = 0;
     int max_blocks_sweep = 0, max_blocks_bfs = 0, max_blocks_first = 0, max_blocks_bfs2 = 0;
-    bool bfs2 = true;  // k_bfs_level2 (IM_BFS=1: the original level kernel)
     cudaEvent_t ev[2] = {nullptr, nullptr};
 };
 

@@ -63,7 +63,7 @@ constexpr int HIST_BINS = 4096;
 #define BFS_EP 2  // edges in flight per lane of k_bfs_level2 (3 and 4 measured slower on C4)
 #endif
 #ifndef BFS_MINB
-#define BFS_MINB 1  // min resident blocks per SM k_bfs_level2 is compiled for
+#define BFS_MINB 5  // min resident blocks per SM k_bfs_level2 is compiled for (48 registers, no spills)
 #endif
 constexpr int CU = 8;  // vertex groups of BLOCK per block iteration of the frontier compactions
 constexpr int AG = 4;  // vertex groups in flight per warp in k_argmax
@@ -273,7 +273,7 @@ __global__ void k_argmax_decode(int nv, const int32_t* __restrict__ list, const 
 // Alg. 1 lines 11, 13-14: S <- S + s; R_G(S) by a multi-simulation BFS from s over live edges
 // (same samples as the sketches, R13) carrying J-bit masks; visited bits only ever set.
 __global__ void k_seed_start(int32_t n, int32_t J, const ull* key, const uint32_t* __restrict__ M32,
-                             const uint8_t* __restrict__ MS, uint8_t* inS, uint32_t* vis, uint32_t* delta0,
+                             const uint8_t* __restrict__ MS, uint8_t* inS, uint32_t* vis, uint2* vd, uint32_t* delta0,
                              const int32_t* __restrict__ off, int4* items0, int32_t* vl0, IterCounters* ctr0,
                              ull* sigma_count, StepDev* rec) {
     const int lane = threadIdx.x, W = J >> 5, Jw = J >> 2;
@@ -299,6 +299,7 @@ __global__ void k_seed_start(int32_t n, int32_t J, const ull* key, const uint32_
     for (int w = lane; w < W; w += 32) {
         uint32_t d = ~vis[(size_t)s * W + w];
         vis[(size_t)s * W + w] = IM_FULL;
+        vd[(size_t)s * W + w].x = IM_FULL;
         delta0[(size_t)s * W + w] = d;
         bits += __popc(d);
         any |= d;
@@ -332,126 +333,10 @@ struct BfsArgs {
     const uint32_t* Xs;
     const uint16_t* s12;
     int J;
-    uint32_t* vis;
+    uint2* vd;         // {visited R_G(S), new in this level} word pairs: the visited test and both ORs touch one sector
     const uint32_t* din;
-    uint32_t* dout;
     uint32_t* nbits;   // per vertex: which 32-simulation words got new bits in this level
 };
-
-// one 32-simulation word w of one edge (u,v): the simulations new at v are Delta_u & live & ~visited(v).
-// All updates are fire-and-forget ORs: a bit that two threads both find new is new either way, and
-// the next frontier / the new-bit count are built afterwards by k_bfs_compact from the OR-ed words.
-__device__ __forceinline__ void bfs_word(const BfsArgs& a, const uint32_t* sX, uint32_t u, uint32_t v, int w, uint32_t h,
-                                         uint32_t T, int lo, int hi) {
-    const int W = a.J >> 5;
-    uint32_t d = a.din[(size_t)u * W + w];
-    if (!d) return;
-    int i0 = max(lo, w << 5), i1 = min(hi, (w << 5) + 32);
-    uint32_t live = 0;
-    for (int i = i0; i < i1; ++i) live |= ((sX[i] ^ h) < T) ? (1u << (i & 31)) : 0u;
-    uint32_t nv = d & live;
-    if (!nv) return;
-    nv &= ~__ldcg(&a.vis[(size_t)v * W + w]);
-    if (!nv) return;
-    atomicOr(&a.vis[(size_t)v * W + w], nv);
-    atomicOr(&a.dout[(size_t)v * W + w], nv);
-    atomicOr(&a.nbits[v], 1u << w);
-}
-
-template <bool CONST_T>
-__global__ void __launch_bounds__(BLOCK) k_bfs_level(BfsArgs a) {
-    __shared__ uint32_t sX[1024];
-    __shared__ uint16_t sS[4098];
-    __shared__ int sSlot[BLOCK / 32][32];
-    for (int i = threadIdx.x; i < a.J; i += blockDim.x) sX[i] = a.Xs[i];
-    for (int i = threadIdx.x; i < 4097; i += blockDim.x) sS[i] = a.s12[i];
-    __syncthreads();
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    int base = 0, left = 0;  // 128-item grabs (4 batches of 32)
-    for (;;) {
-        if (left == 0) {
-            if (lane == 0) base = atomicAdd(&a.ctr_next->batch, 128);
-            base = __shfl_sync(IM_FULL, base, 0);
-            left = 4;
-        } else {
-            base += 32;
-        }
-        --left;
-        if (base >= a.n_items) break;
-        int it = base + lane;
-        int u = 0, eb = 0, cnt = 0;
-        if (it < a.n_items) {
-            int4 I = a.items[it];
-            u = I.x;
-            eb = I.y;
-            cnt = I.z - I.y;
-        }
-        int incl = warp_incl_scan(cnt, lane);
-        int total = __shfl_sync(IM_FULL, incl, 31);
-        int start = incl - cnt;
-        int carry = 0;
-        for (int e0 = 0; e0 < total; e0 += 32) {
-            bool starts = cnt > 0 && start >= e0 && start < e0 + 32;
-            if (starts) sSlot[wib][start - e0] = lane;
-            uint32_t smask = __reduce_or_sync(IM_FULL, starts ? (1u << (start - e0)) : 0u);
-            __syncwarp();
-            uint32_t below = smask & ((2u << lane) - 1u);
-            int owner = below ? sSlot[wib][31 - __clz(below)] : carry;
-            __syncwarp();
-            carry = __shfl_sync(IM_FULL, owner, 31);
-            int ou = __shfl_sync(IM_FULL, u, owner);
-            int oeb = __shfl_sync(IM_FULL, eb, owner);
-            int ost = __shfl_sync(IM_FULL, start, owner);
-            int idx = e0 + lane;
-            uint32_t v = 0, h = 0, T = 0;
-            int lo = 0, hi = 0;
-            bool dense = false;
-            if (idx < total) {
-                int e = oeb + (idx - ost);
-                uint2 f = a.fwd[e];
-                v = f.x;
-                h = f.y;
-                T = CONST_T ? a.T0 : a.fwdT[e];
-                if (T) {
-                    edge_window(h, T, sX, sS, a.J, lo, hi);
-                    if (hi - lo > DENSE_WIN) dense = true;
-                    else if (lo < hi)
-                        for (int w = lo >> 5; w <= (hi - 1) >> 5; ++w) bfs_word(a, sX, (uint32_t)ou, v, w, h, T, lo, hi);
-                }
-            }
-            // wide windows: one simulation per lane, the 32-bit live words come from ballots, then
-            // lane (w & 31) applies word w (a window spans <= J/32 <= 32 words)
-            uint32_t dmask = __ballot_sync(IM_FULL, dense);
-            while (dmask) {
-                int l = __ffs(dmask) - 1;
-                dmask &= dmask - 1;
-                uint32_t dv = __shfl_sync(IM_FULL, v, l), dh = __shfl_sync(IM_FULL, h, l), dT = __shfl_sync(IM_FULL, T, l);
-                int dlo = __shfl_sync(IM_FULL, lo, l), dhi = __shfl_sync(IM_FULL, hi, l);
-                uint32_t du = (uint32_t)__shfl_sync(IM_FULL, ou, l);
-                const int w0 = dlo >> 5, w1 = (dhi - 1) >> 5, W = a.J >> 5;
-                uint32_t mylive = 0;
-                int myw = -1;
-                for (int w = w0; w <= w1; ++w) {
-                    int i = 32 * w + lane;
-                    uint32_t lv = __ballot_sync(IM_FULL, i >= dlo && i < dhi && (sX[i] ^ dh) < dT);
-                    if ((w & 31) == lane) {
-                        mylive = lv;
-                        myw = w;
-                    }
-                }
-                if (myw >= 0 && mylive) {
-                    uint32_t nv = a.din[(size_t)du * W + myw] & mylive;
-                    if (nv) nv &= ~__ldcg(&a.vis[(size_t)dv * W + myw]);
-                    if (nv) {
-                        atomicOr(&a.vis[(size_t)dv * W + myw], nv);
-                        atomicOr(&a.dout[(size_t)dv * W + myw], nv);
-                        atomicOr(&a.nbits[dv], 1u << myw);
-                    }
-                }
-            }
-        }
-    }
-}
 
 // Same level, reworked for memory-level parallelism (the level is bound by dependent random loads):
 // the Delta rows of a warp's 32 items are staged in shared memory once (coalesced), so an edge's
@@ -554,21 +439,15 @@ __global__ void __launch_bounds__(BLOCK, BFS_MINB) k_bfs_level2(BfsArgs a) {
 #pragma unroll
             for (int s = 0; s < EP; s++) {  // every edge's visited words in flight
                 const size_t r = (size_t)f[s].x * W + w0[s];
-                x0[s] = nv0[s] ? __ldcg(&a.vis[r]) : 0u;
-                x1[s] = nv1[s] ? __ldcg(&a.vis[r + 1]) : 0u;
+                x0[s] = nv0[s] ? __ldcg(&a.vd[r].x) : 0u;
+                x1[s] = nv1[s] ? __ldcg(&a.vd[r + 1].x) : 0u;
             }
 #pragma unroll
             for (int s = 0; s < EP; s++) {
                 const size_t r = (size_t)f[s].x * W + w0[s];
                 const uint32_t n0 = nv0[s] & ~x0[s], n1 = nv1[s] & ~x1[s];
-                if (n0) {
-                    atomicOr(&a.vis[r], n0);
-                    atomicOr(&a.dout[r], n0);
-                }
-                if (n1) {
-                    atomicOr(&a.vis[r + 1], n1);
-                    atomicOr(&a.dout[r + 1], n1);
-                }
+                if (n0) atomicOr(reinterpret_cast<ull*>(&a.vd[r]), ((ull)n0 << 32) | n0);  // visited and Delta_out
+                if (n1) atomicOr(reinterpret_cast<ull*>(&a.vd[r + 1]), ((ull)n1 << 32) | n1);
                 if (n0 | n1) atomicOr(&a.nbits[f[s].x], (n0 ? 1u << w0[s] : 0u) | (n1 ? 2u << w0[s] : 0u));
             }
             // wide windows: one simulation per lane (as in k_bfs_level)
@@ -595,10 +474,9 @@ __global__ void __launch_bounds__(BLOCK, BFS_MINB) k_bfs_level2(BfsArgs a) {
                     }
                     if (myw >= 0 && mylive) {
                         uint32_t nv = sD[downer * W + myw] & mylive;
-                        if (nv) nv &= ~__ldcg(&a.vis[(size_t)dv * W + myw]);
+                        if (nv) nv &= ~__ldcg(&a.vd[(size_t)dv * W + myw].x);
                         if (nv) {
-                            atomicOr(&a.vis[(size_t)dv * W + myw], nv);
-                            atomicOr(&a.dout[(size_t)dv * W + myw], nv);
+                            atomicOr(reinterpret_cast<ull*>(&a.vd[(size_t)dv * W + myw]), ((ull)nv << 32) | nv);
                             atomicOr(&a.nbits[dv], 1u << myw);
                         }
                     }
@@ -612,7 +490,12 @@ __global__ void __launch_bounds__(BLOCK, BFS_MINB) k_bfs_level2(BfsArgs a) {
 // (vertex, simulation) pairs (popcount of the OR-ed Delta words) into sigma, lists the vertex (to
 // clear its Delta after the next level), emits its out-edge items (long rows of a hash-sorted
 // graph go to k_slices_big) and clears nbits for the next level.
-__global__ void k_bfs_compact(int32_t n, int J, bool sorted, uint32_t* __restrict__ nbits, const uint32_t* __restrict__ dout,
+// VDM (the selection BFS): the level left its new bits in vd[].y; they move to the next level's
+// Delta rows (dout), the visited words are copied to vis (R_G(S) for every other kernel) and vd[].y
+// is cleared.  Otherwise (the evaluator) dout already holds them.
+template <bool VDM>
+__global__ void k_bfs_compact(int32_t n, int J, bool sorted, uint32_t* __restrict__ nbits, uint32_t* __restrict__ dout,
+                              uint2* __restrict__ vd, uint32_t* __restrict__ vis,
                               const int32_t* __restrict__ off, int32_t* __restrict__ vl, int4* __restrict__ items,
                               int32_t* __restrict__ big, IterCounters* ctr, ull* sigma_count) {
     const int lane = threadIdx.x & 31, W = J >> 5;
@@ -640,7 +523,18 @@ __global__ void k_bfs_compact(int32_t n, int J, bool sorted, uint32_t* __restric
         bool isbig = false;
         if (b) {
             nbits[v] = 0u;
-            for (uint32_t t = b; t; t &= t - 1) newbits += __popc(dout[(size_t)v * W + (__ffs(t) - 1)]);
+            for (uint32_t t = b; t; t &= t - 1) {
+                const size_t i = (size_t)v * W + (__ffs(t) - 1);
+                if (VDM) {
+                    const uint2 p = vd[i];
+                    dout[i] = p.y;
+                    vis[i] = p.x;
+                    vd[i] = make_uint2(p.x, 0u);
+                    newbits += __popc(p.y);
+                } else {
+                    newbits += __popc(dout[i]);
+                }
+            }
             rb = off[v];
             rd = off[v + 1] - rb;
             isbig = sorted && rd > SEG;
@@ -830,7 +724,7 @@ cudaError_t launch_argmax_list_finish(Ctx& c, int list_len) {
 }
 cudaError_t launch_seed_start(Ctx& c, int k) {
     (void)k;
-    k_seed_start<<<1, 32, 0, c.stream>>>(c.n, c.J, c.key, reinterpret_cast<const uint32_t*>(c.M), c.MS, c.inS, c.vis,
+    k_seed_start<<<1, 32, 0, c.stream>>>(c.n, c.J, c.key, reinterpret_cast<const uint32_t*>(c.M), c.MS, c.inS, c.vis, c.vd,
                                           c.delta[0], c.off, c.bitems[0], c.bvl[0], &c.ctr[0], c.sigma_count, c.rec);
     return LAUNCHED(c);
 }
@@ -848,25 +742,20 @@ cudaError_t launch_bfs_level(Ctx& c, int cur, int n_items, uint32_t tag) {
     a.Xs = c.Xs;
     a.s12 = c.s12;
     a.J = c.J;
-    a.vis = c.vis;
+    a.vd = c.vd;
     a.din = c.delta[cur];
-    a.dout = c.delta[cur ^ 1];
     a.nbits = c.nbits;
     int64_t want = ((int64_t)n_items + 32 * (BLOCK / 32) - 1) / (32 * (BLOCK / 32));
-    if (c.bfs2) {
+    {
         const size_t smem = (size_t)BLOCK * (c.J >> 5) * sizeof(uint32_t);
         int grid = (int)(want < 1 ? 1 : (want > c.max_blocks_bfs2 ? c.max_blocks_bfs2 : want));
         if (c.constT) k_bfs_level2<true><<<grid, BLOCK, smem, c.stream>>>(a);
         else k_bfs_level2<false><<<grid, BLOCK, smem, c.stream>>>(a);
-    } else {
-        int grid = (int)(want < 1 ? 1 : (want > c.max_blocks_bfs ? c.max_blocks_bfs : want));
-        if (c.constT) k_bfs_level<true><<<grid, BLOCK, 0, c.stream>>>(a);
-        else k_bfs_level<false><<<grid, BLOCK, 0, c.stream>>>(a);
     }
     cudaError_t e = LAUNCHED(c);
     if (e) return e;
     const int nxt = cur ^ 1;
-    k_bfs_compact<<<grid_for(c, c.n), BLOCK, 0, c.stream>>>(c.n, c.J, c.sorted_h, c.nbits, c.delta[nxt], c.off, c.bvl[nxt],
+    k_bfs_compact<true><<<grid_for(c, c.n), BLOCK, 0, c.stream>>>(c.n, c.J, c.sorted_h, c.nbits, c.delta[nxt], c.vd, c.vis, c.off, c.bvl[nxt],
                                                             c.bitems[nxt], c.big, &c.ctr[nxt], c.sigma_count);
     if ((e = LAUNCHED(c))) return e;
     if (!c.sorted_h) return e;
@@ -881,7 +770,8 @@ cudaError_t launch_bfs_items(Ctx& c, int buf) {
 // the same compaction / item / clear kernels on caller-chosen buffers, unsorted rows (evaluator, im_eval.cu)
 cudaError_t launch_bfs_compact_raw(Ctx& c, int J, uint32_t* nbits, const uint32_t* dout, int32_t* vl, int4* items,
                                    IterCounters* ctr, ull* count) {
-    k_bfs_compact<<<grid_for(c, c.n), BLOCK, 0, c.stream>>>(c.n, J, false, nbits, dout, c.off, vl, items, nullptr, ctr, count);
+    k_bfs_compact<false><<<grid_for(c, c.n), BLOCK, 0, c.stream>>>(c.n, J, false, nbits, const_cast<uint32_t*>(dout), nullptr, nullptr,
+                                                                   c.off, vl, items, nullptr, ctr, count);
     return LAUNCHED(c);
 }
 cudaError_t launch_bfs_items_raw(Ctx& c, const int32_t* vl, int4* items, IterCounters* ctr) {
@@ -908,8 +798,9 @@ cudaError_t launch_gather_rows(Ctx& c, const int32_t* rows, int64_t nrows, uint8
     return LAUNCHED(c);
 }
 
-int occupancy_bfs(int* blocks_per_sm) {
-    return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_bfs_level<true>, BLOCK, 0);
+int occupancy_bfs(int* blocks_per_sm) {  // grid cap of the evaluator's level kernel (persistent; any grid is correct)
+    *blocks_per_sm = 8;
+    return 0;
 }
 // k_bfs_level2 for this J (dynamic shared memory: the Delta rows of every warp's 32 items)
 int occupancy_bfs2(int J, int* blocks_per_sm) {
