@@ -110,6 +110,8 @@ int ensure_device() {
     g.trace = getenv("IM_TRACE") != nullptr;
     if (const char* pf = getenv("IM_PULL_FRAC")) g.pull_frac = atof(pf);
     if (const char* lm = getenv("IM_LIST_MAX")) g.list_max = atoll(lm);
+    if (const char* sm = getenv("IM_SLICE_MIN")) g.slice_min = atoi(sm);
+    if (const char* sb = getenv("IM_SLICE_MIN_BFS")) g.slice_min_bfs = atoi(sb);
     if (!g.own_stream) CK(cudaStreamCreateWithFlags(&g.own_stream, cudaStreamNonBlocking));
     if (!g.stream) g.stream = g.own_stream;
     if (!g.hpin) CK(cudaMallocHost(&g.hpin, 4096));
@@ -287,7 +289,7 @@ int alloc_sketch_state(int32_t J) {
     TRY(dalloc(g.vis, n * W + 16384));
     TRY(dalloc(g.vd, n * W));
     for (int i = 0; i < 2; i++) {
-        TRY(dalloc(g.items[i], (size_t)g.n_ritems + 4 * n + 1));  // slices add <= 3 partial segments per vertex
+        TRY(dalloc(g.items[i], (size_t)g.n_ritems + (MAX_SLICES + 1) * n + 1));  // slices add <= MAX_SLICES partial segments per vertex
         // a completed build leaves the change buffers zero; fresh ones are cleared by simulate()
         TRY(dalloc(g.bits[i], n, &fr));
         if (fr) g.sweep_dirty = true;
@@ -295,7 +297,7 @@ int alloc_sketch_state(int32_t J) {
         if (fr) g.sweep_dirty = true;
         TRY(dalloc(g.delta[i], n * W, &fr));
         if (fr || g.J != J) CK(cudaMemsetAsync(g.delta[i], 0, n * W * sizeof(uint32_t), g.stream));
-        TRY(dalloc(g.bitems[i], (size_t)g.n_fitems_cap + 4 * n + 1));
+        TRY(dalloc(g.bitems[i], (size_t)g.n_fitems_cap + (MAX_SLICES + 1) * n + 1));
         TRY(dalloc(g.bvl[i], n));
     }
     TRY(dalloc(g.inS, n));

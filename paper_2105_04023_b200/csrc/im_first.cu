@@ -151,23 +151,28 @@ __device__ __forceinline__ void gather_multi(const FirstArgs& a, const uint32_t*
         }
     }
     int lo[U], hi[U];
-    uint32_t pre[U], hv[U];
+    uint32_t pre[U], pre2[U], hv[U];
 #pragma unroll
     for (int k = 0; k < U; k++) {
         lo[k] = hi[k] = 0;
-        hv[k] = pre[k] = 0u;
+        hv[k] = pre[k] = pre2[k] = 0u;
         if (T[k]) edge_window(f[k].y, T[k], sX, sS, a.J, lo[k], hi[k]);
         if (lo[k] < hi[k]) {
             wcount++;
             if (!MEM) hv[k] = murmur_word(f[k].x, a.seedV);
-            else if (hi[k] - lo[k] <= DENSE_WIN) pre[k] = reinterpret_cast<const uint32_t*>(a.M)[(size_t)f[k].x * (a.J >> 2) + (lo[k] >> 2)];
+            else if (hi[k] - lo[k] <= DENSE_WIN) {  // the first two window words (a 4-simulation window spans two words 3/4 of the time)
+                const uint32_t* rv = reinterpret_cast<const uint32_t*>(a.M) + (size_t)f[k].x * (a.J >> 2);
+                pre[k] = rv[lo[k] >> 2];
+                if (((hi[k] - 1) >> 2) > (lo[k] >> 2)) pre2[k] = rv[(lo[k] >> 2) + 1];
+            }
         }
     }
 #pragma unroll
     for (int k = 0; k < U; k++) {
         if (lo[k] < hi[k] && hi[k] - lo[k] <= DENSE_WIN)
             for (int w = lo[k] >> 2; w <= (hi[k] - 1) >> 2; ++w)
-                merge_word<BLOCKED, MEM>(a, sX, sHJ, sVis, row, f[k].x, hv[k], f[k].y, T[k], lo[k], hi[k], w, w == (lo[k] >> 2), pre[k]);
+                merge_word<BLOCKED, MEM>(a, sX, sHJ, sVis, row, f[k].x, hv[k], f[k].y, T[k], lo[k], hi[k], w, w - (lo[k] >> 2) < 2,
+                                         w == (lo[k] >> 2) ? pre[k] : pre2[k]);
         uint32_t dmask = __ballot_sync(IM_FULL, hi[k] - lo[k] > DENSE_WIN);
         while (dmask) {
             const int l = __ffs(dmask) - 1;
@@ -227,14 +232,15 @@ __device__ __forceinline__ void first_small(const FirstArgs& a, const uint32_t* 
     const uint32_t hu = MEM ? 0u : murmur_word(u, a.seedV);
     const int w0 = lo >> 2, w1 = lo < hi ? (hi - 1) >> 2 : w0 - 1;
     // MEM: the out-neighbour's first window word is loaded now, in flight with the row words below
-    const uint32_t pre = MEM && lo < hi ? reinterpret_cast<const uint32_t*>(a.M)[(size_t)v * (J >> 2) + w0] : 0u;
+    const uint32_t* rv = reinterpret_cast<const uint32_t*>(a.M) + (size_t)v * (J >> 2);
+    const uint32_t pre = MEM && lo < hi ? rv[w0] : 0u, pre2 = MEM && w1 > w0 ? rv[w0 + 1] : 0u;
     if (lane < NB) bm[lane] = 0u;
     if (lane < W) scm[lane] = 0u;
     __syncwarp();
     for (int w = w0; w <= w1; ++w) atomicOr(&bm[w >> 5], 1u << (w & 31));
     for (int w = w0; w <= w1; ++w) row[w] = start_word<MEM>(a, sHJ, hu, u, w);  // same value from every writer
     __syncwarp();
-    for (int w = w0; w <= w1; ++w) merge_word<BLOCKED, MEM>(a, sX, sHJ, sVis, row, v, hv, h, T, lo, hi, w, w == w0, pre);
+    for (int w = w0; w <= w1; ++w) merge_word<BLOCKED, MEM>(a, sX, sHJ, sVis, row, v, hv, h, T, lo, hi, w, w - w0 < 2, w == w0 ? pre : pre2);
     __syncwarp();
     // every touched word is finished once, by the lane that clears its bitmap bit first; its change
     // nibble goes to the warp's change-mask words (word w >> 3 of the row's J/32)

@@ -13,6 +13,7 @@ namespace im {
 typedef unsigned long long ull;
 
 constexpr int SEG = 256;        // max edges per work item (a segment of one vertex's edge list)
+constexpr int MAX_SLICES = 8; // hash slices per long row (more non-zero mask words: the whole row)
 constexpr int DENSE_WIN = 32;   // windows wider than this many simulations take the warp-cooperative path
 constexpr int BLOCK = 256;      // threads per block of the persistent work-list kernels
 constexpr int FIRST_BIG = 2048; // first sweep: rows with more out-edges are gathered by a whole block
@@ -86,6 +87,8 @@ struct Ctx {
     int32_t* big = nullptr;                  // long rows awaiting slicing
     bool sweep_dirty = true;   // change buffers may hold stale bits (fresh / aborted build)
     bool trace = false;        // IM_TRACE: per-sweep / per-level lines on stderr
+    int slice_min = SEG;       // sweeps: in-rows longer than this are enumerated by hash slices (IM_SLICE_MIN)
+    int slice_min_bfs = SEG;   // BFS levels: out-rows longer than this are enumerated by hash slices (IM_SLICE_MIN_BFS)
     int64_t list_max = 65536;  // cap of the lazy argmax candidate list length (IM_LIST_MAX)
     double pull_frac = 0.97;   // gather sweep when the push frontier's in-edges exceed this share of m (IM_PULL_FRAC)
     IterCounters* ctr = nullptr;   // [2]
@@ -178,7 +181,7 @@ cudaError_t launch_sweep(Ctx& c, const int4* items, int n_items, const uint32_t*
                          uint32_t* bits_out, IterCounters* ctr, bool blocked);
 cudaError_t launch_commit(Ctx& c, const uint32_t* bits_new);
 cudaError_t launch_slices_big(Ctx& c, const int32_t* big, const uint32_t* mask, const int32_t* offs, const uint2* rec,
-                              int4* items_out, IterCounters* ctr);
+                              int4* items_out, IterCounters* ctr, bool whole_dense);
 // bits_out: this sweep's chunk-change bits (red.or); counters in *ctr (zeroed by the caller)
 cudaError_t launch_sweep(Ctx& c, const int4* items, int n_items, const uint32_t* bits_in, uint32_t* bits_out,
                          IterCounters* ctr, bool blocked);

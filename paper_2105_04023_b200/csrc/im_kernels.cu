@@ -9,6 +9,8 @@
 // INT pipes.  All work-list kernels are persistent (grid <= resident blocks)
 // and pull 32-item batches from a device cursor.
 
+#include <climits>
+
 #include "im_device.cuh"
 #include "im_internal.h"
 
@@ -494,7 +496,7 @@ __global__ void __launch_bounds__(BLOCK, BFS_MINB) k_bfs_level2(BfsArgs a) {
 // Delta rows (dout), the visited words are copied to vis (R_G(S) for every other kernel) and vd[].y
 // is cleared.  Otherwise (the evaluator) dout already holds them.
 template <bool VDM>
-__global__ void k_bfs_compact(int32_t n, int J, bool sorted, uint32_t* __restrict__ nbits, uint32_t* __restrict__ dout,
+__global__ void k_bfs_compact(int32_t n, int J, int slice_min, uint32_t* __restrict__ nbits, uint32_t* __restrict__ dout,
                               uint2* __restrict__ vd, uint32_t* __restrict__ vis,
                               const int32_t* __restrict__ off, int32_t* __restrict__ vl, int4* __restrict__ items,
                               int32_t* __restrict__ big, IterCounters* ctr, ull* sigma_count) {
@@ -537,7 +539,7 @@ __global__ void k_bfs_compact(int32_t n, int J, bool sorted, uint32_t* __restric
             }
             rb = off[v];
             rd = off[v + 1] - rb;
-            isbig = sorted && rd > SEG;
+            isbig = rd > slice_min;
             ns = isbig ? 0 : (rd + SEG - 1) / SEG;
         }
         uint32_t fmask = __ballot_sync(IM_FULL, b != 0u);
@@ -566,7 +568,7 @@ __global__ void k_bfs_compact(int32_t n, int J, bool sorted, uint32_t* __restric
 // Work items of a BFS frontier: for every vertex v of vl, its out-edges; a long row of a
 // hash-sorted graph is queued for k_slices_big (im_sweep.cu), which emits only the slices whose
 // candidate windows can meet a simulation of Delta_v.
-__global__ void k_bfs_items(bool sorted, const int32_t* __restrict__ vl, const int32_t* __restrict__ off,
+__global__ void k_bfs_items(int slice_min, const int32_t* __restrict__ vl, const int32_t* __restrict__ off,
                             int4* __restrict__ items, int32_t* __restrict__ big, IterCounters* ctr) {
     const int lane = threadIdx.x & 31;
     const int nv = ctr->changed;
@@ -578,7 +580,7 @@ __global__ void k_bfs_items(bool sorted, const int32_t* __restrict__ vl, const i
         if (i < nv) {
             rb = off[v];
             rd = off[v + 1] - rb;
-            isbig = sorted && rd > SEG;
+            isbig = rd > slice_min;
             ns = isbig ? 0 : (rd + SEG - 1) / SEG;
         }
         uint32_t bmask = __ballot_sync(IM_FULL, isbig);
@@ -755,27 +757,27 @@ cudaError_t launch_bfs_level(Ctx& c, int cur, int n_items, uint32_t tag) {
     cudaError_t e = LAUNCHED(c);
     if (e) return e;
     const int nxt = cur ^ 1;
-    k_bfs_compact<true><<<grid_for(c, c.n), BLOCK, 0, c.stream>>>(c.n, c.J, c.sorted_h, c.nbits, c.delta[nxt], c.vd, c.vis, c.off, c.bvl[nxt],
+    k_bfs_compact<true><<<grid_for(c, c.n), BLOCK, 0, c.stream>>>(c.n, c.J, c.sorted_h ? c.slice_min_bfs : INT_MAX, c.nbits, c.delta[nxt], c.vd, c.vis, c.off, c.bvl[nxt],
                                                             c.bitems[nxt], c.big, &c.ctr[nxt], c.sigma_count);
     if ((e = LAUNCHED(c))) return e;
     if (!c.sorted_h) return e;
-    return launch_slices_big(c, c.big, c.delta[nxt], c.off, c.fwd, c.bitems[nxt], &c.ctr[nxt]);
+    return launch_slices_big(c, c.big, c.delta[nxt], c.off, c.fwd, c.bitems[nxt], &c.ctr[nxt], true);
 }
 cudaError_t launch_bfs_items(Ctx& c, int buf) {
-    k_bfs_items<<<c.num_sms * 4, BLOCK, 0, c.stream>>>(c.sorted_h, c.bvl[buf], c.off, c.bitems[buf], c.big, &c.ctr[buf]);
+    k_bfs_items<<<c.num_sms * 4, BLOCK, 0, c.stream>>>(c.sorted_h ? c.slice_min_bfs : INT_MAX, c.bvl[buf], c.off, c.bitems[buf], c.big, &c.ctr[buf]);
     cudaError_t e = LAUNCHED(c);
     if (e || !c.sorted_h) return e;
-    return launch_slices_big(c, c.big, c.delta[buf], c.off, c.fwd, c.bitems[buf], &c.ctr[buf]);
+    return launch_slices_big(c, c.big, c.delta[buf], c.off, c.fwd, c.bitems[buf], &c.ctr[buf], true);
 }
 // the same compaction / item / clear kernels on caller-chosen buffers, unsorted rows (evaluator, im_eval.cu)
 cudaError_t launch_bfs_compact_raw(Ctx& c, int J, uint32_t* nbits, const uint32_t* dout, int32_t* vl, int4* items,
                                    IterCounters* ctr, ull* count) {
-    k_bfs_compact<false><<<grid_for(c, c.n), BLOCK, 0, c.stream>>>(c.n, J, false, nbits, const_cast<uint32_t*>(dout), nullptr, nullptr,
+    k_bfs_compact<false><<<grid_for(c, c.n), BLOCK, 0, c.stream>>>(c.n, J, INT_MAX, nbits, const_cast<uint32_t*>(dout), nullptr, nullptr,
                                                                    c.off, vl, items, nullptr, ctr, count);
     return LAUNCHED(c);
 }
 cudaError_t launch_bfs_items_raw(Ctx& c, const int32_t* vl, int4* items, IterCounters* ctr) {
-    k_bfs_items<<<c.num_sms * 4, BLOCK, 0, c.stream>>>(false, vl, c.off, items, nullptr, ctr);
+    k_bfs_items<<<c.num_sms * 4, BLOCK, 0, c.stream>>>(INT_MAX, vl, c.off, items, nullptr, ctr);
     return LAUNCHED(c);
 }
 cudaError_t launch_bfs_clear_raw(Ctx& c, int n_v, int W, const int32_t* vl, uint32_t* delta) {

@@ -14,6 +14,8 @@
 // form one contiguous window [lo, hi) (im_device.cuh).  A lane owns one edge; it touches only the
 // 8-byte words of M_u / M_v inside the window and merges with a bytewise-max CAS.  Windows wider
 // than DENSE_WIN simulations are walked by the whole warp.  Two edges per lane are kept in flight.
+#include <climits>
+
 #include "im_device.cuh"
 #include "im_internal.h"
 
@@ -278,7 +280,7 @@ __global__ void __launch_bounds__(BLOCK, 4) k_sweep(SweepArgs a) {
 // row of a hash-sorted graph is queued for k_slices_big, which emits, per 32-simulation word of
 // v's change mask, the slice of the row whose windows can meet those simulations.  The buffers
 // of the sweep before are cleared here for the next sweep's writes.
-__global__ void k_compact(int32_t n, int J, bool sorted, const uint32_t* __restrict__ bits_new, uint32_t* __restrict__ bits_clear,
+__global__ void k_compact(int32_t n, int J, int slice_min, const uint32_t* __restrict__ bits_new, uint32_t* __restrict__ bits_clear,
                           uint32_t* __restrict__ cm_clear, const int32_t* __restrict__ roff, int4* __restrict__ items,
                           int32_t* __restrict__ big, IterCounters* ctr) {
     const int lane = threadIdx.x & 31, W = J >> 5;
@@ -315,7 +317,7 @@ __global__ void k_compact(int32_t n, int J, bool sorted, const uint32_t* __restr
         if (b) {
             rb = roff[v];
             rd = roff[v + 1] - rb;
-            isbig = sorted && rd > SEG;
+            isbig = rd > slice_min;
             ns = isbig ? 0 : (rd > 0 ? (rd + SEG - 1) / SEG : 0);
         }
         uint32_t fmask = __ballot_sync(IM_FULL, b != 0u);
@@ -336,10 +338,14 @@ __global__ void k_compact(int32_t n, int J, bool sorted, const uint32_t* __restr
 }
 
 // warp per long row: one slice per non-zero 32-simulation word of the vertex's mask (change mask
-// for sweeps, Delta for BFS levels), trimmed so slices do not overlap, cut into <= SEG items
+// for sweeps, Delta for BFS levels), trimmed so slices do not overlap, cut into <= SEG items.
+// More than MAX_SLICES non-zero words: the slices of G = W / MAX_SLICES consecutive words are
+// merged (their union plus the buckets between them), which bounds a row's items by
+// ceil(len / SEG) + MAX_SLICES (the item buffers' capacity, im_abi.cu).  whole_dense (BFS): with
+// at least 3/4 of the words set the whole row is emitted without the binary searches.
 __global__ void k_slices_big(int J, int B, const uint32_t* __restrict__ Xs, const int32_t* __restrict__ big,
                              const uint32_t* __restrict__ mask, const int32_t* __restrict__ offs, const uint2* __restrict__ rec,
-                             int4* __restrict__ items, IterCounters* ctr) {
+                             int4* __restrict__ items, IterCounters* ctr, bool whole_dense) {
     const int lane = threadIdx.x & 31, W = J >> 5;
     const int nb = ctr->big;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -347,13 +353,39 @@ __global__ void k_slices_big(int J, int B, const uint32_t* __restrict__ Xs, cons
         const int v = big[i];
         const int rb = offs[v], re = offs[v + 1];
         int b0 = re, e0 = re;
+        const uint32_t m = lane < W ? mask[(size_t)v * W + lane] : 0u;
+        const int nzw = __popc(__ballot_sync(IM_FULL, m != 0u));
+        if (whole_dense && 4 * nzw >= 3 * W) {  // the per-edge test of the level drops the rest
+            const int ns = (re - rb + SEG - 1) / SEG;
+            int pos = 0;
+            if (lane == 0) {
+                pos = atomicAdd(&ctr->next_items, ns);
+                atomicAdd(&ctr->next_edges, (ull)(re - rb));
+            }
+            pos = __shfl_sync(IM_FULL, pos, 0);
+            for (int k = lane; k < ns; k += 32) items[pos + k] = make_int4(v, rb + k * SEG, min(rb + (k + 1) * SEG, re), 0);
+            continue;
+        }
         if (lane < W) {
-            uint32_t m = mask[(size_t)v * W + lane];
             if (m) {
                 int sa = 32 * lane + __ffs(m) - 1, sb = 32 * lane + 31 - __clz(m);
                 uint32_t klo = (__ldg(&Xs[sa]) >> B) << B, khi = ((__ldg(&Xs[sb]) >> B) + 1u) << B;
                 b0 = lower_bound_h(rec, rb, re, klo);
                 e0 = lower_bound_h(rec, b0, re, khi);
+            }
+        }
+        if (nzw > MAX_SLICES) {  // union of the slices of each group of G consecutive words, kept by its first lane
+            const int G = W / MAX_SLICES;  // W and MAX_SLICES are powers of two
+            int gb = b0 < e0 ? b0 : INT_MAX, ge = b0 < e0 ? e0 : INT_MIN;
+            for (int o = 1; o < G; o <<= 1) {
+                gb = min(gb, __shfl_xor_sync(IM_FULL, gb, o));
+                ge = max(ge, __shfl_xor_sync(IM_FULL, ge, o));
+            }
+            if ((lane & (G - 1)) == 0 && gb < ge) {
+                b0 = gb;
+                e0 = ge;
+            } else {
+                b0 = e0 = re;
             }
         }
         // trim against the furthest end of the lanes before (slice bounds grow with the word index)
@@ -443,16 +475,16 @@ cudaError_t launch_commit(Ctx& c, const uint32_t* bits_new) {
 
 cudaError_t launch_compact(Ctx& c, const uint32_t* bits_new, uint32_t* bits_clear, const uint32_t* cm_new,
                            uint32_t* cm_clear, int4* items_out, IterCounters* ctr) {
-    k_compact<<<grid_for(c, c.n), BLOCK, 0, c.stream>>>(c.n, c.J, c.sorted_h, bits_new, bits_clear, cm_clear, c.roff,
+    k_compact<<<grid_for(c, c.n), BLOCK, 0, c.stream>>>(c.n, c.J, c.sorted_h ? c.slice_min : INT_MAX, bits_new, bits_clear, cm_clear, c.roff,
                                                         items_out, c.big, ctr);
     cudaError_t e = LAUNCHED(c);
     if (e || !c.sorted_h) return e;
-    return launch_slices_big(c, c.big, cm_new, c.roff, c.rev, items_out, ctr);
+    return launch_slices_big(c, c.big, cm_new, c.roff, c.rev, items_out, ctr, false);
 }
 
 cudaError_t launch_slices_big(Ctx& c, const int32_t* big, const uint32_t* mask, const int32_t* offs, const uint2* rec,
-                              int4* items_out, IterCounters* ctr) {
-    k_slices_big<<<c.num_sms * 4, BLOCK, 0, c.stream>>>(c.J, c.B0, c.Xs, big, mask, offs, rec, items_out, ctr);
+                              int4* items_out, IterCounters* ctr, bool whole_dense) {
+    k_slices_big<<<c.num_sms * 4, BLOCK, 0, c.stream>>>(c.J, c.B0, c.Xs, big, mask, offs, rec, items_out, ctr, whole_dense);
     return LAUNCHED(c);
 }
 
