@@ -112,6 +112,7 @@ int ensure_device() {
     if (const char* lm = getenv("IM_LIST_MAX")) g.list_max = atoll(lm);
     if (const char* sm = getenv("IM_SLICE_MIN")) g.slice_min = atoi(sm);
     if (const char* sb = getenv("IM_SLICE_MIN_BFS")) g.slice_min_bfs = atoi(sb);
+    if (const char* se = getenv("IM_SMALL_EDGES")) g.small_edges = atoll(se);
     if (!g.own_stream) CK(cudaStreamCreateWithFlags(&g.own_stream, cudaStreamNonBlocking));
     if (!g.stream) g.stream = g.own_stream;
     if (!g.hpin) CK(cudaMallocHost(&g.hpin, 4096));
@@ -143,7 +144,7 @@ void release_all() {
     for (int i = 0; i < 2; i++) { dfree(g.items[i]); dfree(g.bits[i]); dfree(g.cm[i]); dfree(g.delta[i]); dfree(g.bitems[i]); dfree(g.bvl[i]); }
     dfree(g.inS); dfree(g.MS); dfree(g.btag); dfree(g.nbits); dfree(g.gain); dfree(g.big); dfree(g.list); dfree(g.lcount); dfree(g.hist);
     dfree(g.off); dfree(g.fwd); dfree(g.fwdT); dfree(g.roff); dfree(g.rev); dfree(g.revT); dfree(g.ritems); dfree(g.fbig);
-    dfree(g.ctr); dfree(g.rec); dfree(g.varsigma); dfree(g.key); dfree(g.first); dfree(g.sigma_count);
+    dfree(g.ctr); dfree(g.rec); dfree(g.sbo); dfree(g.varsigma); dfree(g.key); dfree(g.first); dfree(g.sigma_count);
     dfree(g.lval); dfree(g.sigma_g); dfree(g.bcount); dfree(g.Mold);
     dfree(g.ev_vis); dfree(g.ev_nbits); dfree(g.ev_ctr); dfree(g.ev_count);
     for (int i = 0; i < 2; i++) { dfree(g.ev_delta[i]); dfree(g.ev_items[i]); dfree(g.ev_vl[i]); }
@@ -249,6 +250,7 @@ int load_common(int32_t n, int64_t m, const int32_t* d_off_src, const int32_t* d
     // small per-graph state
     TRY(dalloc(g.ctr, 2));
     TRY(dalloc(g.rec, 1));
+    TRY(dalloc(g.sbo, 1));
     TRY(dalloc(g.varsigma, 1));
     TRY(dalloc(g.key, 1));
     TRY(dalloc(g.first, 1));
@@ -667,6 +669,23 @@ int im_select_seeds_ex(int32_t K, double eps_l, double eps_g, int32_t* out_seeds
         TRY(readback(&g.ctr[0], sizeof hc, &hc));
         int cur = 0;
         while (hc.next_items > 0) {
+            if ((long long)hc.next_edges <= g.small_edges) {  // small frontier: the next levels in one launch
+                g.st.bfs_edges += (int64_t)hc.next_edges;
+                CK(launch_bfs_small(g, cur, hc.changed, g.small_edges));
+                BfsSmallOut so;
+                TRY(readback(g.sbo, sizeof so, &so));
+                g.st.bfs_levels += so.levels;
+                g.st.bfs_edges += so.edges;
+                cur = so.cur;
+                if (g.trace)
+                    fprintf(stderr, "[im] bfs k=%d single-block: %d levels, %lld edges -> %s frontier %d\n", k, so.levels, so.edges,
+                            so.bailed ? "large" : "empty", so.n_v);
+                hc = IterCounters{};
+                if (!so.bailed) break;
+                CK(launch_bfs_items(g, cur));  // continue on the multi-block path from the frontier it left
+                TRY(readback(&g.ctr[cur], sizeof hc, &hc));
+                continue;
+            }
             int n_items = hc.next_items, n_v = hc.changed;
             g.st.bfs_edges += (int64_t)hc.next_edges;
             uint32_t tag = ++g.bt;

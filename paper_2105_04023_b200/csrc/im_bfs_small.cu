@@ -1,0 +1,173 @@
+// im_bfs_small.cu -- the seed diffusion (Alg. 1 lines 13-14) for small frontiers:
+// all levels of a BFS whose frontier stays small run inside ONE single-block launch.
+//
+// After the first seed most greedy steps reach only a few hundred (vertex, simulation) pairs per
+// level, and the multi-block level path (k_bfs_level2 + k_bfs_compact + k_slices_big + k_bfs_clear,
+// one host round trip per level) is then dominated by launch and synchronisation latency.  This
+// kernel carries the same state (frontier list bvl[cur], Delta rows delta[cur], the {visited,
+// new} pairs vd, R_G(S) words vis, per-vertex new-word flags nbits) through the levels with block
+// barriers: a warp takes a frontier vertex u and walks its whole out-row, lane per edge; for each
+// candidate word the simulations new at v are Delta_u & live & ~visited(v) (the same test and the
+// same fire-and-forget ORs as k_bfs_level2); v is appended to the next frontier by the thread whose
+// OR set its first new-word flag.  Between levels the new bits move to the next Delta rows and to vis
+// and are counted into sigma, exactly like k_bfs_compact.  When the next frontier's out-edges exceed
+// max_edges the kernel stops and leaves that frontier (list, Delta rows, counters) for the
+// multi-block path, which continues from it.
+#include "im_device.cuh"
+#include "im_internal.h"
+
+namespace im {
+
+constexpr int SB_THREADS = 1024;
+
+struct BfsSmallArgs {
+    int J;
+    const int32_t* off;
+    const uint2* fwd;
+    const uint32_t* fwdT;
+    uint32_t T0;
+    const uint32_t* Xs;
+    const uint16_t* s12;
+    uint2* vd;
+    uint32_t* vis;
+    uint32_t* nbits;
+    uint32_t* delta0;
+    uint32_t* delta1;
+    int32_t* vl0;
+    int32_t* vl1;
+    IterCounters* ctr;  // [2]
+    ull* sigma_count;
+    int cur, n_v;
+    long long max_edges;
+    BfsSmallOut* out;
+};
+
+template <bool CONST_T>
+__global__ void __launch_bounds__(SB_THREADS) k_bfs_small(BfsSmallArgs a) {
+    __shared__ uint32_t sX[1024];
+    __shared__ uint16_t sS[4098];
+    __shared__ uint32_t sD[SB_THREADS / 32][32];  // Delta row of each warp's frontier vertex
+    __shared__ int s_next;
+    __shared__ unsigned long long s_edges, s_bits;
+    const int W = a.J >> 5, lane = threadIdx.x & 31, wib = threadIdx.x >> 5, NWARP = SB_THREADS / 32;
+    for (int i = threadIdx.x; i < a.J; i += blockDim.x) sX[i] = a.Xs[i];
+    for (int i = threadIdx.x; i < 4097; i += blockDim.x) sS[i] = a.s12[i];
+    int cur = a.cur, n_v = a.n_v, levels = 0;
+    long long edges_total = 0;
+    bool bailed = false;
+    __syncthreads();
+    while (n_v > 0) {
+        const int32_t* vl = cur ? a.vl1 : a.vl0;
+        int32_t* vln = cur ? a.vl0 : a.vl1;
+        uint32_t* dcur = cur ? a.delta1 : a.delta0;
+        uint32_t* dnxt = cur ? a.delta0 : a.delta1;
+        if (threadIdx.x == 0) {
+            s_next = 0;
+            s_edges = 0ull;
+            s_bits = 0ull;
+        }
+        __syncthreads();
+        // level: every out-edge of every frontier vertex (warp per vertex, lane per edge)
+        for (int i = wib; i < n_v; i += NWARP) {
+            const uint32_t u = (uint32_t)vl[i];
+            if (lane < W) sD[wib][lane] = dcur[(size_t)u * W + lane];
+            __syncwarp();
+            const int eb = a.off[u], ee = a.off[u + 1];
+            for (int e = eb + lane; e < ee; e += 32) {
+                const uint2 f = a.fwd[e];
+                const uint32_t T = CONST_T ? a.T0 : a.fwdT[e];
+                if (!T) continue;
+                int lo, hi;
+                edge_window(f.y, T, sX, sS, a.J, lo, hi);
+                for (int w = lo >> 5; lo < hi && w <= (hi - 1) >> 5; ++w) {
+                    const uint32_t d = sD[wib][w];
+                    if (!d) continue;
+                    const int i0 = max(lo, w << 5), i1 = min(hi, (w << 5) + 32);
+                    uint32_t live = 0u;
+                    for (int k = i0; k < i1; ++k) live |= ((sX[k] ^ f.y) < T) ? (1u << (k & 31)) : 0u;
+                    uint32_t nv = live & d;
+                    if (!nv) continue;
+                    const size_t r = (size_t)f.x * W + w;
+                    nv &= ~__ldcg(&a.vd[r].x);
+                    if (!nv) continue;
+                    atomicOr(reinterpret_cast<ull*>(&a.vd[r]), ((ull)nv << 32) | nv);
+                    if (atomicOr(&a.nbits[f.x], 1u << w) == 0u) vln[atomicAdd(&s_next, 1)] = (int32_t)f.x;
+                }
+            }
+            __syncwarp();
+        }
+        __syncthreads();
+        // the level's frontier is consumed: clear its Delta rows (this buffer is the next level's output)
+        for (int64_t i = threadIdx.x; i < (int64_t)n_v * W; i += blockDim.x) dcur[(size_t)vl[i / W] * W + (i % W)] = 0u;
+        const int nn = s_next;
+        // compaction: new bits -> next Delta rows, R_G(S) words and sigma; out-edges of the next frontier
+        unsigned long long bits = 0ull, ed = 0ull;
+        for (int i = threadIdx.x; i < nn; i += blockDim.x) {
+            const uint32_t v = (uint32_t)vln[i];
+            uint32_t b = a.nbits[v];
+            a.nbits[v] = 0u;
+            for (; b; b &= b - 1) {
+                const size_t r = (size_t)v * W + (__ffs(b) - 1);
+                const uint2 p = a.vd[r];
+                dnxt[r] = p.y;
+                a.vis[r] = p.x;
+                a.vd[r] = make_uint2(p.x, 0u);
+                bits += __popc(p.y);
+            }
+            ed += (unsigned long long)(a.off[v + 1] - a.off[v]);
+        }
+        bits = __reduce_add_sync(IM_FULL, (uint32_t)bits);  // < 2^32 per warp (<= nn * J bits)
+        if (lane == 0 && bits) atomicAdd(&s_bits, bits);
+        if (ed) atomicAdd(&s_edges, ed);
+        __syncthreads();
+        edges_total += (long long)s_edges;  // the next level's enumerated edges
+        if (threadIdx.x == 0 && s_bits) *a.sigma_count += s_bits;
+        levels++;
+        cur ^= 1;
+        n_v = nn;
+        if (n_v > 0 && (long long)s_edges > a.max_edges) {
+            bailed = true;
+            break;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        a.out->levels = levels;
+        a.out->cur = cur;
+        a.out->n_v = n_v;
+        a.out->bailed = bailed ? 1 : 0;
+        a.out->edges = bailed ? edges_total - (long long)s_edges : edges_total;
+        IterCounters z{};
+        z.changed = n_v;
+        a.ctr[cur] = z;  // the multi-block path builds this frontier's items (k_bfs_items reads .changed)
+    }
+}
+
+cudaError_t launch_bfs_small(Ctx& c, int cur, int n_v, long long max_edges) {
+    BfsSmallArgs a;
+    a.J = c.J;
+    a.off = c.off;
+    a.fwd = c.fwd;
+    a.fwdT = c.fwdT;
+    a.T0 = c.T0;
+    a.Xs = c.Xs;
+    a.s12 = c.s12;
+    a.vd = c.vd;
+    a.vis = c.vis;
+    a.nbits = c.nbits;
+    a.delta0 = c.delta[0];
+    a.delta1 = c.delta[1];
+    a.vl0 = c.bvl[0];
+    a.vl1 = c.bvl[1];
+    a.ctr = c.ctr;
+    a.sigma_count = c.sigma_count;
+    a.cur = cur;
+    a.n_v = n_v;
+    a.max_edges = max_edges;
+    a.out = c.sbo;
+    if (c.constT) k_bfs_small<true><<<1, SB_THREADS, 0, c.stream>>>(a);
+    else k_bfs_small<false><<<1, SB_THREADS, 0, c.stream>>>(a);
+    return LAUNCHED(c);
+}
+
+}  // namespace im

@@ -30,6 +30,15 @@ struct IterCounters {
     ull win_edges;      // sweep: edges with a non-empty candidate window (after the change filter)
 };
 
+// result of a single-block small-frontier BFS run (im_bfs_small.cu)
+struct BfsSmallOut {
+    int levels;      // levels run
+    int cur;         // frontier buffer holding the frontier left (bailed) / the last one
+    int n_v;         // its vertices (0: the BFS is complete)
+    int bailed;      // 1: stopped because the next frontier's out-edges exceed max_edges
+    long long edges; // edges enumerated by the levels run, after the entry frontier's
+};
+
 struct StepDev {  // mirrors im_step
     int32_t vertex, pad;
     int64_t score;
@@ -102,6 +111,8 @@ struct Ctx {
     uint32_t bt = 0;
     uint32_t* nbits = nullptr;   // BFS: per-vertex words with new bits in the current level
     StepDev* rec = nullptr;
+    BfsSmallOut* sbo = nullptr;
+    long long small_edges = 8192;  // frontiers with at most this many out-edges: single-block BFS (IM_SMALL_EDGES; 0 = off)
     double* varsigma = nullptr;
     ull* key = nullptr;
     int* first = nullptr;
@@ -199,6 +210,8 @@ cudaError_t launch_seed_start(Ctx& c, int k);
 // the next frontier's vertex list / items and adds the level's new bits to sigma
 cudaError_t launch_bfs_level(Ctx& c, int cur, int n_items, uint32_t tag);
 cudaError_t launch_bfs_clear(Ctx& c, int cur, int n_v);
+// the rest of a BFS from frontier buffer cur (n_v vertices) in one single-block launch (result in c.sbo)
+cudaError_t launch_bfs_small(Ctx& c, int cur, int n_v, long long max_edges);
 cudaError_t launch_bfs_items(Ctx& c, int buf);
 cudaError_t launch_error_check(Ctx& c, int k, int K, double eps_l, double eps_g);
 cudaError_t launch_bfs_compact_raw(Ctx& c, int J, uint32_t* nbits, const uint32_t* dout, int32_t* vl, int4* items,
