@@ -17,18 +17,35 @@
 namespace im {
 
 // ============================================================ a5: Eq. 2 estimate
+// A warp sums EV rows per iteration (16-byte loads, all EV rows' loads in flight before the
+// reductions); lane k finishes row k, so the EV exp2 run in parallel.  Exact integer sums.
+constexpr int EV = 4;
 template <bool SUMS>
 __global__ void k_estimate(int32_t n, int32_t J, const uint32_t* __restrict__ M32, double* __restrict__ out, int32_t* sums) {
-    const int lane = threadIdx.x & 31, Jw = J >> 2;
+    const int lane = threadIdx.x & 31, nch = J >> 4;
+    const uint4* M16 = reinterpret_cast<const uint4*>(M32);
     const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < n; v += warps) {
-        uint32_t s = 0;
-        for (int w = lane; w < Jw; w += 32) s += __vsadu4(__ldcs(&M32[v * Jw + w]), 0u);
+    for (int64_t v0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * EV; v0 < n; v0 += warps * EV) {
+        uint32_t s[EV];
 #pragma unroll
-        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(IM_FULL, s, o);
-        if (lane == 0) {
-            if (SUMS) sums[v] = (int32_t)s;
-            else out[v] = exp2((double)s / (double)J) / 0.77351;
+        for (int k = 0; k < EV; k++) {
+            s[k] = 0u;
+            if (v0 + k < n)
+                for (int c = lane; c < nch; c += 32) {
+                    const uint4 x = __ldcs(&M16[(v0 + k) * nch + c]);
+                    s[k] += __vsadu4(x.x, 0u) + __vsadu4(x.y, 0u) + __vsadu4(x.z, 0u) + __vsadu4(x.w, 0u);
+                }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1)
+#pragma unroll
+            for (int k = 0; k < EV; k++) s[k] += __shfl_xor_sync(IM_FULL, s[k], o);
+        uint32_t mine = s[0];
+#pragma unroll
+        for (int k = 1; k < EV; k++) mine = lane == k ? s[k] : mine;
+        if (lane < EV && v0 + lane < n) {
+            if (SUMS) sums[v0 + lane] = (int32_t)mine;
+            else out[v0 + lane] = exp2((double)mine / (double)J) / 0.77351;
         }
     }
 }
@@ -68,7 +85,8 @@ constexpr int HIST_BINS = 4096;
 #define BFS_MINB 5  // min resident blocks per SM k_bfs_level2 is compiled for (48 registers, no spills)
 #endif
 constexpr int CU = 8;  // vertex groups of BLOCK per block iteration of the frontier compactions
-constexpr int AG = 4;  // vertex groups in flight per warp in k_argmax
+constexpr int AG = 2;  // vertex groups in flight per warp in k_argmax
+constexpr int AC = 4;  // max 16-byte chunks per lane in k_argmax (L = max(8, J/64))
 
 // LIST = false: every vertex (full pass: stores gains + histogram); LIST = true: the vertices in list[0..*count)
 // SHARD (list only): writes the packed local value gain + (in local pool) << 24 to gain_out[i] for list entry i
@@ -87,11 +105,11 @@ __global__ void __launch_bounds__(BLOCK) k_argmax(int32_t n, int32_t J, int L, i
     __syncthreads();
     const int nv = LIST ? *list_count : n;
     const int lane = threadIdx.x & 31, q = lane & (L - 1), sub = lane / L, VPW = 32 / L;
-    uint4 ms[2];
+    uint4 ms[AC];
     uint32_t msum = 0;  // sum of this lane's M_S' bytes (only over chunks the lane actually loads)
 #pragma unroll
-    for (int c = 0; c < 2; c++) {
-        int ci = q * C + c;
+    for (int c = 0; c < AC; c++) {
+        int ci = c * L + q;  // interleaved: the L lanes of a vertex read 16*L contiguous bytes per c
         ms[c] = (c < C && ci < nch) ? sMS[ci] : make_uint4(0, 0, 0, 0);
         msum += sum16(ms[c]);
     }
@@ -100,7 +118,7 @@ __global__ void __launch_bounds__(BLOCK) k_argmax(int32_t n, int32_t J, int L, i
     const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     ull best = 0;
     for (int64_t g0 = gw; g0 < groups; g0 += AG * nwarps) {
-        uint4 x[AG][2];
+        uint4 x[AG][AC];
         int64_t vv[AG];
         bool ok[AG];
 #pragma unroll
@@ -109,14 +127,16 @@ __global__ void __launch_bounds__(BLOCK) k_argmax(int32_t n, int32_t J, int L, i
             ok[u] = (g0 + u * nwarps) < groups && idx < nv;
             vv[u] = ok[u] ? (LIST ? (int64_t)list[idx] : idx) : 0;
 #pragma unroll
-            for (int c = 0; c < 2; c++) {
-                int ci = q * C + c;
+            for (int c = 0; c < AC; c++) {
+                int ci = c * L + q;
                 x[u][c] = (ok[u] && c < C && ci < nch) ? __ldcs(&M16[vv[u] * nch + ci]) : make_uint4(0, 0, 0, 0);
             }
         }
 #pragma unroll
         for (int u = 0; u < AG; u++) {
-            uint32_t gn = gain16x2(x[u][0], ms[0]) + gain16x2(x[u][1], ms[1]) - msum;
+            uint32_t gn = 0u - msum;
+#pragma unroll
+            for (int c = 0; c < AC; c++) gn += gain16x2(x[u][c], ms[c]);
             int full = 1;
             if (POOL && ok[u])
                 for (int w = q; w < W; w += L) full &= __ldcs(&vis[vv[u] * W + w]) == IM_FULL;
@@ -161,14 +181,33 @@ __global__ void __launch_bounds__(BLOCK) k_argmax(int32_t n, int32_t J, int L, i
 
 // theta = lower edge of the highest histogram bin at which the suffix count reaches T
 __global__ void k_theta(const uint32_t* __restrict__ hist, int shift, int T, int* theta) {
-    if (threadIdx.x == 0) {
-        long long acc = 0;
-        int b = HIST_BINS - 1;
-        for (; b > 0; --b) {
+    // the largest bin b >= 1 whose suffix count sum_{i >= b} hist[i] reaches T (0 if none), by one
+    // warp: lane l owns bins [l * PB, (l + 1) * PB); the lane where the suffix count crosses T walks
+    // its bins from the top
+    constexpr int PB = HIST_BINS / 32;
+    const int lane = threadIdx.x;
+    long long tot = 0;
+    for (int i = 0; i < PB; i++) tot += hist[lane * PB + i];
+    long long suf = tot;  // sum over lanes >= this one
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_down_sync(IM_FULL, suf, o);
+        if (lane + o < 32) suf += y;
+    }
+    const long long above = suf - tot;
+    const bool mine = above < (long long)T && (long long)T <= suf;
+    if (!__any_sync(IM_FULL, mine)) {
+        if (lane == 0) *theta = 0;
+        return;
+    }
+    if (mine) {
+        long long acc = above;
+        int b = lane * PB + PB - 1;
+        for (;; --b) {
             acc += hist[b];
-            if (acc >= T) break;
+            if (acc >= T || b == lane * PB) break;
         }
-        *theta = b << shift;
+        *theta = (b < 1 ? 0 : b) << shift;
     }
 }
 
@@ -663,11 +702,13 @@ cudaError_t launch_estimate_fin(Ctx& c, const int32_t* sums, double* out) {
     k_estimate_fin<<<grid_for(c, c.n), BLOCK, 0, c.stream>>>(c.n, c.Jt, sums, out);
     return LAUNCHED(c);
 }
+// lanes per vertex and chunks per lane of the list pass: L = max(min(8, pow2 >= J/16), J/64), C <= AC
 static void argmax_geometry(const Ctx& c, int& L, int& C) {
     const int nch = c.J >> 4;
-    C = nch > 32 ? 2 : 1;
     L = 1;
-    while (L * C < nch) L <<= 1;
+    while (L < 8 && L < nch) L <<= 1;
+    while (L * AC < nch) L <<= 1;
+    C = (nch + L - 1) / L;
 }
 static int hist_shift(const Ctx& c) {
     int sh = 0;
