@@ -86,6 +86,8 @@ int dalloc(T*& p, size_t count, bool* fresh = nullptr) {
     return 0;
 }
 
+cudaError_t tab_alloc(int32_t*& p, size_t count) { return dalloc(p, count) ? cudaErrorMemoryAllocation : cudaSuccess; }
+
 using clk = std::chrono::steady_clock;
 double ms_since(clk::time_point t0) { return std::chrono::duration<double, std::milli>(clk::now() - t0).count(); }
 
@@ -144,6 +146,7 @@ void release_all() {
     for (int i = 0; i < 2; i++) { dfree(g.items[i]); dfree(g.bits[i]); dfree(g.cm[i]); dfree(g.delta[i]); dfree(g.bitems[i]); dfree(g.bvl[i]); }
     dfree(g.inS); dfree(g.MS); dfree(g.btag); dfree(g.nbits); dfree(g.gain); dfree(g.big); dfree(g.list); dfree(g.lcount); dfree(g.hist);
     dfree(g.off); dfree(g.fwd); dfree(g.fwdT); dfree(g.roff); dfree(g.rev); dfree(g.revT); dfree(g.ritems); dfree(g.fbig);
+    dfree(g.ftidx); dfree(g.rtidx); dfree(g.ftab); dfree(g.rtab); dfree(g.t_tabrows);
     dfree(g.ctr); dfree(g.rec); dfree(g.sbo); dfree(g.varsigma); dfree(g.key); dfree(g.first); dfree(g.sigma_count);
     dfree(g.lval); dfree(g.sigma_g); dfree(g.bcount); dfree(g.Mold);
     dfree(g.ev_vis); dfree(g.ev_nbits); dfree(g.ev_ctr); dfree(g.ev_count);
@@ -222,6 +225,15 @@ int load_common(int32_t n, int64_t m, const int32_t* d_off_src, const int32_t* d
     for (int i = 0; i < 5; i++) {
         TRY(dalloc(g.t_prep[i], sz[i]));
         scr[i] = g.t_prep[i];
+    }
+    // bucket offset tables of the long rows (hash slices without binary searches), written by the prep
+    g.nbk = 0;
+    if (rows_path(g) && m > 0) {
+        g.nbk = (1 << (31 - g.B0)) + 1;
+        TRY(dalloc(g.ftidx, (size_t)n));
+        TRY(dalloc(g.rtidx, (size_t)n));
+        TRY(dalloc(g.t_tabrows, (size_t)n));
+        g.alloc_i32 = tab_alloc;
     }
     CK(prep_edges(g, d_tgt, d_prob, indeg, nullptr, scr, sz));
     // work items: reverse segments of every vertex (sweep 1), forward item capacity (BFS)

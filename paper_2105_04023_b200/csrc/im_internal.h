@@ -13,6 +13,7 @@ namespace im {
 typedef unsigned long long ull;
 
 constexpr int SEG = 256;        // max edges per work item (a segment of one vertex's edge list)
+constexpr int TAB_MIN = SEG;  // rows longer than this get a bucket offset table (rows path)
 constexpr int MAX_SLICES = 8; // hash slices per long row (more non-zero mask words: the whole row)
 constexpr int DENSE_WIN = 32;   // windows wider than this many simulations take the warp-cooperative path
 constexpr int BLOCK = 256;      // threads per block of the persistent work-list kernels
@@ -67,6 +68,13 @@ struct Ctx {
     int B0 = 0;                 // thr_bits(T0): candidate windows are salt blocks of 2^B0
     bool sorted_h = false;      // adjacency rows sorted by h (constant threshold only)
     int4* ritems = nullptr;     // all reverse segments {v, eb, ee, 0}
+    int nbk = 0;                // bucket offset tables: 2^KB + 1 entries per long row (0: none, binary search)
+    int32_t* ftidx = nullptr;   // per vertex: its forward row's table, -1 if none
+    int32_t* rtidx = nullptr;
+    int32_t* ftab = nullptr;    // forward tables [rows x nbk]
+    int32_t* rtab = nullptr;
+    int32_t* t_tabrows = nullptr;
+    cudaError_t (*alloc_i32)(int32_t*&, size_t) = nullptr;  // device allocation with capacity reuse (im_abi.cu)
     int32_t n_ritems = 0;
     int32_t n_fitems_cap = 0;   // sum_v ceil(outdeg/SEG)
     int32_t* fbig = nullptr;    // vertices with > FIRST_BIG out-edges
@@ -177,6 +185,8 @@ int setup_first(int J, int* blocks_per_sm);  // smem opt-in + occupancy of the f
 // register init + first sweep (gather, im_first.cu): writes every row, its change mask and chunk bits
 cudaError_t launch_first(Ctx& c, uint32_t* cm_out, uint32_t* bits_out, IterCounters* ctr, bool blocked, bool from_memory);
 cudaError_t launch_list_big_rows(Ctx& c, int32_t* out, int* count);
+bool rows_path(const Ctx& c);  // constant threshold with KB <= 8: row-local bucket order, bucket tables
+
 cudaError_t launch_validate(Ctx& c, const int32_t* off, const int32_t* tgt, const float* prob, int* flags);
 cudaError_t launch_const_check(Ctx& c, const float* prob, int* flag);
 cudaError_t prep_scratch_sizes(Ctx& c, size_t* sz);  // 5 sizes (bytes) for prep_edges scratch

@@ -143,7 +143,20 @@ struct RowSortArgs {
     const int32_t* lst;     // k_rows_big: rows longer than PREP_BIG
     const int* lcount;
     int* batch;             // dynamic row-batch cursor (zeroed)
+    const int32_t* tidx;    // bucket offset table of each row (-1: none), tables tab[rows x nbk]
+    int32_t* tab;
+    int nbk;
 };
+
+// the bucket offsets of a row with a table: hist holds the exclusive scan of its bucket counts
+template <typename K>
+__device__ __forceinline__ void write_row_table(const RowSortArgs<K>& a, uint32_t u, int eb, int ee, const int* hist, int NB,
+                                                int tid, int nthreads) {
+    const int t = a.tidx ? a.tidx[u] : -1;
+    if (t < 0) return;
+    int32_t* tb = a.tab + (int64_t)t * a.nbk;
+    for (int kb = tid; kb <= NB; kb += nthreads) tb[kb] = kb < NB ? eb + hist[kb] : ee;
+}
 
 // record {v, h(u,v)} of input edge e of row u (+ its reverse key and payload on the first visit)
 template <typename K>
@@ -232,6 +245,7 @@ __global__ void __launch_bounds__(BLOCK) k_rows(RowSortArgs<K> a) {
             }
             warp_scan_bins(hist, NB, lane);
             __syncwarp();
+            write_row_table(a, (uint32_t)u, eb, ee, hist, NB, lane, 32);
             for (int e0 = eb; e0 < ee; e0 += 32) {  // pass 2: place (stable)
                 const bool have = e0 + lane < ee;
                 uint2 r = make_uint2(0, 0);
@@ -272,6 +286,8 @@ __global__ void __launch_bounds__(BLOCK) k_rows_big(RowSortArgs<K> a) {
         __syncthreads();
         if (threadIdx.x < 32) warp_scan_bins(hist, NB, threadIdx.x);
         __syncthreads();
+        write_row_table(a, u, eb, ee, hist, NB, threadIdx.x, blockDim.x);
+        __syncthreads();  // the table is read from hist before the placement below advances it
         for (int e0 = eb; e0 < ee; e0 += blockDim.x) {
             const bool have = e0 + (int)threadIdx.x < ee;
             uint2 r = make_uint2(0, 0);
@@ -299,6 +315,57 @@ __global__ void k_row_bounds(int64_t m, int32_t n, const K* __restrict__ keys, i
         const int64_t p = i > 0 ? (int64_t)(keys[i - 1] >> KB) : -1;
         for (int64_t v = p + 1; v <= r; ++v) roff[v] = (int32_t)i;
     }
+}
+
+// reverse-row bucket tables from the sorted keys (row = key >> KB, bucket = low KB bits): position i
+// starts buckets (previous bucket of its row, bucket(i)]; the row's last position ends the rest
+template <typename K>
+__global__ void k_rev_tabs(int64_t m, const K* __restrict__ keys, int KB, const int32_t* __restrict__ tidx, int nbk,
+                           int32_t* __restrict__ tab) {
+    const K mask = ((K)1 << KB) - 1;
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += stride) {
+        const K k = keys[i];
+        const int64_t r = (int64_t)(k >> KB);
+        const int t = tidx[r];
+        if (t < 0) continue;
+        int32_t* tb = tab + (int64_t)t * nbk;
+        const int b = (int)(k & mask);
+        const int pb = (i > 0 && (int64_t)(keys[i - 1] >> KB) == r) ? (int)(keys[i - 1] & mask) : -1;
+        for (int kb = pb + 1; kb <= b; ++kb) tb[kb] = (int32_t)i;
+        if (i + 1 == m || (int64_t)(keys[i + 1] >> KB) != r)
+            for (int kb = b + 1; kb < nbk; ++kb) tb[kb] = (int32_t)(i + 1);
+    }
+}
+
+// ------------------------------------------------------------------ bucket offset tables of long rows
+// For a bucket-ordered row longer than TAB_MIN, tab[kb] = first position whose bucket h >> B is
+// >= kb (kb = 0 .. 2^KB; the row end if none): the hash slices of k_slices_big (im_sweep.cu) are
+// then two table reads instead of two binary searches over the row.
+__global__ void k_tab_index(int32_t n, const int32_t* __restrict__ offs, int32_t* __restrict__ tidx, int32_t* __restrict__ rows,
+                            int* count) {
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += stride) {
+        int t = -1;
+        if (offs[v + 1] - offs[v] > TAB_MIN) {
+            t = atomicAdd(count, 1);
+            rows[t] = (int32_t)v;
+        }
+        tidx[v] = t;
+    }
+}
+
+// rows longer than TAB_MIN get a table: index per vertex, count read back, tables allocated
+static cudaError_t setup_tables(Ctx& c, const int32_t* offs, int32_t* tidx, int32_t*& tab, int* d_count) {
+    cudaError_t e;
+    if ((e = cudaMemsetAsync(d_count, 0, sizeof(int), c.stream))) return e;
+    k_tab_index<<<grid_for(c, c.n), BLOCK, 0, c.stream>>>(c.n, offs, tidx, c.t_tabrows, d_count);
+    if ((e = LAUNCHED(c))) return e;
+    int h = 0;
+    if ((e = cudaMemcpyAsync(c.hpin, d_count, sizeof(int), cudaMemcpyDeviceToHost, c.stream))) return e;
+    if ((e = cudaStreamSynchronize(c.stream))) return e;
+    h = *(int*)c.hpin;
+    return h ? c.alloc_i32(tab, (size_t)h * c.nbk) : cudaSuccess;
 }
 
 // ------------------------------------------------------------------ a2: register init
@@ -378,14 +445,14 @@ void prep_key_bits(const Ctx& c, int& KB, int& end_bit, bool& wide) {
 }
 
 // the row-local bucket ordering applies (constant threshold, at most 2^PREP_KB_MAX buckets)
-static bool rows_path(const Ctx& c) { return c.sorted_h && 31 - c.B0 <= PREP_KB_MAX; }
+bool rows_path(const Ctx& c) { return c.sorted_h && 31 - c.B0 <= PREP_KB_MAX; }
 
 template <typename K>
 static cudaError_t prep_rows(Ctx& c, const int32_t* tgt, void** scr, size_t tb, int KB, int end_bit) {
     cudaError_t e;
     const int n = c.n;
     int32_t* lf = (int32_t*)scr[0];
-    int* cnt = (int*)(lf + n);  // [0] long-row count, [1] batch cursor
+    int* cnt = (int*)(lf + n);  // [0] long-row count, [1] batch cursor, [2] table count
     if ((e = cudaMemsetAsync(cnt, 0, 2 * sizeof(int), c.stream))) return e;
     k_list_long<<<grid_for(c, n), BLOCK, 0, c.stream>>>(n, c.off, lf, cnt);
     if ((e = LAUNCHED(c))) return e;
@@ -401,6 +468,12 @@ static cudaError_t prep_rows(Ctx& c, const int32_t* tgt, void** scr, size_t tb, 
     a.lst = lf;
     a.lcount = cnt;
     a.batch = cnt + 1;
+    if (c.nbk) {  // forward bucket tables, written by the row sort itself
+        if ((e = setup_tables(c, c.off, c.ftidx, c.ftab, cnt + 2))) return e;
+        a.tidx = c.ftidx;
+        a.tab = c.ftab;
+        a.nbk = c.nbk;
+    }
     k_rows<K><<<c.num_sms * 8, BLOCK, 0, c.stream>>>(a);
     if ((e = LAUNCHED(c))) return e;
     k_rows_big<K><<<c.num_sms * 4, BLOCK, 0, c.stream>>>(a);
@@ -409,6 +482,9 @@ static cudaError_t prep_rows(Ctx& c, const int32_t* tgt, void** scr, size_t tb, 
     c.launches += (end_bit + 7) / 8 + 1;
     if (e) return e;
     k_row_bounds<K><<<grid_for(c, c.m + 1), BLOCK, 0, c.stream>>>(c.m, n, (const K*)scr[2], KB, c.roff);
+    if ((e = LAUNCHED(c)) || !c.nbk) return e;
+    if ((e = setup_tables(c, c.roff, c.rtidx, c.rtab, cnt + 2))) return e;  // reverse bucket tables
+    k_rev_tabs<K><<<grid_for(c, c.m), BLOCK, 0, c.stream>>>(c.m, (const K*)scr[2], KB, c.rtidx, c.nbk, c.rtab);
     return LAUNCHED(c);
 }
 

@@ -14,6 +14,7 @@
 // form one contiguous window [lo, hi) (im_device.cuh).  A lane owns one edge; it touches only the
 // 8-byte words of M_u / M_v inside the window and merges with a bytewise-max CAS.  Windows wider
 // than DENSE_WIN simulations are walked by the whole warp.  Two edges per lane are kept in flight.
+#include <algorithm>
 #include <climits>
 
 #include "im_device.cuh"
@@ -22,6 +23,9 @@
 namespace im {
 #ifndef IM_NS
 #define IM_NS 2
+#endif
+#ifndef SWEEP_MINB
+#define SWEEP_MINB 4  // resident blocks per SM k_sweep is compiled for
 #endif
 
 struct SweepArgs {
@@ -40,6 +44,7 @@ struct SweepArgs {
     const uint32_t* cm_in;   // per-simulation change mask of the previous sweep, n x J/32 words (FILTER)
     uint32_t* cm_out;        // this sweep's per-simulation change mask
     uint32_t* bits_out;      // this sweep's per-vertex 32-simulation-chunk summary
+    int ipw;                 // items per warp batch (<= 32; fewer when the sweep is small, to spread it over the SMs)
 };
 
 __device__ __forceinline__ ull vmax8(ull a, ull b) {
@@ -133,7 +138,7 @@ __device__ __forceinline__ bool live_changed(const uint32_t* __restrict__ cm, ui
 constexpr int NS = IM_NS;  // edges in flight per lane
 
 template <bool CONST_T, bool BLOCKED, bool FILTER>
-__global__ void __launch_bounds__(BLOCK, 4) k_sweep(SweepArgs a) {
+__global__ void __launch_bounds__(BLOCK, SWEEP_MINB) k_sweep(SweepArgs a) {
     __shared__ uint32_t sX[1024];
     __shared__ uint16_t sS[4098];
     __shared__ int sSlot[BLOCK / 32][32];
@@ -148,17 +153,17 @@ __global__ void __launch_bounds__(BLOCK, 4) k_sweep(SweepArgs a) {
     int base = 0, left = 0;  // 128-item grabs (4 batches of 32) keep the cursor atomic off the critical path
     for (;;) {
         if (left == 0) {
-            if (lane == 0) base = atomicAdd(&a.ctr->batch, 128);
+            if (lane == 0) base = atomicAdd(&a.ctr->batch, 4 * a.ipw);
             base = __shfl_sync(IM_FULL, base, 0);
             left = 4;
         } else {
-            base += 32;
+            base += a.ipw;
         }
         --left;
         if (base >= a.n_items) break;
         int it = base + lane;
         int v = 0, eb = 0, cnt = 0;
-        if (it < a.n_items) {
+        if (lane < a.ipw && it < a.n_items) {
             int4 I = a.items[it];
             v = I.x;
             eb = I.y;
@@ -345,7 +350,8 @@ __global__ void k_compact(int32_t n, int J, int slice_min, const uint32_t* __res
 // at least 3/4 of the words set the whole row is emitted without the binary searches.
 __global__ void k_slices_big(int J, int B, const uint32_t* __restrict__ Xs, const int32_t* __restrict__ big,
                              const uint32_t* __restrict__ mask, const int32_t* __restrict__ offs, const uint2* __restrict__ rec,
-                             int4* __restrict__ items, IterCounters* ctr, bool whole_dense) {
+                             int4* __restrict__ items, IterCounters* ctr, bool whole_dense, const int32_t* __restrict__ tidx,
+                             const int32_t* __restrict__ tab, int nbk) {
     const int lane = threadIdx.x & 31, W = J >> 5;
     const int nb = ctr->big;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -369,9 +375,15 @@ __global__ void k_slices_big(int J, int B, const uint32_t* __restrict__ Xs, cons
         if (lane < W) {
             if (m) {
                 int sa = 32 * lane + __ffs(m) - 1, sb = 32 * lane + 31 - __clz(m);
-                uint32_t klo = (__ldg(&Xs[sa]) >> B) << B, khi = ((__ldg(&Xs[sb]) >> B) + 1u) << B;
-                b0 = lower_bound_h(rec, rb, re, klo);
-                e0 = lower_bound_h(rec, b0, re, khi);
+                const uint32_t kbl = __ldg(&Xs[sa]) >> B, kbh = (__ldg(&Xs[sb]) >> B) + 1u;
+                const int t = tidx ? __ldg(&tidx[v]) : -1;
+                if (t >= 0) {  // bucket offset table of the row (im_prep.cu)
+                    b0 = __ldg(&tab[(int64_t)t * nbk + kbl]);
+                    e0 = __ldg(&tab[(int64_t)t * nbk + kbh]);
+                } else {
+                    b0 = lower_bound_h(rec, rb, re, kbl << B);
+                    e0 = lower_bound_h(rec, b0, re, kbh << B);
+                }
             }
         }
         if (nzw > MAX_SLICES) {  // union of the slices of each group of G consecutive words, kept by its first lane
@@ -439,7 +451,10 @@ cudaError_t launch_sweep(Ctx& c, const int4* items, int n_items, const uint32_t*
     a.cm_in = cm_in;
     a.cm_out = cm_out;
     a.bits_out = bits_out;
-    int64_t want = ((int64_t)n_items + 32 * (BLOCK / 32) - 1) / (32 * (BLOCK / 32));
+    // items per warp batch: 32, or fewer so that a small sweep (long hub items) still fills the GPU
+    const int64_t warps_max = (int64_t)c.max_blocks_sweep * (BLOCK / 32);
+    a.ipw = (int)std::min<int64_t>(32, std::max<int64_t>(1, n_items / warps_max));
+    int64_t want = ((int64_t)n_items + (int64_t)a.ipw * (BLOCK / 32) - 1) / ((int64_t)a.ipw * (BLOCK / 32));
     int grid = (int)(want < 1 ? 1 : (want > c.max_blocks_sweep ? c.max_blocks_sweep : want));
     const bool ct = c.constT, f = cm_in != nullptr;
     if (!f) {
@@ -484,7 +499,9 @@ cudaError_t launch_compact(Ctx& c, const uint32_t* bits_new, uint32_t* bits_clea
 
 cudaError_t launch_slices_big(Ctx& c, const int32_t* big, const uint32_t* mask, const int32_t* offs, const uint2* rec,
                               int4* items_out, IterCounters* ctr, bool whole_dense) {
-    k_slices_big<<<c.num_sms * 4, BLOCK, 0, c.stream>>>(c.J, c.B0, c.Xs, big, mask, offs, rec, items_out, ctr, whole_dense);
+    const bool fw = rec == c.fwd;
+    k_slices_big<<<c.num_sms * 4, BLOCK, 0, c.stream>>>(c.J, c.B0, c.Xs, big, mask, offs, rec, items_out, ctr, whole_dense,
+                                                        c.nbk ? (fw ? c.ftidx : c.rtidx) : nullptr, fw ? c.ftab : c.rtab, c.nbk);
     return LAUNCHED(c);
 }
 
