@@ -54,9 +54,10 @@ def report(path):
         for k, v in stalls[:8]:
             print(f"  {k.replace('smsp__average_warps_issue_stalled_', '').replace('_per_issue_active.ratio', ''):30s} {v:8.3f}")
         try:
-            rd = float(d["dram__bytes_read.sum"].replace(",", ""))
-            wr = float(d["dram__bytes_write.sum"].replace(",", ""))
-            print(f"# traffic per launch = {rd + wr:.4g} {u['dram__bytes_read.sum']}")
+            b = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+            rd = float(d["dram__bytes_read.sum"].replace(",", "")) * b[u["dram__bytes_read.sum"]]
+            wr = float(d["dram__bytes_write.sum"].replace(",", "")) * b[u["dram__bytes_write.sum"]]
+            print(f"# traffic per launch = {(rd + wr) / 1e9:.4g} Gbyte")
         except (KeyError, ValueError):
             pass
 
