@@ -73,6 +73,29 @@ __device__ __forceinline__ void edge_window(uint32_t h, uint32_t T, const uint32
     hi = salt_lb(khi, sX, s12, J);
 }
 
+// live bits of a sparse window (<= 32 simulations): bit k <=> simulation lo + k is live (Eq. 5)
+__device__ __forceinline__ uint32_t window_live_bits(const uint32_t* sX, uint32_t h, uint32_t T, int lo, int hi) {
+    uint32_t lb = 0u;
+    for (int i = lo; i < hi; ++i) lb |= ((sX[i] ^ h) < T) ? (1u << (i - lo)) : 0u;
+    return lb;
+}
+// narrow [lo, hi) to its first and last set bit of lb (lb re-based to the new lo); empty if lb == 0
+__device__ __forceinline__ void narrow_window(uint32_t& lb, int& lo, int& hi) {
+    if (!lb) {
+        hi = lo;
+        return;
+    }
+    const int l0 = lo;
+    lo = l0 + __ffs(lb) - 1;
+    hi = l0 + 32 - __clz(lb);
+    lb >>= lo - l0;
+}
+// the n bits of lb (re-based at lo) that cover simulations s0 .. s0 + n - 1
+__device__ __forceinline__ uint32_t bits_at(uint32_t lb, int lo, int s0, int n) {
+    const int sh = s0 - lo;
+    return (sh >= 0 ? (sh >= 32 ? 0u : lb >> sh) : (-sh >= 32 ? 0u : lb << -sh)) & ((1u << n) - 1u);
+}
+
 // byte mask from 4 bits: bit b -> byte b = 0xFF
 __device__ __forceinline__ uint32_t expand4(uint32_t b) { return ((b * 0x00204081u) & 0x01010101u) * 0xFFu; }
 

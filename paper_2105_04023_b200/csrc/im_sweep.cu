@@ -75,6 +75,26 @@ __device__ __forceinline__ ull live8(const SweepArgs& a, const uint32_t* sX, uin
     return live;
 }
 
+// live8 from the window's live bits (same byte mask as live8)
+template <bool BLOCKED>
+__device__ __forceinline__ ull live8_bits(const SweepArgs& a, uint32_t u, int w, uint32_t lb, int lo) {
+    ull live = expand8(bits_at(lb, lo, 8 * w, 8));
+    if (BLOCKED && live) {
+        uint32_t vb = (a.vis[(size_t)u * (a.J >> 5) + (w >> 2)] >> ((w & 3) << 3)) & 0xFFu;
+        live &= ~expand8(vb);
+    }
+    return live;
+}
+// v's previous-sweep change bits over [lo, hi), aligned like window_live_bits
+__device__ __forceinline__ uint32_t window_changed_bits(const uint32_t* __restrict__ cm, uint32_t v, int W, int lo, int hi) {
+    const uint32_t* row = cm + (size_t)v * W;
+    const int w0 = lo >> 5, w1 = (hi - 1) >> 5;
+    const uint32_t m0 = __ldg(&row[w0]), m1 = w1 != w0 ? __ldg(&row[w1]) : 0u;
+    const uint32_t x = (uint32_t)((((ull)m1 << 32) | m0) >> (lo & 31));
+    const int len = hi - lo;
+    return len >= 32 ? x : (x & ((1u << len) - 1u));
+}
+
 // bytewise max of `cand` into *p starting from an observed value `cur`; returns the bits of the
 // registers this thread raised (0 if none: someone else already holds values >= cand)
 __device__ __forceinline__ uint32_t vmax_cas8(ull* p, ull cur, ull cand) {
@@ -93,6 +113,17 @@ __device__ __forceinline__ uint32_t record8(const SweepArgs& a, uint32_t u, int 
     if (!raised) return 0u;
     atomicOr(&a.cm_out[(size_t)u * (a.J >> 5) + (w >> 2)], raised << ((w & 3) << 3));
     return 1u << (w >> 2);
+}
+
+template <bool BLOCKED>
+__device__ __forceinline__ uint32_t pull_word8_bits(const SweepArgs& a, uint32_t u, uint32_t v, int w, uint32_t lb, int lo) {
+    ull live = live8_bits<BLOCKED>(a, u, w, lb, lo);
+    if (!live) return 0u;
+    const size_t J8 = (size_t)(a.J >> 3);
+    ull cand = a.Mr64[v * J8 + w] & live;
+    if (!cand) return 0u;
+    ull* p = &a.M64[u * J8 + w];
+    return record8(a, u, w, vmax_cas8(p, __ldcg(p), cand));
 }
 
 template <bool BLOCKED>
@@ -207,15 +238,20 @@ __global__ void __launch_bounds__(BLOCK, SWEEP_MINB) k_sweep(SweepArgs a) {
             }
             bool sparse[NS];
             ull mv[NS], mu[NS];
+            uint32_t lb[NS];  // sparse windows: live (and, filtered, changed-at-v) simulations, bit k = lo + k
 #pragma unroll
             for (int s = 0; s < NS; s++) {
                 lo[s] = hi[s] = 0;
+                lb[s] = 0u;
                 if (T[s]) {
                     edge_window(h[s], T[s], sX, sS, J, lo[s], hi[s]);
-                    if (FILTER && lo[s] < hi[s] &&
-                        !(hi[s] - lo[s] <= DENSE_WIN ? live_changed(a.cm_in, vv[s], W, sX, h[s], T[s], lo[s], hi[s])
-                                                     : window_changed(a.cm_in, vv[s], W, lo[s], hi[s])))
+                    if (lo[s] < hi[s] && hi[s] - lo[s] <= DENSE_WIN) {
+                        lb[s] = window_live_bits(sX, h[s], T[s], lo[s], hi[s]);
+                        if (FILTER) lb[s] &= window_changed_bits(a.cm_in, vv[s], W, lo[s], hi[s]);
+                        narrow_window(lb[s], lo[s], hi[s]);  // to the live (changed-at-v) simulations; empty if none
+                    } else if (FILTER && lo[s] < hi[s] && !window_changed(a.cm_in, vv[s], W, lo[s], hi[s])) {
                         hi[s] = lo[s];
+                    }
                 }
                 sparse[s] = lo[s] < hi[s] && hi[s] - lo[s] <= DENSE_WIN;
                 if (sparse[s]) {  // first word of the window: both loads in flight before any use
@@ -231,7 +267,7 @@ __global__ void __launch_bounds__(BLOCK, SWEEP_MINB) k_sweep(SweepArgs a) {
                 need[s] = false;
                 if (sparse[s]) {
                     int w = lo[s] >> 3;
-                    cand[s] = mv[s] & live8<BLOCKED>(a, sX, u[s], w, h[s], T[s], lo[s], hi[s]);
+                    cand[s] = mv[s] & live8_bits<BLOCKED>(a, u[s], w, lb[s], lo[s]);
                     nw[s] = vmax8(mu[s], cand[s]);
                     need[s] = nw[s] != mu[s];
                 }
@@ -251,7 +287,7 @@ __global__ void __launch_bounds__(BLOCK, SWEEP_MINB) k_sweep(SweepArgs a) {
                 }
                 if (sparse[s])  // remaining words of a multi-word window
                     for (int w = (lo[s] >> 3) + 1; w <= (hi[s] - 1) >> 3; ++w)
-                        chg[s] |= pull_word8<BLOCKED>(a, sX, u[s], vv[s], w, h[s], T[s], lo[s], hi[s]);
+                        chg[s] |= pull_word8_bits<BLOCKED>(a, u[s], vv[s], w, lb[s], lo[s]);
             }
             // wide windows (w close to 1, weighted cascade): the whole warp walks the window
 #pragma unroll
