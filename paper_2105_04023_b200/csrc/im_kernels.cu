@@ -554,47 +554,61 @@ __global__ void k_bfs_compact(int32_t n, int J, int slice_min, uint32_t* __restr
           anyb |= bb[k] != 0u;
       }
       if (!__syncthreads_or(anyb)) continue;
-#pragma unroll 1
-      for (int k = 0; k < CU; k++) {
-        const int64_t base = base0 + (int64_t)k * blockDim.x;
-        int64_t v = base + threadIdx.x;
-        uint32_t b = bb[k];
-        if (!__syncthreads_or(b != 0u)) continue;  // block-uniform: nothing new in these 256 vertices
-        int rb = 0, rd = 0, ns = 0;
-        bool isbig = false;
-        if (b) {
-            nbits[v] = 0u;
-            for (uint32_t t = b; t; t &= t - 1) {
-                const size_t i = (size_t)v * W + (__ffs(t) - 1);
-                if (VDM) {
-                    const uint2 p = vd[i];
-                    dout[i] = p.y;
-                    vis[i] = p.x;
-                    vd[i] = make_uint2(p.x, 0u);
-                    newbits += __popc(p.y);
-                } else {
-                    newbits += __popc(dout[i]);
-                }
-            }
-            rb = off[v];
-            rd = off[v + 1] - rb;
-            isbig = rd > slice_min;
-            ns = isbig ? 0 : (rd + SEG - 1) / SEG;
-        }
-        uint32_t fmask = __ballot_sync(IM_FULL, b != 0u);
-        uint32_t bmask = __ballot_sync(IM_FULL, isbig);
-        int ninc = warp_incl_scan(ns, lane);
-        long long esum = isbig ? 0 : rd;
+      // every group of this iteration at once: new bits moved / counted and row bounds loaded for
+      // all of the thread's vertices, then one block-wide reservation (frontier list, items, big rows)
+      int rbk[CU], rdk[CU];
+      int t_items = 0, t_changed = 0, t_big = 0;
+      long long t_edges = 0;
 #pragma unroll
-        for (int o = 16; o; o >>= 1) esum += __shfl_xor_sync(IM_FULL, esum, o);
-        BlockTotals wt{ninc, __popc(fmask), __popc(bmask), (unsigned long long)esum};
-        int pos, cpos, bpos;
-        block_reserve<BLOCK / 32>(wt, lane, threadIdx.x >> 5, &ctr->next_items, &ctr->changed, &ctr->next_edges, &ctr->big,
-                                  pos, cpos, bpos);
-        if (b) vl[cpos + __popc(fmask & ((1u << lane) - 1u))] = (int32_t)v;
-        int p = pos + ninc - ns;
-        for (int s0 = rb; s0 < rb + rd && ns; s0 += SEG) items[p++] = make_int4((int)v, s0, min(s0 + SEG, rb + rd), 0);
-        if (isbig) big[bpos + __popc(bmask & ((1u << lane) - 1u))] = (int32_t)v;
+      for (int k = 0; k < CU; k++) {
+          rbk[k] = rdk[k] = 0;
+          const uint32_t b = bb[k];
+          if (!b) continue;
+          const int64_t v = base0 + (int64_t)k * blockDim.x + threadIdx.x;
+          nbits[v] = 0u;
+          for (uint32_t t = b; t; t &= t - 1) {
+              const size_t i = (size_t)v * W + (__ffs(t) - 1);
+              if (VDM) {
+                  const uint2 pr = vd[i];
+                  dout[i] = pr.y;
+                  vis[i] = pr.x;
+                  vd[i] = make_uint2(pr.x, 0u);
+                  newbits += __popc(pr.y);
+              } else {
+                  newbits += __popc(dout[i]);
+              }
+          }
+          rbk[k] = off[v];
+          rdk[k] = off[v + 1] - rbk[k];
+      }
+#pragma unroll
+      for (int k = 0; k < CU; k++)
+          if (bb[k]) {
+              t_changed++;
+              if (rdk[k] > slice_min) t_big++;
+              else {
+                  t_items += (rdk[k] + SEG - 1) / SEG;
+                  t_edges += rdk[k];
+              }
+          }
+      const int ci = warp_incl_scan(t_items, lane), cc = warp_incl_scan(t_changed, lane), cb = warp_incl_scan(t_big, lane);
+      long long esum = t_edges;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) esum += __shfl_xor_sync(IM_FULL, esum, o);
+      BlockTotals wt{ci, cc, cb, (unsigned long long)esum};
+      int pos, cpos, bpos;
+      block_reserve<BLOCK / 32>(wt, lane, threadIdx.x >> 5, &ctr->next_items, &ctr->changed, &ctr->next_edges, &ctr->big,
+                                pos, cpos, bpos);
+      int p = pos + ci - t_items, cp = cpos + cc - t_changed, bp = bpos + cb - t_big;
+#pragma unroll
+      for (int k = 0; k < CU; k++) {
+          if (!bb[k]) continue;
+          const int v = (int)(base0 + (int64_t)k * blockDim.x + threadIdx.x);
+          vl[cp++] = v;
+          const int rb = rbk[k], rd = rdk[k];
+          if (rd > slice_min) big[bp++] = v;
+          else
+              for (int s0 = rb; s0 < rb + rd; s0 += SEG) items[p++] = make_int4(v, s0, min(s0 + SEG, rb + rd), 0);
       }
     }
     newbits = __reduce_add_sync(IM_FULL, (uint32_t)newbits);

@@ -347,33 +347,49 @@ __global__ void k_compact(int32_t n, int J, int slice_min, const uint32_t* __res
           }
       }
       if (!__syncthreads_or(anyn)) continue;
-#pragma unroll 1
-      for (int k = 0; k < CU; k++) {
-        const int64_t base = base0 + (int64_t)k * blockDim.x;
-        int64_t v = base + threadIdx.x;
-        uint32_t b = bn[k];
-        if (!__syncthreads_or(b != 0u)) continue;  // block-uniform: no changed vertex among these 256
-        int rb = 0, rd = 0, ns = 0;
-        bool isbig = false;
-        if (b) {
-            rb = roff[v];
-            rd = roff[v + 1] - rb;
-            isbig = rd > slice_min;
-            ns = isbig ? 0 : (rd > 0 ? (rd + SEG - 1) / SEG : 0);
-        }
-        uint32_t fmask = __ballot_sync(IM_FULL, b != 0u);
-        uint32_t bmask = __ballot_sync(IM_FULL, isbig);
-        int ninc = warp_incl_scan(ns, lane);
-        long long esum = isbig ? 0 : rd;
+      // every group of this iteration at once: the row bounds of all changed vertices are loaded
+      // together, then one block-wide reservation for the thread's items / big rows
+      int rbk[CU], rdk[CU];
 #pragma unroll
-        for (int o = 16; o; o >>= 1) esum += __shfl_xor_sync(IM_FULL, esum, o);
-        BlockTotals wt{ninc, __popc(fmask), __popc(bmask), (unsigned long long)esum};
-        int pos, cpos, bpos;
-        block_reserve<BLOCK / 32>(wt, lane, threadIdx.x >> 5, &ctr->next_items, &ctr->changed, &ctr->next_edges, &ctr->big,
-                                  pos, cpos, bpos);
-        int p = pos + ninc - ns;
-        for (int s0 = rb; s0 < rb + rd && ns; s0 += SEG) items[p++] = make_int4((int)v, s0, min(s0 + SEG, rb + rd), 0);
-        if (isbig) big[bpos + __popc(bmask & ((1u << lane) - 1u))] = (int32_t)v;
+      for (int k = 0; k < CU; k++) {
+          rbk[k] = rdk[k] = 0;
+          if (bn[k]) {
+              const int64_t v = base0 + (int64_t)k * blockDim.x + threadIdx.x;
+              rbk[k] = roff[v];
+              rdk[k] = roff[v + 1] - rbk[k];
+          }
+      }
+      int t_items = 0, t_changed = 0, t_big = 0;
+      long long t_edges = 0;
+#pragma unroll
+      for (int k = 0; k < CU; k++)
+          if (bn[k]) {
+              t_changed++;
+              if (rdk[k] > slice_min) t_big++;
+              else {
+                  t_items += (rdk[k] + SEG - 1) / SEG;
+                  t_edges += rdk[k];
+              }
+          }
+      const int ci = warp_incl_scan(t_items, lane), cc = warp_incl_scan(t_changed, lane), cb = warp_incl_scan(t_big, lane);
+      long long esum = t_edges;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) esum += __shfl_xor_sync(IM_FULL, esum, o);
+      BlockTotals wt{ci, cc, cb, (unsigned long long)esum};
+      int pos, cpos, bpos;
+      block_reserve<BLOCK / 32>(wt, lane, threadIdx.x >> 5, &ctr->next_items, &ctr->changed, &ctr->next_edges, &ctr->big,
+                                pos, cpos, bpos);
+      int p = pos + ci - t_items, bp = bpos + cb - t_big;
+#pragma unroll
+      for (int k = 0; k < CU; k++) {
+          if (!bn[k]) continue;
+          const int v = (int)(base0 + (int64_t)k * blockDim.x + threadIdx.x);
+          const int rb = rbk[k], rd = rdk[k];
+          if (rd > slice_min) {
+              big[bp++] = v;
+          } else {
+              for (int s0 = rb; s0 < rb + rd; s0 += SEG) items[p++] = make_int4(v, s0, min(s0 + SEG, rb + rd), 0);
+          }
       }
     }
 }
