@@ -385,10 +385,13 @@ __global__ void k_init_registers(int32_t n, int32_t J, uint32_t seedV, uint32_t 
                                            murmur_word((uint32_t)perm[j0 + 2], seedJ), murmur_word((uint32_t)perm[j0 + 3], seedJ));
         }
     __syncthreads();
-    const int64_t total = (int64_t)n * cpr, stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += stride) {
-        const uint32_t v = (uint32_t)(idx / cpr);
-        const int c = (int)(idx - (int64_t)v * cpr);
+    // a warp per row (no 64-bit division per chunk), lanes over the row's 16-byte chunks
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; row < n; row += nwarps)
+      for (int c = lane; c < cpr; c += 32) {
+        const uint32_t v = (uint32_t)row;
+        const int64_t idx = row * cpr + c;
         const uint32_t hv = murmur_word(v, seedV);
         uint32_t w[4];
 #pragma unroll
@@ -398,7 +401,7 @@ __global__ void k_init_registers(int32_t n, int32_t J, uint32_t seedV, uint32_t 
                    ((uint32_t)__clz(hv ^ h.w) << 24);
         }
         M16[idx] = make_uint4(w[0], w[1], w[2], w[3]);
-    }
+      }
 }
 
 // ------------------------------------------------------------------ launchers
