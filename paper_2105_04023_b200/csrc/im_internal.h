@@ -17,7 +17,10 @@ constexpr int TAB_MIN = SEG;  // rows longer than this get a bucket offset table
 constexpr int MAX_SLICES = 8; // hash slices per long row (more non-zero mask words: the whole row)
 constexpr int DENSE_WIN = 32;   // windows wider than this many simulations take the warp-cooperative path
 constexpr int BLOCK = 256;      // threads per block of the persistent work-list kernels
-constexpr int FIRST_BIG = 2048; // first sweep: rows with more out-edges are gathered by a whole block
+#ifndef IM_FIRST_BIG
+#define IM_FIRST_BIG 2048
+#endif
+constexpr int FIRST_BIG = IM_FIRST_BIG; // first sweep: rows with more out-edges are gathered by a whole block
 constexpr uint32_t SHARD_POOL_ONE = 1u << 24;  // sharded argmax: gain + (in local pool) << 24, summed over ranks
 
 // device-side counters of one sweep / BFS level (one 32-byte D2H per iteration)
