@@ -143,7 +143,8 @@ def run_reference(args, rank):
 def config_dict(cfg, n, m, args):
     return {"workload": f"{cfg.name}: {cfg.note}", "n": int(n), "m": int(m), "J": cfg.J, "K": cfg.K, "t": cfg.t,
             "p": cfg.p if cfg.p is not None else "weighted-cascade 1/indeg", "salt_seed": cfg.salt_seed,
-            "parallelism": (f"simulation-sharded x{args.gpus} (NCCL allreduce hook)" if args.mode == "shard" else f"replicas x{args.gpus}")
+            "parallelism": (f"simulation-sharded x{args.gpus} ({os.environ.get('IM_BENCH_BACKEND', 'nccl').upper()} allreduce hook)"
+                            if args.mode == "shard" else f"replicas x{args.gpus}")
             if args.gpus > 1 else "single-gpu",
             "l2": "inputs (CSR+hash records) larger than L2" if m * 16 > 126e6 else "L2 flushed (256 MB write) between steps"}
 
