@@ -97,38 +97,28 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def oracle_sample(cfg, n, off, tgt, pr, target_s=12.0):
-    """cpu_baseline: the oracle's first Alg. 2 sweep over a vertex range sized to ~target_s seconds."""
-    import oracle
-
-    J = cfg.J
-    # calibrate on a small range, then size the timed sample
-    u0 = n // 3
-    e_small = 200_000 // max(1, J // 64)
-    u1 = int(np.searchsorted(off, off[u0] + e_small))
-    u1 = max(u0 + 1, min(u1, n))
-    pe, dt, _ = oracle.first_sweep_sample(n, off, tgt, pr, J, cfg.salt_seed, u0, u1)
-    rate = max(pe, 1) / max(dt, 1e-6)  # edges / s
-    want = int(rate * target_s)
-    u2 = int(np.searchsorted(off, off[u0] + want))
-    u2 = max(u0 + 1, min(u2, n))
-    pe, dt, _ = oracle.first_sweep_sample(n, off, tgt, pr, J, cfg.salt_seed, u0, u2)
-    return {"value": pe * J / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"first Alg. 2 sweep (synchronous, all u processed) over vertices [{u0},{u2}) = {pe} edges x J={J}, "
-                      f"{dt:.1f} s single-threaded, gcc {' '.join(oracle.CFLAGS)}",
-            "seconds": dt}
+def cpu_baseline_subprocess(config, seconds=12.0):
+    """The oracle leg in its own process (tools/cpu_baseline.py): this process never maps liboracle.so."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "cpu_baseline.py"), "--config", config,
+                        "--seconds", str(seconds)], capture_output=True, text=True)
+    if r.returncode != 0:
+        return {"value": None, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": f"failed: {r.stderr[-300:]}"}
+    return json.loads(r.stdout.strip().splitlines()[-1])
 
 
 def run_reference(args, rank):
     if rank != 0:
         return
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import cpu_baseline  # the oracle leg (reference arm: the oracle IS the reference here)
+
     cfg = gen.CONFIGS[args.config]
     n, off, tgt, pr = gen.workload(cfg)
     vals = []
     for _ in range(args.warmup):
         pass  # the oracle has no warm-up effects beyond page faults handled inside its setup
     for _ in range(args.steps):
-        vals.append(oracle_sample(cfg, n, off, tgt, pr, target_s=args.ref_seconds))
+        vals.append(cpu_baseline.oracle_sample(cfg, n, off, tgt, pr, target_s=args.ref_seconds))
     v = statistics.median([x["value"] for x in vals])
     cb = dict(vals[-1])
     cb["value"] = v
@@ -138,6 +128,62 @@ def run_reference(args, rank):
             "config": config_dict(cfg, n, len(tgt), args), "cpu_baseline": cb,
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def latest_capture(config):
+    """The newest committed ncu capture of the sweep kernels for this config (profiles/*_traffic_<cfg>.json,
+    written by tools/ncu_summary.py traffic), by its recorded round tag, not by file name."""
+    pdir = os.path.join(ROOT, "profiles")
+    best = None
+    if os.path.isdir(pdir):
+        for f in os.listdir(pdir):
+            if f.endswith(f"_traffic_{config}.json"):
+                tj = json.load(open(os.path.join(pdir, f)))
+                key = (tj.get("round", f[:4]), f)
+                if best is None or key > best[0]:
+                    best = (key, f, tj)
+    return (best[1], best[2]) if best else (None, None)
+
+
+def roofline(cfg, n, m, pr, J, edges, full_sweeps, blocked_full, builder_bytes, sweep_ms, step_ms, peak, peak_kind, config):
+    """SURVEY.md 8(d) algorithmic bytes of the sweep kernels (Alg. 2) per step, over their CUDA-event time:
+      per enumerated edge  : 4 B target + 4 B hash (+ 4 B threshold when w varies)
+                             + the live sectors of the target row, J * (1 - (1 - p)^32) B
+                               (a 32-register sector is needed iff one of its 32 simulations is live;
+                                WC: the mean of that over the edges);
+      per vertex of a full-vertex sweep (first sweep of every build, gather sweeps):
+                               8 B offsets + J B own-row read + J B row write (+ J/8 B blocked bits in rebuilds).
+    edges = enumerated edges of all sweeps of the step (im_stats total_edges)."""
+    rec = 8.0 + (0.0 if cfg.p is not None else 4.0)
+    pe = float(cfg.p) if cfg.p is not None else None
+    live = J * (1.0 - (1.0 - pe) ** 32) if pe is not None else float(J * np.mean(1.0 - (1.0 - pr.astype(np.float64)) ** 32))
+    per_vertex = 8.0 + 2.0 * J
+    alg = edges * (rec + live) + full_sweeps * n * per_vertex + blocked_full * n * J / 8.0
+    s = sweep_ms / 1e3
+    achieved = alg / s / 1e9 if s > 0 else None
+    src, cap = latest_capture(config)
+    traffic = cap["sweep"]["dram_bytes_per_step"] if cap else None
+    roof = {"bound": "hbm", "kernel": "Simulate sweep kernels (k_init_registers, k_first*, k_sweep; all builds of the step)",
+            "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak if achieved else None,
+            "peak_kind": peak_kind + " (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)",
+            "traffic": traffic, "traffic_unit": "bytes per step (ncu dram__bytes_read.sum + dram__bytes_write.sum, same kernels)",
+            "traffic_source": ("profiles/" + src) if src else None,
+            "alg_bytes_per_step": alg, "sweep_kernel_ms_per_step": sweep_ms, "sweep_share_of_step": sweep_ms / step_ms,
+            "alg_def": {"formula": "edges*(rec + J*(1-(1-p)^32)) + full_sweeps*n*(8+2J) + blocked_full*n*J/8 (SURVEY.md 8(d))",
+                        "edges": edges, "rec_bytes": rec, "live_sector_bytes_per_edge": live, "full_sweeps": full_sweeps,
+                        "blocked_full_sweeps": blocked_full, "n": n, "J": J},
+            "builder_model": {"bytes": builder_bytes, "frac": builder_bytes / s / 1e9 / peak if s > 0 else None,
+                              "def": "DESIGN.md section 6: 8 B record (+4 B WC) per enumerated edge + one 32 B sector per worked "
+                                     "window + rows of full sweeps"}}
+    if cap:
+        ms_cap = cap["sweep"].get("ms_per_step")
+        roof["ncu"] = {"commit": cap.get("commit"), "dram_bytes_per_step": traffic,
+                       "dram_gbs": traffic / (ms_cap / 1e3) / 1e9 if ms_cap else None,
+                       "dram_frac": traffic / (ms_cap / 1e3) / 1e9 / peak if ms_cap else None,
+                       "l2_hit_rate_pct": cap["sweep"].get("l2_hit_rate_pct"),
+                       "sectors_per_request": cap["sweep"].get("sectors_per_request"),
+                       "traffic_over_alg": traffic / alg if alg else None}
+    return roof
 
 
 def config_dict(cfg, n, m, args):
@@ -249,6 +295,7 @@ def main():
     for _ in range(args.warmup):
         step_device()
     times, edges, wedges, sweep_ms, sweeps, launches_sweep, rebuilds, launches, algb = [], [], [], [], [], [], [], [], []
+    full_sweeps, blocked_full = [], []
     first_build = {}
     clocks = Clocks(int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[0]) if os.environ.get("CUDA_VISIBLE_DEVICES", "").strip().isdigit() else local)
     for i in range(args.steps):
@@ -270,6 +317,9 @@ def main():
         sweeps.append(sb["total_sweeps"] + ss["total_sweeps"])
         launches_sweep.append(sb["sweep_launches"] + ss["sweep_launches"])
         rebuilds.append(ss["rebuilds"])
+        # full-vertex sweeps (every row read and written): the first sweep of every build + gather sweeps
+        full_sweeps.append(1 + ss["rebuilds"] + sb["gather_sweeps"] + ss["gather_sweeps"])
+        blocked_full.append(ss["rebuilds"])
         first_build = {"ms": sb["last_build_ms"], "sweeps": sb["last_build_sweeps"], "edges": sb["last_build_edges"],
                        "sweep_kernel_ms": sb["sweep_kernel_ms"], "prep_ms": sb["prep_ms"]}
     clk = clocks.stop()
@@ -304,24 +354,9 @@ def main():
         total_work = world * work
     value = total_work / (ms / 1e3) / 1e9
     hbm_peak, peak_kind, _ = load_peaks()
-    alg_bytes = statistics.mean(algb)
-    sweep_s = statistics.mean(sweep_ms) / 1e3
-    achieved = alg_bytes / sweep_s / 1e9 if sweep_s > 0 else None
-    traffic, traffic_src = None, None
-    tfiles = sorted(f for f in os.listdir(os.path.join(ROOT, "profiles")) if f.endswith(f"_traffic_{args.config}.json")) \
-        if os.path.isdir(os.path.join(ROOT, "profiles")) else []
-    if tfiles:  # DRAM bytes of the same kernels per step, from the committed ncu capture (tools/ncu_summary.py traffic)
-        tj = json.load(open(os.path.join(ROOT, "profiles", tfiles[-1])))
-        traffic, traffic_src = tj["sweep"]["dram_bytes_per_step"], "profiles/" + tfiles[-1]
-    roof = {"bound": "hbm", "kernel": "k_sweep (Simulate sweeps, all builds of the step)",
-            "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak if achieved else None,
-            "peak_kind": peak_kind, "traffic": traffic, "traffic_unit": "bytes per step (ncu dram__bytes_read.sum + dram__bytes_write.sum)",
-            "traffic_source": traffic_src,
-            "alg_bytes_per_step": alg_bytes, "sweep_kernel_ms_per_step": statistics.mean(sweep_ms),
-            "sweep_share_of_step": statistics.mean(sweep_ms) / ms,
-            "unit_def": "DESIGN.md section 6: per enumerated edge 8 B record (+4 B threshold when w varies) + one 32 B register "
-                        "sector per worked candidate window; + n*J row write (first sweep), + 2*n*J row read/write (gather sweeps), "
-                        "+ change masks"}
+    roof = roofline(cfg, n, m, pr, j1 - j0, statistics.mean(edges), statistics.mean(full_sweeps),
+                    statistics.mean(blocked_full), statistics.mean(algb), statistics.mean(sweep_ms), ms, hbm_peak, peak_kind,
+                    args.config)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "strong" if shard else "weak", "vs_baseline": None, "dtype": "u8/u32",
             "data": "synthetic", "config": config_dict(cfg, n, m, args), "clocks": clk,
@@ -341,7 +376,7 @@ def main():
                        "h2d_bytes_per_step": int((n + 1) * 4 + m * 8), "d2h_bytes_per_step": int(n * 8 + cfg.K * 12),
                        "ms_per_step": e2e_ms}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = oracle_sample(cfg, n, off, tgt, pr)
+        line["cpu_baseline"] = cpu_baseline_subprocess(args.config)
         line["cpu_baseline"].pop("seconds", None)
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -18,7 +18,7 @@
  *  - One global context, not thread-safe.  The library owns all device state
  *    from im_load_csr* until im_free() or the next im_load_csr*.
  *  - Host pointers are caller-owned and only read/written during the call.
- *  - All work runs on one CUDA stream (im_set_stream, default: a library stream)
+ *  - All work runs on one CUDA stream (im_set_stream; before it: a library stream)
  *    on the current CUDA device, which must be sm_100 (B200); otherwise IM_ECUDA.
  *    There is no CPU fallback.
  */
@@ -210,7 +210,9 @@ int im_get_reach(uint32_t *out);
 /* step log of the last selection: HOST im_step[cap]; returns the number of steps written (>= 0) */
 int im_get_step_log(im_step *out, int32_t cap);
 int im_get_stats(im_stats *out);
-/* run all device work on this cudaStream_t (NULL: the library's own stream) */
+/* run all device work on this cudaStream_t from now on.  NULL = CUDA's stream 0 (the legacy default
+ * stream; torch's default stream has handle 0), so the library's work is ordered after the caller's
+ * kernels on it.  Before the first call the library uses a stream of its own. */
 int im_set_stream(void *cuda_stream);
 /* number of kernel launches issued by the library since load (diagnostic) */
 int64_t im_kernel_launch_count(void);

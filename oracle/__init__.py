@@ -18,8 +18,14 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
-_LIB = os.path.join(_HERE, "liboracle.so")
-CFLAGS = ["-O2", "-fPIC", "-shared"]
+# ORACLE_GOLDEN=1 (offline golden writer only, tests/golden/make_oracle_digests.py): the same
+# source built with OpenMP over the independent u-loop of a synchronous sweep and -O3; IEEE double
+# without contraction or fast-math, so every result is identical to the default build's.  Tests,
+# smoke() and the bench's cpu_baseline always use the default single-threaded -O2 build.
+_GOLDEN = os.environ.get("ORACLE_GOLDEN") == "1"
+_LIB = os.path.join(_HERE, "liboracle_golden.so" if _GOLDEN else "liboracle.so")
+CFLAGS = (["-O3", "-march=native", "-ffp-contract=off", "-fopenmp", "-fPIC", "-shared"] if _GOLDEN
+          else ["-O2", "-fPIC", "-shared"])
 PHI = 0.77351  # PAPER.md:170 (R8)
 _lib = None
 
@@ -65,7 +71,7 @@ def _load():
             "or_estimate_row": (f64, [vp, i32]),
             "or_estimate": (None, [i32, i32, vp, vp]),
             "or_simulate": (ctypes.c_int, [i32, vp, vp, vp, i32, vp, vp, vp, vp, vp, i32, f64]),
-            "or_select_seeds": (ctypes.c_int, [i32, vp, vp, vp, i32, u64, i32, f64, f64, f64, vp, vp, vp, vp, vp, vp]),
+            "or_select_seeds": (ctypes.c_int, [i32, vp, vp, vp, i32, u64, i32, f64, f64, f64, vp, vp, vp, vp, vp, vp, vp]),
             "or_reach_register": (ctypes.c_int, [i32, vp, vp, vp, i32, u64, i64, vp, vp, vp]),
             "or_seed_sigma": (ctypes.c_int, [i32, vp, vp, vp, i32, u64, i32, vp, vp]),
             "or_mix64": (u64, [u64]),
@@ -159,8 +165,9 @@ def simulate(n, offsets, targets, probs, J, seed, blocked=None, M=None, eps_c=0.
                "processed_vertices": st.processed_vertices, "changed": log[: min(st.sweeps, cap)].tolist()}
 
 
-def select_seeds(n, offsets, targets, probs, J, seed, K, eps_l, eps_g=None, want_vis=False, want_final=False, eps_c=0.0):
-    """Alg. 1.  Returns dict(seeds, scores, steps[list of dict], stats, vis?, M_final?)."""
+def select_seeds(n, offsets, targets, probs, J, seed, K, eps_l, eps_g=None, want_vis=False, want_final=False, eps_c=0.0,
+                 want_first=False):
+    """Alg. 1.  Returns dict(seeds, scores, steps[list of dict], stats, vis?, M_final?, M_first?)."""
     if eps_g is None:
         eps_g = eps_l
     offsets, targets, probs = _csr(offsets, targets, probs)
@@ -169,9 +176,11 @@ def select_seeds(n, offsets, targets, probs, J, seed, K, eps_l, eps_g=None, want
     log = (Step * max(K, 1))()
     vis = np.zeros((n, J), dtype=np.uint8) if want_vis else None
     Mf = np.zeros((n, J), dtype=np.uint8) if want_final else None
+    M1 = np.zeros((n, J), dtype=np.uint8) if want_first else None
     st = SelectStats()
     rc = _load().or_select_seeds(n, _p(offsets), _p(targets), _p(probs), J, seed, K, float(eps_l), float(eps_g), float(eps_c),
-                                 _p(seeds), _p(scores), ctypes.cast(log, ctypes.c_void_p), _p(vis), _p(Mf), ctypes.byref(st))
+                                 _p(seeds), _p(scores), ctypes.cast(log, ctypes.c_void_p), _p(vis), _p(Mf), ctypes.byref(st),
+                                 _p(M1))
     if rc != 0:
         raise MemoryError(rc)
     steps = [{f: getattr(log[k], f) for f, _ in Step._fields_ if f != "pad"} for k in range(K)]
@@ -181,6 +190,8 @@ def select_seeds(n, offsets, targets, probs, J, seed, K, eps_l, eps_g=None, want
         out["vis"] = vis
     if want_final:
         out["M_final"] = Mf
+    if want_first:
+        out["M_first"] = M1
     return out
 
 

@@ -232,16 +232,21 @@ int or_simulate(int32_t n, const int32_t *offsets, const int32_t *targets, const
     while ((double)Lsize / (double)n > eps_c) { /* Alg. 2 line 3 */
         memcpy(Mold, M, (size_t)n * (size_t)J);
         memset(inLnext, 0, (size_t)n);
-        int64_t next = 0;
+        int64_t next = 0, pv = 0, pe = 0;
+        /* The iterations over u are independent within a synchronous sweep (u writes only its
+         * own row M_u and inLnext[u]; every read is of Mold / inL): the pragma is ignored by the
+         * default single-threaded build (CFLAGS in oracle/__init__.py) and only used by the
+         * offline golden writer's -fopenmp build, with identical results. */
+#pragma omp parallel for schedule(dynamic, 512) reduction(+ : next, pv, pe)
         for (int32_t u = 0; u < n; u++) {
             /* u in Gamma^-(L): some out-neighbour of u is in L (every u in the first sweep) */
             int in_gamma = first;
             for (int64_t e = offsets[u]; e < offsets[u + 1] && !in_gamma; e++) in_gamma = inL[targets[e]];
             if (!in_gamma) continue;
-            st.processed_vertices++;
+            pv++;
             uint8_t *Mu = M + (int64_t)u * J;
             for (int64_t e = offsets[u]; e < offsets[u + 1]; e++) {
-                st.processed_edges++;
+                pe++;
                 const uint8_t *Mv = Mold + (int64_t)targets[e] * J;
                 for (int32_t j = 0; j < J; j++) {
                     if (or_live(X[j], h[e], probs[e]) && !(blocked && blocked[(int64_t)u * J + j])) {
@@ -254,6 +259,8 @@ int or_simulate(int32_t n, const int32_t *offsets, const int32_t *targets, const
                 next++;
             }
         }
+        st.processed_vertices += pv;
+        st.processed_edges += pe;
         if (change_log && st.sweeps < change_cap) change_log[st.sweeps] = (int32_t)next;
         st.sweeps++;
         memcpy(inL, inLnext, (size_t)n);
@@ -324,11 +331,12 @@ typedef struct {
  * readings R12-R21.  Starts from freshly built sketches (Simulate with R_S = {}).
  * out_seeds[k], out_scores[k] = sigma after k+1 seeds (R21).  vis_out (optional,
  * n*J bytes) receives the final R_G(S).  M_final (optional) receives the registers
- * at return (after the last executed rebuild, or the first build if none ran).
+ * at return (after the last executed rebuild, or the first build if none ran); M_first
+ * (optional) the registers of the first build (lines 2-6).
  */
 int or_select_seeds(int32_t n, const int32_t *offsets, const int32_t *targets, const float *probs, int32_t J,
                     uint64_t seed, int32_t K, double eps_l, double eps_g, double eps_c, int32_t *out_seeds, double *out_scores,
-                    or_step *log, uint8_t *vis_out, uint8_t *M_final, or_select_stats *sstats) {
+                    or_step *log, uint8_t *vis_out, uint8_t *M_final, or_select_stats *sstats, uint8_t *M_first) {
     int64_t m = offsets[n];
     uint32_t seed_v, seed_j;
     uint32_t *X = (uint32_t *)malloc((size_t)J * sizeof(uint32_t));
@@ -351,6 +359,7 @@ int or_select_seeds(int32_t n, const int32_t *offsets, const int32_t *targets, c
     ss.builds++;
     ss.total_sweeps += st.sweeps;
     ss.total_processed_edges += st.processed_edges;
+    if (M_first) memcpy(M_first, M, (size_t)n * (size_t)J);
     /* lines 7-8: M_S' <- zeros(J); varsigma <- 0 */
     double varsigma = 0.0;
     int64_t sigma_count = 0;

@@ -161,7 +161,17 @@ class Library:
         self._check(self.L.im_evaluate(len(s), ps if len(s) else None, seed & 0xFFFFFFFFFFFFFFFF, int(r0), int(R), out.ctypes.data))
         return out[: len(s)].copy()
 
-    def im_estimate(self, n: int) -> np.ndarray:
+    def _shape(self, n=None, J=None):
+        """(n, J) of the held context; caller-passed values must agree (the library writes n*J)."""
+        st = self.im_get_stats()
+        if st["n"] == 0:  # nothing loaded: the library reports IM_ESTATE without writing
+            return n or 0, J or 0
+        if (n is not None and n != st["n"]) or (J is not None and st["J"] and J != st["J"]):
+            raise IMError(IM_EINVAL, f"n / J ({n}, {J}) do not match the loaded context ({st['n']}, {st['J']})")
+        return st["n"], st["J"]
+
+    def im_estimate(self, n: int | None = None) -> np.ndarray:
+        n, _ = self._shape(n)
         out = np.empty(n, dtype=np.float64)
         self._check(self.L.im_estimate(out.ctypes.data))
         return out
@@ -183,19 +193,22 @@ class Library:
         """Allocation-free variant writing into caller arrays (e.g. pinned host buffers)."""
         self._check(self.L.im_select_seeds(K, float(err_threshold), seeds.ctypes.data, scores.ctypes.data))
 
-    def im_get_registers(self, n: int, J: int) -> np.ndarray:
+    def im_get_registers(self, n: int | None = None, J: int | None = None) -> np.ndarray:
         """J = the simulations this context holds (j1 - j0 when sharded)."""
+        n, J = self._shape(n, J)
         out = np.empty((n, J), dtype=np.uint8)
         self._check(self.L.im_get_registers(out.ctypes.data))
         return out
 
-    def im_get_register_rows(self, rows, J: int) -> np.ndarray:
+    def im_get_register_rows(self, rows, J: int | None = None) -> np.ndarray:
+        _, J = self._shape(None, J)
         r, pr = _host(rows, np.int32)
         out = np.empty((len(r), J), dtype=np.uint8)
         self._check(self.L.im_get_register_rows(len(r), pr, out.ctypes.data))
         return out
 
-    def im_get_reach(self, n: int, J: int) -> np.ndarray:
+    def im_get_reach(self, n: int | None = None, J: int | None = None) -> np.ndarray:
+        n, J = self._shape(n, J)
         out = np.empty((n, J // 32), dtype=np.uint32)
         self._check(self.L.im_get_reach(out.ctypes.data))
         return out
@@ -211,7 +224,8 @@ class Library:
         return {f: getattr(s, f) for f, _ in im_stats._fields_}
 
     def im_set_stream(self, stream) -> None:
-        """torch.cuda.Stream, raw cudaStream_t int, or None (library stream)."""
+        """torch.cuda.Stream or raw cudaStream_t int; None / handle 0 = CUDA's legacy default stream
+        (torch's default stream), as in include/im.h."""
         h = 0 if stream is None else (stream if isinstance(stream, int) else int(stream.cuda_stream))
         self._check(self.L.im_set_stream(h or None))
 

@@ -492,7 +492,9 @@ int64_t im_kernel_launch_count(void) { return g.launches; }
 
 int im_set_stream(void* s) {
     TRY(ensure_device());
-    g.stream = s ? (cudaStream_t)s : g.own_stream;
+    // NULL is CUDA's stream 0 (the legacy default stream, which torch's default stream wraps), so
+    // work is ordered after the caller's kernels on it; until the first call: the library's stream
+    g.stream = s ? (cudaStream_t)s : cudaStreamLegacy;
     return 0;
 }
 
@@ -503,7 +505,8 @@ void im_free(void) {
 
 int im_load_csr(int32_t n, const int32_t* offsets, const int32_t* targets, const float* probs) {
     TRY(ensure_device());
-    if (!offsets || (n >= 1 && !targets && offsets[n] > 0) || (!probs && n >= 1 && offsets[n] > 0))
+    if (n < 1) return fail(IM_EINVAL, "n must be >= 1 (got %d)", n);  // before offsets[n] is read
+    if (!offsets || (!targets && offsets[n] > 0) || (!probs && offsets[n] > 0))
         return fail(IM_EINVAL, "null pointer argument");
     TRY(check_csr_args(n, offsets[n]));
     if (offsets[0] != 0) return fail(IM_EINVAL, "offsets[0] must be 0");

@@ -21,6 +21,8 @@ def shard_range(J_total: int, rank: int, world: int) -> tuple[int, int]:
     never get fewer).  Raises if some rank would get no word or more than 1024 simulations."""
     if J_total % 32 or J_total < 32:
         raise ValueError(f"J_total must be a positive multiple of 32 (got {J_total})")
+    if world >= 256:  # the packed argmax value counts in-pool ranks in 8 bits (gain + count << 24)
+        raise ValueError(f"world size {world} >= 256 is not supported by the packed argmax exchange")
     if not 0 <= rank < world:
         raise ValueError(f"rank {rank} not in [0, {world})")
     words = J_total // 32

@@ -84,3 +84,36 @@ def test_binding_struct_layouts_match_header(tmp_path):
         cls = fields[cname]
         want = ctypes.sizeof(cls) if f == "size" else getattr(cls, f).offset
         assert int(v) == want, (cname, f, v, want)
+
+
+def test_c_program_consumes_the_header(tmp_path):
+    """A plain C program compiled against include/im.h and linked to libim_b200.so: the
+    declarations, error codes and call-order checks work from C without Python or a GPU."""
+    src = r'''
+#include <stdio.h>
+#include <string.h>
+#include "im.h"
+int main(void) {
+    im_stats st;
+    int32_t seeds[1]; double scores[1];
+    if (im_version() != 102) return 1;
+    im_free();
+    if (im_build_sketches(64, 1) != IM_ESTATE) return 2;
+    if (strlen(im_last_error()) == 0) return 3;
+    if (im_select_seeds(1, 0.05, seeds, scores) != IM_ESTATE) return 4;
+    if (im_get_stats(NULL) != IM_EINVAL) return 5;
+    if (im_get_stats(&st) != IM_OK || st.n != 0 || st.J != 0) return 6;
+    if (im_set_policy(-1.0, 0.0, 0.0) != IM_EINVAL) return 7;
+    if (im_get_step_log(NULL, -1) != IM_EINVAL) return 8;
+    printf("ok %s\n", im_last_error());
+    return 0;
+}
+'''
+    c = tmp_path / "consumer.c"
+    c.write_text(src)
+    exe = tmp_path / "consumer"
+    libdir = os.path.dirname(im.LIB_PATH)
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"), str(c), "-o", str(exe),
+                    f"-L{libdir}", "-l:libim_b200.so", f"-Wl,-rpath,{libdir}"], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0 and r.stdout.startswith("ok"), (r.returncode, r.stdout, r.stderr)

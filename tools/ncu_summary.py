@@ -67,7 +67,7 @@ BYTES = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 SWEEP_KERNELS = ("k_init_registers", "k_first", "k_first_big", "k_sweep")
 
 
-def traffic(path, config="c4"):
+def traffic(path, config="c4", round_tag=None, commit=None):
     """DRAM bytes per kernel from an `ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,
     gpu__time_duration.sum --csv` log of ONE hot-path step (tools/profile_step.py --what step); prints
     the JSON bench.py reads for roofline.traffic (the sweep kernels' bytes per step)."""
@@ -75,21 +75,50 @@ def traffic(path, config="c4"):
     rows = [r for r in csv.reader(open(path)) if len(r) > 5]
     hdr = rows[0]
     ik, iid, im_, iv, iu = (hdr.index(x) for x in ("Kernel Name", "ID", "Metric Name", "Metric Value", "Metric Unit"))
-    per = collections.defaultdict(lambda: {"launches": set(), "dram_bytes": 0.0, "ms": 0.0})
+    per = collections.defaultdict(lambda: {"launches": set(), "dram_bytes": 0.0, "ms": 0.0, "sect": 0.0, "req": 0.0,
+                                           "hit_w": 0.0, "hit_ms": 0.0})
+    lms = {}
+    hits = []
     for r in rows[1:]:
         name = r[ik].split("(")[0].replace("void ", "").split("<")[0].replace("im::", "")
-        v = float(r[iv].replace(",", ""))
+        try:
+            v = float(r[iv].replace(",", ""))
+        except ValueError:
+            continue
         d = per[name]
         d["launches"].add(r[iid])
         if r[im_].startswith("dram__bytes_"):
             d["dram_bytes"] += v * BYTES[r[iu]]
         elif r[im_] == "gpu__time_duration.sum":
             d["ms"] += v * UNIT[r[iu]]
-    out = {k: {"launches": len(d["launches"]), "dram_bytes": d["dram_bytes"], "ms": d["ms"]} for k, d in per.items()}
-    sw = [out[k] for k in SWEEP_KERNELS if k in out]
-    res = {"source": path, "config": config, "kernels": out,
-           "sweep": {"kernels": list(SWEEP_KERNELS), "dram_bytes_per_step": sum(x["dram_bytes"] for x in sw),
-                     "ms_per_step": sum(x["ms"] for x in sw), "launches": sum(x["launches"] for x in sw)}}
+            lms[r[iid]] = v * UNIT[r[iu]]
+        elif r[im_] == "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum":
+            d["sect"] += v
+        elif r[im_] == "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum":
+            d["req"] += v
+        elif r[im_] == "lts__t_sector_hit_rate.pct":
+            hits.append((name, r[iid], v))
+    for name, lid, v in hits:  # L2 hit rate weighted by launch duration
+        per[name]["hit_w"] += v * lms.get(lid, 0.0)
+        per[name]["hit_ms"] += lms.get(lid, 0.0)
+
+    def fin(d):
+        o = {"launches": len(d["launches"]), "dram_bytes": d["dram_bytes"], "ms": d["ms"]}
+        if d["req"]:
+            o["sectors_per_request"] = d["sect"] / d["req"]
+        if d["hit_ms"]:
+            o["l2_hit_rate_pct"] = d["hit_w"] / d["hit_ms"]
+        return o
+    out = {k: fin(d) for k, d in per.items()}
+    sw = [k for k in SWEEP_KERNELS if k in out]
+    sect = sum(per[k]["sect"] for k in sw)
+    req = sum(per[k]["req"] for k in sw)
+    hms = sum(per[k]["hit_ms"] for k in sw)
+    res = {"source": path, "config": config, "round": round_tag, "commit": commit, "kernels": out,
+           "sweep": {"kernels": list(SWEEP_KERNELS), "dram_bytes_per_step": sum(out[k]["dram_bytes"] for k in sw),
+                     "ms_per_step": sum(out[k]["ms"] for k in sw), "launches": sum(out[k]["launches"] for k in sw),
+                     "sectors_per_request": sect / req if req else None,
+                     "l2_hit_rate_pct": sum(per[k]["hit_w"] for k in sw) / hms if hms else None}}
     print(json.dumps(res, indent=1))
 
 
