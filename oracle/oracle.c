@@ -25,14 +25,18 @@
  *                     register within s hops (hop distances by scipy's shortest_path), and the
  *                     run stops at the first s with |changed_s| <= eps_c * n
  *   or_estimate    <- closed forms of Eq. 2 (all-0 -> 1.29281, all-10 -> 1323.84)
- *   or_select      <- star / two-star / K=1 reductions, t=0 / t=inf variants,
- *                     sigma vs brute-force BFS, invariants (monotone sigma, ...)
+ *   or_select      <- field by field (seed, score, e, sigma, delta, err_l, err_g, decisions, final
+ *                     R_G(S) and registers) vs tests/brute.select_seeds, a whole-array restatement of
+ *                     Alg. 1 on closure-based registers / reach sets, 32 graphs incl. (eps_l, eps_g) =
+ *                     (0.3, 0.01), eps_c = 0.02, alternating keeps / rebuilds, M_S'-decided picks;
+ *                     star / two-star / K=1 reductions, t=0 / t=inf variants
+ *   or_init_rows, or_first_sweep_sample (cpu_baseline helpers) <- sklearn-Murmur3 init rows and the
+ *                     1-hop closed form
  *   or_reach_register, or_khop_register, or_seed_sigma <- brute force on small graphs
  *   or_mix64       <- SplitMix64 published reference outputs (seed 0)
  *   or_mc_influence<- closed forms (w = 0, w = 1 -> BFS reach, star 1 + L w, chain sum w^i within
  *                     CLT bounds), draw uniformity / independence
- * The full greedy K-loop beyond these is "pinned by construction + invariants"
- * (the method is a heuristic with no closed form); see DESIGN.md "Parity".
+ * All functions are pinned; see DESIGN.md "Parity".
  */
 #include <math.h>
 #include <stdint.h>

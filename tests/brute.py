@@ -161,3 +161,65 @@ def random_graph(rng: np.random.Generator, n: int, m: int, p=None, allow_dups=Tr
     else:
         probs = np.full(len(targets), p, dtype=np.float32)
     return offsets, targets, probs
+
+
+def simulate_registers(n, offsets, targets, probs, J, seed, blocked=None, eps_c=0.0) -> np.ndarray:
+    """Registers after Alg. 2 with early exit eps_c (reading R22) in closed form: after s synchronous
+    sweeps M = khop_registers(s); the run stops after the first s with |changed_s| / n <= eps_c
+    (no sweep at all when eps_c >= 1).  eps_c = 0: the reach-max fixpoint (`registers`)."""
+    if eps_c == 0.0:
+        return registers(n, offsets, targets, probs, J, seed, blocked)
+    prev = init_registers(n, J, seed)
+    if not (1.0 > eps_c):
+        return prev
+    for s in range(1, n + 2):
+        cur = khop_registers(n, offsets, targets, probs, J, seed, s, blocked=blocked)
+        changed = int(np.any(cur != prev, axis=1).sum())
+        prev = cur
+        if not (changed / n > eps_c):
+            return cur
+    return prev
+
+
+def select_seeds(n, offsets, targets, probs, J, seed, K, eps_l, eps_g, eps_c=0.0):
+    """Alg. 1 restated with whole-array numpy operations and the closed forms above,
+    readings R12-R21: registers = reach-max (or k-hop, eps_c > 0) on the residual samples, R_G(S) by
+    transitive closure, pool = vertices not visited in every sample (empty -> lowest id not in S),
+    argmax of the integer merged score with the lowest id on ties, keep iff err_l < eps_l or
+    err_g < eps_g, else rebuild (not after the last pick, R18) with M_S' = 0 and varsigma = sigma.
+    Returns a list of per-step dicts with the fields of the oracle's step log, plus 'ms_mattered'
+    (the argmax would differ with M_S' = 0)."""
+    M = simulate_registers(n, offsets, targets, probs, J, seed, eps_c=eps_c).astype(np.int64)
+    MS = np.zeros(J, np.int64)
+    varsigma = 0.0
+    S = []
+    vis = np.zeros((n, J), dtype=bool)
+    steps = []
+    for k in range(K):
+        pool = ~vis.all(axis=1)
+        score = np.maximum(M, MS[None, :]).sum(axis=1)
+        if pool.any():
+            s = int(np.argmax(np.where(pool, score, -1)))
+            alt = int(np.argmax(np.where(pool, M.sum(axis=1), -1)))
+        else:
+            s = alt = min(v for v in range(n) if v not in S)
+        S.append(s)
+        e = 2.0 ** (float(score[s]) / J) / PHI
+        vis = reach_masks(n, offsets, targets, probs, J, seed, S)
+        sigma_count = int(vis.sum())
+        sigma = sigma_count / J
+        delta = sigma - varsigma
+        err_l = abs((e - delta) / delta) if delta != 0 else math.inf
+        err_g = abs((e - delta) / sigma)
+        rebuild = not (err_l < eps_l or err_g < eps_g)
+        executed = False
+        if not rebuild:
+            MS = np.maximum(MS, M[s])
+        elif k < K - 1:
+            M = simulate_registers(n, offsets, targets, probs, J, seed, blocked=vis, eps_c=eps_c).astype(np.int64)
+            MS = np.zeros(J, np.int64)
+            varsigma = sigma
+            executed = True
+        steps.append({"vertex": s, "score": int(score[s]), "e": e, "sigma_count": sigma_count, "sigma": sigma, "delta": delta,
+                      "err_l": err_l, "err_g": err_g, "rebuilt": int(rebuild), "executed": int(executed), "ms_mattered": s != alt})
+    return steps, vis, M.astype(np.uint8)

@@ -367,7 +367,8 @@ def test_select_reductions_and_variants():
 
 def test_select_sigma_and_masks_vs_bruteforce():
     """R_G(S) and sigma (Alg. 1 lines 13-14) equal brute-force reach of the chosen seeds; sigma is
-    non-decreasing and <= n; seeds are distinct; decisions follow the keep rule of line 18."""
+    non-decreasing and <= n; seeds are distinct (the keep/rebuild decisions are pinned field by field
+    against the brute-force Alg. 1 in test_select_matches_bruteforce_alg1)."""
     rng = np.random.default_rng(11)
     for g in range(10):
         n = int(rng.integers(10, 90))
@@ -382,9 +383,79 @@ def test_select_sigma_and_masks_vs_bruteforce():
         for k in range(K):
             assert r["steps"][k]["sigma_count"] == brute.reach_masks(n, off, tgt, pr, J, seed, seeds[: k + 1]).sum()
             assert r["scores"][k] == r["steps"][k]["sigma_count"] / J
-            s = r["steps"][k]
-            assert s["rebuilt"] == (not (s["err_l"] < t or s["err_g"] < t))
         assert all(np.diff(r["scores"]) >= 0) and r["scores"][-1] <= n
+
+
+def _alg1_cases():
+    """>= 30 tiny graphs: the paper's (eps_l, eps_g) = (0.3, 0.01) and single
+    thresholds t in {0.05, 0.3, inf}, eps_c in {0, 0.02}; p high enough that keeps and rebuilds mix."""
+    rng = np.random.default_rng(1313)
+    cases = []
+    pols = [(0.3, 0.01), (0.05, 0.05), (0.3, 0.3), (math.inf, math.inf)]
+    for g in range(32):
+        n = int(rng.integers(12, 60))
+        p = None if g % 4 == 3 else float(rng.choice([0.1, 0.2, 0.35]))
+        off, tgt, pr = brute.random_graph(rng, n, int(rng.integers(2 * n, 4 * n)), p)
+        eps_l, eps_g = pols[g % 4]
+        eps_c = 0.02 if g % 8 >= 6 else 0.0
+        cases.append((g, n, off, tgt, pr, 32, int(rng.integers(0, 2**32)), min(n, 7), eps_l, eps_g, eps_c))
+    return cases
+
+
+def test_select_matches_bruteforce_alg1():
+    """Alg. 1 field by field against tests/brute.select_seeds, a whole-array restatement
+    on closure-based registers and reach sets: seed, integer merged score, e, sigma count, delta,
+    err_l, err_g, rebuild decision and execution at every step, the final R_G(S) and the registers
+    after the last executed rebuild.  The cases must include keeps and rebuilds alternating within a
+    run, and steps where M_S' (the merge of line 19) changes the argmax."""
+    kinds, alternating, ms_mattered = set(), 0, 0
+    for g, n, off, tgt, pr, J, seed, K, eps_l, eps_g, eps_c in _alg1_cases():
+        r = oracle.select_seeds(n, off, tgt, pr, J, seed, K, eps_l, eps_g, want_vis=True, want_final=True, eps_c=eps_c)
+        want, vis, Mf = brute.select_seeds(n, off, tgt, pr, J, seed, K, eps_l, eps_g, eps_c=eps_c)
+        for k, (got, w) in enumerate(zip(r["steps"], want)):
+            for f in ("vertex", "score", "sigma_count", "rebuilt", "executed"):
+                assert got[f] == w[f], (g, k, f, got[f], w[f])
+            for f in ("e", "sigma", "delta", "err_g"):
+                assert got[f] == pytest.approx(w[f], rel=1e-12, abs=0), (g, k, f)
+            assert (math.isinf(got["err_l"]) and math.isinf(w["err_l"])) or got["err_l"] == pytest.approx(w["err_l"], rel=1e-12)
+            kinds.add(w["rebuilt"])
+            ms_mattered += w["ms_mattered"] and k > 0 and not want[k - 1]["rebuilt"]
+        dec = [w["rebuilt"] for w in want]
+        alternating += any(a != b for a, b in zip(dec, dec[1:]))
+        assert list(r["seeds"]) == [w["vertex"] for w in want]
+        assert np.array_equal(r["vis"].astype(bool), vis)
+        assert np.array_equal(r["M_final"], Mf), g
+    assert kinds == {0, 1} and alternating >= 5 and ms_mattered >= 3, (kinds, alternating, ms_mattered)
+
+
+def test_first_sweep_sample_vs_one_hop_closed_form():
+    """The cpu_baseline helper (or_init_rows + or_first_sweep_sample: the first Alg. 2 sweep over a vertex
+    range) equals the 1-hop closed form: max init register over u and its live
+    out-neighbours in each sample (brute.khop_registers, hops = 1)."""
+    rng = np.random.default_rng(1414)
+    for g in range(6):
+        n = int(rng.integers(20, 90))
+        off, tgt, pr = brute.random_graph(rng, n, 4 * n, None if g % 2 else 0.3)
+        J, seed = 64, int(rng.integers(0, 2**32))
+        want = brute.khop_registers(n, off, tgt, pr, J, seed, 1)
+        u0, u1 = int(rng.integers(0, n // 2)), int(rng.integers(n // 2, n + 1))
+        pe, _, rows = oracle.first_sweep_sample(n, off, tgt, pr, J, seed, u0, u1)
+        assert pe == off[u1] - off[u0]
+        assert np.array_equal(rows, want[u0:u1]), g
+
+
+def test_init_rows_vs_library_hash():
+    """or_init_rows (bounded-sample init, Alg. 1 lines 2-5) writes exactly the listed rows, each equal to
+    the sklearn-Murmur3 definition."""
+    n, J, seed = 300, 64, 5
+    rows = np.array([0, 7, 299, 150], np.int32)
+    M = np.zeros((n, J), np.uint8)
+    oracle._load().or_init_rows(J, seed, len(rows), rows.ctypes.data, M.ctypes.data)
+    want = brute.init_registers(n, J, seed)
+    assert np.array_equal(M[rows], want[rows])
+    mask = np.ones(n, bool)
+    mask[rows] = False
+    assert not M[mask].any()
 
 
 def test_rebuilt_registers_vs_bruteforce():
