@@ -78,6 +78,7 @@ def _load():
             "or_mc_draw": (u32, [u64, i64, i32, i32]),
             "or_mc_influence": (ctypes.c_int, [i32, vp, vp, vp, i32, vp, u64, i64, i64, vp]),
             "or_khop_register": (ctypes.c_int, [i32, vp, vp, vp, i32, u64, i32, i64, vp, vp, vp]),
+            "or_rebuilt_register": (ctypes.c_int, [i32, vp, vp, vp, i32, u64, i32, vp, i64, vp, vp, vp]),
             "or_first_sweep_sample": (i64, [i32, vp, vp, vp, i32, u64, i32, i32, vp, vp]),
             "or_seed_reach_per_sim": (ctypes.c_int, [i32, vp, vp, vp, i32, u64, i32, vp, i32, vp, vp]),
         }
@@ -204,6 +205,25 @@ def reach_register(n, offsets, targets, probs, J, seed, us, js) -> np.ndarray:
     rc = _load().or_reach_register(n, _p(offsets), _p(targets), _p(probs), J, seed, len(us), _p(us), _p(js), _p(out))
     if rc != 0:
         raise MemoryError(rc)
+    return out
+
+
+def rebuilt_register(n, offsets, targets, probs, J, seed, seeds, us, js) -> np.ndarray:
+    """Definition of a register after a rebuild blocked by R_G(seeds) (Alg. 1 lines 21-25, R12), for
+    sampled (u, j) pairs; pairs are sorted by j internally (one R_S[j] BFS per distinct j)."""
+    offsets, targets, probs = _csr(offsets, targets, probs)
+    us = np.ascontiguousarray(us, dtype=np.int32)
+    js = np.ascontiguousarray(js, dtype=np.int32)
+    seeds = np.ascontiguousarray(seeds, dtype=np.int32)
+    order = np.argsort(js, kind="stable")
+    us_s, js_s = np.ascontiguousarray(us[order]), np.ascontiguousarray(js[order])
+    out = np.empty(len(us), dtype=np.uint8)
+    o = np.empty(len(us), dtype=np.uint8)
+    rc = _load().or_rebuilt_register(n, _p(offsets), _p(targets), _p(probs), J, seed, len(seeds), _p(seeds), len(us),
+                                     _p(us_s), _p(js_s), _p(o))
+    if rc != 0:
+        raise MemoryError(rc)
+    out[order] = o
     return out
 
 

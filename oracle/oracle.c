@@ -32,7 +32,7 @@
  *                     star / two-star / K=1 reductions, t=0 / t=inf variants
  *   or_init_rows, or_first_sweep_sample (cpu_baseline helpers) <- sklearn-Murmur3 init rows and the
  *                     1-hop closed form
- *   or_reach_register, or_khop_register, or_seed_sigma <- brute force on small graphs
+ *   or_reach_register, or_khop_register, or_seed_sigma, or_rebuilt_register <- brute force on small graphs
  *   or_mix64       <- SplitMix64 published reference outputs (seed 0)
  *   or_mc_influence<- closed forms (w = 0, w = 1 -> BFS reach, star 1 + L w, chain sum w^i within
  *                     CLT bounds), draw uniformity / independence
@@ -481,6 +481,65 @@ int or_reach_register(int32_t n, const int32_t *offsets, const int32_t *targets,
         out[p] = (uint8_t)best;
     }
     free(X); free(seen); free(queue);
+    return 0;
+}
+
+/*
+ * The plain definition of a register after a rebuild (Alg. 1 lines 21-25; reading
+ * R12): with R_S[j] = R_{G_j}(S) for the seed prefix S = seeds[0..nseeds-1], a blocked vertex never
+ * pulls, so in sample j
+ *   M_u[j] = init(u, j)                                          if u in R_S[j]
+ *          = max over w reachable from u in G_j^S of init(w, j)   otherwise,
+ * G_j^S = {(x,y) live in sample j : x not in R_S[j]} (a blocked y is reached and keeps its init value
+ * but is not expanded).  Pairs are evaluated in the given order; R_S[j] is recomputed by BFS from S
+ * whenever j differs from the previous pair's (sort the pairs by j).
+ */
+int or_rebuilt_register(int32_t n, const int32_t *offsets, const int32_t *targets, const float *probs, int32_t J,
+                        uint64_t seed, int32_t nseeds, const int32_t *seeds, int64_t npairs, const int32_t *us,
+                        const int32_t *js, uint8_t *out) {
+    uint32_t seed_v, seed_j;
+    uint32_t *X = (uint32_t *)malloc((size_t)J * sizeof(uint32_t));
+    or_salts(seed, J, &seed_v, &seed_j, X);
+    uint8_t *blocked = (uint8_t *)calloc((size_t)n, 1);
+    uint8_t *seen = (uint8_t *)calloc((size_t)n, 1);
+    int32_t *queue = (int32_t *)malloc((size_t)n * sizeof(int32_t));
+    if (!X || !blocked || !seen || !queue) return -3;
+    int32_t cur_j = -1;
+    for (int64_t p = 0; p < npairs; p++) {
+        int32_t u = us[p], j = js[p];
+        if (j != cur_j) {  /* R_S[j]: BFS from the seed prefix over the live edges of sample j */
+            memset(blocked, 0, (size_t)n);
+            int64_t qh = 0, qt = 0;
+            for (int32_t k = 0; k < nseeds; k++)
+                if (!blocked[seeds[k]]) { blocked[seeds[k]] = 1; queue[qt++] = seeds[k]; }
+            while (qh < qt) {
+                int32_t x = queue[qh++];
+                for (int64_t e = offsets[x]; e < offsets[x + 1]; e++) {
+                    int32_t y = targets[e];
+                    if (!blocked[y] && or_live(X[j], or_edge_hash(x, y), probs[e])) { blocked[y] = 1; queue[qt++] = y; }
+                }
+            }
+            cur_j = j;
+        }
+        uint32_t hj = hash_index((uint32_t)j, seed_j);
+        int64_t qh = 0, qt = 0;
+        int best = 0;
+        seen[u] = 1;
+        queue[qt++] = u;
+        while (qh < qt) {
+            int32_t x = queue[qh++];
+            int r = clz32(hash_index((uint32_t)x, seed_v) ^ hj);
+            if (r > best) best = r;
+            if (blocked[x]) continue;  /* x in R_S[j] never pulls: its out-edges are not in G_j^S */
+            for (int64_t e = offsets[x]; e < offsets[x + 1]; e++) {
+                int32_t y = targets[e];
+                if (!seen[y] && or_live(X[j], or_edge_hash(x, y), probs[e])) { seen[y] = 1; queue[qt++] = y; }
+            }
+        }
+        for (int64_t q = 0; q < qt; q++) seen[queue[q]] = 0;
+        out[p] = (uint8_t)best;
+    }
+    free(X); free(blocked); free(seen); free(queue);
     return 0;
 }
 

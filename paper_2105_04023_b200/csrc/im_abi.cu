@@ -142,7 +142,7 @@ void reset_graph_state() {
 }
 
 void release_all() {
-    dfree(g.Xs); dfree(g.s12); dfree(g.permd); dfree(g.M); dfree(g.vis); dfree(g.vd);
+    dfree(g.Xs); dfree(g.s12); dfree(g.permd); dfree(g.HV); dfree(g.M); dfree(g.vis); dfree(g.vd);
     for (int i = 0; i < 2; i++) { dfree(g.items[i]); dfree(g.bits[i]); dfree(g.cm[i]); dfree(g.delta[i]); dfree(g.bitems[i]); dfree(g.bvl[i]); }
     dfree(g.inS); dfree(g.MS); dfree(g.btag); dfree(g.nbits); dfree(g.gain); dfree(g.big); dfree(g.list); dfree(g.lcount); dfree(g.hist);
     dfree(g.off); dfree(g.fwd); dfree(g.fwdT); dfree(g.roff); dfree(g.rev); dfree(g.revT); dfree(g.ritems); dfree(g.fbig);
@@ -208,6 +208,7 @@ int load_common(int32_t n, int64_t m, const int32_t* d_off_src, const int32_t* d
     }
     // constant threshold: rows ordered by h >> B0 (im_prep.cu)
     g.B0 = g.T0 <= 1u ? 0 : 32 - __builtin_clz(g.T0 - 1u);
+    g.Bs = sort_shift(g.B0);
     g.sorted_h = g.constT && m > 1;
     // forward records {target, h}, thresholds, reverse records {source, h}
     TRY(dalloc(g.fwd, (size_t)m));
@@ -229,7 +230,7 @@ int load_common(int32_t n, int64_t m, const int32_t* d_off_src, const int32_t* d
     // bucket offset tables of the long rows (hash slices without binary searches), written by the prep
     g.nbk = 0;
     if (rows_path(g) && m > 0) {
-        g.nbk = (1 << (31 - g.B0)) + 1;
+        g.nbk = (1 << (31 - g.Bs)) + 1;
         TRY(dalloc(g.ftidx, (size_t)n));
         TRY(dalloc(g.rtidx, (size_t)n));
         TRY(dalloc(g.t_tabrows, (size_t)n));
@@ -299,11 +300,15 @@ int alloc_sketch_state(int32_t J) {
     TRY(dalloc(g.Xs, (size_t)J));
     TRY(dalloc(g.s12, 4097));
     TRY(dalloc(g.permd, (size_t)J));
+    TRY(dalloc(g.HV, (size_t)g.n));
     TRY(dalloc(g.M, n * (size_t)J + 65536));  // + tail padding read by the TMA argmax tiles
     TRY(dalloc(g.vis, n * W + 16384));
     TRY(dalloc(g.vd, n * W));
+    // slices add <= MAX_SLICES partial segments per vertex (word slices), or <= BSL per long row (bucket
+    // slices; long rows <= m / TAB_MIN)
+    const size_t slack = std::max<size_t>((size_t)(MAX_SLICES + 1) * n, (size_t)BSL * ((size_t)g.m / TAB_MIN + 1));
     for (int i = 0; i < 2; i++) {
-        TRY(dalloc(g.items[i], (size_t)g.n_ritems + (MAX_SLICES + 1) * n + 1));  // slices add <= MAX_SLICES partial segments per vertex
+        TRY(dalloc(g.items[i], (size_t)g.n_ritems + slack + 1));
         // a completed build leaves the change buffers zero; fresh ones are cleared by simulate()
         TRY(dalloc(g.bits[i], n, &fr));
         if (fr) g.sweep_dirty = true;
@@ -311,7 +316,7 @@ int alloc_sketch_state(int32_t J) {
         if (fr) g.sweep_dirty = true;
         TRY(dalloc(g.delta[i], n * W, &fr));
         if (fr || g.J != J) CK(cudaMemsetAsync(g.delta[i], 0, n * W * sizeof(uint32_t), g.stream));
-        TRY(dalloc(g.bitems[i], (size_t)g.n_fitems_cap + (MAX_SLICES + 1) * n + 1));
+        TRY(dalloc(g.bitems[i], (size_t)g.n_fitems_cap + slack + 1));
         TRY(dalloc(g.bvl[i], n));
     }
     TRY(dalloc(g.inS, n));
@@ -356,6 +361,7 @@ int setup_salts(int32_t Jt, int32_t j0, int32_t J, uint64_t seed) {
     std::vector<int32_t> gj(J);
     for (int i = 0; i < J; i++) gj[i] = g.perm[i] + j0;
     CK(cudaMemcpyAsync(g.permd, gj.data(), J * sizeof(int32_t), cudaMemcpyHostToDevice, g.stream));
+    CK(launch_vertex_hash(g));
     TRY(sync());  // host vectors go out of scope
     g.seed = seed;
     g.Jt = Jt;

@@ -132,43 +132,6 @@ __device__ __forceinline__ int warp_incl_scan(int x, int lane) {
 }  // namespace im
 
 namespace im {
-// ---------------------------------------------------------------- hash-sorted adjacency ranges
-// With one threshold T for every edge (B = thr_bits(T)) and each adjacency row sorted by h, the
-// edges whose candidate window meets the sorted simulations [a, b] are exactly those with
-// (h >> B) in [Xs[a] >> B, Xs[b] >> B]: one contiguous slice of the row (lo(h), hi(h) are
-// non-decreasing in h).  Work items are built from at most four such slices per vertex.
-__device__ __forceinline__ int lower_bound_h(const uint2* __restrict__ rec, int b, int e, uint32_t key) {
-    while (b < e) {
-        int mid = (b + e) >> 1;
-        if (__ldg(&rec[mid].y) < key) b = mid + 1; else e = mid;
-    }
-    return b;
-}
-
-// up to 4 edge slices [eb[i], ee[i]) of row [rb, re) covering the sim ranges [sa[i], sb[i]] (sa = -1: none)
-__device__ __forceinline__ int slices_for(const uint2* __restrict__ rec, int rb, int re, const uint32_t* sX, int B,
-                                          const int* sa, const int* sb, int* eb, int* ee) {
-    int k = 0;
-#pragma unroll
-    for (int q = 0; q < 4; q++) {
-        if (sa[q] < 0) continue;
-        uint32_t klo = (sX[sa[q]] >> B) << B;
-        uint32_t khi = ((sX[sb[q]] >> B) + 1u) << B;
-        int b0 = lower_bound_h(rec, rb, re, klo), e0 = lower_bound_h(rec, b0, re, khi);
-        if (b0 >= e0) continue;
-        if (k > 0 && b0 <= ee[k - 1]) {  // overlaps the previous slice: merge
-            ee[k - 1] = max(ee[k - 1], e0);
-        } else {
-            eb[k] = b0;
-            ee[k] = e0;
-            k++;
-        }
-    }
-    return k;
-}
-}  // namespace im
-
-namespace im {
 // Block-aggregated reservation on the per-iteration counters (one atomic per counter per block
 // iteration instead of one per warp).  Every thread of the block calls it; lane 31 of each warp
 // passes its warp's totals.  Returns the warp's base for items / changed / big.

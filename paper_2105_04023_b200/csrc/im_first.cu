@@ -16,6 +16,8 @@
 // The working row lives in shared memory as packed 4-register words; an edge merges the live
 // registers of its window word by word with a shared-memory bytewise-max CAS.
 // Vertices with more than FIRST_BIG out-edges are done by a whole block (k_first_big).
+#include <algorithm>
+
 #include "im_device.cuh"
 #include "im_internal.h"
 
@@ -39,7 +41,21 @@ struct FirstArgs {
     IterCounters* ctr;
     const int32_t* big;  // vertices with > FIRST_BIG out-edges (k_first_big)
     int n_big;
+    int vb;              // vertices per warp batch (<= 256; fewer on small graphs so every warp gets work)
+    const uint32_t* HV;  // hash(v) = Murmur3(LE32 v, seed_V) per vertex (Alg. 1 line 4), this build's
 };
+
+#ifndef FIRST_HV
+#define FIRST_HV 1  // 1: read hash(v) of Alg. 1 line 4 from the per-build table HV (k_vertex_hash) instead of
+                    // recomputing Murmur3 per edge (the from-init gather is ALU-bound)
+#endif
+__device__ __forceinline__ uint32_t vhash(const FirstArgs& a, uint32_t v) {
+#if FIRST_HV
+    return __ldg(&a.HV[v]);
+#else
+    return murmur_word(v, a.seedV);
+#endif
+}
 
 // init registers of simulations 4w..4w+3 of a vertex with hash hv, packed
 __device__ __forceinline__ uint32_t init_word(uint32_t hv, const uint32_t* sHJ, int w) {
@@ -112,7 +128,7 @@ __device__ __forceinline__ void gather_rec(const FirstArgs& a, const uint32_t* s
             edge_window(h, T, sX, sS, a.J, lo, hi);
             if (lo < hi) {
                 wcount++;
-                if (!MEM) hv = murmur_word(v, a.seedV);
+                if (!MEM) hv = vhash(a, v);
             }
         }
     }
@@ -159,7 +175,7 @@ __device__ __forceinline__ void gather_multi(const FirstArgs& a, const uint32_t*
         if (T[k]) edge_window(f[k].y, T[k], sX, sS, a.J, lo[k], hi[k]);
         if (lo[k] < hi[k]) {
             wcount++;
-            if (!MEM) hv[k] = murmur_word(f[k].x, a.seedV);
+            if (!MEM) hv[k] = vhash(a, f[k].x);
             else if (hi[k] - lo[k] <= DENSE_WIN) {  // the first two window words (a 4-simulation window spans two words 3/4 of the time)
                 const uint32_t* rv = reinterpret_cast<const uint32_t*>(a.M) + (size_t)f[k].x * (a.J >> 2);
                 pre[k] = rv[lo[k] >> 2];
@@ -226,10 +242,10 @@ __device__ __forceinline__ void first_small(const FirstArgs& a, const uint32_t* 
         edge_window(h, T, sX, sS, J, lo, hi);
         if (lo < hi) {
             wcount++;
-            if (!MEM) hv = murmur_word(v, a.seedV);
+            if (!MEM) hv = vhash(a, v);
         }
     }
-    const uint32_t hu = MEM ? 0u : murmur_word(u, a.seedV);
+    const uint32_t hu = MEM ? 0u : vhash(a, u);
     const int w0 = lo >> 2, w1 = lo < hi ? (hi - 1) >> 2 : w0 - 1;
     // MEM: the out-neighbour's first window word is loaded now, in flight with the row words below
     const uint32_t* rv = reinterpret_cast<const uint32_t*>(a.M) + (size_t)v * (J >> 2);
@@ -284,10 +300,10 @@ __global__ void __launch_bounds__(BLOCK, 5) k_first(FirstArgs a) {
     int* off_w = sOff[wib];
     for (;;) {
         int base = 0;
-        if (lane == 0) base = atomicAdd(&a.ctr->batch, 256);
+        if (lane == 0) base = atomicAdd(&a.ctr->batch, a.vb);
         base = __shfl_sync(IM_FULL, base, 0);
         if (base >= a.n) break;
-        const int end = min(base + 256, a.n);
+        const int end = min(base + a.vb, a.n);
         for (int i = lane; i <= end - base; i += 32) off_w[i] = a.off[base + i];  // the batch's offsets, one coalesced read
         __syncwarp();
         // first 32 records of the next vertex are prefetched while the current one is processed
@@ -328,7 +344,7 @@ __global__ void __launch_bounds__(BLOCK, 5) k_first(FirstArgs a) {
                                                    wcount);
                 continue;
             }
-            const uint32_t hu = MEM ? 0u : murmur_word((uint32_t)u, a.seedV);
+            const uint32_t hu = MEM ? 0u : vhash(a, (uint32_t)u);
             for (int w = lane; w < NW; w += 32) {
                 uint32_t x = start_word<MEM>(a, sHJ, hu, (uint32_t)u, w);
                 row[w] = x;
@@ -385,7 +401,7 @@ __global__ void __launch_bounds__(BLOCK) k_first_big(FirstArgs a) {
     for (int bi = blockIdx.x; bi < a.n_big; bi += gridDim.x) {
         const uint32_t u = (uint32_t)a.big[bi];
         __syncthreads();
-        const uint32_t hu = MEM ? 0u : murmur_word(u, a.seedV);
+        const uint32_t hu = MEM ? 0u : vhash(a, u);
         for (int w = threadIdx.x; w < NW; w += blockDim.x) {
             uint32_t x = start_word<MEM>(a, sHJ, hu, u, w);
             row[w] = x;
@@ -453,6 +469,11 @@ cudaError_t launch_first(Ctx& c, uint32_t* cm_out, uint32_t* bits_out, IterCount
     a.ctr = ctr;
     a.big = c.fbig;
     a.n_big = c.n_fbig;
+    a.HV = c.HV;
+    {   // a dependent chain of loads per vertex: spread small graphs over every resident warp
+        const int64_t warps = (int64_t)c.max_blocks_first * (BLOCK / 32);
+        a.vb = (int)std::min<int64_t>(256, std::max<int64_t>(1, c.n / warps));
+    }
     if (from_memory) {
         if (c.constT) return blocked ? first_inst<true, true, true>(c, a) : first_inst<true, false, true>(c, a);
         return blocked ? first_inst<false, true, true>(c, a) : first_inst<false, false, true>(c, a);

@@ -15,6 +15,7 @@ typedef unsigned long long ull;
 constexpr int SEG = 256;        // max edges per work item (a segment of one vertex's edge list)
 constexpr int TAB_MIN = SEG;  // rows longer than this get a bucket offset table (rows path)
 constexpr int MAX_SLICES = 8; // hash slices per long row (more non-zero mask words: the whole row)
+constexpr int BSL = 32;       // bucket slices per long row with a bucket table (k_slices_buckets)
 constexpr int DENSE_WIN = 32;   // windows wider than this many simulations take the warp-cooperative path
 constexpr int BLOCK = 256;      // threads per block of the persistent work-list kernels
 #ifndef IM_FIRST_BIG
@@ -69,6 +70,7 @@ struct Ctx {
     bool constT = true;
     uint32_t T0 = 0;
     int B0 = 0;                 // thr_bits(T0): candidate windows are salt blocks of 2^B0
+    int Bs = 0;                 // bucket shift of the row order / bucket tables: max(B0, 23), <= 2^8 buckets
     bool sorted_h = false;      // adjacency rows sorted by h (constant threshold only)
     int4* ritems = nullptr;     // all reverse segments {v, eb, ee, 0}
     int nbk = 0;                // bucket offset tables: 2^KB + 1 entries per long row (0: none, binary search)
@@ -91,6 +93,7 @@ struct Ctx {
     uint32_t* Xs = nullptr;     // sorted salts [J]
     uint16_t* s12 = nullptr;    // [4097]
     int32_t* permd = nullptr;   // [J] internal index -> global simulation j (hash input of Eq. 1)
+    uint32_t* HV = nullptr;     // [n] hash(v) = Murmur3(LE32 v, seed_V) (Alg. 1 line 4), written by setup_salts
     uint8_t* M = nullptr;       // n*J registers, row-major, internal simulation order
     uint8_t* Mold = nullptr;    // pre-sweep copy read by synchronous sweeps (eps_c > 0, R22), n*J
     bool sync_sweeps = false;   // the running Simulate uses synchronous sweeps
@@ -188,7 +191,8 @@ int setup_first(int J, int* blocks_per_sm);  // smem opt-in + occupancy of the f
 // register init + first sweep (gather, im_first.cu): writes every row, its change mask and chunk bits
 cudaError_t launch_first(Ctx& c, uint32_t* cm_out, uint32_t* bits_out, IterCounters* ctr, bool blocked, bool from_memory);
 cudaError_t launch_list_big_rows(Ctx& c, int32_t* out, int* count);
-bool rows_path(const Ctx& c);  // constant threshold with KB <= 8: row-local bucket order, bucket tables
+bool rows_path(const Ctx& c);  // constant threshold: long rows bucket-ordered (h >> Bs), bucket tables
+int sort_shift(int B0);        // Bs for a threshold's B0
 
 cudaError_t launch_validate(Ctx& c, const int32_t* off, const int32_t* tgt, const float* prob, int* flags);
 cudaError_t launch_const_check(Ctx& c, const float* prob, int* flag);
@@ -199,6 +203,7 @@ cudaError_t launch_build_items(Ctx& c, const int32_t* offs, int4* items, int32_t
 cudaError_t scan_exclusive(Ctx& c, const int32_t* in, int32_t* out, int n, void* tmp, size_t& tmp_bytes);
 cudaError_t launch_salt_tables(Ctx& c);
 cudaError_t launch_init_registers(Ctx& c);
+cudaError_t launch_vertex_hash(Ctx& c);  // c.HV[v] = Murmur3(LE32 v, seed_V)
 // one sweep over `items`; cm_in: per-simulation change mask of the previous sweep (null: no filter,
 // sweep 1); cm_out / bits_out: this sweep's change mask and chunk summary; counters in *ctr (zeroed)
 cudaError_t launch_sweep(Ctx& c, const int4* items, int n_items, const uint32_t* cm_in, uint32_t* cm_out,

@@ -9,6 +9,7 @@
 // INT pipes.  All work-list kernels are persistent (grid <= resident blocks)
 // and pull 32-item batches from a device cursor.
 
+#include <algorithm>
 #include <climits>
 
 #include "im_device.cuh"
@@ -377,6 +378,7 @@ struct BfsArgs {
     uint2* vd;         // {visited R_G(S), new in this level} word pairs: the visited test and both ORs touch one sector
     const uint32_t* din;
     uint32_t* nbits;   // per vertex: which 32-simulation words got new bits in this level
+    int ipw;           // items per warp batch (<= 32; fewer when the level is small, to spread it over the SMs)
 };
 
 // Same level, reworked for memory-level parallelism (the level is bound by dependent random loads):
@@ -411,20 +413,20 @@ __global__ void __launch_bounds__(BLOCK, BFS_MINB) k_bfs_level2(BfsArgs a) {
     __syncthreads();
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, W = a.J >> 5;
     uint32_t* sD = sDyn + (size_t)wib * 32 * W;  // Delta rows of this warp's 32 items
-    int base = 0, left = 0;  // 128-item grabs (4 batches of 32)
+    int base = 0, left = 0;  // grabs of 4 batches of ipw items
     for (;;) {
         if (left == 0) {
-            if (lane == 0) base = atomicAdd(&a.ctr_next->batch, 128);
+            if (lane == 0) base = atomicAdd(&a.ctr_next->batch, 4 * a.ipw);
             base = __shfl_sync(IM_FULL, base, 0);
             left = 4;
         } else {
-            base += 32;
+            base += a.ipw;
         }
         --left;
         if (base >= a.n_items) break;
         const int it = base + lane;
         int u = 0, eb = 0, cnt = 0;
-        if (it < a.n_items) {
+        if (lane < a.ipw && it < a.n_items) {
             const int4 I = a.items[it];
             u = I.x;
             eb = I.y;
@@ -434,7 +436,7 @@ __global__ void __launch_bounds__(BLOCK, BFS_MINB) k_bfs_level2(BfsArgs a) {
         for (int idx = lane; idx < 32 * W; idx += 32) {
             const int i = idx / W, w = idx - i * W;
             const int ui = __shfl_sync(IM_FULL, u, i);
-            sD[idx] = base + i < a.n_items ? a.din[(size_t)ui * W + w] : 0u;
+            sD[idx] = i < a.ipw && base + i < a.n_items ? a.din[(size_t)ui * W + w] : 0u;
         }
         __syncwarp();
         const int incl = warp_incl_scan(cnt, lane);
@@ -802,7 +804,11 @@ cudaError_t launch_bfs_level(Ctx& c, int cur, int n_items, uint32_t tag) {
     a.vd = c.vd;
     a.din = c.delta[cur];
     a.nbits = c.nbits;
-    int64_t want = ((int64_t)n_items + 32 * (BLOCK / 32) - 1) / (32 * (BLOCK / 32));
+    // items per warp batch: 32, or fewer so that a small level still occupies every SM (each edge is a
+    // chain of dependent loads, so a level is latency-bound unless many warps are in flight)
+    const int64_t warps_max = (int64_t)c.max_blocks_bfs2 * (BLOCK / 32);
+    a.ipw = (int)std::min<int64_t>(32, std::max<int64_t>(1, n_items / warps_max));
+    int64_t want = ((int64_t)n_items + (int64_t)a.ipw * (BLOCK / 32) - 1) / ((int64_t)a.ipw * (BLOCK / 32));
     {
         const size_t smem = (size_t)BLOCK * (c.J >> 5) * sizeof(uint32_t);
         int grid = (int)(want < 1 ? 1 : (want > c.max_blocks_bfs2 ? c.max_blocks_bfs2 : want));

@@ -1,17 +1,19 @@
 // im_prep.cu -- a0 edge preparation (Eq. 4-5, Sec. 3.3) and a2 register init (Alg. 1 lines 2-5).
 //
-// Edge prep, once per graph:
+// Edge prep, once per graph, all hand-written (no library sort or scan):
 //   validate the CSR; detect a constant w; per edge h(u,v) = Murmur3(u||v) mod 2^31 and the exact
 //   integer threshold T_e (im_device.cuh); build the forward rows {v, h} and the reverse rows {u, h}
-//   (grouped by target) used by the sweeps.  With a constant threshold T (2^(B-1) < T <= 2^B) every
-//   row is additionally ordered by h >> B, so the slice of a row whose candidate windows meet a
-//   given simulation range is contiguous (im_device.cuh "hash-sorted adjacency ranges").  Both
-//   orders come from one LSD radix sort of the composite key (row << (31-B)) | (h >> B); the row
-//   part keeps CSR rows contiguous, so the sort doubles as the transpose.  Per-edge thresholds
-//   (weighted cascade) keep the input row order and use an atomic-cursor transpose.
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
-
+//   (grouped by target) used by the sweeps.
+//   Reverse offsets: in-degree histogram + exclusive scan (k_scan_*).  The transpose is an atomic-cursor
+//   scatter: edge (u,v) goes to roff[v] + (a per-target cursor); the order inside a reverse row is
+//   immaterial except for bucket slicing (below).
+//   With a constant threshold T (2^(B-1) < T <= 2^B) every row longer than TAB_MIN is additionally
+//   ordered by the bucket h >> Bs (Bs = max(B, 23): at most 2^8 buckets; a simulation j can only be
+//   live on edges of bucket X_j >> Bs) and gets a bucket offset table, so the slice of a long row whose
+//   candidate windows meet a set of simulations is a few table reads (k_slices_buckets, im_sweep.cu).
+//   Forward rows are bucket-ordered in place by a row-local counting sort (k_rows / k_rows_big, which
+//   also scatter the reverse records); long reverse rows by a block-local counting sort (k_rev_rows).
+//   Per-edge thresholds (weighted cascade) keep the input row order.
 #include "im_device.cuh"
 #include "im_internal.h"
 
@@ -44,42 +46,106 @@ __global__ void k_const_check(int64_t m, const float* __restrict__ prob, int* fl
     if (__any_sync(IM_FULL, diff) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
 }
 
-// source vertex of every edge: the start position of each non-empty row gets its id, then a max-scan
-__global__ void k_row_markers(int32_t n, const int32_t* __restrict__ off, int32_t* __restrict__ mark) {
-    int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += stride)
-        if (off[u] < off[u + 1]) mark[off[u]] = (int32_t)u;
+// source vertex of every edge (per-edge-threshold path): a warp per row writes its id
+__global__ void k_src(int32_t n, const int32_t* __restrict__ off, int32_t* __restrict__ src) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; u < n; u += nwarps)
+        for (int e = off[u] + lane; e < off[u + 1]; e += 32) src[e] = (int32_t)u;
 }
 
-struct MaxOp {
-    __device__ __forceinline__ int32_t operator()(int32_t a, int32_t b) const { return a > b ? a : b; }
-};
+// in-degree histogram (reverse row lengths); equal targets of a warp are aggregated first
+__global__ void k_indeg(int64_t m, const int32_t* __restrict__ tgt, int32_t* __restrict__ indeg) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int lane = threadIdx.x & 31;
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < m; base += stride) {
+        const int64_t e = base + threadIdx.x;
+        const int v = e < m ? tgt[e] : -1;
+        const uint32_t peers = __match_any_sync(IM_FULL, v);
+        if (v >= 0 && lane == __ffs(peers) - 1) atomicAdd(&indeg[v], __popc(peers));
+    }
+}
 
-// forward records (+ composite sort keys when SORTED); in-degree histogram
-template <typename K, bool SORTED>
+// ---------------------------------------------------------------- exclusive scan of int32 (3 passes)
+// tile = SCAN_T = BLOCK * 16 values: per-tile sums, a one-block scan of the tile sums, per-tile scan
+// with the tile's offset.  Sums fit int32 (CSR offsets, segment counts <= m < 2^31).
+constexpr int SCAN_PER = 16, SCAN_T = BLOCK * SCAN_PER;
+
+__device__ __forceinline__ int block_excl_scan(int x, int* sW, int* total) {
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int incl = warp_incl_scan(x, lane);
+    if (lane == 31) sW[wib] = incl;
+    __syncthreads();
+    if (wib == 0) {
+        const int w = lane < BLOCK / 32 ? sW[lane] : 0;
+        const int wi = warp_incl_scan(w, lane);
+        if (lane < BLOCK / 32) sW[lane] = wi - w;
+        if (lane == BLOCK / 32 - 1) *total = wi;
+    }
+    __syncthreads();
+    const int r = sW[wib] + incl - x;
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(BLOCK) k_scan_reduce(int n, const int32_t* __restrict__ in, int32_t* __restrict__ part) {
+    __shared__ int sW[BLOCK / 32];
+    __shared__ int tot;
+    const int64_t b0 = (int64_t)blockIdx.x * SCAN_T;
+    int s = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_PER; k++) {
+        const int64_t i = b0 + (int64_t)k * BLOCK + threadIdx.x;
+        s += i < n ? in[i] : 0;
+    }
+    block_excl_scan(s, sW, &tot);
+    if (threadIdx.x == 0) part[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(BLOCK) k_scan_top(int nt, int32_t* __restrict__ part) {
+    __shared__ int sW[BLOCK / 32];
+    __shared__ int tot;
+    int carry = 0;
+    for (int b = 0; b < nt; b += BLOCK) {
+        const int i = b + threadIdx.x;
+        const int x = i < nt ? part[i] : 0;
+        const int ex = block_excl_scan(x, sW, &tot);
+        if (i < nt) part[i] = carry + ex;
+        carry += tot;
+    }
+}
+
+__global__ void __launch_bounds__(BLOCK) k_scan_down(int n, const int32_t* __restrict__ in, const int32_t* __restrict__ part,
+                                                     int32_t* __restrict__ out) {
+    __shared__ int sW[BLOCK / 32];
+    __shared__ int tot;
+    const int64_t b0 = (int64_t)blockIdx.x * SCAN_T + (int64_t)threadIdx.x * SCAN_PER;  // thread-contiguous
+    int v[SCAN_PER], s = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_PER; k++) {
+        v[k] = b0 + k < n ? in[b0 + k] : 0;
+        s += v[k];
+    }
+    int run = part[blockIdx.x] + block_excl_scan(s, sW, &tot);
+#pragma unroll
+    for (int k = 0; k < SCAN_PER; k++)
+        if (b0 + k < n) {
+            out[b0 + k] = run;
+            run += v[k];
+        }
+}
+
+// forward records and per-edge thresholds (weighted cascade path); in-degree histogram
 __global__ void k_edge_prep(int64_t m, const int32_t* __restrict__ src, const int32_t* __restrict__ tgt,
-                            const float* __restrict__ prob, int B, int KB, K* __restrict__ keys, uint2* __restrict__ rec,
-                            uint32_t* __restrict__ recT, int32_t* __restrict__ indeg) {
+                            const float* __restrict__ prob, uint2* __restrict__ rec, uint32_t* __restrict__ recT,
+                            int32_t* __restrict__ indeg) {
     int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += stride) {
         uint32_t u = (uint32_t)src[e], v = (uint32_t)tgt[e];
         uint32_t h = edge_hash(u, v);
         rec[e] = make_uint2(v, h);
-        if (SORTED) keys[e] = ((K)u << KB) | (K)(h >> B);
-        else recT[e] = live_threshold(prob[e]);
+        recT[e] = live_threshold(prob[e]);
         atomicAdd(&indeg[v], 1);
-    }
-}
-
-// reverse records {u, h} keyed by (v << KB) | (h >> B); fwd is already row-ordered, so src[e] is its row
-template <typename K>
-__global__ void k_rev_keys(int64_t m, const int32_t* __restrict__ src, const uint2* __restrict__ fwd, int B, int KB,
-                           K* __restrict__ keys, uint2* __restrict__ rec) {
-    int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += stride) {
-        uint2 f = fwd[e];
-        keys[e] = ((K)f.x << KB) | (K)(f.y >> B);
-        rec[e] = make_uint2((uint32_t)src[e], f.y);
     }
 }
 
@@ -111,15 +177,12 @@ __global__ void k_fill_items(int32_t n, const int32_t* __restrict__ offs, const 
 }
 
 // ------------------------------------------------------------------ bucket-ordered rows (constant T)
-// With one threshold T (2^(B-1) < T <= 2^B) a row only has to be grouped by bucket b = h >> B
-// (KB = 31 - B bits); the order inside a bucket is immaterial (every consumer takes the slice of
-// a bucket range, im_device.cuh "hash-sorted adjacency ranges").  For KB <= 8 the forward rows
-// are ordered in place by a row-local counting sort instead of a full-width radix sort of m keys:
-//   k_rows       forward row u: h = Murmur3(u||v) mod 2^31 (Eq. 4), records {v, h} written in
-//                bucket order; at the edge's input position, the reverse sort key (v << KB) | b
-//                and payload {u, h} (coalesced; the radix sort of these is the transpose)
-//   radix sort   reverse records grouped by v, bucket-ordered inside (one LSD sort)
-//   k_row_bounds reverse offsets from the sorted keys (no in-degree atomics)
+// With one threshold T a row only has to be grouped by bucket b = h >> Bs (KB = 31 - Bs <= 8 bits);
+// the order inside a bucket is immaterial (every consumer takes the slice of a bucket range).
+//   k_rows       forward row u: h = Murmur3(u||v) mod 2^31 (Eq. 4), records {v, h} written in bucket
+//                order by a row-local counting sort; every edge is also scattered to its reverse row
+//                (atomic cursor), straight into `rev` for a short reverse row, into `rtmp` for a long one
+//   k_rev_rows   long reverse rows: block-local counting sort rtmp -> rev, bucket table
 // Rows of at most 32 edges are ranked inside one warp by a radix ballot; rows up to PREP_BIG by a
 // warp with a shared-memory histogram; longer rows by a whole block (k_rows_big).
 constexpr int PREP_BIG = 2048;
@@ -131,41 +194,42 @@ __global__ void k_list_long(int32_t n, const int32_t* __restrict__ off, int32_t*
         if (off[u + 1] - off[u] > PREP_BIG) lf[atomicAdd(count, 1)] = (int32_t)u;
 }
 
-template <typename K>
 struct RowSortArgs {
     int32_t n;
-    int B, KB;
+    int B, KB;              // bucket = h >> B (B = Bs), 2^KB buckets
     const int32_t* off;     // forward row offsets
     const int32_t* tgt;     // input targets (CSR order)
     uint2* out;             // bucket-ordered forward records {v, h}
-    K* rkey;                // reverse sort keys (v << KB) | b, input order
-    uint2* rval;            // reverse payload {u, h}, input order
+    const int32_t* roff;    // reverse row offsets
+    int32_t* cursor;        // per-target scatter cursor (zeroed)
+    uint2* rev;             // reverse records {u, h}: short reverse rows final
+    uint2* rtmp;            // long reverse rows (> TAB_MIN), unordered, sorted by k_rev_rows
     const int32_t* lst;     // k_rows_big: rows longer than PREP_BIG
     const int* lcount;
     int* batch;             // dynamic row-batch cursor (zeroed)
-    const int32_t* tidx;    // bucket offset table of each row (-1: none), tables tab[rows x nbk]
+    const int32_t* tidx;    // bucket offset table of each forward row (-1: none), tables tab[rows x nbk]
     int32_t* tab;
     int nbk;
 };
 
 // the bucket offsets of a row with a table: hist holds the exclusive scan of its bucket counts
-template <typename K>
-__device__ __forceinline__ void write_row_table(const RowSortArgs<K>& a, uint32_t u, int eb, int ee, const int* hist, int NB,
-                                                int tid, int nthreads) {
-    const int t = a.tidx ? a.tidx[u] : -1;
+__device__ __forceinline__ void write_row_table(const int32_t* tidx, int32_t* tab, int nbk, uint32_t u, int eb, int ee,
+                                                const int* hist, int NB, int tid, int nthreads) {
+    const int t = tidx ? tidx[u] : -1;
     if (t < 0) return;
-    int32_t* tb = a.tab + (int64_t)t * a.nbk;
+    int32_t* tb = tab + (int64_t)t * nbk;
     for (int kb = tid; kb <= NB; kb += nthreads) tb[kb] = kb < NB ? eb + hist[kb] : ee;
 }
 
-// record {v, h(u,v)} of input edge e of row u (+ its reverse key and payload on the first visit)
-template <typename K>
-__device__ __forceinline__ uint2 row_rec(const RowSortArgs<K>& a, int64_t e, uint32_t u, bool first) {
+// record {v, h(u,v)} of input edge e of row u; on the first visit the edge is also scattered to its
+// reverse row (the transpose)
+__device__ __forceinline__ uint2 row_rec(const RowSortArgs& a, int64_t e, uint32_t u, bool first) {
     const uint32_t v = (uint32_t)a.tgt[e];
     const uint32_t h = edge_hash(u, v);
     if (first) {
-        a.rkey[e] = ((K)v << a.KB) | (K)(h >> a.B);
-        a.rval[e] = make_uint2(u, h);
+        const int rb = a.roff[v], d = a.roff[v + 1] - rb;
+        const int p = rb + atomicAdd(&a.cursor[v], 1);
+        (d > TAB_MIN ? a.rtmp : a.rev)[p] = make_uint2(u, h);
     }
     return make_uint2(v, h);
 }
@@ -205,8 +269,7 @@ __device__ __forceinline__ void warp_scan_bins(int* hist, int NB, int lane) {
         }
 }
 
-template <typename K>
-__global__ void __launch_bounds__(BLOCK) k_rows(RowSortArgs<K> a) {
+__global__ void __launch_bounds__(BLOCK) k_rows(RowSortArgs a) {
     __shared__ int sH[BLOCK / 32][1 << PREP_KB_MAX];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     int* hist = sH[wib];
@@ -235,7 +298,7 @@ __global__ void __launch_bounds__(BLOCK) k_rows(RowSortArgs<K> a) {
             }
             for (int q = lane; q < NB; q += 32) hist[q] = 0;
             __syncwarp();
-            for (int e0 = eb; e0 < ee; e0 += 32) {  // pass 1: bucket counts
+            for (int e0 = eb; e0 < ee; e0 += 32) {  // pass 1: bucket counts (+ the reverse scatter)
                 const bool have = e0 + lane < ee;
                 uint32_t b = 0xFFFFFFFFu;
                 if (have) b = row_rec(a, e0 + lane, (uint32_t)u, true).y >> a.B;
@@ -245,7 +308,7 @@ __global__ void __launch_bounds__(BLOCK) k_rows(RowSortArgs<K> a) {
             }
             warp_scan_bins(hist, NB, lane);
             __syncwarp();
-            write_row_table(a, (uint32_t)u, eb, ee, hist, NB, lane, 32);
+            write_row_table(a.tidx, a.tab, a.nbk, (uint32_t)u, eb, ee, hist, NB, lane, 32);
             for (int e0 = eb; e0 < ee; e0 += 32) {  // pass 2: place (stable)
                 const bool have = e0 + lane < ee;
                 uint2 r = make_uint2(0, 0);
@@ -264,77 +327,58 @@ __global__ void __launch_bounds__(BLOCK) k_rows(RowSortArgs<K> a) {
     }
 }
 
-// rows longer than PREP_BIG: one block per row, shared-memory histogram, atomic placement
-template <typename K>
-__global__ void __launch_bounds__(BLOCK) k_rows_big(RowSortArgs<K> a) {
+// counting sort of one row [eb, ee) by bucket (y >> B) into `out` by a whole block, with the row's bucket
+// table; rec(e, first) yields the record of position e (called twice per position: first = true once);
+// hist: 2^KB shared counters
+template <typename Rec>
+__device__ __forceinline__ void block_row_sort(Rec rec, uint2* out, int eb, int ee, int B, int NB, int* hist,
+                                               const int32_t* tidx, int32_t* tab, int nbk, uint32_t row) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < NB; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    for (int e0 = eb; e0 < ee; e0 += blockDim.x) {  // block-uniform trip count
+        const bool have = e0 + (int)threadIdx.x < ee;
+        const uint32_t b = have ? rec(e0 + threadIdx.x, true).y >> B : 0xFFFFFFFFu;
+        const uint32_t peers = __match_any_sync(IM_FULL, b);
+        if (have && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[b], __popc(peers));
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) warp_scan_bins(hist, NB, threadIdx.x);
+    __syncthreads();
+    write_row_table(tidx, tab, nbk, row, eb, ee, hist, NB, threadIdx.x, blockDim.x);
+    __syncthreads();  // the table is read from hist before the placement below advances it
+    for (int e0 = eb; e0 < ee; e0 += blockDim.x) {
+        const bool have = e0 + (int)threadIdx.x < ee;
+        const uint2 r = have ? rec(e0 + threadIdx.x, false) : make_uint2(0, 0);
+        const uint32_t b = have ? r.y >> B : 0xFFFFFFFFu;
+        const uint32_t peers = __match_any_sync(IM_FULL, b);
+        const int lane = threadIdx.x & 31, leader = __ffs(peers) - 1;
+        int p = 0;
+        if (have && lane == leader) p = atomicAdd(&hist[b], __popc(peers));
+        p = __shfl_sync(IM_FULL, p, leader);
+        if (have) out[eb + p + __popc(peers & ((1u << lane) - 1u))] = r;
+    }
+}
+
+// forward rows longer than PREP_BIG: one block per row (records recomputed in the placement pass)
+__global__ void __launch_bounds__(BLOCK) k_rows_big(RowSortArgs a) {
     __shared__ int hist[1 << PREP_KB_MAX];
-    const int NB = 1 << a.KB;
     const int cnt = *a.lcount;
     for (int bi = blockIdx.x; bi < cnt; bi += gridDim.x) {
         const uint32_t u = (uint32_t)a.lst[bi];
-        const int eb = a.off[u], ee = a.off[u + 1];
-        __syncthreads();
-        for (int i = threadIdx.x; i < NB; i += blockDim.x) hist[i] = 0;
-        __syncthreads();
-        for (int e0 = eb; e0 < ee; e0 += blockDim.x) {  // block-uniform trip count
-            const bool have = e0 + (int)threadIdx.x < ee;
-            uint32_t b = 0xFFFFFFFFu;
-            if (have) b = row_rec(a, e0 + threadIdx.x, u, true).y >> a.B;
-            const uint32_t peers = __match_any_sync(IM_FULL, b);
-            if (have && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[b], __popc(peers));
-        }
-        __syncthreads();
-        if (threadIdx.x < 32) warp_scan_bins(hist, NB, threadIdx.x);
-        __syncthreads();
-        write_row_table(a, u, eb, ee, hist, NB, threadIdx.x, blockDim.x);
-        __syncthreads();  // the table is read from hist before the placement below advances it
-        for (int e0 = eb; e0 < ee; e0 += blockDim.x) {
-            const bool have = e0 + (int)threadIdx.x < ee;
-            uint2 r = make_uint2(0, 0);
-            uint32_t b = 0xFFFFFFFFu;
-            if (have) {
-                r = row_rec(a, e0 + threadIdx.x, u, false);
-                b = r.y >> a.B;
-            }
-            const uint32_t peers = __match_any_sync(IM_FULL, b);
-            const int lane = threadIdx.x & 31, leader = __ffs(peers) - 1;
-            int p = 0;
-            if (have && lane == leader) p = atomicAdd(&hist[b], __popc(peers));
-            p = __shfl_sync(IM_FULL, p, leader);
-            if (have) a.out[eb + p + __popc(peers & ((1u << lane) - 1u))] = r;
-        }
+        block_row_sort([&](int64_t e, bool first) { return row_rec(a, e, u, first); }, a.out, a.off[u], a.off[u + 1], a.B,
+                       1 << a.KB, hist, a.tidx, a.tab, a.nbk, u);
     }
 }
 
-// reverse offsets from the sorted keys (row = key >> KB): roff[v] = first position with row >= v
-template <typename K>
-__global__ void k_row_bounds(int64_t m, int32_t n, const K* __restrict__ keys, int KB, int32_t* __restrict__ roff) {
-    int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= m; i += stride) {
-        const int64_t r = i < m ? (int64_t)(keys[i] >> KB) : (int64_t)n;
-        const int64_t p = i > 0 ? (int64_t)(keys[i - 1] >> KB) : -1;
-        for (int64_t v = p + 1; v <= r; ++v) roff[v] = (int32_t)i;
-    }
-}
-
-// reverse-row bucket tables from the sorted keys (row = key >> KB, bucket = low KB bits): position i
-// starts buckets (previous bucket of its row, bucket(i)]; the row's last position ends the rest
-template <typename K>
-__global__ void k_rev_tabs(int64_t m, const K* __restrict__ keys, int KB, const int32_t* __restrict__ tidx, int nbk,
-                           int32_t* __restrict__ tab) {
-    const K mask = ((K)1 << KB) - 1;
-    int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += stride) {
-        const K k = keys[i];
-        const int64_t r = (int64_t)(k >> KB);
-        const int t = tidx[r];
-        if (t < 0) continue;
-        int32_t* tb = tab + (int64_t)t * nbk;
-        const int b = (int)(k & mask);
-        const int pb = (i > 0 && (int64_t)(keys[i - 1] >> KB) == r) ? (int)(keys[i - 1] & mask) : -1;
-        for (int kb = pb + 1; kb <= b; ++kb) tb[kb] = (int32_t)i;
-        if (i + 1 == m || (int64_t)(keys[i + 1] >> KB) != r)
-            for (int kb = b + 1; kb < nbk; ++kb) tb[kb] = (int32_t)(i + 1);
+// long reverse rows (> TAB_MIN, listed by k_tab_index): block-local counting sort rtmp -> rev + table
+__global__ void __launch_bounds__(BLOCK) k_rev_rows(int nrows, const int32_t* __restrict__ rows, const int32_t* __restrict__ roff,
+                                                    const uint2* __restrict__ rtmp, uint2* __restrict__ rev, int B, int KB,
+                                                    const int32_t* __restrict__ tidx, int32_t* __restrict__ tab, int nbk) {
+    __shared__ int hist[1 << PREP_KB_MAX];
+    for (int t = blockIdx.x; t < nrows; t += gridDim.x) {
+        const uint32_t v = (uint32_t)rows[t];
+        block_row_sort([&](int64_t e, bool) { return rtmp[e]; }, rev, roff[v], roff[v + 1], B, 1 << KB, hist, tidx, tab, nbk, v);
     }
 }
 
@@ -356,7 +400,7 @@ __global__ void k_tab_index(int32_t n, const int32_t* __restrict__ offs, int32_t
 }
 
 // rows longer than TAB_MIN get a table: index per vertex, count read back, tables allocated
-static cudaError_t setup_tables(Ctx& c, const int32_t* offs, int32_t* tidx, int32_t*& tab, int* d_count) {
+static cudaError_t setup_tables(Ctx& c, const int32_t* offs, int32_t* tidx, int32_t*& tab, int* d_count, int* count = nullptr) {
     cudaError_t e;
     if ((e = cudaMemsetAsync(d_count, 0, sizeof(int), c.stream))) return e;
     k_tab_index<<<grid_for(c, c.n), BLOCK, 0, c.stream>>>(c.n, offs, tidx, c.t_tabrows, d_count);
@@ -365,6 +409,7 @@ static cudaError_t setup_tables(Ctx& c, const int32_t* offs, int32_t* tidx, int3
     if ((e = cudaMemcpyAsync(c.hpin, d_count, sizeof(int), cudaMemcpyDeviceToHost, c.stream))) return e;
     if ((e = cudaStreamSynchronize(c.stream))) return e;
     h = *(int*)c.hpin;
+    if (count) *count = h;
     return h ? c.alloc_i32(tab, (size_t)h * c.nbk) : cudaSuccess;
 }
 
@@ -404,7 +449,18 @@ __global__ void k_init_registers(int32_t n, int32_t J, uint32_t seedV, uint32_t 
       }
 }
 
+// hash(v) of Alg. 1 line 4 (reading R5) for every vertex, once per salt setup: the
+// first sweep of every build reads it per edge instead of recomputing Murmur3
+__global__ void k_vertex_hash(int32_t n, uint32_t seedV, uint32_t* __restrict__ HV) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += stride) HV[v] = murmur_word((uint32_t)v, seedV);
+}
+
 // ------------------------------------------------------------------ launchers
+cudaError_t launch_vertex_hash(Ctx& c) {
+    k_vertex_hash<<<grid_for(c, c.n), BLOCK, 0, c.stream>>>(c.n, c.seedV, c.HV);
+    return LAUNCHED(c);
+}
 cudaError_t launch_validate(Ctx& c, const int32_t* off, const int32_t* tgt, const float* prob, int* flags) {
     k_validate<<<grid_for(c, c.m > c.n ? c.m : c.n), BLOCK, 0, c.stream>>>(c.n, c.m, off, tgt, prob, flags);
     return LAUNCHED(c);
@@ -413,10 +469,22 @@ cudaError_t launch_const_check(Ctx& c, const float* prob, int* flag) {
     k_const_check<<<grid_for(c, c.m), BLOCK, 0, c.stream>>>(c.m, prob, flag);
     return LAUNCHED(c);
 }
+// exclusive sum of n int32 (tmp == nullptr: tmp_bytes <- the scratch it needs, like the call below)
 cudaError_t scan_exclusive(Ctx& c, const int32_t* in, int32_t* out, int n, void* tmp, size_t& tmp_bytes) {
-    cudaError_t e = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, in, out, n, c.stream);
-    if (tmp) c.launches++;
-    return e;
+    const int nt = (n + SCAN_T - 1) / SCAN_T;
+    if (!tmp) {
+        tmp_bytes = ((size_t)nt + 1) * sizeof(int32_t);
+        return cudaSuccess;
+    }
+    if (n <= 0) return cudaSuccess;
+    int32_t* part = (int32_t*)tmp;
+    k_scan_reduce<<<nt, BLOCK, 0, c.stream>>>(n, in, part);
+    cudaError_t e = LAUNCHED(c);
+    if (e) return e;
+    k_scan_top<<<1, BLOCK, 0, c.stream>>>(nt, part);
+    if ((e = LAUNCHED(c))) return e;
+    k_scan_down<<<nt, BLOCK, 0, c.stream>>>(n, in, part, out);
+    return LAUNCHED(c);
 }
 cudaError_t launch_build_items(Ctx& c, const int32_t* offs, int4* items, int32_t* nseg, void* tmp, size_t tmp_bytes) {
     int32_t* base = nseg + (c.n + 1);  // nseg holds 2(n+1) entries: counts, then their exclusive scan
@@ -438,145 +506,87 @@ cudaError_t launch_init_registers(Ctx& c) {
     return LAUNCHED(c);
 }
 
-// bits of the composite key (row << KB) | (h >> B): rows need bits(n-1), the bucket 31-B bits
-void prep_key_bits(const Ctx& c, int& KB, int& end_bit, bool& wide) {
-    KB = 31 - c.B0;
-    int nb = 0;
-    while (nb < 31 && ((int64_t)1 << nb) < (int64_t)c.n) nb++;
-    end_bit = nb + KB;
-    wide = end_bit > 32;
-}
+// the row-local bucket ordering applies (constant threshold): every row longer than TAB_MIN is grouped by
+// bucket h >> Bs (<= 2^PREP_KB_MAX buckets) and gets a bucket table
+bool rows_path(const Ctx& c) { return c.sorted_h; }
+int sort_shift(int B0) { return B0 > 31 - PREP_KB_MAX ? B0 : 31 - PREP_KB_MAX; }
 
-// the row-local bucket ordering applies (constant threshold, at most 2^PREP_KB_MAX buckets)
-bool rows_path(const Ctx& c) { return c.sorted_h && 31 - c.B0 <= PREP_KB_MAX; }
-
-template <typename K>
-static cudaError_t prep_rows(Ctx& c, const int32_t* tgt, void** scr, size_t tb, int KB, int end_bit) {
+// constant threshold: in-degrees + scan (roff), forward row sort + reverse scatter (k_rows, k_rows_big),
+// long reverse rows sorted (k_rev_rows); bucket tables of the long rows in both directions
+static cudaError_t prep_rows(Ctx& c, const int32_t* tgt, int32_t* indeg, void** scr, size_t tb) {
     cudaError_t e;
     const int n = c.n;
+    const int B = c.Bs, KB = 31 - c.Bs;
     int32_t* lf = (int32_t*)scr[0];
     int* cnt = (int*)(lf + n);  // [0] long-row count, [1] batch cursor, [2] table count
+    int32_t* cursor = (int32_t*)scr[1];
+    uint2* rtmp = (uint2*)scr[2];
+    k_indeg<<<grid_for(c, c.m), BLOCK, 0, c.stream>>>(c.m, tgt, indeg);
+    if ((e = LAUNCHED(c))) return e;
+    size_t t2 = tb;
+    if ((e = scan_exclusive(c, indeg, c.roff, n + 1, scr[4], t2))) return e;
+    if ((e = cudaMemsetAsync(cursor, 0, (size_t)n * sizeof(int32_t), c.stream))) return e;
     if ((e = cudaMemsetAsync(cnt, 0, 2 * sizeof(int), c.stream))) return e;
     k_list_long<<<grid_for(c, n), BLOCK, 0, c.stream>>>(n, c.off, lf, cnt);
     if ((e = LAUNCHED(c))) return e;
-    RowSortArgs<K> a{};
+    RowSortArgs a{};
     a.n = n;
-    a.B = c.B0;
+    a.B = B;
     a.KB = KB;
     a.off = c.off;
     a.tgt = tgt;
     a.out = c.fwd;
-    a.rkey = (K*)scr[1];
-    a.rval = (uint2*)scr[3];
+    a.roff = c.roff;
+    a.cursor = cursor;
+    a.rev = c.rev;
+    a.rtmp = rtmp;
     a.lst = lf;
     a.lcount = cnt;
     a.batch = cnt + 1;
-    if (c.nbk) {  // forward bucket tables, written by the row sort itself
-        if ((e = setup_tables(c, c.off, c.ftidx, c.ftab, cnt + 2))) return e;
-        a.tidx = c.ftidx;
-        a.tab = c.ftab;
-        a.nbk = c.nbk;
-    }
-    k_rows<K><<<c.num_sms * 8, BLOCK, 0, c.stream>>>(a);
+    if ((e = setup_tables(c, c.off, c.ftidx, c.ftab, cnt + 2))) return e;  // forward tables, written by the row sort
+    a.tidx = c.ftidx;
+    a.tab = c.ftab;
+    a.nbk = c.nbk;
+    k_rows<<<c.num_sms * 8, BLOCK, 0, c.stream>>>(a);
     if ((e = LAUNCHED(c))) return e;
-    k_rows_big<K><<<c.num_sms * 4, BLOCK, 0, c.stream>>>(a);
+    k_rows_big<<<c.num_sms * 4, BLOCK, 0, c.stream>>>(a);
     if ((e = LAUNCHED(c))) return e;
-    e = cub::DeviceRadixSort::SortPairs(scr[4], tb, (K*)scr[1], (K*)scr[2], (uint2*)scr[3], c.rev, (int)c.m, 0, end_bit, c.stream);
-    c.launches += (end_bit + 7) / 8 + 1;
-    if (e) return e;
-    k_row_bounds<K><<<grid_for(c, c.m + 1), BLOCK, 0, c.stream>>>(c.m, n, (const K*)scr[2], KB, c.roff);
-    if ((e = LAUNCHED(c)) || !c.nbk) return e;
-    if ((e = setup_tables(c, c.roff, c.rtidx, c.rtab, cnt + 2))) return e;  // reverse bucket tables
-    k_rev_tabs<K><<<grid_for(c, c.m), BLOCK, 0, c.stream>>>(c.m, (const K*)scr[2], KB, c.rtidx, c.nbk, c.rtab);
+    int h = 0;  // reverse tables: count of long reverse rows (their list in c.t_tabrows)
+    if ((e = setup_tables(c, c.roff, c.rtidx, c.rtab, cnt + 2, &h))) return e;
+    if (h == 0) return cudaSuccess;
+    k_rev_rows<<<c.num_sms * 8, BLOCK, 0, c.stream>>>(h, c.t_tabrows, c.roff, rtmp, c.rev, B, KB, c.rtidx, c.rtab, c.nbk);
     return LAUNCHED(c);
 }
 
-// scratch sizes (bytes) the edge prep needs: [0] src, [1] mark/keys0, [2] keys1, [3] vals, [4] cub temp
+// scratch sizes (bytes) the edge prep needs: [0] long-row list + counters or the edge sources, [1] scatter
+// cursors, [2] long reverse rows before their sort, [3] unused, [4] scan temp
 cudaError_t prep_scratch_sizes(Ctx& c, size_t* sz) {
     const size_t m = (size_t)(c.m ? c.m : 1);
-    int KB, end_bit;
-    bool wide;
-    prep_key_bits(c, KB, end_bit, wide);
-    const size_t ks = wide ? 8 : 4;
-    sz[0] = rows_path(c) ? ((size_t)c.n + 8) * 4 : m * 4;  // long-row list + counters, or the edge sources
-    sz[1] = m * (c.sorted_h ? ks : 4);
-    sz[2] = c.sorted_h ? m * ks : 4;
-    sz[3] = c.sorted_h ? m * 8 : 8;
-    size_t t1 = 0, t2 = 0;
-    cudaError_t e = cub::DeviceScan::InclusiveScan(nullptr, t1, (int32_t*)nullptr, (int32_t*)nullptr, MaxOp(), (int)m, c.stream);
-    if (e) return e;
-    if (c.sorted_h) {
-        if (wide)
-            e = cub::DeviceRadixSort::SortPairs(nullptr, t2, (ull*)nullptr, (ull*)nullptr, (uint2*)nullptr, (uint2*)nullptr,
-                                                (int)m, 0, end_bit, c.stream);
-        else
-            e = cub::DeviceRadixSort::SortPairs(nullptr, t2, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint2*)nullptr,
-                                                (uint2*)nullptr, (int)m, 0, end_bit, c.stream);
-    }
-    if (e) return e;
-    size_t t3 = 0;
-    e = cub::DeviceScan::ExclusiveSum(nullptr, t3, (int32_t*)nullptr, (int32_t*)nullptr, c.n + 1, c.stream);
-    size_t t = t1 > t2 ? t1 : t2;
-    sz[4] = (t > t3 ? t : t3) + 256;
+    sz[0] = rows_path(c) ? ((size_t)c.n + 8) * 4 : m * 4;
+    sz[1] = ((size_t)c.n + 1) * 4;
+    sz[2] = rows_path(c) ? m * 8 : 8;
+    sz[3] = 8;
+    size_t t = 0;
+    cudaError_t e = scan_exclusive(c, nullptr, nullptr, c.n + 1, nullptr, t);
+    sz[4] = t + 256;
     return e;
 }
 
-template <typename K>
-static cudaError_t prep_sorted(Ctx& c, const int32_t* src, const int32_t* tgt, const float* prob, int32_t* indeg,
-                               void** scr, size_t temp_bytes, int KB, int end_bit) {
-    K* k0 = (K*)scr[1];
-    K* k1 = (K*)scr[2];
-    uint2* vals = (uint2*)scr[3];
-    cudaError_t e;
-    // forward: (u << KB | h >> B) -> rows stay in place, ordered by bucket inside
-    k_edge_prep<K, true><<<grid_for(c, c.m), BLOCK, 0, c.stream>>>(c.m, src, tgt, prob, c.B0, KB, k0, vals, nullptr, indeg);
-    if ((e = LAUNCHED(c))) return e;
-    e = cub::DeviceRadixSort::SortPairs(scr[4], temp_bytes, k0, k1, vals, c.fwd, (int)c.m, 0, end_bit, c.stream);
-    c.launches += (end_bit + 7) / 8 + 1;
-    if (e) return e;
-    // reverse: (v << KB | h >> B) with payload {u, h}: the sort is the transpose
-    k_rev_keys<K><<<grid_for(c, c.m), BLOCK, 0, c.stream>>>(c.m, src, c.fwd, c.B0, KB, k0, vals);
-    if ((e = LAUNCHED(c))) return e;
-    e = cub::DeviceRadixSort::SortPairs(scr[4], temp_bytes, k0, k1, vals, c.rev, (int)c.m, 0, end_bit, c.stream);
-    c.launches += (end_bit + 7) / 8 + 1;
-    return e;
-}
-
-// the whole edge prep after validation: fills c.fwd (+fwdT), c.roff, c.rev (+revT)
+// the whole edge prep after validation: fills c.fwd (+fwdT), c.roff, c.rev (+revT), bucket tables
 cudaError_t prep_edges(Ctx& c, const int32_t* tgt, const float* prob, int32_t* indeg, int32_t* scan_tmp_i,
                        void** scr, const size_t* sz) {
     cudaError_t e;
     const int64_t m = c.m;
-    int32_t* src = (int32_t*)scr[0];
-    int32_t* mark = (int32_t*)scr[1];
     size_t tb = sz[4];
     (void)scan_tmp_i;
     if ((e = cudaMemsetAsync(indeg, 0, ((size_t)c.n + 1) * sizeof(int32_t), c.stream))) return e;
-    if (rows_path(c) && c.m > 0) {
-        int KB, end_bit;
-        bool wide;
-        prep_key_bits(c, KB, end_bit, wide);
-        return wide ? prep_rows<ull>(c, tgt, scr, tb, KB, end_bit) : prep_rows<uint32_t>(c, tgt, scr, tb, KB, end_bit);
-    }
+    if (rows_path(c) && c.m > 0) return prep_rows(c, tgt, indeg, scr, tb);
+    // per-edge thresholds (weighted cascade): input row order, atomic-cursor transpose
+    int32_t* src = (int32_t*)scr[0];
     if (m > 0) {
-        if ((e = cudaMemsetAsync(mark, 0, (size_t)m * sizeof(int32_t), c.stream))) return e;
-        k_row_markers<<<grid_for(c, c.n), BLOCK, 0, c.stream>>>(c.n, c.off, mark);
+        k_src<<<grid_for(c, (int64_t)c.n * 32), BLOCK, 0, c.stream>>>(c.n, c.off, src);
         if ((e = LAUNCHED(c))) return e;
-        if ((e = cub::DeviceScan::InclusiveScan(scr[4], tb, mark, src, MaxOp(), (int)m, c.stream))) return e;
-        c.launches += 2;
-    }
-    if (c.sorted_h) {
-        int KB, end_bit;
-        bool wide;
-        prep_key_bits(c, KB, end_bit, wide);
-        e = wide ? prep_sorted<ull>(c, src, tgt, prob, indeg, scr, tb, KB, end_bit)
-                 : prep_sorted<uint32_t>(c, src, tgt, prob, indeg, scr, tb, KB, end_bit);
-        if (e) return e;
-        size_t t2 = tb;
-        return scan_exclusive(c, indeg, c.roff, c.n + 1, scr[4], t2);
-    }
-    if (m > 0) {
-        k_edge_prep<uint32_t, false><<<grid_for(c, m), BLOCK, 0, c.stream>>>(m, src, tgt, prob, 0, 0, nullptr, c.fwd, c.fwdT, indeg);
+        k_edge_prep<<<grid_for(c, m), BLOCK, 0, c.stream>>>(m, src, tgt, prob, c.fwd, c.fwdT, indeg);
         if ((e = LAUNCHED(c))) return e;
     }
     size_t t2 = tb;

@@ -394,89 +394,77 @@ __global__ void k_compact(int32_t n, int J, int slice_min, const uint32_t* __res
     }
 }
 
-// warp per long row: one slice per non-zero 32-simulation word of the vertex's mask (change mask
-// for sweeps, Delta for BFS levels), trimmed so slices do not overlap, cut into <= SEG items.
-// More than MAX_SLICES non-zero words: the slices of G = W / MAX_SLICES consecutive words are
-// merged (their union plus the buckets between them), which bounds a row's items by
-// ceil(len / SEG) + MAX_SLICES (the item buffers' capacity, im_abi.cu).  whole_dense (BFS): with
-// at least 3/4 of the words set the whole row is emitted without the binary searches.
-__global__ void k_slices_big(int J, int B, const uint32_t* __restrict__ Xs, const int32_t* __restrict__ big,
-                             const uint32_t* __restrict__ mask, const int32_t* __restrict__ offs, const uint2* __restrict__ rec,
-                             int4* __restrict__ items, IterCounters* ctr, bool whole_dense, const int32_t* __restrict__ tidx,
-                             const int32_t* __restrict__ tab, int nbk) {
-    const int lane = threadIdx.x & 31, W = J >> 5;
+// Bucket slices (rows with a bucket offset table, im_prep.cu): the edges of a bucket-ordered row whose
+// candidate windows can hold simulation j are exactly its bucket Xs[j] >> B (Eq. 5: (X xor h) < T <= 2^B
+// implies X >> B == h >> B).  A warp per long row marks the buckets of the set simulations of the row's
+// mask (the change mask for a sweep, Delta for a BFS level) in a 2^KB-bit set, turns its runs of
+// consecutive buckets into row slices (two table reads each) and cuts them into <= SEG items.  More
+// than BSL runs, or runs covering >= 3/4 of the buckets: the whole row (the per-edge test drops the
+// rest).  Items per row <= ceil(len / SEG) + BSL (buffer capacity, im_abi.cu).
+__global__ void k_slices_buckets(int J, int B, int KB, const uint32_t* __restrict__ Xs, const int32_t* __restrict__ big,
+                                 const uint32_t* __restrict__ mask, const int32_t* __restrict__ offs, int4* __restrict__ items,
+                                 IterCounters* ctr, const int32_t* __restrict__ tidx, const int32_t* __restrict__ tab, int nbk) {
+    __shared__ uint32_t sBm[BLOCK / 32][8];
+    __shared__ int sRs[BLOCK / 32][BSL], sRe[BLOCK / 32][BSL];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, W = J >> 5;
+    const int NBW = ((1 << KB) + 31) >> 5;  // words of the bucket set (<= 8)
     const int nb = ctr->big;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < nb; i += nwarps) {
         const int v = big[i];
         const int rb = offs[v], re = offs[v + 1];
-        int b0 = re, e0 = re;
+        const int t = __ldg(&tidx[v]);
+        if (lane < 8) sBm[wib][lane] = 0u;
+        __syncwarp();
         const uint32_t m = lane < W ? mask[(size_t)v * W + lane] : 0u;
-        const int nzw = __popc(__ballot_sync(IM_FULL, m != 0u));
-        if (whole_dense && 4 * nzw >= 3 * W) {  // the per-edge test of the level drops the rest
-            const int ns = (re - rb + SEG - 1) / SEG;
+        for (uint32_t tt = m; tt; tt &= tt - 1) {
+            const uint32_t b = __ldg(&Xs[32 * lane + __ffs(tt) - 1]) >> B;
+            atomicOr(&sBm[wib][b >> 5], 1u << (b & 31));
+        }
+        __syncwarp();
+        const uint32_t x = lane < NBW ? sBm[wib][lane] : 0u;
+        uint32_t prev = __shfl_up_sync(IM_FULL, x, 1), next = __shfl_down_sync(IM_FULL, x, 1);
+        if (lane == 0) prev = 0u;
+        if (lane == 31) next = 0u;
+        const uint32_t starts = x & ~((x << 1) | (prev >> 31)), ends = x & ~((x >> 1) | (next << 31));
+        const int ns = __popc(starts), ne = __popc(ends);
+        const int R = __reduce_add_sync(IM_FULL, ns), cov = __reduce_add_sync(IM_FULL, __popc(x));
+        if (R == 0) continue;
+        if (t < 0 || R > BSL || 4 * cov >= 3 * (1 << KB)) {  // the whole row
+            const int nsg = (re - rb + SEG - 1) / SEG;
             int pos = 0;
             if (lane == 0) {
-                pos = atomicAdd(&ctr->next_items, ns);
+                pos = atomicAdd(&ctr->next_items, nsg);
                 atomicAdd(&ctr->next_edges, (ull)(re - rb));
             }
             pos = __shfl_sync(IM_FULL, pos, 0);
-            for (int k = lane; k < ns; k += 32) items[pos + k] = make_int4(v, rb + k * SEG, min(rb + (k + 1) * SEG, re), 0);
+            for (int k = lane; k < nsg; k += 32) items[pos + k] = make_int4(v, rb + k * SEG, min(rb + (k + 1) * SEG, re), 0);
             continue;
         }
-        if (lane < W) {
-            if (m) {
-                int sa = 32 * lane + __ffs(m) - 1, sb = 32 * lane + 31 - __clz(m);
-                const uint32_t kbl = __ldg(&Xs[sa]) >> B, kbh = (__ldg(&Xs[sb]) >> B) + 1u;
-                const int t = tidx ? __ldg(&tidx[v]) : -1;
-                if (t >= 0) {  // bucket offset table of the row (im_prep.cu)
-                    b0 = __ldg(&tab[(int64_t)t * nbk + kbl]);
-                    e0 = __ldg(&tab[(int64_t)t * nbk + kbh]);
-                } else {
-                    b0 = lower_bound_h(rec, rb, re, kbl << B);
-                    e0 = lower_bound_h(rec, b0, re, kbh << B);
-                }
-            }
+        // the k-th run starts at the k-th start bit and ends at the k-th end bit
+        int sp = warp_incl_scan(ns, lane) - ns, ep = warp_incl_scan(ne, lane) - ne;
+        for (uint32_t tt = starts; tt; tt &= tt - 1) sRs[wib][sp++] = 32 * lane + __ffs(tt) - 1;
+        for (uint32_t tt = ends; tt; tt &= tt - 1) sRe[wib][ep++] = 32 * lane + __ffs(tt) - 1;
+        __syncwarp();
+        int b0 = 0, len = 0;
+        if (lane < R) {
+            const int32_t* tb = tab + (int64_t)t * nbk;
+            b0 = __ldg(&tb[sRs[wib][lane]]);
+            len = __ldg(&tb[sRe[wib][lane] + 1]) - b0;
         }
-        if (nzw > MAX_SLICES) {  // union of the slices of each group of G consecutive words, kept by its first lane
-            const int G = W / MAX_SLICES;  // W and MAX_SLICES are powers of two
-            int gb = b0 < e0 ? b0 : INT_MAX, ge = b0 < e0 ? e0 : INT_MIN;
-            for (int o = 1; o < G; o <<= 1) {
-                gb = min(gb, __shfl_xor_sync(IM_FULL, gb, o));
-                ge = max(ge, __shfl_xor_sync(IM_FULL, ge, o));
-            }
-            if ((lane & (G - 1)) == 0 && gb < ge) {
-                b0 = gb;
-                e0 = ge;
-            } else {
-                b0 = e0 = re;
-            }
-        }
-        // trim against the furthest end of the lanes before (slice bounds grow with the word index)
-        int pe = b0 < e0 ? e0 : rb;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            int y = __shfl_up_sync(IM_FULL, pe, o);
-            if (lane >= o) pe = max(pe, y);
-        }
-        int prev_end = __shfl_up_sync(IM_FULL, pe, 1);
-        if (lane == 0) prev_end = rb;
-        if (b0 < prev_end) b0 = prev_end;
-        int len = b0 < e0 ? e0 - b0 : 0;
-        int ns = (len + SEG - 1) / SEG;
-        int ninc = warp_incl_scan(ns, lane);
-        int ntot = __shfl_sync(IM_FULL, ninc, 31);
-        int es = len;
-#pragma unroll
-        for (int o = 16; o; o >>= 1) es += __shfl_xor_sync(IM_FULL, es, o);
+        const int nsl = (len + SEG - 1) / SEG;
+        const int ninc = warp_incl_scan(nsl, lane);
+        const int ntot = __shfl_sync(IM_FULL, ninc, 31);
+        const int es = __reduce_add_sync(IM_FULL, len);
         int pos = 0;
         if (lane == 0 && ntot) {
             pos = atomicAdd(&ctr->next_items, ntot);
             atomicAdd(&ctr->next_edges, (ull)es);
         }
         pos = __shfl_sync(IM_FULL, pos, 0);
-        int p = pos + ninc - ns;
+        int p = pos + ninc - nsl;
         for (int s0 = b0; s0 < b0 + len; s0 += SEG) items[p++] = make_int4(v, s0, min(s0 + SEG, b0 + len), 0);
+        __syncwarp();
     }
 }
 
@@ -552,9 +540,11 @@ cudaError_t launch_compact(Ctx& c, const uint32_t* bits_new, uint32_t* bits_clea
 cudaError_t launch_slices_big(Ctx& c, const int32_t* big, const uint32_t* mask, const int32_t* offs, const uint2* rec,
                               int4* items_out, IterCounters* ctr, bool whole_dense) {
     const bool fw = rec == c.fwd;
-    k_slices_big<<<c.num_sms * 4, BLOCK, 0, c.stream>>>(c.J, c.B0, c.Xs, big, mask, offs, rec, items_out, ctr, whole_dense,
-                                                        c.nbk ? (fw ? c.ftidx : c.rtidx) : nullptr, fw ? c.ftab : c.rtab, c.nbk);
+    (void)whole_dense;
+    k_slices_buckets<<<c.num_sms * 4, BLOCK, 0, c.stream>>>(c.J, c.Bs, 31 - c.Bs, c.Xs, big, mask, offs, items_out, ctr,
+                                                           fw ? c.ftidx : c.rtidx, fw ? c.ftab : c.rtab, c.nbk);
     return LAUNCHED(c);
+
 }
 
 int occupancy_sweep(int* blocks_per_sm) {

@@ -458,6 +458,22 @@ def test_init_rows_vs_library_hash():
     assert not M[mask].any()
 
 
+def test_rebuilt_register_definition_vs_bruteforce():
+    """or_rebuilt_register (sampled definition of a rebuilt register, used at full size) vs the closure-based
+    registers on the residual samples with R_S = R_G(seed prefix) blocked (Alg. 1 lines 21-25, R12)."""
+    rng = np.random.default_rng(1515)
+    for g in range(12):
+        n = int(rng.integers(10, 90))
+        off, tgt, pr = brute.random_graph(rng, n, 3 * n, None if g % 3 == 0 else float(rng.choice([0.3, 0.6])))
+        J, seed = 32, int(rng.integers(0, 2**32))
+        seeds = rng.choice(n, int(rng.integers(1, 4)), replace=False).astype(np.int32)
+        blocked = brute.reach_masks(n, off, tgt, pr, J, seed, seeds)
+        want = brute.registers(n, off, tgt, pr, J, seed, blocked=blocked)
+        us = rng.integers(0, n, 200)
+        js = rng.integers(0, J, 200)
+        assert np.array_equal(oracle.rebuilt_register(n, off, tgt, pr, J, seed, seeds, us, js), want[us, js]), g
+
+
 def test_rebuilt_registers_vs_bruteforce():
     """After a rebuild (t = 0, K = 2) the registers are the reach-max on G_j^S with S's reach blocked
     (lines 21-24), and no register exceeds its first-build value."""
