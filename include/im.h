@@ -36,7 +36,7 @@ extern "C" {
 #define IM_ESTATE (-2) /* wrong call order (e.g. im_estimate before im_build_sketches) */
 #define IM_ENOMEM (-3) /* device or host allocation failed */
 #define IM_ECUDA (-4)  /* CUDA error, or no sm_100 device */
-#define IM_ECOMM (-5)  /* the allreduce hook (im_set_allreduce) returned non-zero */
+#define IM_ECOMM (-5)  /* a collective of the communicator (im_set_comm / im_comm_nccl_init) failed */
 
 #define IM_DTYPE_I32 0 /* allreduce element types */
 #define IM_DTYPE_I64 1
@@ -119,17 +119,24 @@ int im_build_sketches(int32_t J, uint64_t seed);
  * Alg. 1 are independent samples (simulation j only reads salt
  * X_j and the hash of j), so a job of J_total simulations can be split over ranks (one
  * process and one GPU each), rank r holding simulations [j0, j1).  Every rank loads the
- * same graph, calls im_set_allreduce with a hook over all ranks, then
+ * same graph, installs a communicator (im_comm_nccl_init, or im_set_comm), then calls
  * im_build_sketches_shard with its range; im_estimate and im_select_seeds* are then
  * collective calls that every rank must make with the same arguments, and all ranks
  * return the same seeds, scores, step log and estimates as one unsharded context with
  * J = J_total would.  Per-rank outputs (im_get_registers / rows / reach) cover the
- * rank's own simulations, columns j - j0.
+ * rank's own simulations, columns j - j0.  Builds and BFS never communicate.
  *
- * Exchanged per greedy step (all in-place SUMs): the packed per-vertex argmax values
- * (gain + (not fully visited) << 24, n int32 for a full pass, list-length int32 for a
- * lazy one), the integer score of the chosen vertex (1 int64) and the sigma count
- * (1 int64); im_estimate exchanges n int32 register sums.
+ * Exchanged per greedy step (Alg. 1 line 10, 12, 14):
+ *   full argmax pass : reduce-scatter (SUM) of the packed per-vertex values
+ *                      gain_local + (not fully visited locally) << 24 (n int32, each rank
+ *                      receives its vertex slice of ceil(n / nranks)); a local argmax over
+ *                      the slice; an all-reduce (MAX) of the 64-bit key (gain << 32 | ~v); an
+ *                      all-reduce (SUM) of the gain histogram (4096 int32); all-gathers of the
+ *                      candidate-list lengths (1 int32) and lists (<= slice int32 each)
+ *   lazy argmax pass : all-reduce (SUM) of the packed values of the candidate list
+ *   chosen vertex    : all-reduce (SUM) of its integer score (1 int64)
+ *   sigma            : all-reduce (SUM) of the visited count (1 int64)
+ * im_estimate exchanges the n int32 register sums (all-reduce SUM).
  *
  * J_total  : multiple of 32 in [32, IM_MAX_J_TOTAL]; salts X_0..X_{J_total-1} are drawn
  *            as in im_build_sketches(J_total, seed) and this context keeps [j0, j1).
@@ -138,16 +145,45 @@ int im_build_sketches(int32_t J, uint64_t seed);
  */
 int im_build_sketches_shard(int32_t J_total, uint64_t seed, int32_t j0, int32_t j1);
 
+#define IM_OP_SUM 0 /* collective reduction operators */
+#define IM_OP_MAX 1
+
 /*
- * Allreduce hook of a sharded job: fn(buf, count, dtype, user) must replace the
- * `count` elements (IM_DTYPE_I32 / IM_DTYPE_I64) at DEVICE pointer buf (on the
- * library's device) by their sum over all ranks and return 0 once the result is in
- * buf.  The library's stream is synchronised before each call.  Non-zero -> IM_ECOMM.
- * fn = NULL (the default) turns sharding off: single-context behaviour, no calls.
- * A sharded context must run with the hook set during im_estimate / im_select_seeds*.
+ * Communicator of a sharded job: three collectives on DEVICE buffers of the library's device.
+ *   allreduce(buf, count, dtype, op)      in place, op IM_OP_SUM / IM_OP_MAX
+ *   reduce_scatter(send, recv, recvcount, dtype)   SUM; send holds nranks * recvcount elements,
+ *                                         rank r receives elements [r * recvcount, (r+1) * recvcount)
+ *   allgather(send, recv, sendcount, dtype)        recv[r * sendcount + i] = send of rank r [i]
+ * dtype: IM_DTYPE_I32 / IM_DTYPE_I64.  stream: the library's cudaStream_t.  Each returns 0 on
+ * success (non-zero -> IM_ECOMM).  stream_ordered = 1: the operation is enqueued on `stream`
+ * (NCCL semantics); 0: the library synchronises its stream first and the call returns with the
+ * result in place (host-staged transports, e.g. gloo).  1 <= nranks < 256 (the packed argmax value
+ * counts in-pool ranks in 8 bits), 0 <= rank < nranks.  The struct is copied.
  */
-typedef int (*im_allreduce_fn)(void *buf, int64_t count, int32_t dtype, void *user);
-int im_set_allreduce(im_allreduce_fn fn, void *user);
+typedef struct {
+    int32_t rank, nranks;
+    int32_t stream_ordered;
+    int32_t pad;
+    int (*allreduce)(void *buf, int64_t count, int32_t dtype, int32_t op, void *stream, void *user);
+    int (*reduce_scatter)(const void *send, void *recv, int64_t recvcount, int32_t dtype, void *stream, void *user);
+    int (*allgather)(const void *send, void *recv, int64_t sendcount, int32_t dtype, void *stream, void *user);
+    void *user;
+} im_comm;
+
+/* Install a caller-implemented communicator (copied); NULL removes it (unsharded behaviour).  A sharded
+ * context must have one installed during im_estimate / im_select_seeds*.  IM_EINVAL on bad fields. */
+int im_set_comm(const im_comm *comm);
+
+/*
+ * The library's own NCCL communicator (NCCL over NVLink / NVSwitch; libnccl.so.2 is loaded at the first
+ * call, no build-time dependency).  im_comm_nccl_unique_id writes the 128-byte ncclUniqueId (rank 0
+ * calls it and shares the bytes with the other ranks, e.g. over torch.distributed); every rank then
+ * calls im_comm_nccl_init with the same id on its own device.  The collectives are enqueued on the
+ * library's stream (stream_ordered), with no host round trip and no Python in the exchange.
+ * IM_ECOMM when NCCL is unavailable or fails; im_set_comm(NULL) / im_free release it.
+ */
+int im_comm_nccl_unique_id(void *out_id128);
+int im_comm_nccl_init(const void *id128, int32_t rank, int32_t nranks);
 
 /* e_v = 2^{mean_j M_v[j]} / 0.77351 for every vertex (Eq. 2, R8).  out: HOST double[n]. */
 int im_estimate(double *out);
@@ -218,7 +254,8 @@ int im_set_stream(void *cuda_stream);
 int64_t im_kernel_launch_count(void);
 void im_free(void);
 const char *im_last_error(void);
-/* ABI version (major*100 + minor): 101 adds sharding (im_build_sketches_shard, im_set_allreduce), 102 im_set_policy */
+/* ABI version (major*100 + minor): 101 adds sharding (im_build_sketches_shard), 102 im_set_policy,
+ * 103 replaces the allreduce hook by the communicator (im_set_comm, im_comm_nccl_*) */
 int32_t im_version(void);
 
 #ifdef __cplusplus

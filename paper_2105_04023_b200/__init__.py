@@ -72,9 +72,24 @@ SIGNATURES = {
     "im_version": (_i32, []),
 }
 
-ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p)
+# communicator of a sharded job (include/im.h im_comm)
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, _vp, _i64, _i32, _i32, _vp, _vp)
+RSCATTER_FN = ctypes.CFUNCTYPE(ctypes.c_int, _vp, _vp, _i64, _i32, _vp, _vp)
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, _vp, _vp, _i64, _i32, _vp, _vp)
+
+
+class im_comm(ctypes.Structure):
+    _fields_ = [
+        ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32), ("stream_ordered", ctypes.c_int32), ("pad", ctypes.c_int32),
+        ("allreduce", ALLREDUCE_FN), ("reduce_scatter", RSCATTER_FN), ("allgather", ALLGATHER_FN), ("user", _vp),
+    ]
+
+
+IM_OP_SUM, IM_OP_MAX = 0, 1
 SIGNATURES["im_build_sketches_shard"] = (ctypes.c_int, [_i32, _u64, _i32, _i32])
-SIGNATURES["im_set_allreduce"] = (ctypes.c_int, [ALLREDUCE_FN, _vp])
+SIGNATURES["im_set_comm"] = (ctypes.c_int, [_vp])
+SIGNATURES["im_comm_nccl_unique_id"] = (ctypes.c_int, [_vp])
+SIGNATURES["im_comm_nccl_init"] = (ctypes.c_int, [_vp, _i32, _i32])
 SIGNATURES["im_set_policy"] = (ctypes.c_int, [_f64, _f64, _f64])
 SIGNATURES["im_evaluate"] = (ctypes.c_int, [_i32, _vp, _u64, _i64, _i64, _vp])
 IM_ECOMM = -5
@@ -130,25 +145,44 @@ class Library:
     def im_build_sketches_shard(self, J_total: int, seed: int, j0: int, j1: int) -> None:
         self._check(self.L.im_build_sketches_shard(J_total, seed & 0xFFFFFFFFFFFFFFFF, j0, j1))
 
-    def im_set_allreduce(self, fn) -> None:
-        """fn(ptr: int, count: int, dtype: int) -> None sums `count` IM_DTYPE_* elements at device
-        pointer ptr over all ranks in place (see shard.py); None turns sharding off."""
-        if fn is None:
+    def im_set_comm(self, comm) -> None:
+        """Install a host-implemented communicator (None removes it).  `comm` provides rank, nranks and
+        allreduce(ptr, count, dtype, op), reduce_scatter(send, recv, recvcount, dtype),
+        allgather(send, recv, sendcount, dtype) on device pointers, each returning once the result is in
+        place (stream_ordered = 0: the library drains its stream before every call); see shard.py."""
+        if comm is None:
             self._hook = None
-            self._check(self.L.im_set_allreduce(ALLREDUCE_FN(), None))
+            self._check(self.L.im_set_comm(None))
             return
 
-        def tramp(ptr, count, dtype, user):
-            try:
-                fn(int(ptr), int(count), int(dtype))
-                return 0
-            except Exception as e:  # reported as IM_ECOMM by the library
-                import sys
-                print(f"[im] allreduce hook failed: {e!r}", file=sys.stderr)
-                return 1
+        def guard(f):
+            def g(*args):
+                try:
+                    f(*[int(a) if a is not None else 0 for a in args[:-2]])
+                    return 0
+                except Exception as e:  # reported as IM_ECOMM by the library
+                    import sys
+                    print(f"[im] collective failed: {e!r}", file=sys.stderr)
+                    return 1
+            return g
 
-        self._hook = ALLREDUCE_FN(tramp)
-        self._check(self.L.im_set_allreduce(self._hook, None))
+        c = im_comm()
+        c.rank, c.nranks, c.stream_ordered = int(comm.rank), int(comm.nranks), 0
+        c.allreduce = ALLREDUCE_FN(guard(comm.allreduce))
+        c.reduce_scatter = RSCATTER_FN(guard(comm.reduce_scatter))
+        c.allgather = ALLGATHER_FN(guard(comm.allgather))
+        self._hook = c  # the callbacks must outlive the installation
+        self._check(self.L.im_set_comm(ctypes.byref(c)))
+
+    def im_comm_nccl_unique_id(self) -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        self._check(self.L.im_comm_nccl_unique_id(buf))
+        return buf.raw
+
+    def im_comm_nccl_init(self, unique_id: bytes, rank: int, nranks: int) -> None:
+        """The library's own NCCL communicator (stream-ordered collectives, no Python in the exchange)."""
+        buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+        self._check(self.L.im_comm_nccl_init(buf, int(rank), int(nranks)))
 
     def im_set_policy(self, eps_l: float = float("nan"), eps_g: float = float("nan"), eps_c: float = 0.0) -> None:
         """Alg. 1 thresholds used by im_select_seeds (NaN: its err_threshold) and Alg. 2's early exit."""

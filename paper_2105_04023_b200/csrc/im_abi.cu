@@ -142,13 +142,13 @@ void reset_graph_state() {
 }
 
 void release_all() {
-    dfree(g.Xs); dfree(g.s12); dfree(g.permd); dfree(g.HV); dfree(g.M); dfree(g.vis); dfree(g.vd);
+    dfree(g.Xs); dfree(g.s12); dfree(g.permd); dfree(g.M); dfree(g.vis); dfree(g.vd);
     for (int i = 0; i < 2; i++) { dfree(g.items[i]); dfree(g.bits[i]); dfree(g.cm[i]); dfree(g.delta[i]); dfree(g.bitems[i]); dfree(g.bvl[i]); }
     dfree(g.inS); dfree(g.MS); dfree(g.btag); dfree(g.nbits); dfree(g.gain); dfree(g.big); dfree(g.list); dfree(g.lcount); dfree(g.hist);
     dfree(g.off); dfree(g.fwd); dfree(g.fwdT); dfree(g.roff); dfree(g.rev); dfree(g.revT); dfree(g.ritems); dfree(g.fbig);
     dfree(g.ftidx); dfree(g.rtidx); dfree(g.ftab); dfree(g.rtab); dfree(g.t_tabrows);
     dfree(g.ctr); dfree(g.rec); dfree(g.sbo); dfree(g.varsigma); dfree(g.key); dfree(g.first); dfree(g.sigma_count);
-    dfree(g.lval); dfree(g.sigma_g); dfree(g.bcount); dfree(g.Mold);
+    dfree(g.lval); dfree(g.sigma_g); dfree(g.bcount); dfree(g.Mold); dfree(g.gslice); dfree(g.llist); dfree(g.lcnt_all);
     dfree(g.ev_vis); dfree(g.ev_nbits); dfree(g.ev_ctr); dfree(g.ev_count);
     for (int i = 0; i < 2; i++) { dfree(g.ev_delta[i]); dfree(g.ev_items[i]); dfree(g.ev_vl[i]); }
     dfree(g.t_flags); dfree(g.t_indeg); dfree(g.t_nseg); dfree(g.t_scan); dfree(g.t_off); dfree(g.t_tgt); dfree(g.t_prob);
@@ -162,15 +162,39 @@ int sync() {
     return 0;
 }
 
-// Simulation sharding: in-place SUM over all ranks of `count` elements at the
-// device pointer `buf`, through the caller's hook (im_set_allreduce).  The stream is drained first;
-// the hook returns after the reduced values are in `buf`.  No-op when unsharded.
-int allreduce(void* buf, int64_t count, int32_t dtype) {
-    if (!g.ar) return 0;
-    TRY(sync());
-    int r = g.ar(buf, count, dtype, g.ar_user);
-    if (r) return fail(IM_ECOMM, "allreduce hook failed (%d) on %lld elements", r, (long long)count);
+// Simulation sharding: the collectives of the installed communicator.  A host-staged
+// communicator (stream_ordered = 0) gets a drained stream and returns with the result in place; NCCL
+// (stream_ordered = 1) is enqueued on the library's stream.  No-ops when unsharded.
+int coll_pre() {
+    if (!g.comm.stream_ordered) TRY(sync());
     return 0;
+}
+int c_allreduce(void* buf, int64_t count, int32_t dtype, int32_t op) {
+    if (!g.ar) return 0;
+    TRY(coll_pre());
+    int r = g.comm.allreduce(buf, count, dtype, op, (void*)g.stream, g.comm.user);
+    if (r) return fail(IM_ECOMM, "allreduce (%s) of %lld elements failed (%d)", op == IM_OP_MAX ? "max" : "sum", (long long)count, r);
+    return 0;
+}
+int c_reduce_scatter(const void* send, void* recv, int64_t recvcount, int32_t dtype) {
+    TRY(coll_pre());
+    int r = g.comm.reduce_scatter(send, recv, recvcount, dtype, (void*)g.stream, g.comm.user);
+    if (r) return fail(IM_ECOMM, "reduce-scatter of %lld elements per rank failed (%d)", (long long)recvcount, r);
+    return 0;
+}
+int c_allgather(const void* send, void* recv, int64_t sendcount, int32_t dtype) {
+    TRY(coll_pre());
+    int r = g.comm.allgather(send, recv, sendcount, dtype, (void*)g.stream, g.comm.user);
+    if (r) return fail(IM_ECOMM, "allgather of %lld elements per rank failed (%d)", (long long)sendcount, r);
+    return 0;
+}
+int allreduce(void* buf, int64_t count, int32_t dtype) { return c_allreduce(buf, count, dtype, IM_OP_SUM); }
+
+void comm_release() {
+    if (g.nccl) nccl_release(g.nccl);
+    g.nccl = nullptr;
+    g.comm = im_comm{};
+    g.ar = false;
 }
 
 // read `bytes` of device memory to the pinned scratch (synchronous)
@@ -300,7 +324,6 @@ int alloc_sketch_state(int32_t J) {
     TRY(dalloc(g.Xs, (size_t)J));
     TRY(dalloc(g.s12, 4097));
     TRY(dalloc(g.permd, (size_t)J));
-    TRY(dalloc(g.HV, (size_t)g.n));
     TRY(dalloc(g.M, n * (size_t)J + 65536));  // + tail padding read by the TMA argmax tiles
     TRY(dalloc(g.vis, n * W + 16384));
     TRY(dalloc(g.vd, n * W));
@@ -322,9 +345,19 @@ int alloc_sketch_state(int32_t J) {
     TRY(dalloc(g.inS, n));
     TRY(dalloc(g.MS, (size_t)J));
     TRY(dalloc(g.big, n));
-    TRY(dalloc(g.gain, n));
-    TRY(dalloc(g.list, n));
-    TRY(dalloc(g.lval, n));
+    // sharded: the reduce-scatter needs nranks * S packed values (S = ceil(n / nranks)), and the gathered
+    // candidate list holds nranks lists of <= S entries
+    const int64_t nr = g.ar ? g.comm.nranks : 1, S = ((int64_t)n + nr - 1) / nr;
+    TRY(dalloc(g.gain, (size_t)(nr * S)));
+    TRY(dalloc(g.list, (size_t)(nr * S)));
+    TRY(dalloc(g.lval, (size_t)(nr * S)));
+    if (g.ar) {
+        TRY(dalloc(g.gslice, (size_t)S));
+        TRY(dalloc(g.llist, (size_t)S));
+        TRY(dalloc(g.lcnt_all, (size_t)nr));
+        CK(cudaMemsetAsync(g.gain, 0, (size_t)(nr * S) * sizeof(int32_t), g.stream));  // the pad beyond n stays 0
+    }
+    g.S = S;
     TRY(dalloc(g.lcount, 2));
     TRY(dalloc(g.bcount, (size_t)g.num_sms * 8));
     TRY(dalloc(g.hist, 4096));
@@ -361,7 +394,6 @@ int setup_salts(int32_t Jt, int32_t j0, int32_t J, uint64_t seed) {
     std::vector<int32_t> gj(J);
     for (int i = 0; i < J; i++) gj[i] = g.perm[i] + j0;
     CK(cudaMemcpyAsync(g.permd, gj.data(), J * sizeof(int32_t), cudaMemcpyHostToDevice, g.stream));
-    CK(launch_vertex_hash(g));
     TRY(sync());  // host vectors go out of scope
     g.seed = seed;
     g.Jt = Jt;
@@ -490,7 +522,7 @@ int build_fresh() {
 // =========================================================== C ABI
 extern "C" {
 
-int32_t im_version(void) { return 102; }
+int32_t im_version(void) { return 103; }
 
 const char* im_last_error(void) { return g_err.c_str(); }
 
@@ -507,6 +539,7 @@ int im_set_stream(void* s) {
 void im_free(void) {
     if (g.dev >= 0) cudaStreamSynchronize(g.stream);
     release_all();
+    comm_release();
 }
 
 int im_load_csr(int32_t n, const int32_t* offsets, const int32_t* targets, const float* probs) {
@@ -578,14 +611,52 @@ int im_build_sketches(int32_t J, uint64_t seed) {
     return im_build_sketches_shard(J, seed, 0, J);
 }
 
-int im_set_allreduce(im_allreduce_fn fn, void* user) {
-    g.ar = fn;
-    g.ar_user = fn ? user : nullptr;
+int im_set_comm(const im_comm* comm) {
+    if (comm) {
+        if (comm->nranks < 1 || comm->nranks >= 256 || comm->rank < 0 || comm->rank >= comm->nranks)
+            return fail(IM_EINVAL, "communicator: need 1 <= nranks < 256 and 0 <= rank < nranks (got rank %d of %d)", comm->rank,
+                        comm->nranks);
+        if (!comm->allreduce || !comm->reduce_scatter || !comm->allgather) return fail(IM_EINVAL, "communicator: null collective");
+    }
+    if (g.dev >= 0) TRY(sync());
+    comm_release();
+    if (comm) {
+        g.comm = *comm;
+        g.ar = true;
+    }
+    g.S = 0;  // argmax buffers are re-sized for the new rank count by the next build
+    return 0;
+}
+
+int im_comm_nccl_unique_id(void* out_id128) {
+    if (!out_id128) return fail(IM_EINVAL, "null output");
+    char err[256];
+    if (nccl_unique_id(out_id128, err, sizeof err)) return fail(IM_ECOMM, "%s", err);
+    return 0;
+}
+
+int im_comm_nccl_init(const void* id128, int32_t rank, int32_t nranks) {
+    TRY(ensure_device());
+    if (!id128) return fail(IM_EINVAL, "null unique id");
+    if (nranks < 1 || nranks >= 256 || rank < 0 || rank >= nranks)
+        return fail(IM_EINVAL, "need 1 <= nranks < 256 and 0 <= rank < nranks (got rank %d of %d)", rank, nranks);
+    TRY(sync());
+    comm_release();
+    im_comm c;
+    void* st = nullptr;
+    char err[256];
+    if (nccl_init(id128, rank, nranks, &c, &st, err, sizeof err)) return fail(IM_ECOMM, "%s", err);
+    g.comm = c;
+    g.nccl = st;
+    g.ar = true;
+    g.S = 0;
     return 0;
 }
 
 static int shard_check(const char* what) {
-    if (g.J != g.Jt && !g.ar) return fail(IM_ESTATE, "%s: sharded sketches (%d of %d simulations) need im_set_allreduce", what, g.J, g.Jt);
+    if (g.J != g.Jt && !g.ar) return fail(IM_ESTATE, "%s: sharded sketches (%d of %d simulations) need a communicator (im_set_comm)", what, g.J, g.Jt);
+    if (g.ar && g.S != ((int64_t)g.n + g.comm.nranks - 1) / g.comm.nranks)
+        return fail(IM_ESTATE, "%s: the communicator changed after the build; rebuild the sketches", what);
     return 0;
 }
 
@@ -658,8 +729,8 @@ int im_select_seeds_ex(int32_t K, double eps_l, double eps_g, int32_t* out_seeds
         // line 10: argmax over the pool (exact lazy evaluation, im_kernels.cu "a6")
         if (!need_full) {
             CK(launch_argmax_list(g, list_len));
-            if (g.ar) {  // sharded: sum the packed local values, then decode (im_kernels.cu)
-                TRY(allreduce(g.lval, list_len, IM_DTYPE_I32));
+            if (g.ar) {  // sharded: sum the packed local values of the list, then decode (im_kernels.cu)
+                TRY(c_allreduce(g.lval, list_len, IM_DTYPE_I32, IM_OP_SUM));
                 CK(launch_argmax_list_finish(g, list_len));
             }
             ull hk;
@@ -672,12 +743,33 @@ int im_select_seeds_ex(int32_t K, double eps_l, double eps_g, int32_t* out_seeds
         }
         if (need_full) {
             CK(launch_argmax_full(g, pool_check));
-            TRY(allreduce(g.gain, g.n, IM_DTYPE_I32));
-            CK(launch_argmax_full_finish(g, T));
-            int lc[2];
-            TRY(readback(g.lcount, sizeof lc, lc));
-            list_len = lc[0];
-            theta = lc[1];
+            if (!g.ar) {
+                CK(launch_argmax_full_finish(g, T));
+                int lc[2];
+                TRY(readback(g.lcount, sizeof lc, lc));
+                list_len = lc[0];
+                theta = lc[1];
+            } else {  // reduce-scatter, local argmax over the slice, max of the keys, lists gathered
+                const int r = g.comm.rank, N = g.comm.nranks;
+                const int64_t v0 = (int64_t)r * g.S;
+                const int nv = (int)std::max<int64_t>(0, std::min<int64_t>(g.S, (int64_t)g.n - v0));
+                TRY(c_reduce_scatter(g.gain, g.gslice, g.S, IM_DTYPE_I32));
+                CK(launch_argmax_slice_decode(g, v0, nv));
+                TRY(c_allreduce(g.key, 1, IM_DTYPE_I64, IM_OP_MAX));
+                TRY(c_allreduce(g.hist, 4096, IM_DTYPE_I32, IM_OP_SUM));
+                CK(launch_argmax_slice_list(g, T, v0, nv));
+                TRY(c_allgather(g.lcount, g.lcnt_all, 1, IM_DTYPE_I32));
+                std::vector<int32_t> cnt(N);
+                TRY(readback(g.lcnt_all, N * sizeof(int32_t), cnt.data()));
+                int th;
+                TRY(readback(g.lcount + 1, sizeof th, &th));
+                const int maxc = std::max(1, *std::max_element(cnt.begin(), cnt.end()));
+                CK(launch_list_pad(g, g.llist, g.lcount, maxc));
+                TRY(c_allgather(g.llist, g.list, maxc, IM_DTYPE_I32));
+                list_len = N * maxc;  // with holes (-1) after each shorter rank list
+                CK(launch_set_count(g, g.lcount, list_len));
+                theta = th;
+            }
             need_full = false;
             g.st_argmax_full++;
         }

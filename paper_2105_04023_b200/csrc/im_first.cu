@@ -42,20 +42,10 @@ struct FirstArgs {
     const int32_t* big;  // vertices with > FIRST_BIG out-edges (k_first_big)
     int n_big;
     int vb;              // vertices per warp batch (<= 256; fewer on small graphs so every warp gets work)
-    const uint32_t* HV;  // hash(v) = Murmur3(LE32 v, seed_V) per vertex (Alg. 1 line 4), this build's
 };
 
-#ifndef FIRST_HV
-#define FIRST_HV 1  // 1: read hash(v) of Alg. 1 line 4 from the per-build table HV (k_vertex_hash) instead of
-                    // recomputing Murmur3 per edge (the from-init gather is ALU-bound)
-#endif
-__device__ __forceinline__ uint32_t vhash(const FirstArgs& a, uint32_t v) {
-#if FIRST_HV
-    return __ldg(&a.HV[v]);
-#else
-    return murmur_word(v, a.seedV);
-#endif
-}
+// hash(v) of Alg. 1 line 4, recomputed per edge (a per-build table of it read per edge measured no faster)
+__device__ __forceinline__ uint32_t vhash(const FirstArgs& a, uint32_t v) { return murmur_word(v, a.seedV); }
 
 // init registers of simulations 4w..4w+3 of a vertex with hash hv, packed
 __device__ __forceinline__ uint32_t init_word(uint32_t hv, const uint32_t* sHJ, int w) {
@@ -469,7 +459,6 @@ cudaError_t launch_first(Ctx& c, uint32_t* cm_out, uint32_t* bits_out, IterCount
     a.ctr = ctr;
     a.big = c.fbig;
     a.n_big = c.n_fbig;
-    a.HV = c.HV;
     {   // a dependent chain of loads per vertex: spread small graphs over every resident warp
         const int64_t warps = (int64_t)c.max_blocks_first * (BLOCK / 32);
         a.vb = (int)std::min<int64_t>(256, std::max<int64_t>(1, c.n / warps));

@@ -93,7 +93,6 @@ struct Ctx {
     uint32_t* Xs = nullptr;     // sorted salts [J]
     uint16_t* s12 = nullptr;    // [4097]
     int32_t* permd = nullptr;   // [J] internal index -> global simulation j (hash input of Eq. 1)
-    uint32_t* HV = nullptr;     // [n] hash(v) = Murmur3(LE32 v, seed_V) (Alg. 1 line 4), written by setup_salts
     uint8_t* M = nullptr;       // n*J registers, row-major, internal simulation order
     uint8_t* Mold = nullptr;    // pre-sweep copy read by synchronous sweeps (eps_c > 0, R22), n*J
     bool sync_sweeps = false;   // the running Simulate uses synchronous sweeps
@@ -136,9 +135,14 @@ struct Ctx {
     int* bcount = nullptr;       // per-block match counts of the ordered list build [num_sms * 8]
     uint32_t* hist = nullptr;    // gain histogram of the full pass
     ull* sigma_count = nullptr;
-    // simulation sharding: in-place SUM over ranks, null when unsharded
-    im_allreduce_fn ar = nullptr;
-    void* ar_user = nullptr;
+    // simulation sharding: the communicator (im_set_comm / im_comm_nccl_init)
+    im_comm comm{};
+    bool ar = false;             // a communicator is installed (sharded exchanges on)
+    void* nccl = nullptr;        // the library's own NCCL communicator state (im_comm.cu), or null
+    int64_t S = 0;               // vertex slice per rank of the reduce-scatter: ceil(n / nranks)
+    int32_t* gslice = nullptr;   // this rank's slice of the summed packed argmax values / stored gains [S]
+    int32_t* llist = nullptr;    // this rank's candidate list (its slice's vertices with gain >= theta) [S]
+    int32_t* lcnt_all = nullptr; // candidate-list lengths of every rank [nranks]
     int32_t* lval = nullptr;     // packed local values of the lazy-list argmax [list capacity]
     ull* sigma_g = nullptr;      // sigma count summed over ranks
     // Monte-Carlo evaluator (im_eval.cu): B-sample masks, frontier buffers
@@ -203,7 +207,6 @@ cudaError_t launch_build_items(Ctx& c, const int32_t* offs, int4* items, int32_t
 cudaError_t scan_exclusive(Ctx& c, const int32_t* in, int32_t* out, int n, void* tmp, size_t& tmp_bytes);
 cudaError_t launch_salt_tables(Ctx& c);
 cudaError_t launch_init_registers(Ctx& c);
-cudaError_t launch_vertex_hash(Ctx& c);  // c.HV[v] = Murmur3(LE32 v, seed_V)
 // one sweep over `items`; cm_in: per-simulation change mask of the previous sweep (null: no filter,
 // sweep 1); cm_out / bits_out: this sweep's change mask and chunk summary; counters in *ctr (zeroed)
 cudaError_t launch_sweep(Ctx& c, const int4* items, int n_items, const uint32_t* cm_in, uint32_t* cm_out,
@@ -219,6 +222,12 @@ cudaError_t launch_estimate_sums(Ctx& c, int32_t* sums);
 cudaError_t launch_estimate_fin(Ctx& c, const int32_t* sums, double* out);
 cudaError_t launch_argmax_full(Ctx& c, bool pool);
 cudaError_t launch_argmax_full_finish(Ctx& c, int T);
+// sharded full pass after the reduce-scatter: decode this rank's slice (key, stored gains, histogram)
+cudaError_t launch_argmax_slice_decode(Ctx& c, int64_t v0, int nv);
+// sharded: theta from the (summed) histogram, this rank's slice list into c.llist, its length into c.lcount[0]
+cudaError_t launch_argmax_slice_list(Ctx& c, int T, int64_t v0, int nv);
+cudaError_t launch_list_pad(Ctx& c, int32_t* list, const int* count, int cap);  // list[count..cap) = -1
+cudaError_t launch_set_count(Ctx& c, int* p, int v);  // *p = v on the stream
 cudaError_t launch_argmax_list_finish(Ctx& c, int list_len);
 cudaError_t launch_argmax_tma(Ctx& c, bool pool, int L, int C, int shift);
 int setup_argmax_tma();
@@ -240,5 +249,10 @@ cudaError_t launch_bfs_clear_raw(Ctx& c, int n_v, int W, const int32_t* vl, uint
 cudaError_t launch_mc_start(Ctx& c, int32_t s, int W, ull* count);
 cudaError_t launch_mc_level(Ctx& c, int cur, int n_items, int W, ull seed, ull r0, ull* count);
 cudaError_t launch_gather_rows(Ctx& c, const int32_t* rows, int64_t nrows, uint8_t* out);
+
+// the library's own NCCL communicator (im_comm.cu); 0 on success, else -1 with a message in err
+int nccl_unique_id(void* out128, char* err, size_t errn);
+int nccl_init(const void* id128, int rank, int nranks, im_comm* comm, void** state, char* err, size_t errn);
+void nccl_release(void* state);
 
 }  // namespace im

@@ -127,6 +127,11 @@ __global__ void __launch_bounds__(BLOCK) k_argmax(int32_t n, int32_t J, int L, i
             int64_t idx = (g0 + u * nwarps) * VPW + sub;
             ok[u] = (g0 + u * nwarps) < groups && idx < nv;
             vv[u] = ok[u] ? (LIST ? (int64_t)list[idx] : idx) : 0;
+            if (LIST && vv[u] < 0) {  // a hole of a sharded job's gathered list (padding of a shorter rank list)
+                if (SHARD && q == 0) gain_out[idx] = 0;
+                ok[u] = false;
+                vv[u] = 0;
+            }
 #pragma unroll
             for (int c = 0; c < AC; c++) {
                 int ci = c * L + q;
@@ -222,7 +227,7 @@ __device__ __forceinline__ void list_range(int32_t n, int b, int nb, int64_t& v0
     v1 = min((int64_t)n, v0 + chunk);
 }
 
-__global__ void k_list_count(int32_t n, const int32_t* __restrict__ gain, const int* theta, int* bcount) {
+__global__ void k_list_count(int32_t n, const int32_t* __restrict__ gain, const int* theta, int* bcount) {  // gain[0..n)
     __shared__ int sW[BLOCK / 32];
     const int th = *theta;
     int64_t v0, v1;
@@ -240,7 +245,7 @@ __global__ void k_list_count(int32_t n, const int32_t* __restrict__ gain, const 
 }
 
 __global__ void k_list_write(int32_t n, const int32_t* __restrict__ gain, const int* theta, const int* __restrict__ bcount,
-                             int32_t* list, int* count) {
+                             int32_t* list, int* count, int64_t vbase) {  // lists vertex vbase + i for gain[i] >= theta
     __shared__ int sW[BLOCK / 32];
     __shared__ int sBase;
     const int th = *theta, lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -271,7 +276,7 @@ __global__ void k_list_write(int32_t n, const int32_t* __restrict__ gain, const 
             before += i < wib ? sW[i] : 0;
             total += sW[i];
         }
-        if (take) list[base + before + __popc(m & ((1u << lane) - 1u))] = (int32_t)v;
+        if (take) list[base + before + __popc(m & ((1u << lane) - 1u))] = (int32_t)(vbase + v);
         base += total;
     }
 }
@@ -281,15 +286,16 @@ __global__ void k_list_write(int32_t n, const int32_t* __restrict__ gain, const 
 // of it (R14); its global gain is the low 24 bits.  Writes the key (and, for the full pass, the stored
 // gains and histogram) exactly as the unsharded kernels do.
 __global__ void k_argmax_decode(int nv, const int32_t* __restrict__ list, const int* list_count, const int32_t* __restrict__ vals,
-                                int32_t* gain_out, ull* key, uint32_t* hist, int shift) {
+                                int32_t* gain_out, ull* key, uint32_t* hist, int shift, int64_t v0) {
     __shared__ ull sKey[BLOCK / 32];
     if (list) nv = *list_count;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     ull best = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv; i += stride) {
         const uint32_t x = (uint32_t)vals[i];
-        const uint32_t gn = x & (SHARD_POOL_ONE - 1u), v = list ? (uint32_t)list[i] : (uint32_t)i;
-        const bool inpool = (x >> 24) != 0u;
+        const int64_t vi = list ? (int64_t)list[i] : v0 + i;  // list hole: -1, packed value 0 (not in the pool)
+        const uint32_t gn = x & (SHARD_POOL_ONE - 1u), v = (uint32_t)vi;
+        const bool inpool = vi >= 0 && (x >> 24) != 0u;
         if (inpool) {
             ull k = ((ull)gn << 32) | (ull)(0xFFFFFFFFu - v);
             best = k > best ? k : best;
@@ -748,16 +754,45 @@ cudaError_t launch_argmax_full(Ctx& c, bool pool) {
 cudaError_t launch_argmax_full_finish(Ctx& c, int T) {
     const int sh = hist_shift(c);
     cudaError_t e;
-    if (c.ar) {
-        k_argmax_decode<<<grid_for(c, c.n), BLOCK, 0, c.stream>>>(c.n, nullptr, nullptr, c.gain, c.gain, c.key, c.hist, sh);
-        if ((e = LAUNCHED(c))) return e;
-    }
     k_theta<<<1, 32, 0, c.stream>>>(c.hist, sh, T, c.lcount + 1);
     if ((e = LAUNCHED(c))) return e;
     const int nb = grid_for(c, c.n);  // <= LIST_BLOCKS(c)
     k_list_count<<<nb, BLOCK, 0, c.stream>>>(c.n, c.gain, c.lcount + 1, c.bcount);
     if ((e = LAUNCHED(c))) return e;
-    k_list_write<<<nb, BLOCK, 0, c.stream>>>(c.n, c.gain, c.lcount + 1, c.bcount, c.list, c.lcount);
+    k_list_write<<<nb, BLOCK, 0, c.stream>>>(c.n, c.gain, c.lcount + 1, c.bcount, c.list, c.lcount, 0);
+    return LAUNCHED(c);
+}
+// sharded full pass: after the reduce-scatter, c.gslice[i] is the summed packed value of
+// vertex v0 + i; decode it into the local argmax key, the stored gains of the slice and the histogram
+cudaError_t launch_argmax_slice_decode(Ctx& c, int64_t v0, int nv) {
+    if (nv <= 0) return cudaSuccess;
+    k_argmax_decode<<<grid_for(c, nv), BLOCK, 0, c.stream>>>(nv, nullptr, nullptr, c.gslice, c.gslice, c.key, c.hist,
+                                                             hist_shift(c), v0);
+    return LAUNCHED(c);
+}
+// theta from the summed histogram, then this rank's candidate list (its slice's vertices with gain >= theta,
+// ascending) into c.llist, its length into c.lcount[0]
+cudaError_t launch_argmax_slice_list(Ctx& c, int T, int64_t v0, int nv) {
+    const int sh = hist_shift(c);
+    k_theta<<<1, 32, 0, c.stream>>>(c.hist, sh, T, c.lcount + 1);
+    cudaError_t e = LAUNCHED(c);
+    if (e || nv <= 0) return e;
+    const int nb = grid_for(c, nv);
+    k_list_count<<<nb, BLOCK, 0, c.stream>>>(nv, c.gslice, c.lcount + 1, c.bcount);
+    if ((e = LAUNCHED(c))) return e;
+    k_list_write<<<nb, BLOCK, 0, c.stream>>>(nv, c.gslice, c.lcount + 1, c.bcount, c.llist, c.lcount, v0);
+    return LAUNCHED(c);
+}
+__global__ void k_set_count(int* p, int v) { *p = v; }
+cudaError_t launch_set_count(Ctx& c, int* p, int v) {
+    k_set_count<<<1, 1, 0, c.stream>>>(p, v);
+    return LAUNCHED(c);
+}
+__global__ void k_list_pad(int32_t* list, const int* count, int cap) {
+    for (int i = *count + blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += gridDim.x * blockDim.x) list[i] = -1;
+}
+cudaError_t launch_list_pad(Ctx& c, int32_t* list, const int* count, int cap) {
+    k_list_pad<<<grid_for(c, cap), BLOCK, 0, c.stream>>>(list, count, cap);
     return LAUNCHED(c);
 }
 
@@ -778,7 +813,7 @@ cudaError_t launch_argmax_list(Ctx& c, int list_len) {
 }
 cudaError_t launch_argmax_list_finish(Ctx& c, int list_len) {
     if (!c.ar) return cudaSuccess;
-    k_argmax_decode<<<grid_for(c, list_len), BLOCK, 0, c.stream>>>(list_len, c.list, c.lcount, c.lval, nullptr, c.key, nullptr, 0);
+    k_argmax_decode<<<grid_for(c, list_len), BLOCK, 0, c.stream>>>(list_len, c.list, c.lcount, c.lval, nullptr, c.key, nullptr, 0, 0);
     return LAUNCHED(c);
 }
 cudaError_t launch_seed_start(Ctx& c, int k) {

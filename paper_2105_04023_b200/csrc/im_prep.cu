@@ -180,8 +180,9 @@ __global__ void k_fill_items(int32_t n, const int32_t* __restrict__ offs, const 
 // With one threshold T a row only has to be grouped by bucket b = h >> Bs (KB = 31 - Bs <= 8 bits);
 // the order inside a bucket is immaterial (every consumer takes the slice of a bucket range).
 //   k_rows       forward row u: h = Murmur3(u||v) mod 2^31 (Eq. 4), records {v, h} written in bucket
-//                order by a row-local counting sort; every edge is also scattered to its reverse row
-//                (atomic cursor), straight into `rev` for a short reverse row, into `rtmp` for a long one
+//                order by a row-local counting sort
+//   k_scatter    every edge to its reverse row (atomic cursor), straight into `rev` for a short reverse
+//                row, into `rtmp` for a long one
 //   k_rev_rows   long reverse rows: block-local counting sort rtmp -> rev, bucket table
 // Rows of at most 32 edges are ranked inside one warp by a radix ballot; rows up to PREP_BIG by a
 // warp with a shared-memory histogram; longer rows by a whole block (k_rows_big).
@@ -221,17 +222,41 @@ __device__ __forceinline__ void write_row_table(const int32_t* tidx, int32_t* ta
     for (int kb = tid; kb <= NB; kb += nthreads) tb[kb] = kb < NB ? eb + hist[kb] : ee;
 }
 
-// record {v, h(u,v)} of input edge e of row u; on the first visit the edge is also scattered to its
-// reverse row (the transpose)
+// record {v, h(u,v)} of input edge e of row u
 __device__ __forceinline__ uint2 row_rec(const RowSortArgs& a, int64_t e, uint32_t u, bool first) {
+    (void)first;
     const uint32_t v = (uint32_t)a.tgt[e];
-    const uint32_t h = edge_hash(u, v);
-    if (first) {
-        const int rb = a.roff[v], d = a.roff[v + 1] - rb;
-        const int p = rb + atomicAdd(&a.cursor[v], 1);
-        (d > TAB_MIN ? a.rtmp : a.rev)[p] = make_uint2(u, h);
+    return make_uint2(v, edge_hash(u, v));
+}
+
+// the transpose: edge (u -> v, h) of forward position e goes to its reverse row at roff[v] + a per-target
+// cursor, straight into `rev` for a short reverse row, into `rtmp` for a long one (bucket-sorted after).
+// SU edges per thread: their loads, then their cursor atomics, then their stores, all in flight together.
+constexpr int SU = 4;
+__global__ void __launch_bounds__(BLOCK) k_scatter(int64_t m, const int32_t* __restrict__ src, const uint2* __restrict__ fwd,
+                                                   const int32_t* __restrict__ roff, int32_t* __restrict__ cursor,
+                                                   uint2* __restrict__ rev, uint2* __restrict__ rtmp) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * SU;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x * SU + threadIdx.x; base < m; base += stride) {
+        uint2 f[SU];
+        int32_t u[SU], rb[SU], re[SU], p[SU];
+#pragma unroll
+        for (int k = 0; k < SU; k++) {
+            const int64_t e = base + (int64_t)k * blockDim.x;
+            f[k] = e < m ? fwd[e] : make_uint2(0, 0);
+            u[k] = e < m ? src[e] : -1;
+        }
+#pragma unroll
+        for (int k = 0; k < SU; k++) {
+            rb[k] = u[k] >= 0 ? __ldg(&roff[f[k].x]) : 0;
+            re[k] = u[k] >= 0 ? __ldg(&roff[f[k].x + 1]) : 0;
+        }
+#pragma unroll
+        for (int k = 0; k < SU; k++) p[k] = u[k] >= 0 ? atomicAdd(&cursor[f[k].x], 1) : 0;
+#pragma unroll
+        for (int k = 0; k < SU; k++)
+            if (u[k] >= 0) (re[k] - rb[k] > TAB_MIN ? rtmp : rev)[rb[k] + p[k]] = make_uint2((uint32_t)u[k], f[k].y);
     }
-    return make_uint2(v, h);
 }
 
 // rank of this lane's key among the lanes of `act` (keys < mine, then equal keys of lower lanes)
@@ -449,18 +474,7 @@ __global__ void k_init_registers(int32_t n, int32_t J, uint32_t seedV, uint32_t 
       }
 }
 
-// hash(v) of Alg. 1 line 4 (reading R5) for every vertex, once per salt setup: the
-// first sweep of every build reads it per edge instead of recomputing Murmur3
-__global__ void k_vertex_hash(int32_t n, uint32_t seedV, uint32_t* __restrict__ HV) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += stride) HV[v] = murmur_word((uint32_t)v, seedV);
-}
-
 // ------------------------------------------------------------------ launchers
-cudaError_t launch_vertex_hash(Ctx& c) {
-    k_vertex_hash<<<grid_for(c, c.n), BLOCK, 0, c.stream>>>(c.n, c.seedV, c.HV);
-    return LAUNCHED(c);
-}
 cudaError_t launch_validate(Ctx& c, const int32_t* off, const int32_t* tgt, const float* prob, int* flags) {
     k_validate<<<grid_for(c, c.m > c.n ? c.m : c.n), BLOCK, 0, c.stream>>>(c.n, c.m, off, tgt, prob, flags);
     return LAUNCHED(c);
@@ -551,6 +565,11 @@ static cudaError_t prep_rows(Ctx& c, const int32_t* tgt, int32_t* indeg, void** 
     if ((e = LAUNCHED(c))) return e;
     k_rows_big<<<c.num_sms * 4, BLOCK, 0, c.stream>>>(a);
     if ((e = LAUNCHED(c))) return e;
+    int32_t* src = (int32_t*)scr[3];
+    k_src<<<grid_for(c, (int64_t)n * 32), BLOCK, 0, c.stream>>>(n, c.off, src);
+    if ((e = LAUNCHED(c))) return e;
+    k_scatter<<<grid_for(c, (c.m + SU - 1) / SU), BLOCK, 0, c.stream>>>(c.m, src, c.fwd, c.roff, cursor, c.rev, rtmp);
+    if ((e = LAUNCHED(c))) return e;
     int h = 0;  // reverse tables: count of long reverse rows (their list in c.t_tabrows)
     if ((e = setup_tables(c, c.roff, c.rtidx, c.rtab, cnt + 2, &h))) return e;
     if (h == 0) return cudaSuccess;
@@ -565,7 +584,7 @@ cudaError_t prep_scratch_sizes(Ctx& c, size_t* sz) {
     sz[0] = rows_path(c) ? ((size_t)c.n + 8) * 4 : m * 4;
     sz[1] = ((size_t)c.n + 1) * 4;
     sz[2] = rows_path(c) ? m * 8 : 8;
-    sz[3] = 8;
+    sz[3] = rows_path(c) ? m * 4 : 8;  // edge sources of the scatter
     size_t t = 0;
     cudaError_t e = scan_exclusive(c, nullptr, nullptr, c.n + 1, nullptr, t);
     sz[4] = t + 256;

@@ -194,7 +194,7 @@ cudaError_t launch_argmax_tma(Ctx& c, bool pool, int L, int C, int shift) {
     const int TV = tma_tv(c.J, L), ntiles = (c.n + TV - 1) / TV;
     const int grid = ntiles < c.num_sms * 2 ? ntiles : c.num_sms * 2;
     const size_t smem = tma_smem(c.J, TV, pool);
-    const bool sh = c.ar != nullptr;
+    const bool sh = c.ar;
     auto kf = pool ? (sh ? k_argmax_tma<true, true> : k_argmax_tma<true, false>)
                    : (sh ? k_argmax_tma<false, true> : k_argmax_tma<false, false>);
     kf<<<grid, BLOCK, smem, c.stream>>>(c.n, c.J, L, C, c.M, c.MS, c.vis, c.key, c.gain, c.hist, shift, TV);

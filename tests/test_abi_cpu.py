@@ -35,7 +35,7 @@ def test_library_loads_and_binds():
     L = im.lib()
     for name in declared_symbols():
         assert hasattr(L, name)
-    assert im.im_version() == 102
+    assert im.im_version() == 103
 
 
 def test_call_order_errors_without_gpu():
@@ -96,7 +96,7 @@ def test_c_program_consumes_the_header(tmp_path):
 int main(void) {
     im_stats st;
     int32_t seeds[1]; double scores[1];
-    if (im_version() != 102) return 1;
+    if (im_version() != 103) return 1;
     im_free();
     if (im_build_sketches(64, 1) != IM_ESTATE) return 2;
     if (strlen(im_last_error()) == 0) return 3;

@@ -1,9 +1,9 @@
 """Simulation sharding on one GPU: two library contexts (two copies of the
 .so, one thread each) hold the two halves of the simulations and exchange through an in-process
-allreduce hook.  Every rank's seeds, scores, step log and estimates must equal the unsharded
+communicator (the im_comm protocol of include/im.h: reduce-scatter, all-reduce sum / max, all-gather).  Every rank's seeds, scores, step log and estimates must equal the unsharded
 context's, and its registers / reach bits must equal the unsharded columns [j0, j1).
 
-The ranks only wait for each other on the host (inside the hook, with the library's stream
+The ranks only wait for each other on the host (inside the collectives, with the library's stream
 drained), never inside a kernel, so running them on one GPU is safe."""
 import os
 import shutil
@@ -32,8 +32,9 @@ def shard_libs(world):
     return _libs[:world]
 
 
-class ThreadAllreduce:
-    """SUM over `world` threads of one process: device -> host, sum, host -> device."""
+class ThreadComm:
+    """The communicator protocol (include/im.h im_comm) over `world` threads of one process, host-staged:
+    device -> host, combine, host -> device."""
 
     def __init__(self, world):
         import torch
@@ -44,26 +45,52 @@ class ThreadAllreduce:
         self.parts = [None] * world
         self.calls = 0
 
-    def hook(self, rank):
-        torch = self.torch
+    def _gather(self, rank, arr):
+        self.parts[rank] = arr
+        self.bar.wait()
+        allp = list(self.parts)
+        self.bar.wait()
+        return allp
 
-        def f(ptr, count, dtype):
-            t = torch.as_tensor(_DevArray(ptr, count, dtype), device="cuda")
-            self.parts[rank] = t.cpu().numpy().astype(np.int64)
-            self.bar.wait()
-            tot = np.sum(self.parts, axis=0)
-            self.bar.wait()
-            t.copy_(torch.from_numpy(tot.astype(t.cpu().numpy().dtype)))
-            torch.cuda.synchronize()
-            if rank == 0:
-                self.calls += 1
+    def comm(self, rank):
+        torch, tc = self.torch, self
 
-        return f
+        class C:
+            nranks = tc.world
+
+            def __init__(self):
+                self.rank = rank
+
+            def allreduce(self, ptr, count, dtype, op):
+                t = torch.as_tensor(_DevArray(ptr, count, dtype), device="cuda")
+                allp = tc._gather(rank, t.cpu().numpy().astype(np.int64))
+                tot = np.max(allp, axis=0) if op == im.IM_OP_MAX else np.sum(allp, axis=0)
+                t.copy_(torch.from_numpy(tot.astype(t.cpu().numpy().dtype)))
+                torch.cuda.synchronize()
+                if rank == 0:
+                    tc.calls += 1
+
+            def reduce_scatter(self, send, recv, recvcount, dtype):
+                s = torch.as_tensor(_DevArray(send, recvcount * tc.world, dtype), device="cuda")
+                r = torch.as_tensor(_DevArray(recv, recvcount, dtype), device="cuda")
+                allp = tc._gather(rank, s.cpu().numpy().astype(np.int64))
+                tot = np.sum(allp, axis=0)[rank * recvcount:(rank + 1) * recvcount]
+                r.copy_(torch.from_numpy(tot.astype(r.cpu().numpy().dtype)))
+                torch.cuda.synchronize()
+
+            def allgather(self, send, recv, sendcount, dtype):
+                s = torch.as_tensor(_DevArray(send, sendcount, dtype), device="cuda")
+                r = torch.as_tensor(_DevArray(recv, sendcount * tc.world, dtype), device="cuda")
+                allp = tc._gather(rank, s.cpu().numpy())
+                r.copy_(torch.from_numpy(np.concatenate(allp)))
+                torch.cuda.synchronize()
+
+        return C()
 
 
 def run_sharded(world, n, off, tgt, pr, Jt, seed, K, eps, want_est=True):
     libs = shard_libs(world)
-    ar = ThreadAllreduce(world)
+    tcomm = ThreadComm(world)
     out = [None] * world
     err = []
 
@@ -71,19 +98,17 @@ def run_sharded(world, n, off, tgt, pr, Jt, seed, K, eps, want_est=True):
         try:
             L = libs[r]
             j0, j1 = shard_range(Jt, r, world)
-            L.im_set_allreduce(None)
+            L.im_set_comm(tcomm.comm(r))  # before the build: it sizes the exchange buffers
             L.im_load_csr(n, off, tgt, pr)
             L.im_build_sketches_shard(Jt, seed, j0, j1)
-            L.im_set_allreduce(ar.hook(r))
             est = L.im_estimate(n) if want_est else None
             s, sc = L.im_select_seeds(K, eps)
             out[r] = {"j0": j0, "j1": j1, "seeds": s, "scores": sc, "log": L.im_get_step_log(K), "est": est,
                       "M": L.im_get_registers(n, j1 - j0), "reach": L.im_get_reach(n, j1 - j0),
                       "stats": L.im_get_stats()}
-            L.im_set_allreduce(None)
         except Exception as e:  # surfaced below
             err.append((r, e))
-            ar.bar.abort()
+            tcomm.bar.abort()
 
     ts = [threading.Thread(target=rank_main, args=(r,)) for r in range(world)]
     for t in ts:
@@ -91,7 +116,7 @@ def run_sharded(world, n, off, tgt, pr, Jt, seed, K, eps, want_est=True):
     for t in ts:
         t.join()
     assert not err, err
-    return out, ar.calls
+    return out, tcomm.calls
 
 
 def unsharded(n, off, tgt, pr, J, seed, K, eps):
@@ -138,25 +163,41 @@ def test_sharded_small_matches_unsharded(J, world, eps):
 def test_shard_validation_and_state():
     n, off, tgt, pr = 10, np.arange(11, dtype=np.int32), np.arange(1, 11, dtype=np.int32) % 10, np.full(10, 0.5, np.float32)
     L = shard_libs(1)[0]
-    L.im_set_allreduce(None)
+    L.im_set_comm(None)
     L.im_load_csr(n, off, tgt, pr)
     for args in [(64, 1, 0, 16), (64, 1, 32, 32), (64, 1, 32, 96), (100, 1, 0, 32), (4096, 1, 0, 2048)]:
         with pytest.raises(im.IMError) as e:
             L.im_build_sketches_shard(*args)
         assert e.value.code == im.IM_EINVAL
     L.im_build_sketches_shard(64, 1, 32, 64)
-    with pytest.raises(im.IMError) as e:  # sharded sketches without a hook
+    with pytest.raises(im.IMError) as e:  # sharded sketches without a communicator
         L.im_select_seeds(2, 0.1)
     assert e.value.code == im.IM_ESTATE
 
-    def bad(ptr, count, dtype):
-        raise RuntimeError("peer gone")
+    class Bad:
+        rank, nranks = 0, 2
 
-    L.im_set_allreduce(bad)
+        def allreduce(self, *a):
+            raise RuntimeError("peer gone")
+
+        reduce_scatter = allgather = allreduce
+
+    L.im_set_comm(Bad())
+    with pytest.raises(im.IMError) as e:  # communicator changed after the build
+        L.im_estimate(n)
+    assert e.value.code == im.IM_ESTATE
+    L.im_build_sketches_shard(64, 1, 32, 64)
     with pytest.raises(im.IMError) as e:
         L.im_estimate(n)
     assert e.value.code == im.IM_ECOMM
-    L.im_set_allreduce(None)
+
+    class BadRank(Bad):
+        rank, nranks = 3, 2
+
+    with pytest.raises(im.IMError) as e:
+        L.im_set_comm(BadRank())
+    assert e.value.code == im.IM_EINVAL
+    L.im_set_comm(None)
     L.im_build_sketches_shard(64, 1, 0, 64)  # whole range: an ordinary context again
     s, _ = L.im_select_seeds(2, 0.1)
     assert len(s) == 2
