@@ -153,7 +153,7 @@ void release_all() {
     for (int i = 0; i < 2; i++) { dfree(g.ev_delta[i]); dfree(g.ev_items[i]); dfree(g.ev_vl[i]); }
     dfree(g.t_flags); dfree(g.t_indeg); dfree(g.t_nseg); dfree(g.t_scan); dfree(g.t_off); dfree(g.t_tgt); dfree(g.t_prob);
     dfree(g.t_est); dfree(g.t_rows); dfree(g.t_rowsout);
-    for (int i = 0; i < 5; i++) dfree(g.t_prep[i]);
+    for (int i = 0; i < 9; i++) dfree(g.t_prep[i]);
     reset_graph_state();
 }
 
@@ -244,10 +244,10 @@ int load_common(int32_t n, int64_t m, const int32_t* d_off_src, const int32_t* d
     TRY(dalloc(g.roff, (size_t)n + 1));
     int32_t*& indeg = g.t_indeg;
     TRY(dalloc(indeg, 2 * ((size_t)n + 1)));
-    size_t sz[5];
+    size_t sz[9];
     CK(prep_scratch_sizes(g, sz));
-    void* scr[5];
-    for (int i = 0; i < 5; i++) {
+    void* scr[9];
+    for (int i = 0; i < 9; i++) {
         TRY(dalloc(g.t_prep[i], sz[i]));
         scr[i] = g.t_prep[i];
     }
@@ -279,10 +279,12 @@ int load_common(int32_t n, int64_t m, const int32_t* d_off_src, const int32_t* d
     TRY(readback(nseg + (n + 1) + n, sizeof(int32_t), &total[1]));
     g.n_fitems_cap = total[1];
     // rows gathered by a whole block in the first sweep
-    TRY(dalloc(g.fbig, (size_t)n));
+    CK(cudaMemsetAsync(g.t_flags + 2, 0, sizeof(int), g.stream));
+    CK(launch_list_big_rows(g, nullptr, g.t_flags + 2));
+    TRY(readback(g.t_flags + 2, sizeof(int), &g.n_fbig));
+    TRY(dalloc(g.fbig, (size_t)g.n_fbig));
     CK(cudaMemsetAsync(g.t_flags + 2, 0, sizeof(int), g.stream));
     CK(launch_list_big_rows(g, g.fbig, g.t_flags + 2));
-    TRY(readback(g.t_flags + 2, sizeof(int), &g.n_fbig));
     TRY(sync());
     // small per-graph state
     TRY(dalloc(g.ctr, 2));
@@ -305,7 +307,7 @@ int load_common(int32_t n, int64_t m, const int32_t* d_off_src, const int32_t* d
 }
 
 int check_csr_args(int32_t n, int64_t m) {
-    if (n < 1) return fail(IM_EINVAL, "n must be >= 1 (got %d)", n);
+    if (n < 1 || n > (1 << 28)) return fail(IM_EINVAL, "n must be in [1, 2^28] (got %d)", n);
     if (m < 0 || m > 2147483647LL) return fail(IM_EINVAL, "m must be in [0, 2^31-1] (got %lld)", (long long)m);
     return 0;
 }

@@ -39,7 +39,7 @@ struct FirstArgs {
     uint32_t* cm_out;
     uint32_t* bits_out;
     IterCounters* ctr;
-    const int32_t* big;  // vertices with > FIRST_BIG out-edges (k_first_big)
+    const int4* big_units;  // {u, eb, ee}: rows with > FIRST_BIG out-edges in units of <= FIRST_CHUNK (k_first_big)
     int n_big;
     int vb;              // vertices per warp batch (<= 256; fewer on small graphs so every warp gets work)
 };
@@ -371,7 +371,26 @@ __global__ void __launch_bounds__(BLOCK, 5) k_first(FirstArgs a) {
     if (lane == 0 && wcount) atomicAdd(&a.ctr->win_edges, (ull)wcount);
 }
 
-// one block per vertex with more than FIRST_BIG out-edges
+// global bytewise max of val into *p; returns the 4 change bits (one per register) this call raised
+__device__ __forceinline__ uint32_t gmax4_raised(uint32_t* p, uint32_t val) {
+    uint32_t cur = __ldcg(p), nw = __vmaxu4(cur, val);
+    while (nw != cur) {
+        const uint32_t prev = atomicCAS(p, cur, nw);
+        if (prev == cur) {
+            const uint32_t eq = __vcmpeq4(cur, nw);
+            return ((((~eq) & 0x01010101u) * 0x00204081u) >> 21) & 0xFu;
+        }
+        cur = prev;
+        nw = __vmaxu4(cur, val);
+    }
+    return 0u;
+}
+
+// Vertices with more than FIRST_BIG out-edges, in work units of <= FIRST_CHUNK edges (a 700k-edge hub of
+// RMAT-24 is ~90 units instead of one block's serial tail): a block gathers its unit's edges into a
+// shared-memory copy of row u started from the row's value (init or current), then max-merges the words
+// it raised into the global row with a bytewise-max CAS; the change bits it raised go to u's change mask
+// and chunk bits with atomicOr (the buffers start zeroed), so several units of one row compose.
 template <bool CONST_T, bool BLOCKED, bool MEM>
 __global__ void __launch_bounds__(BLOCK) k_first_big(FirstArgs a) {
     __shared__ uint32_t sX[1024];
@@ -389,11 +408,13 @@ __global__ void __launch_bounds__(BLOCK) k_first_big(FirstArgs a) {
     for (int i = threadIdx.x; i < 4097; i += blockDim.x) sS[i] = a.s12[i];
     uint32_t wcount = 0;
     for (int bi = blockIdx.x; bi < a.n_big; bi += gridDim.x) {
-        const uint32_t u = (uint32_t)a.big[bi];
+        const int4 U = a.big_units[bi];
+        const uint32_t u = (uint32_t)U.x;
+        const int eb = U.y, ee = U.z;
         __syncthreads();
         const uint32_t hu = MEM ? 0u : vhash(a, u);
         for (int w = threadIdx.x; w < NW; w += blockDim.x) {
-            uint32_t x = start_word<MEM>(a, sHJ, hu, u, w);
+            uint32_t x = MEM ? __ldcg(reinterpret_cast<const uint32_t*>(a.M) + (size_t)u * (J >> 2) + w) : init_word(hu, sHJ, w);
             row[w] = x;
             sOld[w] = x;
         }
@@ -402,20 +423,22 @@ __global__ void __launch_bounds__(BLOCK) k_first_big(FirstArgs a) {
             if (BLOCKED) sVis[threadIdx.x] = a.vis[(size_t)u * W + threadIdx.x];
         }
         __syncthreads();
-        const int eb = a.off[u], ee = a.off[u + 1];
         for (int e0 = eb + (threadIdx.x & ~31); e0 < ee; e0 += (MEM ? UB : 1) * blockDim.x)  // warp-uniform trip count
             gather_multi<CONST_T, BLOCKED, MEM, MEM ? UB : 1>(a, sX, sS, sHJ, sVis, row, e0, ee, blockDim.x, wcount);
         __syncthreads();
         for (int w = threadIdx.x; w < NW; w += blockDim.x) {
-            uint32_t nib = finish_word(a, row, u, w, sOld[w], false);
-            if (nib) atomicOr(&sMask[w >> 3], nib << ((w & 7) << 2));
+            const uint32_t x = row[w];
+            if (x != sOld[w]) {
+                const uint32_t nib = gmax4_raised(reinterpret_cast<uint32_t*>(a.M) + (size_t)u * (J >> 2) + w, x);
+                if (nib) atomicOr(&sMask[w >> 3], nib << ((w & 7) << 2));
+            }
         }
         __syncthreads();
         if (threadIdx.x < 32) {
-            uint32_t m = threadIdx.x < W ? sMask[threadIdx.x] : 0u;
-            if (threadIdx.x < W) a.cm_out[(size_t)u * W + threadIdx.x] = m;
-            uint32_t chunks = __ballot_sync(IM_FULL, m != 0u);
-            if (threadIdx.x == 0) a.bits_out[u] = chunks;
+            const uint32_t m = threadIdx.x < W ? sMask[threadIdx.x] : 0u;
+            if (m) atomicOr(&a.cm_out[(size_t)u * W + threadIdx.x], m);
+            const uint32_t chunks = __ballot_sync(IM_FULL, m != 0u);
+            if (threadIdx.x == 0 && chunks) atomicOr(&a.bits_out[u], chunks);
         }
     }
     const int lane = threadIdx.x & 31;
@@ -457,7 +480,7 @@ cudaError_t launch_first(Ctx& c, uint32_t* cm_out, uint32_t* bits_out, IterCount
     a.cm_out = cm_out;
     a.bits_out = bits_out;
     a.ctr = ctr;
-    a.big = c.fbig;
+    a.big_units = c.fbig;
     a.n_big = c.n_fbig;
     {   // a dependent chain of loads per vertex: spread small graphs over every resident warp
         const int64_t warps = (int64_t)c.max_blocks_first * (BLOCK / 32);
@@ -471,15 +494,22 @@ cudaError_t launch_first(Ctx& c, uint32_t* cm_out, uint32_t* bits_out, IterCount
     return blocked ? first_inst<false, true, false>(c, a) : first_inst<false, false, false>(c, a);
 }
 
-// vertices with more than FIRST_BIG out-edges (once per graph)
-__global__ void k_list_big_rows(int32_t n, const int32_t* __restrict__ off, int32_t* __restrict__ out, int* count) {
+// work units of the rows with more than FIRST_BIG out-edges (once per graph): pass 1 counts them
+// (units == nullptr), pass 2 writes {u, eb, ee} for each chunk of <= FIRST_CHUNK edges
+__global__ void k_list_big_rows(int32_t n, const int32_t* __restrict__ off, int4* __restrict__ units, int* count) {
     int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += stride)
-        if (off[u + 1] - off[u] > FIRST_BIG) out[atomicAdd(count, 1)] = (int32_t)u;
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += stride) {
+        const int eb = off[u], ee = off[u + 1];
+        if (ee - eb <= FIRST_BIG) continue;
+        const int nch = (ee - eb + FIRST_CHUNK - 1) / FIRST_CHUNK;
+        const int p = atomicAdd(count, nch);
+        if (units)
+            for (int k = 0; k < nch; k++) units[p + k] = make_int4((int)u, eb + k * FIRST_CHUNK, min(eb + (k + 1) * FIRST_CHUNK, ee), 0);
+    }
 }
 
-cudaError_t launch_list_big_rows(Ctx& c, int32_t* out, int* count) {
-    k_list_big_rows<<<grid_for(c, c.n), BLOCK, 0, c.stream>>>(c.n, c.off, out, count);
+cudaError_t launch_list_big_rows(Ctx& c, int4* units, int* count) {
+    k_list_big_rows<<<grid_for(c, c.n), BLOCK, 0, c.stream>>>(c.n, c.off, units, count);
     return LAUNCHED(c);
 }
 

@@ -21,7 +21,8 @@ constexpr int BLOCK = 256;      // threads per block of the persistent work-list
 #ifndef IM_FIRST_BIG
 #define IM_FIRST_BIG 2048
 #endif
-constexpr int FIRST_BIG = IM_FIRST_BIG; // first sweep: rows with more out-edges are gathered by a whole block
+constexpr int FIRST_BIG = IM_FIRST_BIG; // first sweep: rows with more out-edges are gathered by whole blocks
+constexpr int FIRST_CHUNK = 8192;       // edges per work unit of such a row (k_first_big)
 constexpr uint32_t SHARD_POOL_ONE = 1u << 24;  // sharded argmax: gain + (in local pool) << 24, summed over ranks
 
 // device-side counters of one sweep / BFS level (one 32-byte D2H per iteration)
@@ -82,7 +83,7 @@ struct Ctx {
     cudaError_t (*alloc_i32)(int32_t*&, size_t) = nullptr;  // device allocation with capacity reuse (im_abi.cu)
     int32_t n_ritems = 0;
     int32_t n_fitems_cap = 0;   // sum_v ceil(outdeg/SEG)
-    int32_t* fbig = nullptr;    // vertices with > FIRST_BIG out-edges
+    int4* fbig = nullptr;       // work units {u, eb, ee} of the rows with > FIRST_BIG out-edges (<= FIRST_CHUNK edges each)
     int32_t n_fbig = 0;
     // sketches
     int32_t J = 0;              // simulations held here (this rank's shard)
@@ -163,7 +164,7 @@ struct Ctx {
     float* t_prob = nullptr;
     double* t_est = nullptr;
     int32_t* t_rows = nullptr;
-    char* t_prep[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // edge-prep scratch (src, keys, vals, cub)
+    char* t_prep[9] = {};  // edge-prep scratch (im_prep.cu)
     uint8_t* t_rowsout = nullptr;
     // host pinned scratch
     void* hpin = nullptr;
@@ -194,13 +195,13 @@ int occupancy_bfs2(int J, int* blocks_per_sm);
 int setup_first(int J, int* blocks_per_sm);  // smem opt-in + occupancy of the first-sweep kernel for this J
 // register init + first sweep (gather, im_first.cu): writes every row, its change mask and chunk bits
 cudaError_t launch_first(Ctx& c, uint32_t* cm_out, uint32_t* bits_out, IterCounters* ctr, bool blocked, bool from_memory);
-cudaError_t launch_list_big_rows(Ctx& c, int32_t* out, int* count);
+cudaError_t launch_list_big_rows(Ctx& c, int4* units, int* count);  // units == nullptr: count only
 bool rows_path(const Ctx& c);  // constant threshold: long rows bucket-ordered (h >> Bs), bucket tables
 int sort_shift(int B0);        // Bs for a threshold's B0
 
 cudaError_t launch_validate(Ctx& c, const int32_t* off, const int32_t* tgt, const float* prob, int* flags);
 cudaError_t launch_const_check(Ctx& c, const float* prob, int* flag);
-cudaError_t prep_scratch_sizes(Ctx& c, size_t* sz);  // 5 sizes (bytes) for prep_edges scratch
+cudaError_t prep_scratch_sizes(Ctx& c, size_t* sz);  // 9 sizes (bytes) for prep_edges scratch
 cudaError_t prep_edges(Ctx& c, const int32_t* tgt, const float* prob, int32_t* indeg, int32_t* unused, void** scr,
                        const size_t* sz);
 cudaError_t launch_build_items(Ctx& c, const int32_t* offs, int4* items, int32_t* nseg_scratch, void* tmp, size_t tmp_bytes);

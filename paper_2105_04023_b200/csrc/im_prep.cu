@@ -14,6 +14,8 @@
 //   Forward rows are bucket-ordered in place by a row-local counting sort (k_rows / k_rows_big, which
 //   also scatter the reverse records); long reverse rows by a block-local counting sort (k_rev_rows).
 //   Per-edge thresholds (weighted cascade) keep the input row order.
+#include <algorithm>
+
 #include "im_device.cuh"
 #include "im_internal.h"
 
@@ -189,10 +191,27 @@ __global__ void k_fill_items(int32_t n, const int32_t* __restrict__ offs, const 
 constexpr int PREP_BIG = 2048;
 constexpr int PREP_KB_MAX = 8;
 
-__global__ void k_list_long(int32_t n, const int32_t* __restrict__ off, int32_t* __restrict__ lf, int* count) {
+constexpr int HCH = 16384;  // rows longer than this ("huge": RMAT hubs reach ~700k) are bucket-sorted by several blocks
+
+// rows with PREP_BIG < length <= HCH into lf (count[0]); longer ones into huge (hcount[0])
+__global__ void k_list_long(int32_t n, const int32_t* __restrict__ off, int32_t* __restrict__ lf, int* count,
+                            int32_t* __restrict__ huge, int* hcount) {
     int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += stride)
-        if (off[u + 1] - off[u] > PREP_BIG) lf[atomicAdd(count, 1)] = (int32_t)u;
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += stride) {
+        const int d = off[u + 1] - off[u];
+        if (d > HCH) huge[atomicAdd(hcount, 1)] = (int32_t)u;
+        else if (d > PREP_BIG) lf[atomicAdd(count, 1)] = (int32_t)u;
+    }
+}
+
+// the huge rows of a list of rows (rows[0..*nrows))
+__global__ void k_list_huge(const int32_t* __restrict__ rows, const int* nrows, const int32_t* __restrict__ off,
+                            int32_t* __restrict__ huge, int* hcount) {
+    const int nr = *nrows;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nr; i += gridDim.x * blockDim.x) {
+        const int v = rows[i];
+        if (off[v + 1] - off[v] > HCH) huge[atomicAdd(hcount, 1)] = v;
+    }
 }
 
 struct RowSortArgs {
@@ -229,33 +248,201 @@ __device__ __forceinline__ uint2 row_rec(const RowSortArgs& a, int64_t e, uint32
     return make_uint2(v, edge_hash(u, v));
 }
 
-// the transpose: edge (u -> v, h) of forward position e goes to its reverse row at roff[v] + a per-target
-// cursor, straight into `rev` for a short reverse row, into `rtmp` for a long one (bucket-sorted after).
-// SU edges per thread: their loads, then their cursor atomics, then their stores, all in flight together.
-constexpr int SU = 4;
-__global__ void __launch_bounds__(BLOCK) k_scatter(int64_t m, const int32_t* __restrict__ src, const uint2* __restrict__ fwd,
-                                                   const int32_t* __restrict__ roff, int32_t* __restrict__ cursor,
-                                                   uint2* __restrict__ rev, uint2* __restrict__ rtmp) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x * SU;
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x * SU + threadIdx.x; base < m; base += stride) {
-        uint2 f[SU];
-        int32_t u[SU], rb[SU], re[SU], p[SU];
+// ---------------------------------------------------------------- the transpose
+// Reverse row v occupies [roff[v], roff[v+1]).  The forward edges are first grouped by v's high bits in
+// L <= 2 radix partition passes of 256 digits each (MSD: digit = (v >> shift) & 255, pass k refines the
+// 256^k segments of pass k-1), which leaves every block of 2^LB consecutive vertices (LB <= 12) in one
+// contiguous segment; k_place then places each such partition's records into their reverse rows with
+// per-vertex counters in shared memory.  A partition pass works on units of <= PT records of one
+// segment: k_pcount counts digits per segment (shared histogram, one global add per digit and unit),
+// k_pscan turns the counts into the sub-segment offsets, k_pscatter ranks a unit's records by digit in
+// shared memory, reserves each digit's run with one global atomic, stages the unit sorted by digit in
+// shared memory and writes every run contiguously (coalesced).  The order inside a reverse row is
+// immaterial except for the bucket order of long rows (k_rev_rows).
+constexpr int PT = 3072;    // records per partition-pass unit (staged in dynamic shared memory: 3072 x 13 B, 5 blocks / SM)
+constexpr size_t PSCAT_SMEM = (size_t)PT * (sizeof(uint2) + sizeof(int) + 1);
+constexpr int PCH = 16384;  // staged records per k_place work unit
+constexpr int NPMAX = 4096; // vertices per k_place partition (shared counters)
+constexpr int PSEG_MAX = 65536;  // segments after two passes (256^2)
+
+// segment of unit un: last s with ustart[s] <= un (binary search over nseg + 1 unit starts)
+__device__ __forceinline__ int unit_segment(const int32_t* __restrict__ ustart, int nseg, int un) {
+    int lo = 0, hi = nseg - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (ustart[mid] <= un) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+// unit starts of a pass over nseg segments [soff[s], soff[s+1]) in units of <= chunk records (one block)
+__global__ void __launch_bounds__(BLOCK) k_seg_units(int nseg, const int32_t* __restrict__ soff, int chunk,
+                                                     int32_t* __restrict__ ustart) {
+    __shared__ int sW[BLOCK / 32];
+    __shared__ int tot;
+    int carry = 0;
+    for (int b = 0; b < nseg; b += BLOCK) {
+        const int sg = b + threadIdx.x;
+        const int x = sg < nseg ? (soff[sg + 1] - soff[sg] + chunk - 1) / chunk : 0;
+        const int ex = block_excl_scan(x, sW, &tot);
+        if (sg < nseg) ustart[sg] = carry + ex;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) ustart[nseg] = carry;
+}
+
+// the input record / target of position e of a pass: pass 0 reads the forward edges (src, fwd), later
+// passes the previous pass's output
+struct PartIn {
+    const int32_t* src;  // pass 0: source vertex per forward position, else null
+    const uint2* fwd;    // pass 0: forward records {v, h}
+    const uint2* rec;    // later passes: {u, h}
+    const int32_t* v;    // later passes: targets
+    __device__ __forceinline__ int32_t tv(int e) const { return src ? (int32_t)fwd[e].x : v[e]; }
+    __device__ __forceinline__ uint2 rc(int e) const { return src ? make_uint2((uint32_t)src[e], fwd[e].y) : rec[e]; }
+};
+
+__global__ void __launch_bounds__(BLOCK) k_pcount(PartIn in, int nseg, const int32_t* __restrict__ soff,
+                                                  const int32_t* __restrict__ ustart, int shift, int32_t* __restrict__ counts) {
+    __shared__ int hist[256];
+    __shared__ int sseg;
+    const int nunits = ustart[nseg];
+    for (int un = blockIdx.x; un < nunits; un += gridDim.x) {
+        __syncthreads();
+        if (threadIdx.x == 0) sseg = unit_segment(ustart, nseg, un);
+        hist[threadIdx.x] = 0;  // BLOCK == 256
+        __syncthreads();
+        const int sg = sseg, e0 = soff[sg] + (un - ustart[sg]) * PT, e1 = min(soff[sg + 1], e0 + PT);
+        for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) atomicAdd(&hist[(in.tv(e) >> shift) & 255], 1);
+        __syncthreads();
+        if (hist[threadIdx.x]) atomicAdd(&counts[(size_t)sg * 256 + threadIdx.x], hist[threadIdx.x]);
+    }
+}
+
+// per segment: sub-segment offsets (next pass's segment table, nseg * 256 + 1 entries) and cursors
+__global__ void __launch_bounds__(BLOCK) k_pscan(int nseg, const int32_t* __restrict__ soff, const int32_t* __restrict__ counts,
+                                                 int32_t* __restrict__ nsoff, int32_t* __restrict__ cursor) {
+    __shared__ int sW[BLOCK / 32];
+    __shared__ int tot;
+    for (int sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
+        const int c = counts[(size_t)sg * 256 + threadIdx.x];
+        const int o = soff[sg] + block_excl_scan(c, sW, &tot);
+        nsoff[(size_t)sg * 256 + threadIdx.x] = o;
+        cursor[(size_t)sg * 256 + threadIdx.x] = o;
+        if (sg == nseg - 1 && threadIdx.x == 0) nsoff[(size_t)nseg * 256] = soff[nseg];
+    }
+}
+
+__global__ void __launch_bounds__(BLOCK) k_pscatter(PartIn in, int nseg, const int32_t* __restrict__ soff,
+                                                    const int32_t* __restrict__ ustart, int shift, int32_t* __restrict__ cursor,
+                                                    uint2* __restrict__ orec, int32_t* __restrict__ ov) {
+    __shared__ int hist[256], loff[256], gbase[256];
+    extern __shared__ __align__(16) unsigned char dyn[];
+    uint2* srec = reinterpret_cast<uint2*>(dyn);
+    int* sv = reinterpret_cast<int*>(dyn + PT * sizeof(uint2));
+    unsigned char* sdig = dyn + PT * (sizeof(uint2) + sizeof(int));
+    __shared__ int sW[BLOCK / 32];
+    __shared__ int tot, sseg;
+    const int nunits = ustart[nseg];
+    for (int un = blockIdx.x; un < nunits; un += gridDim.x) {
+        __syncthreads();
+        if (threadIdx.x == 0) sseg = unit_segment(ustart, nseg, un);
+        hist[threadIdx.x] = 0;
+        __syncthreads();
+        const int sg = sseg, e0 = soff[sg] + (un - ustart[sg]) * PT, e1 = min(soff[sg + 1], e0 + PT);
+        constexpr int PU = PT / BLOCK;  // records per thread, all loads in flight together
+        int vv[PU];
 #pragma unroll
-        for (int k = 0; k < SU; k++) {
-            const int64_t e = base + (int64_t)k * blockDim.x;
-            f[k] = e < m ? fwd[e] : make_uint2(0, 0);
-            u[k] = e < m ? src[e] : -1;
+        for (int k = 0; k < PU; k++) {
+            const int e = e0 + k * BLOCK + threadIdx.x;
+            vv[k] = e < e1 ? in.tv(e) : -1;
         }
 #pragma unroll
-        for (int k = 0; k < SU; k++) {
-            rb[k] = u[k] >= 0 ? __ldg(&roff[f[k].x]) : 0;
-            re[k] = u[k] >= 0 ? __ldg(&roff[f[k].x + 1]) : 0;
+        for (int k = 0; k < PU; k++)
+            if (vv[k] >= 0) atomicAdd(&hist[(vv[k] >> shift) & 255], 1);
+        __syncthreads();
+        const int c = hist[threadIdx.x];
+        loff[threadIdx.x] = block_excl_scan(c, sW, &tot);  // contains the barriers
+        gbase[threadIdx.x] = c ? atomicAdd(&cursor[(size_t)sg * 256 + threadIdx.x], c) : 0;
+        hist[threadIdx.x] = loff[threadIdx.x];  // now the local placement cursor
+        __syncthreads();
+        uint2 rr[PU];
+#pragma unroll
+        for (int k = 0; k < PU; k++) {
+            const int e = e0 + k * BLOCK + threadIdx.x;
+            rr[k] = vv[k] >= 0 ? in.rc(e) : make_uint2(0, 0);
         }
 #pragma unroll
-        for (int k = 0; k < SU; k++) p[k] = u[k] >= 0 ? atomicAdd(&cursor[f[k].x], 1) : 0;
-#pragma unroll
-        for (int k = 0; k < SU; k++)
-            if (u[k] >= 0) (re[k] - rb[k] > TAB_MIN ? rtmp : rev)[rb[k] + p[k]] = make_uint2((uint32_t)u[k], f[k].y);
+        for (int k = 0; k < PU; k++) {  // stage the unit sorted by digit
+            if (vv[k] < 0) continue;
+            const int d = (vv[k] >> shift) & 255;
+            const int q = atomicAdd(&hist[d], 1);
+            srec[q] = rr[k];
+            sv[q] = vv[k];
+            sdig[q] = (unsigned char)d;
+        }
+        __syncthreads();
+        for (int q = threadIdx.x; q < e1 - e0; q += blockDim.x) {  // each digit's run is contiguous here and there
+            const int d = sdig[q];
+            const int pos = gbase[d] + (q - loff[d]);
+            orec[pos] = srec[q];
+            ov[pos] = sv[q];
+        }
+    }
+}
+
+// unit starts of k_place: partition p = vertices [p << LB, (p+1) << LB) covers [roff[p << LB], roff[...])
+__global__ void __launch_bounds__(BLOCK) k_seg_units_roff(int n, int LB, int NP, const int32_t* __restrict__ roff, int chunk,
+                                                          int32_t* __restrict__ ustart) {
+    __shared__ int sW[BLOCK / 32];
+    __shared__ int tot;
+    int carry = 0;
+    for (int b = 0; b < NP; b += BLOCK) {
+        const int p = b + threadIdx.x;
+        int x = 0;
+        if (p < NP) {
+            const int64_t v0 = (int64_t)p << LB, v1 = min((int64_t)n, (int64_t)(p + 1) << LB);
+            x = (roff[v1] - roff[v0] + chunk - 1) / chunk;
+        }
+        const int ex = block_excl_scan(x, sW, &tot);
+        if (p < NP) ustart[p] = carry + ex;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) ustart[NP] = carry;
+}
+
+// a work unit = <= PCH staged records of one partition (their positions are the partition's range of the
+// reverse order): count them per target in shared memory, reserve each target's run with one global atomic
+// per distinct target, write each record to its reverse row (short rows straight into rev, long rows into
+// ltmp for k_rev_rows)
+__global__ void __launch_bounds__(BLOCK) k_place(int n, int LB, int NP, const int32_t* __restrict__ ustart,
+                                                 const int32_t* __restrict__ roff, int32_t* __restrict__ cursor, PartIn in,
+                                                 uint2* __restrict__ rev, uint2* __restrict__ ltmp) {
+    __shared__ int cnt[NPMAX];
+    __shared__ int sp;
+    const int nunits = ustart[NP];
+    const int V = 1 << LB;
+    for (int un = blockIdx.x; un < nunits; un += gridDim.x) {
+        __syncthreads();
+        if (threadIdx.x == 0) sp = unit_segment(ustart, NP, un);  // the partition owning unit un
+        for (int i = threadIdx.x; i < V; i += blockDim.x) cnt[i] = 0;
+        __syncthreads();
+        const int p = sp;
+        const int64_t vb = (int64_t)p << LB;
+        const int rb = roff[vb], re = roff[min((int64_t)n, vb + V)];
+        const int e0 = rb + (un - ustart[p]) * PCH, e1 = min(re, e0 + PCH);
+        for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) atomicAdd(&cnt[in.tv(e) - vb], 1);
+        __syncthreads();
+        for (int i = threadIdx.x; i < V; i += blockDim.x) {  // this unit's run of target vb + i
+            const int c = cnt[i];
+            cnt[i] = c ? roff[vb + i] + atomicAdd(&cursor[vb + i], c) : 0;
+        }
+        __syncthreads();
+        for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+            const int v = in.tv(e);
+            const int pos = atomicAdd(&cnt[v - vb], 1);
+            (roff[v + 1] - roff[v] > TAB_MIN ? ltmp : rev)[pos] = in.rc(e);
+        }
     }
 }
 
@@ -403,8 +590,117 @@ __global__ void __launch_bounds__(BLOCK) k_rev_rows(int nrows, const int32_t* __
     __shared__ int hist[1 << PREP_KB_MAX];
     for (int t = blockIdx.x; t < nrows; t += gridDim.x) {
         const uint32_t v = (uint32_t)rows[t];
+        if (roff[v + 1] - roff[v] > HCH) continue;  // huge: k_huge_*
         block_row_sort([&](int64_t e, bool) { return rtmp[e]; }, rev, roff[v], roff[v + 1], B, 1 << KB, hist, tidx, tab, nbk, v);
     }
+}
+
+// Huge rows (> HCH entries), bucket-sorted by units of <= HCH entries on several blocks: k_huge_count adds
+// each unit's bucket counts to the row's 256 counters, k_huge_scan turns them into the row's bucket
+// table and placement cursors, k_huge_place reserves each unit's run per bucket with one global atomic
+// and writes its records there (inside the row's region of the output: L2-resident writes).
+struct HugeSort {
+    const int32_t* huge;   // huge rows
+    const int* nhuge;      // their count (device)
+    const int32_t* offs;   // row offsets
+    const int32_t* ustart; // unit starts per huge row (k_huge_units)
+    const int32_t* tgt;    // forward rows: records {tgt[e], h(u, tgt[e])} (Eq. 4); null: in[e]
+    const uint2* in;
+    uint2* out;
+    int B, KB;
+    int32_t* cnt;          // 256 counters per huge row (zeroed), then cursors
+    const int32_t* tidx;
+    int32_t* tab;
+    int nbk;
+};
+
+__device__ __forceinline__ uint2 huge_rec(const HugeSort& a, int e, uint32_t u) {
+    if (!a.tgt) return a.in[e];
+    const uint32_t v = (uint32_t)a.tgt[e];
+    return make_uint2(v, edge_hash(u, v));
+}
+
+__global__ void __launch_bounds__(BLOCK) k_huge_units(HugeSort a) {
+    __shared__ int sW[BLOCK / 32];
+    __shared__ int tot;
+    const int nh = *a.nhuge;
+    int carry = 0;
+    for (int b = 0; b < nh; b += BLOCK) {
+        const int r = b + threadIdx.x;
+        int x = 0;
+        if (r < nh) {
+            const int u = a.huge[r];
+            x = (a.offs[u + 1] - a.offs[u] + HCH - 1) / HCH;
+        }
+        const int ex = block_excl_scan(x, sW, &tot);
+        if (r < nh) const_cast<int32_t*>(a.ustart)[r] = carry + ex;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) const_cast<int32_t*>(a.ustart)[nh] = carry;
+}
+
+template <bool PLACE>
+__global__ void __launch_bounds__(BLOCK) k_huge_pass(HugeSort a) {
+    __shared__ int hist[256];
+    __shared__ int sr;
+    const int nh = *a.nhuge;
+    if (nh == 0) return;
+    const int nunits = a.ustart[nh];
+    for (int un = blockIdx.x; un < nunits; un += gridDim.x) {
+        __syncthreads();
+        if (threadIdx.x == 0) sr = unit_segment(a.ustart, nh, un);
+        hist[threadIdx.x] = 0;
+        __syncthreads();
+        const int r = sr;
+        const uint32_t u = (uint32_t)a.huge[r];
+        const int e0 = a.offs[u] + (un - a.ustart[r]) * HCH, e1 = min(a.offs[u + 1], e0 + HCH);
+        for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) atomicAdd(&hist[huge_rec(a, e, u).y >> a.B], 1);
+        __syncthreads();
+        const int c = hist[threadIdx.x];
+        if (!PLACE) {
+            if (c) atomicAdd(&a.cnt[(size_t)r * 256 + threadIdx.x], c);
+            continue;
+        }
+        hist[threadIdx.x] = c ? atomicAdd(&a.cnt[(size_t)r * 256 + threadIdx.x], c) : 0;  // this unit's run per bucket
+        __syncthreads();
+        for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+            const uint2 rec = huge_rec(a, e, u);
+            a.out[atomicAdd(&hist[rec.y >> a.B], 1)] = rec;
+        }
+    }
+}
+
+// per huge row: bucket table and placement cursors from the counts
+__global__ void __launch_bounds__(BLOCK) k_huge_scan(HugeSort a) {
+    __shared__ int sW[BLOCK / 32];
+    __shared__ int tot;
+    const int nh = *a.nhuge, NB = 1 << a.KB;
+    for (int r = blockIdx.x; r < nh; r += gridDim.x) {
+        const int u = a.huge[r];
+        const int c = threadIdx.x < NB ? a.cnt[(size_t)r * 256 + threadIdx.x] : 0;
+        const int o = a.offs[u] + block_excl_scan(c, sW, &tot);
+        a.cnt[(size_t)r * 256 + threadIdx.x] = o;
+        const int t = a.tidx[u];
+        if (t >= 0) {
+            int32_t* tb = a.tab + (int64_t)t * a.nbk;
+            if (threadIdx.x < NB) tb[threadIdx.x] = o;
+            if (threadIdx.x == 0) tb[NB] = a.offs[u + 1];
+        }
+    }
+}
+
+static cudaError_t huge_sort(Ctx& c, HugeSort& a, int32_t* ustart, int max_huge) {
+    cudaError_t e;
+    a.ustart = ustart;
+    if ((e = cudaMemsetAsync(a.cnt, 0, (size_t)max_huge * 256 * sizeof(int32_t), c.stream))) return e;
+    k_huge_units<<<1, BLOCK, 0, c.stream>>>(a);
+    if ((e = LAUNCHED(c))) return e;
+    k_huge_pass<false><<<c.num_sms * 4, BLOCK, 0, c.stream>>>(a);
+    if ((e = LAUNCHED(c))) return e;
+    k_huge_scan<<<c.num_sms * 4, BLOCK, 0, c.stream>>>(a);
+    if ((e = LAUNCHED(c))) return e;
+    k_huge_pass<true><<<c.num_sms * 4, BLOCK, 0, c.stream>>>(a);
+    return LAUNCHED(c);
 }
 
 // ------------------------------------------------------------------ bucket offset tables of long rows
@@ -540,8 +836,17 @@ static cudaError_t prep_rows(Ctx& c, const int32_t* tgt, int32_t* indeg, void** 
     size_t t2 = tb;
     if ((e = scan_exclusive(c, indeg, c.roff, n + 1, scr[4], t2))) return e;
     if ((e = cudaMemsetAsync(cursor, 0, (size_t)n * sizeof(int32_t), c.stream))) return e;
+    // huge rows: lists (forward, reverse), their counters and unit starts
+    const int max_huge = (int)(c.m / HCH + 2);
+    int32_t* hz = (int32_t*)scr[8];
+    int* hcnt = hz;                               // [0] forward huge count, [1] reverse huge count
+    int32_t* fhuge = hz + 8;
+    int32_t* rhuge = fhuge + max_huge;
+    int32_t* hustart = rhuge + max_huge;          // max_huge + 1
+    int32_t* hcounters = hustart + max_huge + 8;  // max_huge x 256
+    if ((e = cudaMemsetAsync(hcnt, 0, 8 * sizeof(int), c.stream))) return e;
     if ((e = cudaMemsetAsync(cnt, 0, 2 * sizeof(int), c.stream))) return e;
-    k_list_long<<<grid_for(c, n), BLOCK, 0, c.stream>>>(n, c.off, lf, cnt);
+    k_list_long<<<grid_for(c, n), BLOCK, 0, c.stream>>>(n, c.off, lf, cnt, fhuge, hcnt);
     if ((e = LAUNCHED(c))) return e;
     RowSortArgs a{};
     a.n = n;
@@ -565,16 +870,75 @@ static cudaError_t prep_rows(Ctx& c, const int32_t* tgt, int32_t* indeg, void** 
     if ((e = LAUNCHED(c))) return e;
     k_rows_big<<<c.num_sms * 4, BLOCK, 0, c.stream>>>(a);
     if ((e = LAUNCHED(c))) return e;
+    {
+        HugeSort hs{fhuge, hcnt, c.off, nullptr, tgt, nullptr, c.fwd, B, KB, hcounters, c.ftidx, c.ftab, c.nbk};
+        if ((e = huge_sort(c, hs, hustart, max_huge))) return e;
+    }
+    // the transpose: L radix partition passes over 8-bit digits of v, then k_place per 2^LB-vertex partition
+    int NB = 1;
+    while (NB < 31 && ((int64_t)1 << NB) < (int64_t)n) NB++;
+    const int L = NB <= 12 ? 0 : (NB - 12 + 7) / 8, LB = NB - 8 * L;
+    const int NP = (int)(((int64_t)n + (1 << LB) - 1) >> LB);
     int32_t* src = (int32_t*)scr[3];
+    uint2* recA = (uint2*)scr[5];
+    int32_t* vA = (int32_t*)scr[6];
+    uint2* recB = rtmp;
+    int32_t* vB = src;  // free once pass 0 has read the sources
+    int32_t* seg = (int32_t*)scr[7];                 // segment offsets of the current pass (<= 65536 + 1)
+    int32_t* nseg_off = seg + (PSEG_MAX + 1);        // of the next pass
+    int32_t* cnt2 = nseg_off + (PSEG_MAX + 1);       // digit counts / cursors per (segment, digit)
+    int32_t* ustart = cnt2 + PSEG_MAX;               // unit starts (<= PSEG_MAX + 1, or NP + 1 for k_place)
     k_src<<<grid_for(c, (int64_t)n * 32), BLOCK, 0, c.stream>>>(n, c.off, src);
     if ((e = LAUNCHED(c))) return e;
-    k_scatter<<<grid_for(c, (c.m + SU - 1) / SU), BLOCK, 0, c.stream>>>(c.m, src, c.fwd, c.roff, cursor, c.rev, rtmp);
+    {
+        const int32_t zm[2] = {0, (int32_t)c.m};
+        if ((e = cudaMemcpyAsync(seg, zm, sizeof zm, cudaMemcpyHostToDevice, c.stream))) return e;
+        if ((e = cudaStreamSynchronize(c.stream))) return e;  // zm goes out of scope
+    }
+    PartIn in{src, c.fwd, nullptr, nullptr};
+    const uint2* rec_final = nullptr;
+    int nseg = 1;
+    for (int k = 0; k < L; k++) {
+        const int shift = NB - 8 * (k + 1);
+        uint2* orec = (k & 1) ? recB : recA;
+        int32_t* ov = (k & 1) ? vB : vA;
+        k_seg_units<<<1, BLOCK, 0, c.stream>>>(nseg, seg, PT, ustart);
+        if ((e = LAUNCHED(c))) return e;
+        if ((e = cudaMemsetAsync(cnt2, 0, (size_t)nseg * 256 * sizeof(int32_t), c.stream))) return e;
+        const int grid = c.num_sms * 8;
+        k_pcount<<<grid, BLOCK, 0, c.stream>>>(in, nseg, seg, ustart, shift, cnt2);
+        if ((e = LAUNCHED(c))) return e;
+        k_pscan<<<std::min(nseg, c.num_sms * 8), BLOCK, 0, c.stream>>>(nseg, seg, cnt2, nseg_off, cnt2);
+        if ((e = LAUNCHED(c))) return e;
+        static bool attr = false;
+        if (!attr) {
+            if ((e = cudaFuncSetAttribute(k_pscatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PSCAT_SMEM))) return e;
+            attr = true;
+        }
+        k_pscatter<<<c.num_sms * 5, BLOCK, PSCAT_SMEM, c.stream>>>(in, nseg, seg, ustart, shift, cnt2, orec, ov);
+        if ((e = LAUNCHED(c))) return e;
+        std::swap(seg, nseg_off);
+        nseg *= 256;
+        in = PartIn{nullptr, nullptr, orec, ov};
+        rec_final = orec;
+    }
+    // long reverse rows land in a buffer the passes no longer need (not the one k_place reads)
+    if (L >= 1 && rec_final == recB) rtmp = recA;
+    k_seg_units_roff<<<1, BLOCK, 0, c.stream>>>(n, LB, NP, c.roff, PCH, ustart);
+    if ((e = LAUNCHED(c))) return e;
+    k_place<<<c.num_sms * 8, BLOCK, 0, c.stream>>>(n, LB, NP, ustart, c.roff, cursor, in, c.rev, rtmp);
     if ((e = LAUNCHED(c))) return e;
     int h = 0;  // reverse tables: count of long reverse rows (their list in c.t_tabrows)
     if ((e = setup_tables(c, c.roff, c.rtidx, c.rtab, cnt + 2, &h))) return e;
     if (h == 0) return cudaSuccess;
     k_rev_rows<<<c.num_sms * 8, BLOCK, 0, c.stream>>>(h, c.t_tabrows, c.roff, rtmp, c.rev, B, KB, c.rtidx, c.rtab, c.nbk);
-    return LAUNCHED(c);
+    if ((e = LAUNCHED(c))) return e;
+    if ((e = cudaMemcpyAsync(cnt + 2, &h, sizeof(int), cudaMemcpyHostToDevice, c.stream))) return e;
+    k_list_huge<<<grid_for(c, h), BLOCK, 0, c.stream>>>(c.t_tabrows, cnt + 2, c.roff, rhuge, hcnt + 1);
+    if ((e = LAUNCHED(c))) return e;
+    HugeSort hs{rhuge, hcnt + 1, c.roff, nullptr, nullptr, rtmp, c.rev, B, KB, hcounters, c.rtidx, c.rtab, c.nbk};
+    if ((e = huge_sort(c, hs, hustart, max_huge))) return e;
+    return cudaStreamSynchronize(c.stream);  // &h is read by the copy above
 }
 
 // scratch sizes (bytes) the edge prep needs: [0] long-row list + counters or the edge sources, [1] scatter
@@ -584,7 +948,11 @@ cudaError_t prep_scratch_sizes(Ctx& c, size_t* sz) {
     sz[0] = rows_path(c) ? ((size_t)c.n + 8) * 4 : m * 4;
     sz[1] = ((size_t)c.n + 1) * 4;
     sz[2] = rows_path(c) ? m * 8 : 8;
-    sz[3] = rows_path(c) ? m * 4 : 8;  // edge sources of the scatter
+    sz[3] = rows_path(c) ? m * 4 : 8;  // edge sources of the transpose
+    sz[5] = rows_path(c) ? m * 8 : 8;  // staged records {u, h}
+    sz[6] = rows_path(c) ? m * 4 : 8;  // their targets
+    sz[7] = (4 * (size_t)PSEG_MAX + 8) * 4;  // segment tables, digit counts, unit starts of the transpose
+    sz[8] = ((size_t)(m / HCH + 2) * 259 + 32) * 4;  // huge-row lists, unit starts, counters
     size_t t = 0;
     cudaError_t e = scan_exclusive(c, nullptr, nullptr, c.n + 1, nullptr, t);
     sz[4] = t + 256;
