@@ -139,7 +139,11 @@ def latest_capture(config):
     if os.path.isdir(pdir):
         for f in os.listdir(pdir):
             if f.endswith(f"_traffic_{config}.json"):
-                tj = json.load(open(os.path.join(pdir, f)))
+                try:
+                    tj = json.load(open(os.path.join(pdir, f)))
+                    tj["sweep"]["dram_bytes_per_step"]
+                except (ValueError, KeyError, TypeError):
+                    continue  # an unusable capture is ignored
                 key = (tj.get("round", f[:4]), f)
                 if best is None or key > best[0]:
                     best = (key, f, tj)

@@ -121,7 +121,10 @@ int ensure_device() {
     if (!g.ev[0]) {
         CK(cudaEventCreate(&g.ev[0]));
         CK(cudaEventCreate(&g.ev[1]));
+        for (int i = 0; i < 2; i++)
+            for (int k = 0; k < 3; k++) CK(cudaEventCreate(&g.pev[i][k]));
     }
+    if (const char* pp = getenv("IM_PIPELINE")) g.pipeline = atoi(pp) != 0;
     return 0;
 }
 
@@ -434,7 +437,6 @@ int simulate(bool blocked) {
             CK(cudaMemsetAsync(g.cm[i], 0, (size_t)g.n * W * sizeof(uint32_t), g.stream));
         }
     g.sweep_dirty = true;  // until this build completes
-    IterCounters hc;
     int sweeps = 0;
     int64_t edges = 0, wedges = 0, launches = 0;
     float kms = 0.f;
@@ -445,13 +447,50 @@ int simulate(bool blocked) {
     const int4* items = g.ritems;
     int n_items = g.n_ritems;
     edges = g.m;
+    // Pipelining (eps_c = 0): once the frontier is sparse, sweep s is enqueued with its item count read on
+    // the device from sweep s-1's compaction, and the host reads sweep s-1's counters (copied to pinned
+    // memory) while sweep s runs; the stop test is one sweep late, and the extra sweep it then enqueued has
+    // no items (a no-op).  Sweeps stay in stream order, so the registers are those of the host-driven loop.
+    IterCounters* hpc = reinterpret_cast<IterCounters*>(static_cast<char*>(g.hpin) + 1024);  // 2 pinned slots
+    bool piped = false;
+    bool gathers[2] = {false, false};
+    int last_done = 0;  // the last sweep whose counters were accounted
+    // the bookkeeping of a finished sweep; returns false when the loop must stop after it
+    auto account = [&](int s, const IterCounters& hc, bool gather, float t) {
+        kms += t;
+        sweeps++;
+        launches++;
+        wedges += (int64_t)hc.win_edges;
+        {   // algorithmic bytes (DESIGN.md section 6 builder model): records + one 32-B sector per worked window
+            const double nJ = (double)g.n * g.J, rec = 8.0 + (g.constT ? 0.0 : 4.0);
+            const double cmb = (double)g.n * ((double)g.J / 8.0 + 4.0);  // change mask + chunk word per vertex
+            if (s == 1) alg += rec * (double)g.m + nJ + cmb;                // + every row written once
+            else if (gather) alg += rec * (double)g.m + 2.0 * nJ + cmb + 32.0 * (double)hc.win_edges;
+            else alg += rec * (double)edges_in + 32.0 * (double)hc.win_edges;
+            if (gather) ngather++;
+        }
+        if (g.trace)
+            fprintf(stderr, "[im] sweep %d %s%s items %d edges %lld window_edges %llu -> changed %d next_items %d next_edges %llu big %d  %.3f ms\n",
+                    s, s == 1 ? "init+gather" : gather ? "gather" : "push", piped ? " (piped)" : "", n_items,
+                    (long long)(s == 1 || gather ? g.m : (int64_t)edges_in), hc.win_edges, hc.changed, hc.next_items, hc.next_edges,
+                    hc.big, t);
+        edges_in = (int64_t)hc.next_edges;
+        dirty = hc.changed > 0;  // this sweep's change bits stay set until the next sweep consumes them
+        if (!((double)hc.changed / (double)g.n > eps_c)) return false;  // Alg. 2 line 3 (eps_c = 0: nothing changed)
+        if (hc.next_items == 0) return false;                            // changed vertices without in-edges
+        n_items = hc.next_items;
+        edges += (double)hc.next_edges > g.pull_frac * (double)g.m ? g.m : (int64_t)hc.next_edges;
+        return true;
+    };
     for (int s = 1;; s++) {
-        IterCounters* ctr = &g.ctr[s & 1];
+        const int sl = s & 1;
+        IterCounters* ctr = &g.ctr[sl];
         CK(cudaMemsetAsync(ctr, 0, sizeof(IterCounters), g.stream));
-        CK(cudaEventRecord(g.ev[0], g.stream));
+        CK(cudaEventRecord(g.pev[sl][0], g.stream));
         // direction-optimised: a frontier whose in-edges cover most of the graph is swept by a full
         // in-place gather (every row owned by one warp, no atomics); sparse frontiers are pushed
-        const bool gather = s > 1 && !g.sync_sweeps && (double)edges_in > g.pull_frac * (double)g.m;
+        const bool gather = !piped && s > 1 && !g.sync_sweeps && (double)edges_in > g.pull_frac * (double)g.m;
+        gathers[sl] = gather;
         if (s == 1) {  // streaming register init, then the first sweep as a gather from init values
             CK(launch_init_registers(g));
             CK(cudaMemsetAsync(g.cm[1], 0, (size_t)g.n * W * sizeof(uint32_t), g.stream));
@@ -459,41 +498,45 @@ int simulate(bool blocked) {
             CK(launch_first(g, g.cm[1], g.bits[1], ctr, blocked, false));
         }
         else if (gather)
-            CK(launch_first(g, g.cm[s & 1], g.bits[s & 1], ctr, blocked, true));
+            CK(launch_first(g, g.cm[sl], g.bits[sl], ctr, blocked, true));
         else
-            CK(launch_sweep(g, items, n_items, g.cm[(s - 1) & 1], g.cm[s & 1], g.bits[s & 1], ctr, blocked));
-        CK(cudaEventRecord(g.ev[1], g.stream));
-        CK(launch_compact(g, g.bits[s & 1], g.bits[(s - 1) & 1], g.cm[s & 1], g.cm[(s - 1) & 1], g.items[s & 1], ctr));
+            CK(launch_sweep(g, items, n_items, g.cm[(s - 1) & 1], g.cm[sl], g.bits[sl], ctr, blocked, piped ? &g.ctr[(s - 1) & 1] : nullptr));
+        CK(cudaEventRecord(g.pev[sl][1], g.stream));
+        CK(launch_compact(g, g.bits[sl], g.bits[(s - 1) & 1], g.cm[sl], g.cm[(s - 1) & 1], g.items[sl], ctr));
         if (g.sync_sweeps) {  // Mold <- M (all rows after the first sweep, changed chunks after later ones)
             if (s == 1) CK(cudaMemcpyAsync(g.Mold, g.M, (size_t)g.n * g.J, cudaMemcpyDeviceToDevice, g.stream));
-            else CK(launch_commit(g, g.bits[s & 1]));
+            else CK(launch_commit(g, g.bits[sl]));
         }
-        TRY(readback(ctr, sizeof hc, &hc));
-        float t;
-        CK(cudaEventElapsedTime(&t, g.ev[0], g.ev[1]));
-        kms += t;
-        sweeps++;
-        launches++;
-        wedges += (int64_t)hc.win_edges;
-        {   // algorithmic bytes: records + one 32-B sector per worked window
-            const double nJ = (double)g.n * g.J, rec = 8.0 + (g.constT ? 0.0 : 4.0);
-            const double cmb = (double)g.n * ((double)g.J / 8.0 + 4.0);  // change mask + chunk word per vertex
-            if (s == 1) alg += rec * (double)g.m + nJ + cmb;               // + every row written once
-            else if (gather) alg += rec * (double)g.m + 2.0 * nJ + cmb + 32.0 * (double)hc.win_edges;
-            else alg += rec * (double)edges_in + 32.0 * (double)hc.win_edges;
-            if (gather) ngather++;
+        items = g.items[sl];
+        if (!piped) {
+            IterCounters hc;
+            CK(cudaMemcpyAsync(&hpc[sl], ctr, sizeof(IterCounters), cudaMemcpyDeviceToHost, g.stream));
+            CK(cudaEventRecord(g.pev[sl][2], g.stream));
+            CK(cudaEventSynchronize(g.pev[sl][2]));
+            hc = hpc[sl];
+            float t;
+            CK(cudaEventElapsedTime(&t, g.pev[sl][0], g.pev[sl][1]));
+            if (!account(s, hc, gather, t)) break;
+            last_done = s;
+            // enter the pipelined mode once the next frontier is clearly sparse (no gather sweep any more)
+            piped = g.pipeline && !g.sync_sweeps && s >= 2 && (double)hc.next_edges < 0.25 * g.pull_frac * (double)g.m;
+            continue;
         }
-        if (g.trace)
-            fprintf(stderr, "[im] sweep %d %s items %d edges %lld window_edges %llu -> changed %d next_items %d next_edges %llu big %d  %.3f ms\n",
-                    s, s == 1 ? "init+gather" : gather ? "gather" : "push", n_items, (long long)(s == 1 || gather ? g.m : (int64_t)edges_in),
-                    hc.win_edges, hc.changed, hc.next_items, hc.next_edges, hc.big, t);
-        edges_in = (int64_t)hc.next_edges;
-        dirty = hc.changed > 0;  // this sweep's change bits stay set until the next sweep consumes them
-        if (!((double)hc.changed / (double)g.n > eps_c)) break;  // Alg. 2 line 3 (eps_c = 0: nothing changed)
-        if (hc.next_items == 0) break;                            // changed vertices without in-edges
-        items = g.items[s & 1];
-        n_items = hc.next_items;
-        edges += (double)hc.next_edges > g.pull_frac * (double)g.m ? g.m : (int64_t)hc.next_edges;
+        CK(cudaMemcpyAsync(&hpc[sl], ctr, sizeof(IterCounters), cudaMemcpyDeviceToHost, g.stream));
+        CK(cudaEventRecord(g.pev[sl][2], g.stream));
+        // the previous sweep's counters (its copy was enqueued one iteration ago), unless already accounted
+        const int ps = (s - 1) & 1;
+        if (s - 1 > last_done) {
+            CK(cudaEventSynchronize(g.pev[ps][2]));
+            float t;
+            CK(cudaEventElapsedTime(&t, g.pev[ps][0], g.pev[ps][1]));
+            if (!account(s - 1, hpc[ps], gathers[ps], t)) {  // sweep s was enqueued with no items: a no-op
+                CK(cudaEventSynchronize(g.pev[sl][2]));
+                dirty = true;  // conservative: the no-op's compaction cleared sweep s-1's bits; a fresh build re-zeroes
+                break;
+            }
+            last_done = s - 1;
+        }
     }
     g.sweep_dirty = dirty;  // a last sweep without changes leaves every change buffer zero
     g.st.builds++;

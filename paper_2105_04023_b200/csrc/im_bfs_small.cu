@@ -80,12 +80,14 @@ __global__ void __launch_bounds__(SB_THREADS) k_bfs_small(BfsSmallArgs a) {
                 int lo, hi;
                 edge_window(f.y, T, sX, sS, a.J, lo, hi);
                 for (int w = lo >> 5; lo < hi && w <= (hi - 1) >> 5; ++w) {
-                    const uint32_t d = sD[wib][w];
-                    if (!d) continue;
+                    // only the simulations new at u (Delta_u) inside the window can be new at v: test those
                     const int i0 = max(lo, w << 5), i1 = min(hi, (w << 5) + 32);
-                    uint32_t live = 0u;
-                    for (int k = i0; k < i1; ++k) live |= ((sX[k] ^ f.y) < T) ? (1u << (k & 31)) : 0u;
-                    uint32_t nv = live & d;
+                    uint32_t cand = sD[wib][w] & bit_range(i0 & 31, (i1 - 1) & 31);
+                    uint32_t nv = 0u;
+                    for (; cand; cand &= cand - 1) {
+                        const int k = (w << 5) + __ffs(cand) - 1;
+                        nv |= ((sX[k] ^ f.y) < T) ? (1u << (k & 31)) : 0u;
+                    }
                     if (!nv) continue;
                     const size_t r = (size_t)f.x * W + w;
                     nv &= ~__ldcg(&a.vd[r].x);

@@ -110,6 +110,8 @@ struct Ctx {
     int32_t* big = nullptr;                  // long rows awaiting slicing
     bool sweep_dirty = true;   // change buffers may hold stale bits (fresh / aborted build)
     bool trace = false;        // IM_TRACE: per-sweep / per-level lines on stderr
+    bool pipeline = true;      // IM_PIPELINE=0 disables: sparse sweeps are enqueued before the previous one's counters are read
+    cudaEvent_t pev[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};  // per slot: sweep start / end, counters copied
     int slice_min = SEG;       // sweeps: in-rows longer than this are enumerated by hash slices (IM_SLICE_MIN)
     int slice_min_bfs = SEG;   // BFS levels: out-rows longer than this are enumerated by hash slices (IM_SLICE_MIN_BFS)
     int64_t list_max = 65536;  // cap of the lazy argmax candidate list length (IM_LIST_MAX)
@@ -210,14 +212,12 @@ cudaError_t launch_salt_tables(Ctx& c);
 cudaError_t launch_init_registers(Ctx& c);
 // one sweep over `items`; cm_in: per-simulation change mask of the previous sweep (null: no filter,
 // sweep 1); cm_out / bits_out: this sweep's change mask and chunk summary; counters in *ctr (zeroed)
+// nin non-null: the item count is read on the device from nin->next_items (n_items ignored)
 cudaError_t launch_sweep(Ctx& c, const int4* items, int n_items, const uint32_t* cm_in, uint32_t* cm_out,
-                         uint32_t* bits_out, IterCounters* ctr, bool blocked);
+                         uint32_t* bits_out, IterCounters* ctr, bool blocked, const IterCounters* nin = nullptr);
 cudaError_t launch_commit(Ctx& c, const uint32_t* bits_new);
 cudaError_t launch_slices_big(Ctx& c, const int32_t* big, const uint32_t* mask, const int32_t* offs, const uint2* rec,
                               int4* items_out, IterCounters* ctr, bool whole_dense);
-// bits_out: this sweep's chunk-change bits (red.or); counters in *ctr (zeroed by the caller)
-cudaError_t launch_sweep(Ctx& c, const int4* items, int n_items, const uint32_t* bits_in, uint32_t* bits_out,
-                         IterCounters* ctr, bool blocked);
 cudaError_t launch_estimate(Ctx& c, double* out);
 cudaError_t launch_estimate_sums(Ctx& c, int32_t* sums);
 cudaError_t launch_estimate_fin(Ctx& c, const int32_t* sums, double* out);

@@ -391,20 +391,23 @@ struct BfsArgs {
 // the Delta rows of a warp's 32 items are staged in shared memory once (coalesced), so an edge's
 // chain is record -> visited word only; edges are taken two per lane (e0, e0 + 32) and both visited
 // words are loaded before either is used.  Windows wider than DENSE_WIN go through the warp path.
+// live test only for the simulations of the window that are new at u (Delta_u): only those can be new at v
+__device__ __forceinline__ uint32_t bfs_word_live(const uint32_t* sX, uint32_t h, uint32_t T, uint32_t cand, int w) {
+    uint32_t nv = 0u;
+    for (; cand; cand &= cand - 1) {
+        const int k = (w << 5) + __ffs(cand) - 1;
+        nv |= ((sX[k] ^ h) < T) ? (1u << (k & 31)) : 0u;
+    }
+    return nv;
+}
 __device__ __forceinline__ void bfs_sparse(const uint32_t* sX, const uint32_t* dRow, uint32_t h, uint32_t T, int lo, int hi,
                                            int& w0, uint32_t& nv0, uint32_t& nv1) {
     w0 = lo >> 5;
     const int w1 = (hi - 1) >> 5;
-    const uint32_t d0 = dRow[w0], d1 = w1 != w0 ? dRow[w1] : 0u;
-    nv0 = nv1 = 0u;
-    if (!(d0 | d1)) return;
-    for (int i = lo; i < hi; ++i) {
-        const uint32_t ok = (sX[i] ^ h) < T ? 1u : 0u;
-        if ((i >> 5) == w0) nv0 |= ok << (i & 31);
-        else nv1 |= ok << (i & 31);
-    }
-    nv0 &= d0;
-    nv1 &= d1;
+    const uint32_t d0 = dRow[w0] & bit_range(lo & 31, w1 != w0 ? 31 : (hi - 1) & 31);
+    const uint32_t d1 = w1 != w0 ? dRow[w1] & bit_range(0, (hi - 1) & 31) : 0u;
+    nv0 = bfs_word_live(sX, h, T, d0, w0);
+    nv1 = bfs_word_live(sX, h, T, d1, w1);
 }
 
 template <bool CONST_T>
@@ -499,36 +502,23 @@ __global__ void __launch_bounds__(BLOCK, BFS_MINB) k_bfs_level2(BfsArgs a) {
                 if (n1) atomicOr(reinterpret_cast<ull*>(&a.vd[r + 1]), ((ull)n1 << 32) | n1);
                 if (n0 | n1) atomicOr(&a.nbits[f[s].x], (n0 ? 1u << w0[s] : 0u) | (n1 ? 2u << w0[s] : 0u));
             }
-            // wide windows: one simulation per lane (as in k_bfs_level)
+            // wide windows (> DENSE_WIN simulations, e.g. weighted cascade with small in-degree): each lane walks
+            // its own edge's window words and tests only the Delta_u simulations in them
 #pragma unroll
             for (int s = 0; s < EP; s++) {
-                uint32_t dmask = __ballot_sync(IM_FULL, dense[s]);
-                while (dmask) {
-                    const int l = __ffs(dmask) - 1;
-                    dmask &= dmask - 1;
-                    const uint32_t dv = __shfl_sync(IM_FULL, f[s].x, l), dh = __shfl_sync(IM_FULL, f[s].y, l);
-                    const uint32_t dT = __shfl_sync(IM_FULL, T[s], l);
-                    const int dlo = __shfl_sync(IM_FULL, lo[s], l), dhi = __shfl_sync(IM_FULL, hi[s], l);
-                    const int downer = __shfl_sync(IM_FULL, own[s], l);
-                    const int ww0 = dlo >> 5, ww1 = (dhi - 1) >> 5;
-                    uint32_t mylive = 0;
-                    int myw = -1;
-                    for (int w = ww0; w <= ww1; ++w) {
-                        const int i = 32 * w + lane;
-                        const uint32_t lv = __ballot_sync(IM_FULL, i >= dlo && i < dhi && (sX[i] ^ dh) < dT);
-                        if ((w & 31) == lane) {
-                            mylive = lv;
-                            myw = w;
-                        }
-                    }
-                    if (myw >= 0 && mylive) {
-                        uint32_t nv = sD[downer * W + myw] & mylive;
-                        if (nv) nv &= ~__ldcg(&a.vd[(size_t)dv * W + myw].x);
-                        if (nv) {
-                            atomicOr(reinterpret_cast<ull*>(&a.vd[(size_t)dv * W + myw]), ((ull)nv << 32) | nv);
-                            atomicOr(&a.nbits[dv], 1u << myw);
-                        }
-                    }
+                if (!dense[s]) continue;
+                const uint32_t* dRow = sD + own[s] * W;
+                for (int w = lo[s] >> 5; w <= (hi[s] - 1) >> 5; ++w) {
+                    const int i0 = max(lo[s], w << 5), i1 = min(hi[s], (w << 5) + 32);
+                    const uint32_t cand = dRow[w] & bit_range(i0 & 31, (i1 - 1) & 31);
+                    if (!cand) continue;
+                    uint32_t nv = bfs_word_live(sX, f[s].y, T[s], cand, w);
+                    if (!nv) continue;
+                    const size_t r = (size_t)f[s].x * W + w;
+                    nv &= ~__ldcg(&a.vd[r].x);
+                    if (!nv) continue;
+                    atomicOr(reinterpret_cast<ull*>(&a.vd[r]), ((ull)nv << 32) | nv);
+                    atomicOr(&a.nbits[f[s].x], 1u << w);
                 }
             }
         }

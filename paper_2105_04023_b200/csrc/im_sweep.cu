@@ -45,6 +45,8 @@ struct SweepArgs {
     uint32_t* cm_out;        // this sweep's per-simulation change mask
     uint32_t* bits_out;      // this sweep's per-vertex 32-simulation-chunk summary
     int ipw;                 // items per warp batch (<= 32; fewer when the sweep is small, to spread it over the SMs)
+    const IterCounters* nin; // non-null: n_items = nin->next_items on the device (pipelined sweeps), ipw derived here
+    int warps_max;           // resident warps of the grid (for the device-side ipw)
 };
 
 __device__ __forceinline__ ull vmax8(ull a, ull b) {
@@ -126,10 +128,24 @@ __device__ __forceinline__ uint32_t pull_word8_bits(const SweepArgs& a, uint32_t
     return record8(a, u, w, vmax_cas8(p, __ldcg(p), cand));
 }
 
-template <bool BLOCKED>
+template <bool BLOCKED, bool FILTER = false>
 __device__ __forceinline__ uint32_t pull_word8(const SweepArgs& a, const uint32_t* sX, uint32_t u, uint32_t v, int w,
                                                uint32_t h, uint32_t T, int lo, int hi) {
-    ull live = live8<BLOCKED>(a, sX, u, w, h, T, lo, hi);
+    ull live;
+    if (FILTER) {  // only the simulations of word w in which v changed last sweep can raise M_u: test those
+        uint32_t cand = (__ldg(&a.cm_in[(size_t)v * (a.J >> 5) + (w >> 2)]) >> ((w & 3) << 3)) & 0xFFu;
+        live = 0;
+        for (; cand; cand &= cand - 1) {
+            const int b = __ffs(cand) - 1, i = 8 * w + b;
+            if (i >= lo && i < hi && (sX[i] ^ h) < T) live |= 0xFFull << (8 * b);
+        }
+        if (BLOCKED && live) {
+            const uint32_t vb = (a.vis[(size_t)u * (a.J >> 5) + (w >> 2)] >> ((w & 3) << 3)) & 0xFFu;
+            live &= ~expand8(vb);
+        }
+    } else {
+        live = live8<BLOCKED>(a, sX, u, w, h, T, lo, hi);
+    }
     if (!live) return 0u;
     const size_t J8 = (size_t)(a.J >> 3);
     ull cand = a.Mr64[v * J8 + w] & live;
@@ -173,6 +189,12 @@ __global__ void __launch_bounds__(BLOCK, SWEEP_MINB) k_sweep(SweepArgs a) {
     __shared__ uint32_t sX[1024];
     __shared__ uint16_t sS[4098];
     __shared__ int sSlot[BLOCK / 32][32];
+    if (a.nin) {  // item count of the previous compaction, read on the device (no host round trip)
+        a.n_items = a.nin->next_items;
+        a.ipw = min(32, max(1, a.n_items / a.warps_max));
+        // blocks past the work exit before filling shared memory (the batch cursor hands out all items anyway)
+        if (a.n_items == 0 || (blockIdx.x > 0 && (int64_t)blockIdx.x * (BLOCK / 32) * a.ipw >= a.n_items)) return;
+    }
     for (int i = threadIdx.x; i < a.J; i += blockDim.x) sX[i] = a.Xs[i];
     for (int i = threadIdx.x; i < 4097; i += blockDim.x) sS[i] = a.s12[i];
     __syncthreads();
@@ -301,7 +323,7 @@ __global__ void __launch_bounds__(BLOCK, SWEEP_MINB) k_sweep(SweepArgs a) {
                     uint32_t dT = __shfl_sync(IM_FULL, T[s], l), dv = __shfl_sync(IM_FULL, vv[s], l);
                     int dlo = __shfl_sync(IM_FULL, lo[s], l), dhi = __shfl_sync(IM_FULL, hi[s], l);
                     uint32_t c = 0;
-                    for (int w = (dlo >> 3) + lane; w <= (dhi - 1) >> 3; w += 32) c |= pull_word8<BLOCKED>(a, sX, du, dv, w, dh, dT, dlo, dhi);
+                    for (int w = (dlo >> 3) + lane; w <= (dhi - 1) >> 3; w += 32) c |= pull_word8<BLOCKED, FILTER>(a, sX, du, dv, w, dh, dT, dlo, dhi);
                     c = __reduce_or_sync(IM_FULL, c);
                     if (lane == l) chg[s] |= c;
                 }
@@ -474,10 +496,11 @@ static void sweep_inst(int grid, cudaStream_t s, const SweepArgs& a) {
 }
 
 cudaError_t launch_sweep(Ctx& c, const int4* items, int n_items, const uint32_t* cm_in, uint32_t* cm_out,
-                         uint32_t* bits_out, IterCounters* ctr, bool blocked) {
+                         uint32_t* bits_out, IterCounters* ctr, bool blocked, const IterCounters* nin) {
     SweepArgs a;
     a.items = items;
     a.n_items = n_items;
+    a.nin = nin;
     a.ctr = ctr;
     a.rev = c.rev;
     a.revT = c.revT;
@@ -493,9 +516,10 @@ cudaError_t launch_sweep(Ctx& c, const int4* items, int n_items, const uint32_t*
     a.bits_out = bits_out;
     // items per warp batch: 32, or fewer so that a small sweep (long hub items) still fills the GPU
     const int64_t warps_max = (int64_t)c.max_blocks_sweep * (BLOCK / 32);
+    a.warps_max = (int)warps_max;
     a.ipw = (int)std::min<int64_t>(32, std::max<int64_t>(1, n_items / warps_max));
     int64_t want = ((int64_t)n_items + (int64_t)a.ipw * (BLOCK / 32) - 1) / ((int64_t)a.ipw * (BLOCK / 32));
-    int grid = (int)(want < 1 ? 1 : (want > c.max_blocks_sweep ? c.max_blocks_sweep : want));
+    int grid = nin ? c.max_blocks_sweep : (int)(want < 1 ? 1 : (want > c.max_blocks_sweep ? c.max_blocks_sweep : want));
     const bool ct = c.constT, f = cm_in != nullptr;
     if (!f) {
         if (ct) { if (blocked) sweep_inst<true, true, false>(grid, c.stream, a); else sweep_inst<true, false, false>(grid, c.stream, a); }
