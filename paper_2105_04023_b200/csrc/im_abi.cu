@@ -856,6 +856,47 @@ int im_select_seeds_ex(int32_t K, double eps_l, double eps_g, int32_t* out_seeds
                         k, n_items, n_v, hc.changed, hc.next_items, hc.next_edges, hc.big, hc.new_bits);
             cur ^= 1;
             g.st.bfs_levels++;
+            if (!g.pipeline || (long long)hc.next_edges <= 4 * g.small_edges) continue;
+            // Pipelined levels (large frontiers): level L is enqueued with its item count / frontier size read
+            // on the device, then level L-1's counters (copied to pinned memory) are read while L runs; the
+            // stop / small-frontier test is one level late, the level it then enqueued has no items if the
+            // BFS was over (a no-op).  Levels stay in stream order: the visited bits are those of the
+            // host-driven loop.
+            IterCounters* hpc = reinterpret_cast<IterCounters*>(static_cast<char*>(g.hpin) + 1024);
+            bool over = false;
+            int level_done = 0;  // levels whose counters were read (the first piped one has none yet)
+            for (int L = 0;; L++) {
+                const int nx = cur ^ 1;
+                CK(cudaMemsetAsync(&g.ctr[nx], 0, sizeof(IterCounters), g.stream));
+                CK(launch_bfs_level(g, cur, 0, ++g.bt, true));
+                CK(launch_bfs_clear(g, cur, 0, true));
+                CK(cudaMemcpyAsync(&hpc[nx], &g.ctr[nx], sizeof(IterCounters), cudaMemcpyDeviceToHost, g.stream));
+                CK(cudaEventRecord(g.pev[nx][2], g.stream));
+                cur = nx;
+                if (L == 0) {
+                    g.st.bfs_edges += (int64_t)hc.next_edges;  // its input, read by the host loop
+                    continue;
+                }
+                CK(cudaEventSynchronize(g.pev[cur ^ 1][2]));  // the level before the one just enqueued
+                const IterCounters pc = hpc[cur ^ 1];
+                level_done = L;
+                g.st.bfs_levels++;
+                if (pc.next_items == 0) {  // the level just enqueued had no items; its clear ran on the frontier
+                    CK(cudaEventSynchronize(g.pev[cur][2]));
+                    over = true;
+                    break;
+                }
+                g.st.bfs_edges += (int64_t)pc.next_edges;
+                if ((long long)pc.next_edges <= g.small_edges) break;  // back to the host loop (small path)
+            }
+            (void)level_done;
+            if (over) {
+                hc = IterCounters{};
+                break;
+            }
+            CK(cudaEventSynchronize(g.pev[cur][2]));  // the last enqueued level's counters
+            hc = hpc[cur];
+            g.st.bfs_levels++;
         }
         if (hc.changed > 0) CK(launch_bfs_clear(g, cur, hc.changed));  // frontier without work items
         pool_check = true;

@@ -236,8 +236,9 @@ cudaError_t launch_argmax_list(Ctx& c, int list_len);
 cudaError_t launch_seed_start(Ctx& c, int k);
 // one BFS level from frontier buffer cur (items, Delta) into cur^1, plus the compaction that builds
 // the next frontier's vertex list / items and adds the level's new bits to sigma
-cudaError_t launch_bfs_level(Ctx& c, int cur, int n_items, uint32_t tag);
-cudaError_t launch_bfs_clear(Ctx& c, int cur, int n_v);
+// piped: the item count / frontier size are read on the device from c.ctr[cur] (no host round trip)
+cudaError_t launch_bfs_level(Ctx& c, int cur, int n_items, uint32_t tag, bool piped = false);
+cudaError_t launch_bfs_clear(Ctx& c, int cur, int n_v, bool piped = false);
 // the rest of a BFS from frontier buffer cur (n_v vertices) in one single-block launch (result in c.sbo)
 cudaError_t launch_bfs_small(Ctx& c, int cur, int n_v, long long max_edges);
 cudaError_t launch_bfs_items(Ctx& c, int buf);

@@ -385,6 +385,8 @@ struct BfsArgs {
     const uint32_t* din;
     uint32_t* nbits;   // per vertex: which 32-simulation words got new bits in this level
     int ipw;           // items per warp batch (<= 32; fewer when the level is small, to spread it over the SMs)
+    const IterCounters* nin;  // non-null: n_items = nin->next_items on the device (pipelined levels), ipw derived here
+    int warps_max;
 };
 
 // Same level, reworked for memory-level parallelism (the level is bound by dependent random loads):
@@ -417,6 +419,11 @@ __global__ void __launch_bounds__(BLOCK, BFS_MINB) k_bfs_level2(BfsArgs a) {
     __shared__ uint32_t sX[1024];
     __shared__ uint16_t sS[4098];
     __shared__ int sSlot[BLOCK / 32][32];
+    if (a.nin) {  // the previous compaction's item count, read on the device (no host round trip)
+        a.n_items = a.nin->next_items;
+        a.ipw = min(32, max(1, a.n_items / a.warps_max));
+        if (a.n_items == 0 || (blockIdx.x > 0 && (int64_t)blockIdx.x * (BLOCK / 32) * a.ipw >= a.n_items)) return;
+    }
     for (int i = threadIdx.x; i < a.J; i += blockDim.x) sX[i] = a.Xs[i];
     for (int i = threadIdx.x; i < 4097; i += blockDim.x) sS[i] = a.s12[i];
     __syncthreads();
@@ -649,7 +656,9 @@ __global__ void k_bfs_items(int slice_min, const int32_t* __restrict__ vl, const
     }
 }
 
-__global__ void k_bfs_clear(int n_v, int W, const int32_t* __restrict__ vl, uint32_t* __restrict__ delta) {
+__global__ void k_bfs_clear(int n_v, int W, const int32_t* __restrict__ vl, uint32_t* __restrict__ delta,
+                            const IterCounters* nin = nullptr) {
+    if (nin) n_v = nin->changed;  // pipelined levels: the frontier size on the device
     int64_t total = (int64_t)n_v * W, stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += stride)
         delta[(size_t)vl[i / W] * W + (i % W)] = 0u;
@@ -812,11 +821,12 @@ cudaError_t launch_seed_start(Ctx& c, int k) {
                                           c.delta[0], c.off, c.bitems[0], c.bvl[0], &c.ctr[0], c.sigma_count, c.rec);
     return LAUNCHED(c);
 }
-cudaError_t launch_bfs_level(Ctx& c, int cur, int n_items, uint32_t tag) {
+cudaError_t launch_bfs_level(Ctx& c, int cur, int n_items, uint32_t tag, bool piped) {
     (void)tag;
     BfsArgs a;
     a.items = c.bitems[cur];
     a.n_items = n_items;
+    a.nin = piped ? &c.ctr[cur] : nullptr;
     a.ctr_next = &c.ctr[cur ^ 1];
     a.sigma_count = c.sigma_count;
     a.off = c.off;
@@ -832,11 +842,12 @@ cudaError_t launch_bfs_level(Ctx& c, int cur, int n_items, uint32_t tag) {
     // items per warp batch: 32, or fewer so that a small level still occupies every SM (each edge is a
     // chain of dependent loads, so a level is latency-bound unless many warps are in flight)
     const int64_t warps_max = (int64_t)c.max_blocks_bfs2 * (BLOCK / 32);
+    a.warps_max = (int)warps_max;
     a.ipw = (int)std::min<int64_t>(32, std::max<int64_t>(1, n_items / warps_max));
     int64_t want = ((int64_t)n_items + (int64_t)a.ipw * (BLOCK / 32) - 1) / ((int64_t)a.ipw * (BLOCK / 32));
     {
         const size_t smem = (size_t)BLOCK * (c.J >> 5) * sizeof(uint32_t);
-        int grid = (int)(want < 1 ? 1 : (want > c.max_blocks_bfs2 ? c.max_blocks_bfs2 : want));
+        int grid = piped ? c.max_blocks_bfs2 : (int)(want < 1 ? 1 : (want > c.max_blocks_bfs2 ? c.max_blocks_bfs2 : want));
         if (c.constT) k_bfs_level2<true><<<grid, BLOCK, smem, c.stream>>>(a);
         else k_bfs_level2<false><<<grid, BLOCK, smem, c.stream>>>(a);
     }
@@ -871,9 +882,12 @@ cudaError_t launch_bfs_clear_raw(Ctx& c, int n_v, int W, const int32_t* vl, uint
     return LAUNCHED(c);
 }
 
-cudaError_t launch_bfs_clear(Ctx& c, int cur, int n_v) {
+cudaError_t launch_bfs_clear(Ctx& c, int cur, int n_v, bool piped) {
     int W = c.J >> 5;
-    k_bfs_clear<<<grid_for(c, (int64_t)n_v * W), BLOCK, 0, c.stream>>>(n_v, W, c.bvl[cur], c.delta[cur]);
+    if (piped)  // the frontier size is read on the device from the counters that produced it
+        k_bfs_clear<<<c.num_sms * 4, BLOCK, 0, c.stream>>>(0, W, c.bvl[cur], c.delta[cur], &c.ctr[cur]);
+    else
+        k_bfs_clear<<<grid_for(c, (int64_t)n_v * W), BLOCK, 0, c.stream>>>(n_v, W, c.bvl[cur], c.delta[cur]);
     return LAUNCHED(c);
 }
 cudaError_t launch_error_check(Ctx& c, int k, int K, double eps_l, double eps_g) {
