@@ -79,21 +79,34 @@ __global__ void __launch_bounds__(SB_THREADS) k_bfs_small(BfsSmallArgs a) {
                 if (!T) continue;
                 int lo, hi;
                 edge_window(f.y, T, sX, sS, a.J, lo, hi);
-                for (int w = lo >> 5; lo < hi && w <= (hi - 1) >> 5; ++w) {
-                    // only the simulations new at u (Delta_u) inside the window can be new at v: test those
-                    const int i0 = max(lo, w << 5), i1 = min(hi, (w << 5) + 32);
-                    uint32_t cand = sD[wib][w] & bit_range(i0 & 31, (i1 - 1) & 31);
-                    uint32_t nv = 0u;
-                    for (; cand; cand &= cand - 1) {
-                        const int k = (w << 5) + __ffs(cand) - 1;
-                        nv |= ((sX[k] ^ f.y) < T) ? (1u << (k & 31)) : 0u;
+                if (lo >= hi) continue;
+                // the window's words 8 at a time: only the Delta_u simulations are tested, the visited
+                // words of the 8 are loaded together
+                const int wlo = lo >> 5, whi = (hi - 1) >> 5;
+                for (int wb = wlo; wb <= whi; wb += 8) {
+                    uint32_t nv[8], x[8];
+#pragma unroll
+                    for (int k = 0; k < 8; k++) {
+                        const int w = wb + k;
+                        nv[k] = 0u;
+                        if (w <= whi) {
+                            const int i0 = max(lo, w << 5), i1 = min(hi, (w << 5) + 32);
+                            uint32_t cand = sD[wib][w] & bit_range(i0 & 31, (i1 - 1) & 31);
+                            for (; cand; cand &= cand - 1) {
+                                const int q = (w << 5) + __ffs(cand) - 1;
+                                nv[k] |= ((sX[q] ^ f.y) < T) ? (1u << (q & 31)) : 0u;
+                            }
+                        }
                     }
-                    if (!nv) continue;
-                    const size_t r = (size_t)f.x * W + w;
-                    nv &= ~__ldcg(&a.vd[r].x);
-                    if (!nv) continue;
-                    atomicOr(reinterpret_cast<ull*>(&a.vd[r]), ((ull)nv << 32) | nv);
-                    if (atomicOr(&a.nbits[f.x], 1u << w) == 0u) vln[atomicAdd(&s_next, 1)] = (int32_t)f.x;
+#pragma unroll
+                    for (int k = 0; k < 8; k++) x[k] = nv[k] ? __ldcg(&a.vd[(size_t)f.x * W + wb + k].x) : 0u;
+#pragma unroll
+                    for (int k = 0; k < 8; k++) {
+                        const uint32_t n = nv[k] & ~x[k];
+                        if (!n) continue;
+                        atomicOr(reinterpret_cast<ull*>(&a.vd[(size_t)f.x * W + wb + k]), ((ull)n << 32) | n);
+                        if (atomicOr(&a.nbits[f.x], 1u << (wb + k)) == 0u) vln[atomicAdd(&s_next, 1)] = (int32_t)f.x;
+                    }
                 }
             }
             __syncwarp();

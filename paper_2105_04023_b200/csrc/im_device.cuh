@@ -96,6 +96,20 @@ __device__ __forceinline__ uint32_t bits_at(uint32_t lb, int lo, int s0, int n) 
     return (sh >= 0 ? (sh >= 32 ? 0u : lb >> sh) : (-sh >= 32 ? 0u : lb << -sh)) & ((1u << n) - 1u);
 }
 
+// Streamed edge records / thresholds / work items are read once per sweep or level: load them with the
+// evict-first hint so they do not push the reused register rows (hub rows) out of L2 (IM_STREAM_REC=0: plain)
+#ifndef IM_STREAM_REC
+#define IM_STREAM_REC 1
+#endif
+template <class T>
+__device__ __forceinline__ T ld_stream(const T* p) {
+#if IM_STREAM_REC
+    return __ldcs(p);
+#else
+    return *p;
+#endif
+}
+
 // byte mask from 4 bits: bit b -> byte b = 0xFF
 __device__ __forceinline__ uint32_t expand4(uint32_t b) { return ((b * 0x00204081u) & 0x01010101u) * 0xFFu; }
 

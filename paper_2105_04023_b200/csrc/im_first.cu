@@ -97,8 +97,8 @@ __device__ __forceinline__ void gather_edge(const FirstArgs& a, const uint32_t* 
     uint2 f = make_uint2(0, 0);
     uint32_t T = 0;
     if (e >= 0) {
-        f = a.fwd[e];
-        T = CONST_T ? a.T0 : a.fwdT[e];
+        f = ld_stream(&a.fwd[e]);
+        T = CONST_T ? a.T0 : ld_stream(&a.fwdT[e]);
     }
     gather_rec<CONST_T, BLOCKED, MEM>(a, sX, sS, sHJ, sVis, row, e >= 0, f, T, wcount);
 }
@@ -152,8 +152,8 @@ __device__ __forceinline__ void gather_multi(const FirstArgs& a, const uint32_t*
         f[k] = make_uint2(0, 0);
         T[k] = 0u;
         if (e < ee) {
-            f[k] = a.fwd[e];
-            T[k] = CONST_T ? a.T0 : a.fwdT[e];
+            f[k] = ld_stream(&a.fwd[e]);
+            T[k] = CONST_T ? a.T0 : ld_stream(&a.fwdT[e]);
         }
     }
     int lo[U], hi[U];
@@ -302,8 +302,8 @@ __global__ void __launch_bounds__(BLOCK, 5) k_first(FirstArgs a) {
         {
             const int eb0 = off_w[0], ee0 = off_w[1];
             if (ee0 - eb0 <= FIRST_BIG && eb0 + lane < ee0) {
-                nf = a.fwd[eb0 + lane];
-                nT = CONST_T ? a.T0 : a.fwdT[eb0 + lane];
+                nf = ld_stream(&a.fwd[eb0 + lane]);
+                nT = CONST_T ? a.T0 : ld_stream(&a.fwdT[eb0 + lane]);
             }
         }
         for (int u = base; u < end; ++u) {
@@ -315,8 +315,8 @@ __global__ void __launch_bounds__(BLOCK, 5) k_first(FirstArgs a) {
             if (u + 1 < end) {
                 const int eb1 = off_w[u + 1 - base], ee1 = off_w[u + 2 - base];
                 if (ee1 - eb1 <= FIRST_BIG && eb1 + lane < ee1) {
-                    nf = a.fwd[eb1 + lane];
-                    nT = CONST_T ? a.T0 : a.fwdT[eb1 + lane];
+                    nf = ld_stream(&a.fwd[eb1 + lane]);
+                    nT = CONST_T ? a.T0 : ld_stream(&a.fwdT[eb1 + lane]);
                 }
             }
             if (ee - eb > FIRST_BIG) continue;  // done by k_first_big

@@ -412,6 +412,37 @@ __device__ __forceinline__ void bfs_sparse(const uint32_t* sX, const uint32_t* d
     nv1 = bfs_word_live(sX, h, T, d1, w1);
 }
 
+// one edge (-> v) with a wide window [lo, hi): new bits = live & Delta_u & ~visited(v) per window word
+__device__ __forceinline__ void bfs_dense_edge(uint2* vd, uint32_t* nbits, const uint32_t* sX, const uint32_t* dRow, uint32_t v,
+                                               uint32_t h, uint32_t T, int lo, int hi, int W) {
+    const int wlo = lo >> 5, whi = (hi - 1) >> 5;
+    for (int wb = wlo; wb <= whi; wb += 8) {
+        uint32_t nv[8], x[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            const int w = wb + k;
+            nv[k] = 0u;
+            if (w <= whi) {
+                const int i0 = max(lo, w << 5), i1 = min(hi, (w << 5) + 32);
+                const uint32_t cand = dRow[w] & bit_range(i0 & 31, (i1 - 1) & 31);
+                if (cand) nv[k] = bfs_word_live(sX, h, T, cand, w);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 8; k++) x[k] = nv[k] ? __ldcg(&vd[(size_t)v * W + wb + k].x) : 0u;
+        uint32_t words = 0u;
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            const uint32_t n = nv[k] & ~x[k];
+            if (n) {
+                atomicOr(reinterpret_cast<ull*>(&vd[(size_t)v * W + wb + k]), ((ull)n << 32) | n);
+                words |= 1u << (wb + k);
+            }
+        }
+        if (words) atomicOr(&nbits[v], words);
+    }
+}
+
 template <bool CONST_T>
 __global__ void __launch_bounds__(BLOCK, BFS_MINB) k_bfs_level2(BfsArgs a) {
     constexpr int EP = BFS_EP;  // edges in flight per lane
@@ -443,13 +474,13 @@ __global__ void __launch_bounds__(BLOCK, BFS_MINB) k_bfs_level2(BfsArgs a) {
         const int it = base + lane;
         int u = 0, eb = 0, cnt = 0;
         if (lane < a.ipw && it < a.n_items) {
-            const int4 I = a.items[it];
+            const int4 I = ld_stream(&a.items[it]);
             u = I.x;
             eb = I.y;
             cnt = I.z - I.y;
         }
         __syncwarp();
-        for (int idx = lane; idx < 32 * W; idx += 32) {
+        for (int idx = lane; idx < a.ipw * W; idx += 32) {  // only the batch's ipw rows
             const int i = idx / W, w = idx - i * W;
             const int ui = __shfl_sync(IM_FULL, u, i);
             sD[idx] = i < a.ipw && base + i < a.n_items ? a.din[(size_t)ui * W + w] : 0u;
@@ -480,8 +511,8 @@ __global__ void __launch_bounds__(BLOCK, BFS_MINB) k_bfs_level2(BfsArgs a) {
             uint32_t T[EP];
 #pragma unroll
             for (int s = 0; s < EP; s++) {
-                f[s] = ed[s] >= 0 ? a.fwd[ed[s]] : make_uint2(0, 0);
-                T[s] = ed[s] >= 0 ? (CONST_T ? a.T0 : a.fwdT[ed[s]]) : 0u;
+                f[s] = ed[s] >= 0 ? ld_stream(&a.fwd[ed[s]]) : make_uint2(0, 0);
+                T[s] = ed[s] >= 0 ? (CONST_T ? a.T0 : ld_stream(&a.fwdT[ed[s]])) : 0u;
             }
             int lo[EP], hi[EP], w0[EP];
             uint32_t nv0[EP], nv1[EP], x0[EP], x1[EP];
@@ -510,23 +541,13 @@ __global__ void __launch_bounds__(BLOCK, BFS_MINB) k_bfs_level2(BfsArgs a) {
                 if (n0 | n1) atomicOr(&a.nbits[f[s].x], (n0 ? 1u << w0[s] : 0u) | (n1 ? 2u << w0[s] : 0u));
             }
             // wide windows (> DENSE_WIN simulations, e.g. weighted cascade with small in-degree): each lane walks
-            // its own edge's window words and tests only the Delta_u simulations in them
-#pragma unroll
+            // its own edge's window words, 8 at a time, testing only the Delta_u simulations in them; the
+            // visited words of the 8 are loaded together (independent loads in flight, not one per word)
+#pragma unroll 1
             for (int s = 0; s < EP; s++) {
                 if (!dense[s]) continue;
                 const uint32_t* dRow = sD + own[s] * W;
-                for (int w = lo[s] >> 5; w <= (hi[s] - 1) >> 5; ++w) {
-                    const int i0 = max(lo[s], w << 5), i1 = min(hi[s], (w << 5) + 32);
-                    const uint32_t cand = dRow[w] & bit_range(i0 & 31, (i1 - 1) & 31);
-                    if (!cand) continue;
-                    uint32_t nv = bfs_word_live(sX, f[s].y, T[s], cand, w);
-                    if (!nv) continue;
-                    const size_t r = (size_t)f[s].x * W + w;
-                    nv &= ~__ldcg(&a.vd[r].x);
-                    if (!nv) continue;
-                    atomicOr(reinterpret_cast<ull*>(&a.vd[r]), ((ull)nv << 32) | nv);
-                    atomicOr(&a.nbits[f[s].x], 1u << w);
-                }
+                bfs_dense_edge(a.vd, a.nbits, sX, dRow, f[s].x, f[s].y, T[s], lo[s], hi[s], W);
             }
         }
     }

@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(BLOCK, SWEEP_MINB) k_sweep(SweepArgs a) {
         int it = base + lane;
         int v = 0, eb = 0, cnt = 0;
         if (lane < a.ipw && it < a.n_items) {
-            int4 I = a.items[it];
+            int4 I = ld_stream(&a.items[it]);
             v = I.x;
             eb = I.y;
             cnt = I.z - I.y;
@@ -252,10 +252,10 @@ __global__ void __launch_bounds__(BLOCK, SWEEP_MINB) k_sweep(SweepArgs a) {
                 u[s] = h[s] = 0u;
                 if (idx < total) {
                     int e = oeb + (idx - ost);
-                    uint2 r = a.rev[e];
+                    uint2 r = ld_stream(&a.rev[e]);
                     u[s] = r.x;
                     h[s] = r.y;
-                    T[s] = CONST_T ? a.T0 : a.revT[e];
+                    T[s] = CONST_T ? a.T0 : ld_stream(&a.revT[e]);
                 }
             }
             bool sparse[NS];
