@@ -480,10 +480,11 @@ __global__ void __launch_bounds__(BLOCK, BFS_MINB) k_bfs_level2(BfsArgs a) {
             cnt = I.z - I.y;
         }
         __syncwarp();
-        for (int idx = lane; idx < a.ipw * W; idx += 32) {  // only the batch's ipw rows
-            const int i = idx / W, w = idx - i * W;
+        const int nst = (a.ipw * W + 31) & ~31;  // only the batch's ipw rows, whole warp per iteration (the shuffle)
+        for (int idx = lane; idx < nst; idx += 32) {
+            const int i = min(idx / W, 31), w = idx - (idx / W) * W;
             const int ui = __shfl_sync(IM_FULL, u, i);
-            sD[idx] = i < a.ipw && base + i < a.n_items ? a.din[(size_t)ui * W + w] : 0u;
+            if (idx < a.ipw * W) sD[idx] = base + i < a.n_items ? a.din[(size_t)ui * W + w] : 0u;
         }
         __syncwarp();
         const int incl = warp_incl_scan(cnt, lane);

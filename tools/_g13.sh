@@ -1,0 +1,8 @@
+set -x
+timeout 1200 python -m pytest tests -m gpu -x -q -k "not c5 and not c4" > gpurun_out/pytest13.log 2>&1; echo pytest rc=$?
+for c in c2 c1 c4 c3; do
+IM_BENCH_CONFIG=$c python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/b13_$c.json 2> gpurun_out/b13_$c.err; echo bench $c rc=$?
+done
+IM_LIB=variants/nostream.so IM_BENCH_CONFIG=c4 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/b13_c4_nostream.json 2>&1; echo ns rc=$?
+ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv --log-file gpurun_out/launches13_c2.csv python tools/profile_step.py --config c2 --what step > gpurun_out/ncu13_c2.log 2>&1; echo ncu c2 rc=$?
+ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv --log-file gpurun_out/launches13_c5.csv python tools/profile_step.py --config c3 --J 1024 --p 0.1 --t 0.3 --K 100 > gpurun_out/ncu13_c5.log 2>&1; echo ncu c5 rc=$?

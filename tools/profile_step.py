@@ -16,9 +16,23 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c3")
 ap.add_argument("--what", default="build", choices=["build", "step"])
 ap.add_argument("--K", type=int)
+ap.add_argument("--J", type=int, help="C5-style override of J (with --p / --t)")
+ap.add_argument("--p", type=float)
+ap.add_argument("--t", type=float)
 a = ap.parse_args()
 cfg = gen.CONFIGS[a.config]
 n, off, tgt, pr = gen.workload(cfg)
+if a.p is not None:
+    import dataclasses
+
+    import numpy as np
+
+    pr = np.full(len(tgt), a.p, np.float32)
+    cfg = dataclasses.replace(cfg, J=a.J or cfg.J, t=cfg.t if a.t is None else a.t)
+elif a.J:
+    import dataclasses
+
+    cfg = dataclasses.replace(cfg, J=a.J)
 t = time.time()
 im.im_load_csr(n, off, tgt, pr)
 im.im_build_sketches(cfg.J, cfg.salt_seed)
