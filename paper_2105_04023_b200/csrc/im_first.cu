@@ -85,60 +85,8 @@ __device__ __forceinline__ void merge_word(const FirstArgs& a, const uint32_t* s
     if (__vmaxu4(row[w], val) != row[w]) smem_vmax(&row[w], val);
 }
 
-// Wide windows (> DENSE_WIN simulations: p = 0.1 gives J/8, weighted cascade up to J): the dense edges of
-// the warp are taken four at a time, eight lanes per edge, each lane a 16-simulation chunk of the window:
-// one 16-byte load of M_v (MEM) or four init words (first sweep), a 16-bit live mask, then the live
-// registers merged into the shared row by word-wise byte-max CAS.  Four edges' chunk loads are in flight
-// together instead of one edge per warp pass.  `dense` / its operands are per lane; warp-uniform call.
-template <bool BLOCKED, bool MEM>
-__device__ __forceinline__ void gather_dense(const FirstArgs& a, const uint32_t* sX, const uint32_t* sHJ, const uint32_t* sVis,
-                                             uint32_t* row, bool dense, uint32_t v, uint32_t hv, uint32_t h, uint32_t T, int lo, int hi) {
-    const int lane = threadIdx.x & 31, grp = lane >> 3, q = lane & 7;
-    uint32_t dmask = __ballot_sync(IM_FULL, dense);
-    while (dmask) {
-        // the next (up to) four dense lanes of the warp, one per group of 8 lanes
-        int src = -1;
-        uint32_t m = dmask;
-        for (int g = 0; g < 4 && m; g++) {
-            const int l = __ffs(m) - 1;
-            m &= m - 1;
-            if (g == grp) src = l;
-        }
-        dmask = m;
-        const int sl = src < 0 ? 0 : src;
-        const uint32_t dh = __shfl_sync(IM_FULL, h, sl), dT = __shfl_sync(IM_FULL, T, sl), dhv = __shfl_sync(IM_FULL, hv, sl);
-        const uint32_t dv = __shfl_sync(IM_FULL, v, sl);
-        const int dlo = __shfl_sync(IM_FULL, lo, sl), dhi = __shfl_sync(IM_FULL, hi, sl);
-        if (src < 0) continue;
-        for (int c = (dlo >> 4) + q; c <= (dhi - 1) >> 4; c += 8) {
-            uint32_t live = 0u;
-#pragma unroll
-            for (int b = 0; b < 16; b++) {
-                const int i = 16 * c + b;
-                live |= ((i >= dlo) & (i < dhi) && (sX[i] ^ dh) < dT) ? (1u << b) : 0u;
-            }
-            if (BLOCKED && live) live &= ~((sVis[c >> 1] >> ((c & 1) << 4)) & 0xFFFFu);
-            if (!live) continue;
-            uint32_t x[4];
-            if (MEM) {
-                const uint4 t = *reinterpret_cast<const uint4*>(a.M + (size_t)dv * a.J + 16 * c);
-                x[0] = t.x; x[1] = t.y; x[2] = t.z; x[3] = t.w;
-            } else {
-#pragma unroll
-                for (int k = 0; k < 4; k++) x[k] = init_word(dhv, sHJ, 4 * c + k);
-            }
-#pragma unroll
-            for (int k = 0; k < 4; k++) {
-                const uint32_t val = x[k] & expand4((live >> (4 * k)) & 0xFu);
-                uint32_t* p = &row[4 * c + k];
-                if (val && __vmaxu4(*p, val) != *p) smem_vmax(p, val);
-            }
-        }
-    }
-}
-
 // `e` is this lane's edge (or -1); the loop around it must be warp-uniform.  Windows wider than
-// DENSE_WIN simulations go through gather_dense.
+// DENSE_WIN simulations (w close to 1) are walked by the whole warp, one word per lane.
 template <bool CONST_T, bool BLOCKED, bool MEM>
 __device__ __forceinline__ void gather_rec(const FirstArgs& a, const uint32_t* sX, const uint16_t* sS, const uint32_t* sHJ,
                                            const uint32_t* sVis, uint32_t* row, bool have, uint2 f, uint32_t Tin, uint32_t& wcount);
@@ -177,8 +125,16 @@ __device__ __forceinline__ void gather_rec(const FirstArgs& a, const uint32_t* s
     const bool dense = hi - lo > DENSE_WIN;
     if (!dense && lo < hi)
         for (int w = lo >> 2; w <= (hi - 1) >> 2; ++w) merge_word<BLOCKED, MEM>(a, sX, sHJ, sVis, row, v, hv, h, T, lo, hi, w);
-    (void)lane;
-    gather_dense<BLOCKED, MEM>(a, sX, sHJ, sVis, row, dense, v, hv, h, T, lo, hi);
+    uint32_t dmask = __ballot_sync(IM_FULL, dense);
+    while (dmask) {
+        int l = __ffs(dmask) - 1;
+        dmask &= dmask - 1;
+        uint32_t dh = __shfl_sync(IM_FULL, h, l), dT = __shfl_sync(IM_FULL, T, l), dhv = __shfl_sync(IM_FULL, hv, l);
+        uint32_t dv = __shfl_sync(IM_FULL, v, l);
+        int dlo = __shfl_sync(IM_FULL, lo, l), dhi = __shfl_sync(IM_FULL, hi, l);
+        for (int w = (dlo >> 2) + lane; w <= (dhi - 1) >> 2; w += 32)
+            merge_word<BLOCKED, MEM>(a, sX, sHJ, sVis, row, dv, dhv, dh, dT, dlo, dhi, w);
+    }
 }
 
 // U edges per lane, e0 + lane + k * stride (k < U): all records are loaded, then every window and
@@ -223,9 +179,17 @@ __device__ __forceinline__ void gather_multi(const FirstArgs& a, const uint32_t*
             for (int w = lo[k] >> 2; w <= (hi[k] - 1) >> 2; ++w)
                 merge_word<BLOCKED, MEM>(a, sX, sHJ, sVis, row, f[k].x, hv[k], f[k].y, T[k], lo[k], hi[k], w, w - (lo[k] >> 2) < 2,
                                          w == (lo[k] >> 2) ? pre[k] : pre2[k]);
-        gather_dense<BLOCKED, MEM>(a, sX, sHJ, sVis, row, hi[k] - lo[k] > DENSE_WIN, f[k].x, hv[k], f[k].y, T[k], lo[k], hi[k]);
+        uint32_t dmask = __ballot_sync(IM_FULL, hi[k] - lo[k] > DENSE_WIN);
+        while (dmask) {
+            const int l = __ffs(dmask) - 1;
+            dmask &= dmask - 1;
+            const uint32_t dh = __shfl_sync(IM_FULL, f[k].y, l), dT = __shfl_sync(IM_FULL, T[k], l), dhv = __shfl_sync(IM_FULL, hv[k], l);
+            const uint32_t dv = __shfl_sync(IM_FULL, f[k].x, l);
+            const int dlo = __shfl_sync(IM_FULL, lo[k], l), dhi = __shfl_sync(IM_FULL, hi[k], l);
+            for (int w = (dlo >> 2) + lane; w <= (dhi - 1) >> 2; w += 32)
+                merge_word<BLOCKED, MEM>(a, sX, sHJ, sVis, row, dv, dhv, dh, dT, dlo, dhi, w);
+        }
     }
-    (void)lane;
 }
 
 constexpr int FW = 8;  // max words per lane of the warp kernel (J/4/32 <= 8)
