@@ -4,7 +4,8 @@
 // After the first seed most greedy steps reach only a few hundred (vertex, simulation) pairs per
 // level, and the multi-block level path (k_bfs_level2 + k_bfs_compact + k_slices_big + k_bfs_clear,
 // one host round trip per level) is then dominated by launch and synchronisation latency.  This
-// kernel carries the same state (frontier list bvl[cur], Delta rows delta[cur], the {visited,
+// kernel runs as ONE thread-block cluster of SB_CLUSTER blocks (8 SMs, distributed shared memory for
+// the level counters, cluster barriers between levels) and carries the same state (frontier list bvl[cur], Delta rows delta[cur], the {visited,
 // new} pairs vd, R_G(S) words vis, per-vertex new-word flags nbits) through the levels with block
 // barriers: a warp takes a frontier vertex u and walks its whole out-row, lane per edge; for each
 // candidate word the simulations new at v are Delta_u & live & ~visited(v) (the same test and the
@@ -13,12 +14,17 @@
 // and are counted into sigma, exactly like k_bfs_compact.  When the next frontier's out-edges exceed
 // max_edges the kernel stops and leaves that frontier (list, Delta rows, counters) for the
 // multi-block path, which continues from it.
+#include <cooperative_groups.h>
+
 #include "im_device.cuh"
 #include "im_internal.h"
+
+namespace cg = cooperative_groups;
 
 namespace im {
 
 constexpr int SB_THREADS = 1024;
+constexpr int SB_CLUSTER = 8;  // blocks of the cluster (portable maximum), one per SM
 
 struct BfsSmallArgs {
     int J;
@@ -43,13 +49,20 @@ struct BfsSmallArgs {
 };
 
 template <bool CONST_T>
-__global__ void __launch_bounds__(SB_THREADS) k_bfs_small(BfsSmallArgs a) {
+__global__ void __cluster_dims__(SB_CLUSTER, 1, 1) __launch_bounds__(SB_THREADS) k_bfs_small(BfsSmallArgs a) {
     __shared__ uint32_t sX[1024];
     __shared__ uint16_t sS[4098];
     __shared__ uint32_t sD[SB_THREADS / 32][32];  // Delta row of each warp's frontier vertex
-    __shared__ int s_next;
+    __shared__ int s_next;                          // the cluster's level counters live in rank 0's copies
     __shared__ unsigned long long s_edges, s_bits;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int crank = (int)cluster.block_rank(), csize = (int)cluster.num_blocks();
+    int* c_next = cluster.map_shared_rank(&s_next, 0);
+    unsigned long long* c_edges = cluster.map_shared_rank(&s_edges, 0);
+    unsigned long long* c_bits = cluster.map_shared_rank(&s_bits, 0);
     const int W = a.J >> 5, lane = threadIdx.x & 31, wib = threadIdx.x >> 5, NWARP = SB_THREADS / 32;
+    const int gw = crank * NWARP + wib, GW = csize * NWARP;               // warp index / warps in the cluster
+    const int gt = crank * SB_THREADS + threadIdx.x, GT = csize * SB_THREADS;  // thread index / threads
     for (int i = threadIdx.x; i < a.J; i += blockDim.x) sX[i] = a.Xs[i];
     for (int i = threadIdx.x; i < 4097; i += blockDim.x) sS[i] = a.s12[i];
     int cur = a.cur, n_v = a.n_v, levels = 0;
@@ -61,14 +74,14 @@ __global__ void __launch_bounds__(SB_THREADS) k_bfs_small(BfsSmallArgs a) {
         int32_t* vln = cur ? a.vl0 : a.vl1;
         uint32_t* dcur = cur ? a.delta1 : a.delta0;
         uint32_t* dnxt = cur ? a.delta0 : a.delta1;
-        if (threadIdx.x == 0) {
+        if (crank == 0 && threadIdx.x == 0) {
             s_next = 0;
             s_edges = 0ull;
             s_bits = 0ull;
         }
-        __syncthreads();
-        // level: every out-edge of every frontier vertex (warp per vertex, lane per edge)
-        for (int i = wib; i < n_v; i += NWARP) {
+        cluster.sync();
+        // level: every out-edge of every frontier vertex (warp per vertex over the cluster, lane per edge)
+        for (int i = gw; i < n_v; i += GW) {
             const uint32_t u = (uint32_t)vl[i];
             if (lane < W) sD[wib][lane] = dcur[(size_t)u * W + lane];
             __syncwarp();
@@ -105,19 +118,19 @@ __global__ void __launch_bounds__(SB_THREADS) k_bfs_small(BfsSmallArgs a) {
                         const uint32_t n = nv[k] & ~x[k];
                         if (!n) continue;
                         atomicOr(reinterpret_cast<ull*>(&a.vd[(size_t)f.x * W + wb + k]), ((ull)n << 32) | n);
-                        if (atomicOr(&a.nbits[f.x], 1u << (wb + k)) == 0u) vln[atomicAdd(&s_next, 1)] = (int32_t)f.x;
+                        if (atomicOr(&a.nbits[f.x], 1u << (wb + k)) == 0u) vln[atomicAdd(c_next, 1)] = (int32_t)f.x;
                     }
                 }
             }
             __syncwarp();
         }
-        __syncthreads();
+        cluster.sync();
         // the level's frontier is consumed: clear its Delta rows (this buffer is the next level's output)
-        for (int64_t i = threadIdx.x; i < (int64_t)n_v * W; i += blockDim.x) dcur[(size_t)vl[i / W] * W + (i % W)] = 0u;
-        const int nn = s_next;
+        for (int64_t i = gt; i < (int64_t)n_v * W; i += GT) dcur[(size_t)vl[i / W] * W + (i % W)] = 0u;
+        const int nn = *c_next;
         // compaction: new bits -> next Delta rows, R_G(S) words and sigma; out-edges of the next frontier
         unsigned long long bits = 0ull, ed = 0ull;
-        for (int i = threadIdx.x; i < nn; i += blockDim.x) {
+        for (int i = gt; i < nn; i += GT) {
             const uint32_t v = (uint32_t)vln[i];
             uint32_t b = a.nbits[v];
             a.nbits[v] = 0u;
@@ -132,26 +145,28 @@ __global__ void __launch_bounds__(SB_THREADS) k_bfs_small(BfsSmallArgs a) {
             ed += (unsigned long long)(a.off[v + 1] - a.off[v]);
         }
         bits = __reduce_add_sync(IM_FULL, (uint32_t)bits);  // < 2^32 per warp (<= nn * J bits)
-        if (lane == 0 && bits) atomicAdd(&s_bits, bits);
-        if (ed) atomicAdd(&s_edges, ed);
-        __syncthreads();
-        edges_total += (long long)s_edges;  // the next level's enumerated edges
-        if (threadIdx.x == 0 && s_bits) *a.sigma_count += s_bits;
+        if (lane == 0 && bits) atomicAdd(c_bits, bits);
+        if (ed) atomicAdd(c_edges, ed);
+        cluster.sync();
+        const unsigned long long lev_edges = *c_edges, lev_bits = *c_bits;
+        edges_total += (long long)lev_edges;  // the next level's enumerated edges
+        if (crank == 0 && threadIdx.x == 0 && lev_bits) *a.sigma_count += lev_bits;
         levels++;
         cur ^= 1;
         n_v = nn;
-        if (n_v > 0 && (long long)s_edges > a.max_edges) {
+        if (n_v > 0 && (long long)lev_edges > a.max_edges) {
             bailed = true;
             break;
         }
-        __syncthreads();
+        cluster.sync();  // every block has read the counters before rank 0 resets them
     }
-    if (threadIdx.x == 0) {
+    cluster.sync();
+    if (crank == 0 && threadIdx.x == 0) {
         a.out->levels = levels;
         a.out->cur = cur;
         a.out->n_v = n_v;
         a.out->bailed = bailed ? 1 : 0;
-        a.out->edges = bailed ? edges_total - (long long)s_edges : edges_total;
+        a.out->edges = bailed ? edges_total - (long long)s_edges : edges_total;  // rank 0: its own s_edges
         IterCounters z{};
         z.changed = n_v;
         a.ctr[cur] = z;  // the multi-block path builds this frontier's items (k_bfs_items reads .changed)
@@ -180,8 +195,8 @@ cudaError_t launch_bfs_small(Ctx& c, int cur, int n_v, long long max_edges) {
     a.n_v = n_v;
     a.max_edges = max_edges;
     a.out = c.sbo;
-    if (c.constT) k_bfs_small<true><<<1, SB_THREADS, 0, c.stream>>>(a);
-    else k_bfs_small<false><<<1, SB_THREADS, 0, c.stream>>>(a);
+    if (c.constT) k_bfs_small<true><<<SB_CLUSTER, SB_THREADS, 0, c.stream>>>(a);
+    else k_bfs_small<false><<<SB_CLUSTER, SB_THREADS, 0, c.stream>>>(a);
     return LAUNCHED(c);
 }
 

@@ -128,7 +128,7 @@ struct Ctx {
     uint32_t* nbits = nullptr;   // BFS: per-vertex words with new bits in the current level
     StepDev* rec = nullptr;
     BfsSmallOut* sbo = nullptr;
-    long long small_edges = 8192;  // frontiers with at most this many out-edges: single-block BFS (IM_SMALL_EDGES; 0 = off)
+    long long small_edges = 32768;  // frontiers with at most this many out-edges: one-cluster BFS (IM_SMALL_EDGES; 0 = off)
     double* varsigma = nullptr;
     ull* key = nullptr;
     int* first = nullptr;

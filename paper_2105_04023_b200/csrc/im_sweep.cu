@@ -311,31 +311,21 @@ __global__ void __launch_bounds__(BLOCK, SWEEP_MINB) k_sweep(SweepArgs a) {
                     for (int w = (lo[s] >> 3) + 1; w <= (hi[s] - 1) >> 3; ++w)
                         chg[s] |= pull_word8_bits<BLOCKED>(a, u[s], vv[s], w, lb[s], lo[s]);
             }
-            // wide windows (p = 0.1: J/8 simulations; weighted cascade up to J): the dense edges of the warp four at
-            // a time, eight lanes per edge, each lane 8-simulation words of the window (their M_v loads and CASes in
-            // flight together); the raised chunk bits go straight to u's chunk word
+            // wide windows (w close to 1, weighted cascade): the whole warp walks the window
 #pragma unroll
             for (int s = 0; s < NS; s++) {
                 uint32_t dmask = __ballot_sync(IM_FULL, hi[s] - lo[s] > DENSE_WIN);
                 wcount += __popc(__ballot_sync(IM_FULL, lo[s] < hi[s]));
-                const int grp = lane >> 3, q = lane & 7;
                 while (dmask) {
-                    int src = -1;
-                    uint32_t m = dmask;
-                    for (int g = 0; g < 4 && m; g++) {
-                        const int l = __ffs(m) - 1;
-                        m &= m - 1;
-                        if (g == grp) src = l;
-                    }
-                    dmask = m;
-                    const int sl = src < 0 ? 0 : src;
-                    const uint32_t du = __shfl_sync(IM_FULL, u[s], sl), dh = __shfl_sync(IM_FULL, h[s], sl);
-                    const uint32_t dT = __shfl_sync(IM_FULL, T[s], sl), dv = __shfl_sync(IM_FULL, vv[s], sl);
-                    const int dlo = __shfl_sync(IM_FULL, lo[s], sl), dhi = __shfl_sync(IM_FULL, hi[s], sl);
-                    if (src < 0) continue;
+                    int l = __ffs(dmask) - 1;
+                    dmask &= dmask - 1;
+                    uint32_t du = __shfl_sync(IM_FULL, u[s], l), dh = __shfl_sync(IM_FULL, h[s], l);
+                    uint32_t dT = __shfl_sync(IM_FULL, T[s], l), dv = __shfl_sync(IM_FULL, vv[s], l);
+                    int dlo = __shfl_sync(IM_FULL, lo[s], l), dhi = __shfl_sync(IM_FULL, hi[s], l);
                     uint32_t c = 0;
-                    for (int w = (dlo >> 3) + q; w <= (dhi - 1) >> 3; w += 8) c |= pull_word8<BLOCKED, FILTER>(a, sX, du, dv, w, dh, dT, dlo, dhi);
-                    if (c) atomicOr(&a.bits_out[du], c);
+                    for (int w = (dlo >> 3) + lane; w <= (dhi - 1) >> 3; w += 32) c |= pull_word8<BLOCKED, FILTER>(a, sX, du, dv, w, dh, dT, dlo, dhi);
+                    c = __reduce_or_sync(IM_FULL, c);
+                    if (lane == l) chg[s] |= c;
                 }
             }
             // which 32-simulation chunks of u rose (fire-and-forget; the compaction builds the next frontier)
