@@ -25,6 +25,7 @@ namespace im {
 
 constexpr int SB_THREADS = 1024;
 constexpr int SB_CLUSTER = 8;  // blocks of the cluster (portable maximum), one per SM
+constexpr int SB_LONG = 256;   // frontier rows longer than this are split over the whole cluster
 
 struct BfsSmallArgs {
     int J;
@@ -46,18 +47,60 @@ struct BfsSmallArgs {
     int cur, n_v;
     long long max_edges;
     BfsSmallOut* out;
+    int32_t* longv;  // the level's long frontier rows (scratch, n entries)
 };
+
+// one out-edge e of a frontier vertex with Delta row dRow (shared): the new (v, simulation) pairs
+template <bool CONST_T>
+__device__ __forceinline__ void small_edge(const BfsSmallArgs& a, const uint32_t* sX, const uint16_t* sS, const uint32_t* dRow,
+                                           int e, int W, int32_t* vln, int* c_next) {
+                    const uint2 f = a.fwd[e];
+                    const uint32_t T = CONST_T ? a.T0 : a.fwdT[e];
+                    if (!T) return;
+                    int lo, hi;
+                    edge_window(f.y, T, sX, sS, a.J, lo, hi);
+                    if (lo >= hi) return;
+                    // the window's words 8 at a time: only the Delta_u simulations are tested, the visited
+                    // words of the 8 are loaded together
+                    const int wlo = lo >> 5, whi = (hi - 1) >> 5;
+                    for (int wb = wlo; wb <= whi; wb += 8) {
+                        uint32_t nv[8], x[8];
+    #pragma unroll
+                        for (int k = 0; k < 8; k++) {
+                            const int w = wb + k;
+                            nv[k] = 0u;
+                            if (w <= whi) {
+                                const int i0 = max(lo, w << 5), i1 = min(hi, (w << 5) + 32);
+                                uint32_t cand = dRow[w] & bit_range(i0 & 31, (i1 - 1) & 31);
+                                for (; cand; cand &= cand - 1) {
+                                    const int q = (w << 5) + __ffs(cand) - 1;
+                                    nv[k] |= ((sX[q] ^ f.y) < T) ? (1u << (q & 31)) : 0u;
+                                }
+                            }
+                        }
+    #pragma unroll
+                        for (int k = 0; k < 8; k++) x[k] = nv[k] ? __ldcg(&a.vd[(size_t)f.x * W + wb + k].x) : 0u;
+    #pragma unroll
+                        for (int k = 0; k < 8; k++) {
+                            const uint32_t n = nv[k] & ~x[k];
+                            if (!n) continue;
+                            atomicOr(reinterpret_cast<ull*>(&a.vd[(size_t)f.x * W + wb + k]), ((ull)n << 32) | n);
+                            if (atomicOr(&a.nbits[f.x], 1u << (wb + k)) == 0u) vln[atomicAdd(c_next, 1)] = (int32_t)f.x;
+                        }
+                    }
+}
 
 template <bool CONST_T>
 __global__ void __cluster_dims__(SB_CLUSTER, 1, 1) __launch_bounds__(SB_THREADS) k_bfs_small(BfsSmallArgs a) {
     __shared__ uint32_t sX[1024];
     __shared__ uint16_t sS[4098];
     __shared__ uint32_t sD[SB_THREADS / 32][32];  // Delta row of each warp's frontier vertex
-    __shared__ int s_next;                          // the cluster's level counters live in rank 0's copies
+    __shared__ int s_next, s_nlong;                 // the cluster's level counters live in rank 0's copies
     __shared__ unsigned long long s_edges, s_bits;
     cg::cluster_group cluster = cg::this_cluster();
     const int crank = (int)cluster.block_rank(), csize = (int)cluster.num_blocks();
     int* c_next = cluster.map_shared_rank(&s_next, 0);
+    int* c_nlong = cluster.map_shared_rank(&s_nlong, 0);
     unsigned long long* c_edges = cluster.map_shared_rank(&s_edges, 0);
     unsigned long long* c_bits = cluster.map_shared_rank(&s_bits, 0);
     const int W = a.J >> 5, lane = threadIdx.x & 31, wib = threadIdx.x >> 5, NWARP = SB_THREADS / 32;
@@ -76,6 +119,7 @@ __global__ void __cluster_dims__(SB_CLUSTER, 1, 1) __launch_bounds__(SB_THREADS)
         uint32_t* dnxt = cur ? a.delta0 : a.delta1;
         if (crank == 0 && threadIdx.x == 0) {
             s_next = 0;
+            s_nlong = 0;
             s_edges = 0ull;
             s_bits = 0ull;
         }
@@ -86,45 +130,27 @@ __global__ void __cluster_dims__(SB_CLUSTER, 1, 1) __launch_bounds__(SB_THREADS)
             if (lane < W) sD[wib][lane] = dcur[(size_t)u * W + lane];
             __syncwarp();
             const int eb = a.off[u], ee = a.off[u + 1];
-            for (int e = eb + lane; e < ee; e += 32) {
-                const uint2 f = a.fwd[e];
-                const uint32_t T = CONST_T ? a.T0 : a.fwdT[e];
-                if (!T) continue;
-                int lo, hi;
-                edge_window(f.y, T, sX, sS, a.J, lo, hi);
-                if (lo >= hi) continue;
-                // the window's words 8 at a time: only the Delta_u simulations are tested, the visited
-                // words of the 8 are loaded together
-                const int wlo = lo >> 5, whi = (hi - 1) >> 5;
-                for (int wb = wlo; wb <= whi; wb += 8) {
-                    uint32_t nv[8], x[8];
-#pragma unroll
-                    for (int k = 0; k < 8; k++) {
-                        const int w = wb + k;
-                        nv[k] = 0u;
-                        if (w <= whi) {
-                            const int i0 = max(lo, w << 5), i1 = min(hi, (w << 5) + 32);
-                            uint32_t cand = sD[wib][w] & bit_range(i0 & 31, (i1 - 1) & 31);
-                            for (; cand; cand &= cand - 1) {
-                                const int q = (w << 5) + __ffs(cand) - 1;
-                                nv[k] |= ((sX[q] ^ f.y) < T) ? (1u << (q & 31)) : 0u;
-                            }
-                        }
-                    }
-#pragma unroll
-                    for (int k = 0; k < 8; k++) x[k] = nv[k] ? __ldcg(&a.vd[(size_t)f.x * W + wb + k].x) : 0u;
-#pragma unroll
-                    for (int k = 0; k < 8; k++) {
-                        const uint32_t n = nv[k] & ~x[k];
-                        if (!n) continue;
-                        atomicOr(reinterpret_cast<ull*>(&a.vd[(size_t)f.x * W + wb + k]), ((ull)n << 32) | n);
-                        if (atomicOr(&a.nbits[f.x], 1u << (wb + k)) == 0u) vln[atomicAdd(c_next, 1)] = (int32_t)f.x;
-                    }
-                }
+            const bool longrow = ee - eb > SB_LONG;
+            if (longrow) {  // walked by every warp of the cluster in phase B
+                if (lane == 0) a.longv[atomicAdd(c_nlong, 1)] = (int32_t)u;
+                continue;
             }
+            for (int e = eb + lane; e < ee; e += 32) small_edge<CONST_T>(a, sX, sS, sD[wib], e, W, vln, c_next);
             __syncwarp();
         }
         cluster.sync();
+        // phase B: the long rows of the frontier (> SB_LONG out-edges, e.g. hubs), each split over every warp
+        // of the cluster (32 edges per warp pass) instead of one warp walking it alone
+        const int nlong = *c_nlong;
+        for (int li = 0; li < nlong; li++) {
+            const uint32_t u = (uint32_t)a.longv[li];
+            if (lane < W) sD[wib][lane] = dcur[(size_t)u * W + lane];
+            __syncwarp();
+            const int eb = a.off[u], ee = a.off[u + 1];
+            for (int e = eb + gw * 32 + lane; e < ee; e += GW * 32) small_edge<CONST_T>(a, sX, sS, sD[wib], e, W, vln, c_next);
+            __syncwarp();
+        }
+        if (nlong) cluster.sync();
         // the level's frontier is consumed: clear its Delta rows (this buffer is the next level's output)
         for (int64_t i = gt; i < (int64_t)n_v * W; i += GT) dcur[(size_t)vl[i / W] * W + (i % W)] = 0u;
         const int nn = *c_next;
@@ -195,6 +221,7 @@ cudaError_t launch_bfs_small(Ctx& c, int cur, int n_v, long long max_edges) {
     a.n_v = n_v;
     a.max_edges = max_edges;
     a.out = c.sbo;
+    a.longv = c.big;
     if (c.constT) k_bfs_small<true><<<SB_CLUSTER, SB_THREADS, 0, c.stream>>>(a);
     else k_bfs_small<false><<<SB_CLUSTER, SB_THREADS, 0, c.stream>>>(a);
     return LAUNCHED(c);
