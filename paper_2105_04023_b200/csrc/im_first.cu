@@ -42,6 +42,9 @@ struct FirstArgs {
     const int4* big_units;  // {u, eb, ee}: rows with > FIRST_BIG out-edges in units of <= FIRST_CHUNK (k_first_big)
     int n_big;
     int vb;              // vertices per warp batch (<= 256; fewer on small graphs so every warp gets work)
+    bool small_rows;     // rows <= 32 edges take the window-words-only path (false: wide windows, e.g. p = 0.1 with
+                         // J >= 512, where every lane walking its own 64+-simulation window serially contends in
+                         // shared memory; the whole-row path merges wide windows with lanes over words instead)
 };
 
 // hash(v) of Alg. 1 line 4, recomputed per edge (a per-build table of it read per edge measured no faster)
@@ -327,7 +330,7 @@ __global__ void __launch_bounds__(BLOCK, 5) k_first(FirstArgs a) {
                 }
                 continue;
             }
-            if (ee - eb <= 32) {  // sparse path: touch only the window words
+            if (ee - eb <= 32 && a.small_rows) {  // sparse path: touch only the window words
                 if (BLOCKED && lane < W) sVis[wib][lane] = a.vis[(size_t)u * W + lane];
                 __syncwarp();
                 first_small<CONST_T, BLOCKED, MEM>(a, sX, sS, sHJ, sVis[wib], row, sBm[wib], sCm[wib], (uint32_t)u, eb + lane < ee, cf, cT,
@@ -482,6 +485,8 @@ cudaError_t launch_first(Ctx& c, uint32_t* cm_out, uint32_t* bits_out, IterCount
     a.ctr = ctr;
     a.big_units = c.fbig;
     a.n_big = c.n_fbig;
+    // nominal candidate window of a constant threshold: J * 2^B0 / 2^31 simulations
+    a.small_rows = !c.constT || ((int64_t)c.J << c.B0) <= ((int64_t)DENSE_WIN << 31);
     {   // a dependent chain of loads per vertex: spread small graphs over every resident warp
         const int64_t warps = (int64_t)c.max_blocks_first * (BLOCK / 32);
         a.vb = (int)std::min<int64_t>(256, std::max<int64_t>(1, c.n / warps));
