@@ -115,6 +115,7 @@ int ensure_device() {
     if (const char* sm = getenv("IM_SLICE_MIN")) g.slice_min = atoi(sm);
     if (const char* sb = getenv("IM_SLICE_MIN_BFS")) g.slice_min_bfs = atoi(sb);
     if (const char* se = getenv("IM_SMALL_EDGES")) g.small_edges = atoll(se);
+    if (const char* ss = getenv("IM_SMALL_SWEEP")) g.small_sweep_edges = atoll(ss);
     if (!g.own_stream) CK(cudaStreamCreateWithFlags(&g.own_stream, cudaStreamNonBlocking));
     if (!g.stream) g.stream = g.own_stream;
     if (!g.hpin) CK(cudaMallocHost(&g.hpin, 4096));
@@ -150,7 +151,7 @@ void release_all() {
     dfree(g.inS); dfree(g.MS); dfree(g.btag); dfree(g.nbits); dfree(g.gain); dfree(g.big); dfree(g.list); dfree(g.lcount); dfree(g.hist);
     dfree(g.off); dfree(g.fwd); dfree(g.fwdT); dfree(g.roff); dfree(g.rev); dfree(g.revT); dfree(g.ritems); dfree(g.fbig);
     dfree(g.ftidx); dfree(g.rtidx); dfree(g.ftab); dfree(g.rtab); dfree(g.t_tabrows);
-    dfree(g.ctr); dfree(g.rec); dfree(g.sbo); dfree(g.varsigma); dfree(g.key); dfree(g.first); dfree(g.sigma_count);
+    dfree(g.ctr); dfree(g.rec); dfree(g.sbo); dfree(g.sso); dfree(g.varsigma); dfree(g.key); dfree(g.first); dfree(g.sigma_count);
     dfree(g.lval); dfree(g.sigma_g); dfree(g.bcount); dfree(g.Mold); dfree(g.gslice); dfree(g.llist); dfree(g.lcnt_all);
     dfree(g.ev_vis); dfree(g.ev_nbits); dfree(g.ev_ctr); dfree(g.ev_count);
     for (int i = 0; i < 2; i++) { dfree(g.ev_delta[i]); dfree(g.ev_items[i]); dfree(g.ev_vl[i]); }
@@ -293,6 +294,7 @@ int load_common(int32_t n, int64_t m, const int32_t* d_off_src, const int32_t* d
     TRY(dalloc(g.ctr, 2));
     TRY(dalloc(g.rec, 1));
     TRY(dalloc(g.sbo, 1));
+    TRY(dalloc(g.sso, 1));
     TRY(dalloc(g.varsigma, 1));
     TRY(dalloc(g.key, 1));
     TRY(dalloc(g.first, 1));
@@ -518,6 +520,46 @@ int simulate(bool blocked) {
             CK(cudaEventElapsedTime(&t, g.pev[sl][0], g.pev[sl][1]));
             if (!account(s, hc, gather, t)) break;
             last_done = s;
+            if (!g.sync_sweeps && g.small_sweep_edges > 0 && (long long)hc.next_edges <= g.small_sweep_edges) {
+                // the rest of the build in one cluster launch (k_sweep_small) while the frontier stays small
+                CK(cudaEventRecord(g.pev[sl][0], g.stream));
+                CK(launch_sweep_small(g, g.items[sl], hc.next_items, s + 1, blocked, g.small_sweep_edges));
+                CK(cudaEventRecord(g.pev[sl][1], g.stream));
+                SweepSmallOut so;
+                TRY(readback(g.sso, sizeof so, &so));
+                float ts;
+                CK(cudaEventElapsedTime(&ts, g.pev[sl][0], g.pev[sl][1]));
+                kms += ts;
+                sweeps += so.sweeps;
+                launches++;
+                wedges += so.win_edges;
+                edges += so.edges - (int64_t)hc.next_edges;  // account() already counted the first one's in-edges
+                alg += (8.0 + (g.constT ? 0.0 : 4.0)) * (double)so.edges + 32.0 * (double)so.win_edges;
+                if (g.trace)
+                    fprintf(stderr, "[im] sweeps %d..%d in one cluster launch: %lld edges, %lld window_edges -> %s, %.3f ms\n", s + 1,
+                            so.t_next - 1, so.edges, so.win_edges, so.bailed ? "frontier handed back" : "fixpoint", ts);
+                if (!so.bailed) {
+                    dirty = false;
+                    break;
+                }
+                // hand back: compact the last cluster sweep's changes (its input masks were cleared in the kernel)
+                const int tl = so.t_next - 1, tb = tl & 1;
+                CK(cudaMemsetAsync(&g.ctr[tb], 0, sizeof(IterCounters), g.stream));
+                CK(launch_compact(g, g.bits[tb], g.bits[tb ^ 1], g.cm[tb], g.cm[tb ^ 1], g.items[tb], &g.ctr[tb]));
+                IterCounters hc2;
+                TRY(readback(&g.ctr[tb], sizeof hc2, &hc2));
+                if (hc2.next_items == 0) {
+                    dirty = hc2.changed > 0;
+                    break;
+                }
+                n_items = hc2.next_items;
+                edges_in = (int64_t)hc2.next_edges;
+                edges += (int64_t)hc2.next_edges;
+                items = g.items[tb];
+                s = tl;
+                last_done = s;
+                continue;
+            }
             // enter the pipelined mode once the next frontier is clearly sparse (no gather sweep any more)
             piped = g.pipeline && !g.sync_sweeps && s >= 2 && (double)hc.next_edges < 0.25 * g.pull_frac * (double)g.m;
             continue;

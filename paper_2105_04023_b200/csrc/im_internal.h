@@ -45,6 +45,17 @@ struct BfsSmallOut {
     long long edges; // edges enumerated by the levels run, after the entry frontier's
 };
 
+// result of a one-cluster small-frontier sweep run (im_sweep.cu k_sweep_small)
+struct SweepSmallOut {
+    int sweeps;            // sweeps run
+    int changed;           // vertices changed by the last one
+    int bailed;            // 1: the next frontier's in-edges exceed max_edges (the host loop continues)
+    int t_next;            // index of the next sweep (buffer parity)
+    long long edges;       // in-edges enumerated by the sweeps run
+    long long win_edges;   // of which with a worked window
+    long long next_edges;  // in-edges of the frontier left (bailed)
+};
+
 struct StepDev {  // mirrors im_step
     int32_t vertex, pad;
     int64_t score;
@@ -128,6 +139,8 @@ struct Ctx {
     uint32_t* nbits = nullptr;   // BFS: per-vertex words with new bits in the current level
     StepDev* rec = nullptr;
     BfsSmallOut* sbo = nullptr;
+    SweepSmallOut* sso = nullptr;
+    long long small_sweep_edges = 32768;  // sweep frontiers with at most this many in-edges: one-cluster sweeps (IM_SMALL_SWEEP; 0 = off)
     long long small_edges = 32768;  // frontiers with at most this many out-edges: one-cluster BFS (IM_SMALL_EDGES; 0 = off)
     double* varsigma = nullptr;
     ull* key = nullptr;
@@ -216,6 +229,8 @@ cudaError_t launch_init_registers(Ctx& c);
 cudaError_t launch_sweep(Ctx& c, const int4* items, int n_items, const uint32_t* cm_in, uint32_t* cm_out,
                          uint32_t* bits_out, IterCounters* ctr, bool blocked, const IterCounters* nin = nullptr);
 cudaError_t launch_commit(Ctx& c, const uint32_t* bits_new);
+// the remaining sweeps of a build from the work items of sweep s0 - 1's compaction, in one cluster launch
+cudaError_t launch_sweep_small(Ctx& c, const int4* items, int n_items, int s0, bool blocked, long long max_edges);
 cudaError_t launch_slices_big(Ctx& c, const int32_t* big, const uint32_t* mask, const int32_t* offs, const uint2* rec,
                               int4* items_out, IterCounters* ctr, bool whole_dense);
 cudaError_t launch_estimate(Ctx& c, double* out);

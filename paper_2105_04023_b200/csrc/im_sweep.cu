@@ -14,11 +14,15 @@
 // form one contiguous window [lo, hi) (im_device.cuh).  A lane owns one edge; it touches only the
 // 8-byte words of M_u / M_v inside the window and merges with a bytewise-max CAS.  Windows wider
 // than DENSE_WIN simulations are walked by the whole warp.  Two edges per lane are kept in flight.
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <climits>
 
 #include "im_device.cuh"
 #include "im_internal.h"
+
+namespace cg = cooperative_groups;
 
 namespace im {
 #ifndef IM_NS
@@ -488,6 +492,245 @@ __global__ void k_slices_buckets(int J, int B, int KB, const uint32_t* __restric
         for (int s0 = b0; s0 < b0 + len; s0 += SEG) items[p++] = make_int4(v, s0, min(s0 + SEG, b0 + len), 0);
         __syncwarp();
     }
+}
+
+// ------------------------------------------------------------------ small-frontier sweeps in one cluster
+// The tail of a build (and most of a rebuild on small graphs) is a long run of sweeps over a few hundred
+// changed vertices, where the multi-block sweep (k_sweep + k_compact + k_slices_buckets and a host round
+// trip) is launch- and latency-bound.  k_sweep_small runs those sweeps inside ONE thread-block cluster
+// (SS_CLUSTER blocks, one per SM): every changed vertex v of the previous sweep has its in-row walked
+// (warp per vertex, lane per edge; rows longer than SS_LONG by every warp of the cluster), each edge (u, v)
+// pushes the live simulations in which v changed into M_u with the byte-max CAS of k_sweep (the same exact
+// filter, in place), and u is appended to the next sweep's vertex list by the lane whose chunk-bit OR
+// first marked it.  Between sweeps: cluster barriers; the previous sweep's change masks are cleared by
+// vertex list.  The first sweep takes the host loop's work items (k_compact's).  It stops at the
+// fixpoint, or hands a frontier whose in-edges exceed max_edges back to the host loop (bits / masks of
+// the last sweep left set, exactly as after a k_sweep).  Only for eps_c = 0 (in-place sweeps).
+constexpr int SS_THREADS = 1024;
+constexpr int SS_CLUSTER = 8;
+constexpr int SS_LONG = 256;
+
+struct SweepSmallArgs {
+    int n, J;
+    const int32_t* roff;
+    const uint2* rev;
+    const uint32_t* revT;
+    uint32_t T0;
+    const uint32_t* Xs;
+    const uint16_t* s12;
+    ull* M64;
+    const uint32_t* vis;
+    uint32_t* cm[2];
+    uint32_t* bits[2];
+    int32_t* vl[2];            // vertex lists (n entries each)
+    int32_t* longv;            // long rows of a sweep (scratch)
+    const int4* items0;        // the first sweep's work items (host loop's compaction) and their count
+    int n_items0;
+    int s0;                    // index of the first sweep (buffer parity)
+    long long max_edges;
+    SweepSmallOut* out;
+};
+
+// one in-edge e of v (source u = rev[e].x): returns the chunk bits of u this edge raised
+template <bool CONST_T, bool BLOCKED>
+__device__ __forceinline__ uint32_t small_push(const SweepSmallArgs& a, const uint32_t* sX, const uint16_t* sS, int e, uint32_t v,
+                                               const uint32_t* cm_in, uint32_t* cm_out, uint32_t& wcount) {
+    const uint2 r = __ldcs(&a.rev[e]);
+    const uint32_t T = CONST_T ? a.T0 : __ldcs(&a.revT[e]);
+    if (!T) return 0u;
+    int lo, hi;
+    edge_window(r.y, T, sX, sS, a.J, lo, hi);
+    if (lo >= hi) return 0u;
+    const int W = a.J >> 5;
+    const size_t J8 = (size_t)(a.J >> 3);
+    const uint32_t u = r.x;
+    uint32_t chg = 0u;
+    bool worked = false;
+    for (int w = lo >> 3; w <= (hi - 1) >> 3; ++w) {
+        uint32_t cand = (__ldg(&cm_in[(size_t)v * W + (w >> 2)]) >> ((w & 3) << 3)) & 0xFFu;
+        if (!cand) continue;
+        ull live = 0;
+        for (; cand; cand &= cand - 1) {
+            const int b = __ffs(cand) - 1, i = 8 * w + b;
+            if (i >= lo && i < hi && (sX[i] ^ r.y) < T) live |= 0xFFull << (8 * b);
+        }
+        if (BLOCKED && live) live &= ~expand8((a.vis[(size_t)u * W + (w >> 2)] >> ((w & 3) << 3)) & 0xFFu);
+        if (!live) continue;
+        worked = true;
+        const ull cv = a.M64[v * J8 + w] & live;
+        if (!cv) continue;
+        ull* p = &a.M64[u * J8 + w];
+        const uint32_t raised = vmax_cas8(p, __ldcg(p), cv);
+        if (raised) {
+            atomicOr(&cm_out[(size_t)u * W + (w >> 2)], raised << ((w & 3) << 3));
+            chg |= 1u << (w >> 2);
+        }
+    }
+    wcount += worked;
+    return chg;
+}
+
+template <bool CONST_T, bool BLOCKED>
+__global__ void __cluster_dims__(SS_CLUSTER, 1, 1) __launch_bounds__(SS_THREADS) k_sweep_small(SweepSmallArgs a) {
+    __shared__ uint32_t sX[1024];
+    __shared__ uint16_t sS[4098];
+    __shared__ int s_next, s_nlong, s_changed;
+    __shared__ unsigned long long s_edges, s_win;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int crank = (int)cluster.block_rank(), csize = (int)cluster.num_blocks();
+    int* c_next = cluster.map_shared_rank(&s_next, 0);
+    int* c_nlong = cluster.map_shared_rank(&s_nlong, 0);
+    unsigned long long* c_edges = cluster.map_shared_rank(&s_edges, 0);
+    unsigned long long* c_win = cluster.map_shared_rank(&s_win, 0);
+    const int W = a.J >> 5, lane = threadIdx.x & 31, wib = threadIdx.x >> 5, NWARP = SS_THREADS / 32;
+    const int gw = crank * NWARP + wib, GW = csize * NWARP, gt = crank * SS_THREADS + threadIdx.x, GT = csize * SS_THREADS;
+    for (int i = threadIdx.x; i < a.J; i += blockDim.x) sX[i] = a.Xs[i];
+    for (int i = threadIdx.x; i < 4097; i += blockDim.x) sS[i] = a.s12[i];
+    int t = a.s0, n_v = -1, sweeps = 0, lst = 0;
+    long long edges_total = 0, win_total = 0, last_edges = 0;
+    int last_changed = 0;
+    bool bailed = false;
+    __syncthreads();
+    for (;;) {
+        const int pi = (t - 1) & 1, ci = t & 1;  // input (previous sweep) / output parity
+        const uint32_t* cm_in = a.cm[pi];
+        uint32_t* cm_out = a.cm[ci];
+        uint32_t* bits_out = a.bits[ci];
+        int32_t* vln = a.vl[lst ^ 1];
+        if (crank == 0 && threadIdx.x == 0) {
+            s_next = 0;
+            s_nlong = 0;
+            s_edges = 0ull;
+            s_win = 0ull;
+        }
+        cluster.sync();
+        uint32_t wcount = 0;
+        unsigned long long ed = 0;
+        auto push_edge = [&](int e, uint32_t v) {
+            const uint32_t chg = small_push<CONST_T, BLOCKED>(a, sX, sS, e, v, cm_in, cm_out, wcount);
+            if (chg) {
+                const uint32_t u = a.rev[e].x;
+                if (atomicOr(&bits_out[u], chg) == 0u) vln[atomicAdd(c_next, 1)] = (int32_t)u;
+            }
+        };
+        if (n_v < 0) {  // the first sweep: the host loop's work items (segments of <= SEG in-edges)
+            for (int it = gw; it < a.n_items0; it += GW) {
+                const int4 I = a.items0[it];
+                for (int e = I.y + lane; e < I.z; e += 32) push_edge(e, (uint32_t)I.x);
+                if (lane == 0) ed += (unsigned long long)(I.z - I.y);
+            }
+        } else {
+            const int32_t* vl = a.vl[lst];
+            for (int i = gw; i < n_v; i += GW) {
+                const uint32_t v = (uint32_t)vl[i];
+                const int eb = a.roff[v], ee = a.roff[v + 1];
+                if (ee - eb > SS_LONG) {
+                    if (lane == 0) a.longv[atomicAdd(c_nlong, 1)] = (int32_t)v;
+                    continue;
+                }
+                for (int e = eb + lane; e < ee; e += 32) push_edge(e, v);
+                if (lane == 0) ed += (unsigned long long)(ee - eb);
+            }
+            cluster.sync();
+            const int nlong = *c_nlong;
+            for (int li = 0; li < nlong; li++) {  // long in-rows: split over every warp of the cluster
+                const uint32_t v = (uint32_t)a.longv[li];
+                const int eb = a.roff[v], ee = a.roff[v + 1];
+                for (int e = eb + gw * 32 + lane; e < ee; e += GW * 32) push_edge(e, v);
+                if (gw == 0 && lane == 0) ed += (unsigned long long)(ee - eb);
+            }
+        }
+        wcount = __reduce_add_sync(IM_FULL, wcount);
+        if (lane == 0 && wcount) atomicAdd(c_win, (unsigned long long)wcount);
+        if (ed) atomicAdd(c_edges, ed);
+        cluster.sync();
+        // the previous sweep's change masks / bits are consumed: clear them (by its vertex list, or by the
+        // first sweep's items); its output is the sweep after next's input
+        if (n_v < 0) {  // every vertex the host-loop sweep changed (with or without in-edges): scan the chunk bits
+            for (int v = gt; v < a.n; v += GT) {
+                const uint32_t b = a.bits[pi][v];
+                if (!b) continue;
+                a.bits[pi][v] = 0u;
+                for (uint32_t bb = b; bb; bb &= bb - 1) a.cm[pi][(size_t)v * W + (__ffs(bb) - 1)] = 0u;
+            }
+        } else {
+            const int32_t* vl = a.vl[lst];
+            for (int64_t i = gt; i < (int64_t)n_v * W; i += GT) {
+                const uint32_t v = (uint32_t)vl[i / W];
+                a.cm[pi][(size_t)v * W + (i % W)] = 0u;
+                if (i % W == 0) a.bits[pi][v] = 0u;
+            }
+        }
+        const int nn = *c_next;
+        edges_total += (long long)*c_edges;
+        win_total += (long long)*c_win;
+        last_changed = nn;
+        sweeps++;
+        t++;
+        lst ^= 1;
+        n_v = nn;
+        // the next sweep's in-edges (for the hand-back test): sum of in-degrees of the new list
+        if (crank == 0 && threadIdx.x == 0) s_edges = 0ull;
+        cluster.sync();
+        if (n_v == 0) break;
+        unsigned long long ne = 0;
+        for (int i = gt; i < n_v; i += GT) {
+            const int v = a.vl[lst][i];
+            ne += (unsigned long long)(a.roff[v + 1] - a.roff[v]);
+        }
+        if (ne) atomicAdd(c_edges, ne);
+        cluster.sync();
+        last_edges = (long long)*c_edges;
+        cluster.sync();  // every block has read the counters before rank 0 resets them
+        if (last_edges == 0) break;  // changed vertices without in-edges: the fixpoint
+        if (last_edges > a.max_edges) {
+            bailed = true;
+            break;
+        }
+    }
+    if (crank == 0 && threadIdx.x == 0) {
+        a.out->sweeps = sweeps;
+        a.out->edges = edges_total;
+        a.out->win_edges = win_total;
+        a.out->changed = last_changed;
+        a.out->bailed = bailed ? 1 : 0;
+        a.out->next_edges = last_edges;
+        a.out->t_next = t;
+    }
+}
+
+cudaError_t launch_sweep_small(Ctx& c, const int4* items, int n_items, int s0, bool blocked, long long max_edges) {
+    SweepSmallArgs a;
+    a.n = c.n;
+    a.J = c.J;
+    a.roff = c.roff;
+    a.rev = c.rev;
+    a.revT = c.revT;
+    a.T0 = c.T0;
+    a.Xs = c.Xs;
+    a.s12 = c.s12;
+    a.M64 = reinterpret_cast<ull*>(c.M);
+    a.vis = c.vis;
+    a.cm[0] = c.cm[0];
+    a.cm[1] = c.cm[1];
+    a.bits[0] = c.bits[0];
+    a.bits[1] = c.bits[1];
+    a.vl[0] = c.bvl[0];
+    a.vl[1] = c.bvl[1];
+    a.longv = c.big;
+    a.items0 = items;
+    a.n_items0 = n_items;
+    a.s0 = s0;
+    a.max_edges = max_edges;
+    a.out = c.sso;
+    if (c.constT) {
+        if (blocked) k_sweep_small<true, true><<<SS_CLUSTER, SS_THREADS, 0, c.stream>>>(a);
+        else k_sweep_small<true, false><<<SS_CLUSTER, SS_THREADS, 0, c.stream>>>(a);
+    } else {
+        if (blocked) k_sweep_small<false, true><<<SS_CLUSTER, SS_THREADS, 0, c.stream>>>(a);
+        else k_sweep_small<false, false><<<SS_CLUSTER, SS_THREADS, 0, c.stream>>>(a);
+    }
+    return LAUNCHED(c);
 }
 
 template <bool C, bool B, bool F>
