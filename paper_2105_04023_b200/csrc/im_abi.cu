@@ -484,6 +484,49 @@ int simulate(bool blocked) {
         edges += (double)hc.next_edges > g.pull_frac * (double)g.m ? g.m : (int64_t)hc.next_edges;
         return true;
     };
+    // k_sweep_small for the rest of the build once the frontier (after sweep s, counters hc) is small:
+    // returns 0 = not taken, 1 = the build is done, 2 = continue the host loop at sweep s + 1, < 0 = error
+    auto run_small = [&](int& s, const IterCounters& hc) -> int {
+        const int sl = s & 1;
+        if (g.sync_sweeps || g.small_sweep_edges <= 0 || (long long)hc.next_edges > g.small_sweep_edges) return 0;
+        CK(cudaEventRecord(g.pev[sl][0], g.stream));
+        CK(launch_sweep_small(g, g.items[sl], hc.next_items, s + 1, blocked, g.small_sweep_edges));
+        CK(cudaEventRecord(g.pev[sl][1], g.stream));
+        SweepSmallOut so;
+        TRY(readback(g.sso, sizeof so, &so));
+        float ts;
+        CK(cudaEventElapsedTime(&ts, g.pev[sl][0], g.pev[sl][1]));
+        kms += ts;
+        sweeps += so.sweeps;
+        launches++;
+        wedges += so.win_edges;
+        edges += so.edges - (int64_t)hc.next_edges;  // account() already counted the first one's in-edges
+        alg += (8.0 + (g.constT ? 0.0 : 4.0)) * (double)so.edges + 32.0 * (double)so.win_edges;
+        if (g.trace)
+            fprintf(stderr, "[im] sweeps %d..%d in one cluster launch: %lld edges, %lld window_edges -> %s, %.3f ms\n", s + 1,
+                    so.t_next - 1, so.edges, so.win_edges, so.bailed ? "frontier handed back" : "fixpoint", ts);
+        if (!so.bailed) {
+            dirty = false;
+            return 1;
+        }
+        // hand back: compact the last cluster sweep's changes (its input masks were cleared in the kernel)
+        const int tl = so.t_next - 1, tb = tl & 1;
+        CK(cudaMemsetAsync(&g.ctr[tb], 0, sizeof(IterCounters), g.stream));
+        CK(launch_compact(g, g.bits[tb], g.bits[tb ^ 1], g.cm[tb], g.cm[tb ^ 1], g.items[tb], &g.ctr[tb]));
+        IterCounters hc2;
+        TRY(readback(&g.ctr[tb], sizeof hc2, &hc2));
+        if (hc2.next_items == 0) {
+            dirty = hc2.changed > 0;
+            return 1;
+        }
+        n_items = hc2.next_items;
+        edges_in = (int64_t)hc2.next_edges;
+        edges += (int64_t)hc2.next_edges;
+        items = g.items[tb];
+        s = tl;
+        last_done = s;
+        return 2;
+    };
     for (int s = 1;; s++) {
         const int sl = s & 1;
         IterCounters* ctr = &g.ctr[sl];
@@ -520,45 +563,11 @@ int simulate(bool blocked) {
             CK(cudaEventElapsedTime(&t, g.pev[sl][0], g.pev[sl][1]));
             if (!account(s, hc, gather, t)) break;
             last_done = s;
-            if (!g.sync_sweeps && g.small_sweep_edges > 0 && (long long)hc.next_edges <= g.small_sweep_edges) {
-                // the rest of the build in one cluster launch (k_sweep_small) while the frontier stays small
-                CK(cudaEventRecord(g.pev[sl][0], g.stream));
-                CK(launch_sweep_small(g, g.items[sl], hc.next_items, s + 1, blocked, g.small_sweep_edges));
-                CK(cudaEventRecord(g.pev[sl][1], g.stream));
-                SweepSmallOut so;
-                TRY(readback(g.sso, sizeof so, &so));
-                float ts;
-                CK(cudaEventElapsedTime(&ts, g.pev[sl][0], g.pev[sl][1]));
-                kms += ts;
-                sweeps += so.sweeps;
-                launches++;
-                wedges += so.win_edges;
-                edges += so.edges - (int64_t)hc.next_edges;  // account() already counted the first one's in-edges
-                alg += (8.0 + (g.constT ? 0.0 : 4.0)) * (double)so.edges + 32.0 * (double)so.win_edges;
-                if (g.trace)
-                    fprintf(stderr, "[im] sweeps %d..%d in one cluster launch: %lld edges, %lld window_edges -> %s, %.3f ms\n", s + 1,
-                            so.t_next - 1, so.edges, so.win_edges, so.bailed ? "frontier handed back" : "fixpoint", ts);
-                if (!so.bailed) {
-                    dirty = false;
-                    break;
-                }
-                // hand back: compact the last cluster sweep's changes (its input masks were cleared in the kernel)
-                const int tl = so.t_next - 1, tb = tl & 1;
-                CK(cudaMemsetAsync(&g.ctr[tb], 0, sizeof(IterCounters), g.stream));
-                CK(launch_compact(g, g.bits[tb], g.bits[tb ^ 1], g.cm[tb], g.cm[tb ^ 1], g.items[tb], &g.ctr[tb]));
-                IterCounters hc2;
-                TRY(readback(&g.ctr[tb], sizeof hc2, &hc2));
-                if (hc2.next_items == 0) {
-                    dirty = hc2.changed > 0;
-                    break;
-                }
-                n_items = hc2.next_items;
-                edges_in = (int64_t)hc2.next_edges;
-                edges += (int64_t)hc2.next_edges;
-                items = g.items[tb];
-                s = tl;
-                last_done = s;
-                continue;
+            {
+                const int r = run_small(s, hc);
+                if (r < 0) return r;
+                if (r == 1) break;
+                if (r == 2) continue;
             }
             // enter the pipelined mode once the next frontier is clearly sparse (no gather sweep any more)
             piped = g.pipeline && !g.sync_sweeps && s >= 2 && (double)hc.next_edges < 0.25 * g.pull_frac * (double)g.m;
@@ -578,6 +587,20 @@ int simulate(bool blocked) {
                 break;
             }
             last_done = s - 1;
+            if (!g.sync_sweeps && g.small_sweep_edges > 0 && (long long)hpc[ps].next_edges <= g.small_sweep_edges) {
+                // sweep s (already enqueued) has a small frontier: finish it on the host side, then the cluster
+                CK(cudaEventSynchronize(g.pev[sl][2]));
+                const IterCounters hs = hpc[sl];
+                float ts;
+                CK(cudaEventElapsedTime(&ts, g.pev[sl][0], g.pev[sl][1]));
+                if (!account(s, hs, false, ts)) break;
+                last_done = s;
+                piped = false;
+                const int r = run_small(s, hs);
+                if (r < 0) return r;
+                if (r == 1) break;
+                continue;  // r == 0 cannot happen here (the frontier only shrinks below the test above); r == 2
+            }
         }
     }
     g.sweep_dirty = dirty;  // a last sweep without changes leaves every change buffer zero
