@@ -330,7 +330,9 @@ __global__ void __launch_bounds__(BLOCK, 5) k_first(FirstArgs a) {
                 }
                 continue;
             }
-            if (ee - eb <= 32 && a.small_rows) {  // sparse path: touch only the window words
+            // per-edge thresholds (weighted cascade): a row with any wide window takes the whole-row path
+            const bool wide = !CONST_T && __any_sync(IM_FULL, cT && ((int64_t)a.J << thr_bits(cT)) > ((int64_t)DENSE_WIN << 31));
+            if (ee - eb <= 32 && a.small_rows && !wide) {  // sparse path: touch only the window words
                 if (BLOCKED && lane < W) sVis[wib][lane] = a.vis[(size_t)u * W + lane];
                 __syncwarp();
                 first_small<CONST_T, BLOCKED, MEM>(a, sX, sS, sHJ, sVis[wib], row, sBm[wib], sCm[wib], (uint32_t)u, eb + lane < ee, cf, cT,
