@@ -111,6 +111,7 @@ int ensure_device() {
     g.max_blocks_bfs = std::max(1, bb) * g.num_sms;
     g.trace = getenv("IM_TRACE") != nullptr;
     if (const char* pf = getenv("IM_PULL_FRAC")) g.pull_frac = atof(pf);
+    if (const char* tr = getenv("IM_THREAD_ROWS")) g.thread_rows = atoi(tr) != 0;
     if (const char* lm = getenv("IM_LIST_MAX")) g.list_max = atoll(lm);
     if (const char* sm = getenv("IM_SLICE_MIN")) g.slice_min = atoi(sm);
     if (const char* sb = getenv("IM_SLICE_MIN_BFS")) g.slice_min_bfs = atoi(sb);

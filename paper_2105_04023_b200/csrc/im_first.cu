@@ -42,6 +42,7 @@ struct FirstArgs {
     const int4* big_units;  // {u, eb, ee}: rows with > FIRST_BIG out-edges in units of <= FIRST_CHUNK (k_first_big)
     int n_big;
     int vb;              // vertices per warp batch (<= 256; fewer on small graphs so every warp gets work)
+    bool thread_rows;    // constant threshold, sparse windows: rows <= 32 edges are gathered one row per lane (first_thread)
     bool small_rows;     // rows <= 32 edges take the window-words-only path (false: wide windows, e.g. p = 0.1 with
                          // J >= 512, where every lane walking its own 64+-simulation window serially contends in
                          // shared memory; the whole-row path merges wide windows with lanes over words instead)
@@ -69,18 +70,22 @@ __device__ __forceinline__ void smem_vmax(uint32_t* p, uint32_t val) {
     }
 }
 
+// byte mask of the simulations 4w..4w+3 that are live for (h, T) (Eq. 5).  No window bounds are needed: the
+// salt of a simulation outside the edge's window lies in another 2^B block than h, so (X xor h) >= 2^B >= T.
+__device__ __forceinline__ uint32_t live_word(const uint32_t* sX, uint32_t h, uint32_t T, int w) {
+    const uint4 x = reinterpret_cast<const uint4*>(sX)[w];
+    return ((x.x ^ h) < T ? 0x000000FFu : 0u) | ((x.y ^ h) < T ? 0x0000FF00u : 0u) | ((x.z ^ h) < T ? 0x00FF0000u : 0u) |
+           ((x.w ^ h) < T ? 0xFF000000u : 0u);
+}
+
 // merge word w of edge (u -> v, h, T) restricted to [lo, hi) into the smem row
 template <bool BLOCKED, bool MEM>
 __device__ __forceinline__ void merge_word(const FirstArgs& a, const uint32_t* sX, const uint32_t* sHJ, const uint32_t* sVis,
                                            uint32_t* row, uint32_t v, uint32_t hv, uint32_t h, uint32_t T, int lo, int hi, int w,
                                            bool have_pre = false, uint32_t pre = 0u) {
-    uint32_t live = 0;
-#pragma unroll
-    for (int b = 0; b < 4; b++) {
-        int i = 4 * w + b;
-        bool ok = (i >= lo) & (i < hi) & ((sX[i] ^ h) < T);
-        live |= ok ? (0xFFu << (8 * b)) : 0u;
-    }
+    uint32_t live = live_word(sX, h, T, w);
+    (void)lo;
+    (void)hi;
     if (BLOCKED && live) live &= ~expand4((sVis[w >> 3] >> ((w & 7) << 2)) & 0xFu);
     if (!live) return;
     uint32_t val = MEM ? (have_pre ? pre : reinterpret_cast<const uint32_t*>(a.M)[(size_t)v * (a.J >> 2) + w]) : init_word(hv, sHJ, w);
@@ -268,9 +273,83 @@ __device__ __forceinline__ void first_small(const FirstArgs& a, const uint32_t* 
     __syncwarp();
 }
 
+// A row of at most 32 out-edges gathered by ONE lane (constant threshold, sparse windows): most rows of a
+// skewed graph are this short (RMAT-24: 45% of the vertices have 1..32 out-edges, 10% of the edges), and a
+// warp per such row leaves most lanes idle behind a fixed per-row cost.  The lane walks its row's edges and
+// their window words alone and raises the registers of its own row in global memory (it is the row's only
+// writer in a gather sweep), with the exact per-simulation change mask; no shared-memory row, no atomics.
+template <bool BLOCKED, bool MEM>
+__device__ __forceinline__ void first_thread(const FirstArgs& a, const uint32_t* sX, const uint16_t* sS, const uint32_t* sHJ,
+                                             uint32_t u, int eb, int ee, uint32_t& wcount) {
+    constexpr int TU = 2;  // edges per iteration: their records, then their window words of M_v / M_u, are loaded together
+    const int J = a.J, W = J >> 5, NW = J >> 2;
+    uint32_t* Mu = reinterpret_cast<uint32_t*>(a.M) + (size_t)u * NW;
+    uint32_t* cmu = a.cm_out + (size_t)u * W;
+    const uint32_t hu = MEM ? 0u : vhash(a, u);
+    const uint32_t T = a.T0;
+    uint32_t chunks = 0u;
+    for (int e0 = eb; e0 < ee; e0 += TU) {
+        uint2 f[TU];
+#pragma unroll
+        for (int k = 0; k < TU; k++) f[k] = e0 + k < ee ? ld_stream(&a.fwd[e0 + k]) : make_uint2(0u, 0u);
+        int lo[TU], hi[TU];
+        uint32_t mv[TU][2], mu[TU][2];
+#pragma unroll
+        for (int k = 0; k < TU; k++) {
+            lo[k] = hi[k] = 0;
+            mv[k][0] = mv[k][1] = mu[k][0] = mu[k][1] = 0u;
+            if (e0 + k < ee) edge_window(f[k].y, T, sX, sS, J, lo[k], hi[k]);
+            if (lo[k] < hi[k]) {
+                wcount++;
+                const int w0 = lo[k] >> 2, w1 = (hi[k] - 1) >> 2;
+                if (MEM) {  // the first two window words of the out-neighbour and of the own row (possibly stale: re-read before a store)
+                    const uint32_t* Mv = reinterpret_cast<const uint32_t*>(a.M) + (size_t)f[k].x * NW;
+                    mv[k][0] = Mv[w0];
+                    mu[k][0] = Mu[w0];
+                    if (w1 > w0) {
+                        mv[k][1] = Mv[w0 + 1];
+                        mu[k][1] = Mu[w0 + 1];
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < TU; k++) {
+            if (lo[k] >= hi[k]) continue;
+            const uint32_t h = f[k].y;
+            const uint32_t hv = MEM ? 0u : vhash(a, f[k].x);
+            const int w0 = lo[k] >> 2, w1 = (hi[k] - 1) >> 2;
+            for (int w = w0; w <= w1; ++w) {
+                uint32_t live = live_word(sX, h, T, w);  // Eq. 5
+                if (BLOCKED && live) live &= ~expand4((__ldg(&a.vis[(size_t)u * W + (w >> 3)]) >> ((w & 7) << 2)) & 0xFu);  // u in R_S[j] does not pull
+                if (!live) continue;
+                uint32_t val;
+                if (MEM) {
+                    const uint32_t pv = w == w0 ? mv[k][0] : mv[k][1], pu = w == w0 ? mu[k][0] : mu[k][1];
+                    val = (w - w0 < 2 ? pv : reinterpret_cast<const uint32_t*>(a.M)[(size_t)f[k].x * NW + w]) & live;
+                    if (w - w0 < 2 && __vmaxu4(pu, val) == pu) continue;  // registers only grow: no raise
+                } else {
+                    val = init_word(hv, sHJ, w) & live;
+                    const uint32_t ci = init_word(hu, sHJ, w);
+                    if (__vmaxu4(ci, val) == ci) continue;  // not above u's init values
+                }
+                const uint32_t cur = Mu[w];  // current value (an earlier edge of the row may have raised it)
+                const uint32_t nw = __vmaxu4(cur, val);
+                if (nw == cur) continue;
+                Mu[w] = nw;
+                const uint32_t eq = __vcmpeq4(nw, cur);
+                const uint32_t nib = ((((~eq) & 0x01010101u) * 0x00204081u) >> 21) & 0xFu;
+                cmu[w >> 3] |= nib << ((w & 7) << 2);  // the row's only writer; the buffer starts zeroed
+                chunks |= 1u << (w >> 3);
+            }
+        }
+    }
+    if (chunks) a.bits_out[u] = chunks;
+}
+
 template <bool CONST_T, bool BLOCKED, bool MEM>
 __global__ void __launch_bounds__(BLOCK, 5) k_first(FirstArgs a) {
-    __shared__ uint32_t sX[1024];
+    __shared__ __align__(16) uint32_t sX[1024];
     __shared__ uint16_t sS[4098];
     __shared__ __align__(16) uint32_t sHJ[1024];
     __shared__ uint32_t sRow[BLOCK / 32][256];
@@ -299,12 +378,36 @@ __global__ void __launch_bounds__(BLOCK, 5) k_first(FirstArgs a) {
         const int end = min(base + a.vb, a.n);
         for (int i = lane; i <= end - base; i += 32) off_w[i] = a.off[base + i];  // the batch's offsets, one coalesced read
         __syncwarp();
+        const bool thr = CONST_T && a.thread_rows;
+        if (thr) {  // rows of 1..32 out-edges, one per lane, in three degree classes (similar trip counts per warp)
+            uint8_t* lst = reinterpret_cast<uint8_t*>(old);
+            const int nv = end - base;
+#pragma unroll 1
+            for (int cls = 0; cls < 3; cls++) {
+                const int dlo = cls == 0 ? 1 : cls == 1 ? 5 : 13, dhi = cls == 0 ? 4 : cls == 1 ? 12 : 32;
+                int cnt = 0;
+                for (int i0 = 0; i0 < nv; i0 += 32) {
+                    const int i = i0 + lane;
+                    const int d = i < nv ? off_w[i + 1] - off_w[i] : 0;
+                    const bool in = d >= dlo && d <= dhi;
+                    const uint32_t mk = __ballot_sync(IM_FULL, in);
+                    if (in) lst[cnt + __popc(mk & ((1u << lane) - 1u))] = (uint8_t)i;
+                    cnt += __popc(mk);
+                }
+                __syncwarp();
+                for (int g = lane; g < cnt; g += 32) {
+                    const int i = lst[g];
+                    first_thread<BLOCKED, MEM>(a, sX, sS, sHJ, (uint32_t)(base + i), off_w[i], off_w[i + 1], wcount);
+                }
+                __syncwarp();
+            }
+        }
         // first 32 records of the next vertex are prefetched while the current one is processed
         uint2 nf = make_uint2(0, 0);
         uint32_t nT = 0;
         {
             const int eb0 = off_w[0], ee0 = off_w[1];
-            if (ee0 - eb0 <= FIRST_BIG && eb0 + lane < ee0) {
+            if (ee0 - eb0 <= FIRST_BIG && eb0 + lane < ee0 && !(thr && ee0 - eb0 <= 32)) {
                 nf = ld_stream(&a.fwd[eb0 + lane]);
                 nT = CONST_T ? a.T0 : ld_stream(&a.fwdT[eb0 + lane]);
             }
@@ -317,12 +420,13 @@ __global__ void __launch_bounds__(BLOCK, 5) k_first(FirstArgs a) {
             nT = 0;
             if (u + 1 < end) {
                 const int eb1 = off_w[u + 1 - base], ee1 = off_w[u + 2 - base];
-                if (ee1 - eb1 <= FIRST_BIG && eb1 + lane < ee1) {
+                if (ee1 - eb1 <= FIRST_BIG && eb1 + lane < ee1 && !(thr && ee1 - eb1 <= 32)) {
                     nf = ld_stream(&a.fwd[eb1 + lane]);
                     nT = CONST_T ? a.T0 : ld_stream(&a.fwdT[eb1 + lane]);
                 }
             }
             if (ee - eb > FIRST_BIG) continue;  // done by k_first_big
+            if (thr && ee - eb <= 32) continue;  // done above (first_thread), or empty
             if (ee == eb) {  // no out-edge: the row keeps its value (init rows and zeroed masks are written before)
                 if (MEM) {
                     if (lane < W) a.cm_out[(size_t)u * W + lane] = 0u;
@@ -398,7 +502,7 @@ __device__ __forceinline__ uint32_t gmax4_raised(uint32_t* p, uint32_t val) {
 // and chunk bits with atomicOr (the buffers start zeroed), so several units of one row compose.
 template <bool CONST_T, bool BLOCKED, bool MEM>
 __global__ void __launch_bounds__(BLOCK) k_first_big(FirstArgs a) {
-    __shared__ uint32_t sX[1024];
+    __shared__ __align__(16) uint32_t sX[1024];
     __shared__ uint16_t sS[4098];
     __shared__ __align__(16) uint32_t sHJ[1024];
     __shared__ uint32_t row[256];
@@ -489,6 +593,7 @@ cudaError_t launch_first(Ctx& c, uint32_t* cm_out, uint32_t* bits_out, IterCount
     a.n_big = c.n_fbig;
     // nominal candidate window of a constant threshold: J * 2^B0 / 2^31 simulations
     a.small_rows = !c.constT || ((int64_t)c.J << c.B0) <= ((int64_t)DENSE_WIN << 31);
+    a.thread_rows = c.constT && a.small_rows && c.thread_rows;
     {   // a dependent chain of loads per vertex: spread small graphs over every resident warp
         const int64_t warps = (int64_t)c.max_blocks_first * (BLOCK / 32);
         a.vb = (int)std::min<int64_t>(256, std::max<int64_t>(1, c.n / warps));

@@ -126,6 +126,7 @@ struct Ctx {
     int slice_min = SEG;       // sweeps: in-rows longer than this are enumerated by hash slices (IM_SLICE_MIN)
     int slice_min_bfs = SEG;   // BFS levels: out-rows longer than this are enumerated by hash slices (IM_SLICE_MIN_BFS)
     int64_t list_max = 65536;  // cap of the lazy argmax candidate list length (IM_LIST_MAX)
+    bool thread_rows = true;   // first / gather sweeps: rows <= 32 out-edges one per lane (IM_THREAD_ROWS=0: warp per row)
     double pull_frac = 0.97;   // gather sweep when the push frontier's in-edges exceed this share of m (IM_PULL_FRAC)
     IterCounters* ctr = nullptr;   // [2]
     // selection buffers
