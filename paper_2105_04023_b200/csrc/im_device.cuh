@@ -79,6 +79,22 @@ __device__ __forceinline__ uint32_t window_live_bits(const uint32_t* sX, uint32_
     for (int i = lo; i < hi; ++i) lb |= ((sX[i] ^ h) < T) ? (1u << (i - lo)) : 0u;
     return lb;
 }
+// the 4 live bits of the aligned simulations 4w .. 4w+3.  No window bounds are needed: the salt of a simulation
+// outside the edge's window lies in another 2^B block than h, so (X xor h) >= 2^B >= T.  sX is 16-byte aligned.
+__device__ __forceinline__ uint32_t live_nibble(const uint32_t* sX, uint32_t h, uint32_t T, int w) {
+    const uint4 x = reinterpret_cast<const uint4*>(sX)[w];
+    return ((x.x ^ h) < T ? 1u : 0u) | ((x.y ^ h) < T ? 2u : 0u) | ((x.z ^ h) < T ? 4u : 0u) | ((x.w ^ h) < T ? 8u : 0u);
+}
+// window_live_bits by aligned 4-simulation words: the first two words (a nominal window of a few simulations)
+// in straight-line code with both salt loads in flight, the rest of a long window in a loop.  sX is 16-byte aligned.
+__device__ __forceinline__ uint32_t window_live_bits4(const uint32_t* sX, uint32_t h, uint32_t T, int lo, int hi) {
+    const int w0 = lo >> 2, w1 = (hi - 1) >> 2, r = lo & 3;
+    const uint32_t n0 = live_nibble(sX, h, T, w0);
+    const uint32_t n1 = w1 > w0 ? live_nibble(sX, h, T, w0 + 1) : 0u;
+    uint32_t lb = (n0 | (n1 << 4)) >> r;
+    for (int w = w0 + 2; w <= w1; ++w) lb |= live_nibble(sX, h, T, w) << (4 * (w - w0) - r);
+    return lb;
+}
 // narrow [lo, hi) to its first and last set bit of lb (lb re-based to the new lo); empty if lb == 0
 __device__ __forceinline__ void narrow_window(uint32_t& lb, int& lo, int& hi) {
     if (!lb) {

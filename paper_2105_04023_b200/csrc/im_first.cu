@@ -200,6 +200,9 @@ __device__ __forceinline__ void gather_multi(const FirstArgs& a, const uint32_t*
     }
 }
 
+#ifndef FIRST_BIG_BPS
+#define FIRST_BIG_BPS 4  // blocks per SM of k_first_big
+#endif
 constexpr int FW = 8;  // max words per lane of the warp kernel (J/4/32 <= 8)
 constexpr int UW = 2;  // edges in flight per lane, rows of the warp kernel
 #ifndef FIRST_UB
@@ -560,7 +563,7 @@ __global__ void __launch_bounds__(BLOCK) k_first_big(FirstArgs a) {
 template <bool C, bool B, bool MEM>
 static cudaError_t first_inst(Ctx& c, const FirstArgs& a) {
     cudaError_t e;
-    const int gb = a.n_big < c.num_sms * 4 ? a.n_big : c.num_sms * 4;
+    const int gb = a.n_big < c.num_sms * FIRST_BIG_BPS ? a.n_big : c.num_sms * FIRST_BIG_BPS;
     if (MEM && a.n_big) {
         k_first_big<C, B, MEM><<<gb, BLOCK, 0, c.stream>>>(a);
         if ((e = LAUNCHED(c))) return e;

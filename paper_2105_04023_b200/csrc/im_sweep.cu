@@ -28,6 +28,9 @@ namespace im {
 #ifndef IM_NS
 #define IM_NS 2
 #endif
+#ifndef IM_LB4
+#define IM_LB4 1  // window live bits by aligned 16-byte salt words (0: one simulation at a time)
+#endif
 #ifndef SWEEP_MINB
 #define SWEEP_MINB 4  // resident blocks per SM k_sweep is compiled for
 #endif
@@ -190,7 +193,7 @@ constexpr int NS = IM_NS;  // edges in flight per lane
 
 template <bool CONST_T, bool BLOCKED, bool FILTER>
 __global__ void __launch_bounds__(BLOCK, SWEEP_MINB) k_sweep(SweepArgs a) {
-    __shared__ uint32_t sX[1024];
+    __shared__ __align__(16) uint32_t sX[1024];
     __shared__ uint16_t sS[4098];
     __shared__ int sSlot[BLOCK / 32][32];
     if (a.nin) {  // item count of the previous compaction, read on the device (no host round trip)
@@ -272,7 +275,11 @@ __global__ void __launch_bounds__(BLOCK, SWEEP_MINB) k_sweep(SweepArgs a) {
                 if (T[s]) {
                     edge_window(h[s], T[s], sX, sS, J, lo[s], hi[s]);
                     if (lo[s] < hi[s] && hi[s] - lo[s] <= DENSE_WIN) {
+#if IM_LB4
+                        lb[s] = window_live_bits4(sX, h[s], T[s], lo[s], hi[s]);
+#else
                         lb[s] = window_live_bits(sX, h[s], T[s], lo[s], hi[s]);
+#endif
                         if (FILTER) lb[s] &= window_changed_bits(a.cm_in, vv[s], W, lo[s], hi[s]);
                         narrow_window(lb[s], lo[s], hi[s]);  // to the live (changed-at-v) simulations; empty if none
                     } else if (FILTER && lo[s] < hi[s] && !window_changed(a.cm_in, vv[s], W, lo[s], hi[s])) {
