@@ -5,7 +5,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libim_b200.so")
-SOURCES = ["im_prep.cu", "im_first.cu", "im_kernels.cu", "im_sweep.cu", "im_stream.cu", "im_bfs_small.cu", "im_eval.cu", "im_comm.cu", "im_abi.cu"]
+SOURCES = ["im_prep.cu", "im_first.cu", "im_kernels.cu", "im_sweep.cu", "im_slab.cu", "im_stream.cu", "im_bfs_small.cu", "im_eval.cu", "im_comm.cu", "im_abi.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC,-O2", "-shared", "-Xptxas", "-v", "-ldl"]
 

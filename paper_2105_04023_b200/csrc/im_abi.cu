@@ -112,6 +112,8 @@ int ensure_device() {
     g.trace = getenv("IM_TRACE") != nullptr;
     if (const char* pf = getenv("IM_PULL_FRAC")) g.pull_frac = atof(pf);
     if (const char* tr = getenv("IM_THREAD_ROWS")) g.thread_rows = atoi(tr) != 0;
+    if (const char* sp = getenv("IM_SLAB_PASSES")) g.slab_passes = atoi(sp);
+    if (const char* sm = getenv("IM_SLAB_MIN_M")) g.slab_min_m = atoll(sm);
     if (const char* lm = getenv("IM_LIST_MAX")) g.list_max = atoll(lm);
     if (const char* sm = getenv("IM_SLICE_MIN")) g.slice_min = atoi(sm);
     if (const char* sb = getenv("IM_SLICE_MIN_BFS")) g.slice_min_bfs = atoi(sb);
@@ -151,6 +153,7 @@ void release_all() {
     for (int i = 0; i < 2; i++) { dfree(g.items[i]); dfree(g.bits[i]); dfree(g.cm[i]); dfree(g.delta[i]); dfree(g.bitems[i]); dfree(g.bvl[i]); }
     dfree(g.inS); dfree(g.MS); dfree(g.btag); dfree(g.nbits); dfree(g.gain); dfree(g.big); dfree(g.list); dfree(g.lcount); dfree(g.hist);
     dfree(g.off); dfree(g.fwd); dfree(g.fwdT); dfree(g.roff); dfree(g.rev); dfree(g.revT); dfree(g.ritems); dfree(g.fbig);
+    dfree(g.brec); dfree(g.bv); dfree(g.slabS); dfree(g.slabC); dfree(g.slabX); dfree(g.slabHJ); dfree(g.slabG);
     dfree(g.ftidx); dfree(g.rtidx); dfree(g.ftab); dfree(g.rtab); dfree(g.t_tabrows);
     dfree(g.ctr); dfree(g.rec); dfree(g.sbo); dfree(g.sso); dfree(g.varsigma); dfree(g.key); dfree(g.first); dfree(g.sigma_count);
     dfree(g.lval); dfree(g.sigma_g); dfree(g.bcount); dfree(g.Mold); dfree(g.gslice); dfree(g.llist); dfree(g.lcnt_all);
@@ -265,6 +268,15 @@ int load_common(int32_t n, int64_t m, const int32_t* d_off_src, const int32_t* d
         TRY(dalloc(g.t_tabrows, (size_t)n));
         g.alloc_i32 = tab_alloc;
     }
+    // bucket-major edge list for the slab form of the full sweeps (im_slab.cu): large constant-threshold graphs
+    if (rows_path(g) && g.T0 > 0 && g.slab_passes > 0 && m >= g.slab_min_m) {
+        TRY(dalloc(g.brec, (size_t)m));
+        TRY(dalloc(g.bv, (size_t)m));
+    } else {
+        dfree(g.brec);
+        dfree(g.bv);
+    }
+    g.boff_h.clear();
     CK(prep_edges(g, d_tgt, d_prob, indeg, nullptr, scr, sz));
     // work items: reverse segments of every vertex (sweep 1), forward item capacity (BFS)
     size_t tmp_bytes = 0;
@@ -397,6 +409,7 @@ int setup_salts(int32_t Jt, int32_t j0, int32_t J, uint64_t seed) {
         while ((int)i < J && (Xs[i] >> 19) < b) i++;
         s12[b] = (uint16_t)i;
     }
+    g.Xs_h = Xs;
     CK(cudaMemcpyAsync(g.Xs, Xs.data(), J * sizeof(uint32_t), cudaMemcpyHostToDevice, g.stream));
     CK(cudaMemcpyAsync(g.s12, s12.data(), 4097 * sizeof(uint16_t), cudaMemcpyHostToDevice, g.stream));
     std::vector<int32_t> gj(J);
@@ -528,6 +541,16 @@ int simulate(bool blocked) {
         last_done = s;
         return 2;
     };
+    // slab form of the first full sweeps: large constant-threshold graphs, eps_c = 0 (any schedule reaches the fixpoint)
+    int slab_G = g.sync_sweeps ? 0 : slab_group_count(g);
+    if (slab_G > 0) {
+        const size_t ns = slab_stride(g.n);
+        TRY(dalloc(g.slabS, (size_t)slab_G * ns));
+        TRY(dalloc(g.slabC, (size_t)slab_G * ns));
+        TRY(dalloc(g.slabX, (size_t)slab_G));
+        TRY(dalloc(g.slabHJ, (size_t)slab_G));
+        TRY(dalloc(g.slabG, (size_t)slab_G));
+    }
     for (int s = 1;; s++) {
         const int sl = s & 1;
         IterCounters* ctr = &g.ctr[sl];
@@ -537,7 +560,9 @@ int simulate(bool blocked) {
         // in-place gather (every row owned by one warp, no atomics); sparse frontiers are pushed
         const bool gather = !piped && s > 1 && !g.sync_sweeps && (double)edges_in > g.pull_frac * (double)g.m;
         gathers[sl] = gather;
-        if (s == 1) {  // streaming register init, then the first sweep as a gather from init values
+        if (s == 1 && slab_G > 0) {  // init + the first full sweeps in bucket-major slabs (im_slab.cu)
+            CK(launch_slab_build(g, blocked, g.slab_passes, g.cm[1], g.bits[1]));
+        } else if (s == 1) {  // streaming register init, then the first sweep as a gather from init values
             CK(launch_init_registers(g));
             CK(cudaMemsetAsync(g.cm[1], 0, (size_t)g.n * W * sizeof(uint32_t), g.stream));
             CK(cudaMemsetAsync(g.bits[1], 0, (size_t)g.n * sizeof(uint32_t), g.stream));
@@ -562,7 +587,12 @@ int simulate(bool blocked) {
             hc = hpc[sl];
             float t;
             CK(cudaEventElapsedTime(&t, g.pev[sl][0], g.pev[sl][1]));
-            if (!account(s, hc, gather, t)) break;
+            const bool go = account(s, hc, gather, t);
+            if (s == 1 && slab_G > 0) {  // the slab build ran slab_passes full sweeps, not one
+                sweeps += g.slab_passes - 1;
+                edges += (int64_t)(g.slab_passes - 1) * g.m;
+            }
+            if (!go) break;
             last_done = s;
             {
                 const int r = run_small(s, hc);

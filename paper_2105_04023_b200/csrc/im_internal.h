@@ -94,6 +94,19 @@ struct Ctx {
     cudaError_t (*alloc_i32)(int32_t*&, size_t) = nullptr;  // device allocation with capacity reuse (im_abi.cu)
     int32_t n_ritems = 0;
     int32_t n_fitems_cap = 0;   // sum_v ceil(outdeg/SEG)
+    // bucket-major edge list and slabs of the full sweeps (im_slab.cu)
+    uint2* brec = nullptr;      // m {source u, h} grouped by bucket h >> Bs (null: no slab path for this graph)
+    int32_t* bv = nullptr;      // m targets v, same order
+    std::vector<int32_t> boff_h;  // bucket offsets [2^(31-Bs) + 1] (host)
+    uint32_t* slabS = nullptr;  // G x n packed registers (4 simulations of one bucket per word)
+    uint8_t* slabC = nullptr;   // G x n change nibbles of the last slab pass
+    uint4* slabX = nullptr;     // [G] salts of the group's simulations
+    uint4* slabHJ = nullptr;    // [G] hash(j) of the group's simulations
+    int4* slabG = nullptr;      // [G] {first simulation s0, count, bucket, byte mask}
+    std::vector<int4> slabG_h;
+    std::vector<uint32_t> Xs_h; // sorted salts (host copy)
+    int slab_passes = 0;        // in-place full passes per build in slab form (IM_SLAB_PASSES; 0 = off, the default: measured slower)
+    int64_t slab_min_m = 8 << 20;  // graphs with fewer edges keep the row-major full sweeps (IM_SLAB_MIN_M)
     int4* fbig = nullptr;       // work units {u, eb, ee} of the rows with > FIRST_BIG out-edges (<= FIRST_CHUNK edges each)
     int32_t n_fbig = 0;
     // sketches
@@ -212,6 +225,11 @@ int setup_first(int J, int* blocks_per_sm);  // smem opt-in + occupancy of the f
 // register init + first sweep (gather, im_first.cu): writes every row, its change mask and chunk bits
 cudaError_t launch_first(Ctx& c, uint32_t* cm_out, uint32_t* bits_out, IterCounters* ctr, bool blocked, bool from_memory);
 cudaError_t launch_list_big_rows(Ctx& c, int4* units, int* count);  // units == nullptr: count only
+// slab form of the first `passes` full sweeps of a build (im_slab.cu): group table for the current salts,
+// then init + passes + transpose into M / cm_out / bits_out
+inline size_t slab_stride(int32_t n) { return ((size_t)n + 31) & ~(size_t)31; }  // entries per group slab
+int slab_group_count(Ctx& c);  // fills c.slabG_h; number of groups, or 0 when the slab path does not apply
+cudaError_t launch_slab_build(Ctx& c, bool blocked, int passes, uint32_t* cm_out, uint32_t* bits_out);
 bool rows_path(const Ctx& c);  // constant threshold: long rows bucket-ordered (h >> Bs), bucket tables
 int sort_shift(int B0);        // Bs for a threshold's B0
 

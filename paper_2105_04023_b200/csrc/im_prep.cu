@@ -391,6 +391,100 @@ __global__ void __launch_bounds__(BLOCK) k_pscatter(PartIn in, int nseg, const i
     }
 }
 
+// ---------------------------------------------------------------- bucket-major edge list (im_slab.cu)
+// All edges grouped by the salt bucket h >> Bs of their hash (<= 256 buckets): an edge can only be live in the
+// simulations whose salt lies in its bucket, so the full sweeps of a build decompose into one independent
+// subproblem per bucket (im_slab.cu).  One counting pass and one shared-memory-staged partition pass
+// (k_pscatter's scheme with the bucket as the digit): brec[pos] = {u, h}, bv[pos] = v.
+__global__ void __launch_bounds__(BLOCK) k_bcount(int64_t m, const uint2* __restrict__ fwd, int Bs, int32_t* __restrict__ counts) {
+    __shared__ int hist[256];
+    hist[threadIdx.x] = 0;  // BLOCK == 256
+    __syncthreads();
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) atomicAdd(&hist[fwd[e].y >> Bs], 1);
+    __syncthreads();
+    if (hist[threadIdx.x]) atomicAdd(&counts[threadIdx.x], hist[threadIdx.x]);
+}
+
+__global__ void __launch_bounds__(BLOCK) k_bscatter(int64_t m, const int32_t* __restrict__ src, const uint2* __restrict__ fwd, int Bs,
+                                                    int32_t* __restrict__ cursor, uint2* __restrict__ orec, int32_t* __restrict__ ov) {
+    __shared__ int hist[256], loff[256], gbase[256];
+    extern __shared__ __align__(16) unsigned char dyn[];
+    uint2* srec = reinterpret_cast<uint2*>(dyn);
+    int* sv = reinterpret_cast<int*>(dyn + PT * sizeof(uint2));
+    unsigned char* sdig = dyn + PT * (sizeof(uint2) + sizeof(int));
+    __shared__ int sW[BLOCK / 32];
+    __shared__ int tot;
+    const int64_t nunits = (m + PT - 1) / PT;
+    for (int64_t un = blockIdx.x; un < nunits; un += gridDim.x) {
+        __syncthreads();
+        hist[threadIdx.x] = 0;
+        __syncthreads();
+        const int64_t e0 = un * PT, e1 = min(m, e0 + (int64_t)PT);
+        constexpr int PU = PT / BLOCK;
+        uint2 ff[PU];
+        int uu[PU];
+#pragma unroll
+        for (int k = 0; k < PU; k++) {
+            const int64_t e = e0 + k * BLOCK + threadIdx.x;
+            ff[k] = e < e1 ? fwd[e] : make_uint2(0u, 0u);
+            uu[k] = e < e1 ? src[e] : -1;
+        }
+#pragma unroll
+        for (int k = 0; k < PU; k++)
+            if (uu[k] >= 0) atomicAdd(&hist[ff[k].y >> Bs], 1);
+        __syncthreads();
+        const int c = hist[threadIdx.x];
+        loff[threadIdx.x] = block_excl_scan(c, sW, &tot);
+        gbase[threadIdx.x] = c ? atomicAdd(&cursor[threadIdx.x], c) : 0;
+        hist[threadIdx.x] = loff[threadIdx.x];
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < PU; k++) {
+            if (uu[k] < 0) continue;
+            const int d = ff[k].y >> Bs;
+            const int q = atomicAdd(&hist[d], 1);
+            srec[q] = make_uint2((uint32_t)uu[k], ff[k].y);
+            sv[q] = (int)ff[k].x;
+            sdig[q] = (unsigned char)d;
+        }
+        __syncthreads();
+        for (int q = threadIdx.x; q < (int)(e1 - e0); q += blockDim.x) {
+            const int d = sdig[q];
+            const int pos = gbase[d] + (q - loff[d]);
+            orec[pos] = srec[q];
+            ov[pos] = sv[q];
+        }
+    }
+}
+
+// boff_h[0 .. nb] (host) and c.brec / c.bv (device) from the finished forward records and their sources
+static cudaError_t bucket_partition(Ctx& c, const int32_t* src, int32_t* cnt256) {
+    cudaError_t e;
+    const int nb = 1 << (31 - c.Bs);
+    if ((e = cudaMemsetAsync(cnt256, 0, 256 * sizeof(int32_t), c.stream))) return e;
+    k_bcount<<<c.num_sms * 8, BLOCK, 0, c.stream>>>(c.m, c.fwd, c.Bs, cnt256);
+    if ((e = LAUNCHED(c))) return e;
+    int32_t hc[256];
+    if ((e = cudaMemcpyAsync(hc, cnt256, sizeof hc, cudaMemcpyDeviceToHost, c.stream))) return e;
+    if ((e = cudaStreamSynchronize(c.stream))) return e;
+    c.boff_h.assign(nb + 1, 0);
+    int32_t cur[256] = {};
+    for (int b = 0; b < nb; b++) {
+        cur[b] = c.boff_h[b];
+        c.boff_h[b + 1] = c.boff_h[b] + hc[b];
+    }
+    if ((e = cudaMemcpyAsync(cnt256, cur, sizeof cur, cudaMemcpyHostToDevice, c.stream))) return e;
+    static bool attr = false;
+    if (!attr) {
+        if ((e = cudaFuncSetAttribute(k_bscatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PSCAT_SMEM))) return e;
+        attr = true;
+    }
+    k_bscatter<<<c.num_sms * 5, BLOCK, PSCAT_SMEM, c.stream>>>(c.m, src, c.fwd, c.Bs, cnt256, c.brec, c.bv);
+    if ((e = LAUNCHED(c))) return e;
+    return cudaStreamSynchronize(c.stream);  // cur is read by the copy above
+}
+
 // unit starts of k_place: partition p = vertices [p << LB, (p+1) << LB) covers [roff[p << LB], roff[...])
 __global__ void __launch_bounds__(BLOCK) k_seg_units_roff(int n, int LB, int NP, const int32_t* __restrict__ roff, int chunk,
                                                           int32_t* __restrict__ ustart) {
@@ -890,6 +984,7 @@ static cudaError_t prep_rows(Ctx& c, const int32_t* tgt, int32_t* indeg, void** 
     int32_t* ustart = cnt2 + PSEG_MAX;               // unit starts (<= PSEG_MAX + 1, or NP + 1 for k_place)
     k_src<<<grid_for(c, (int64_t)n * 32), BLOCK, 0, c.stream>>>(n, c.off, src);
     if ((e = LAUNCHED(c))) return e;
+    if (c.brec && (e = bucket_partition(c, src, cnt2))) return e;  // before the passes below reuse src
     {
         const int32_t zm[2] = {0, (int32_t)c.m};
         if ((e = cudaMemcpyAsync(seg, zm, sizeof zm, cudaMemcpyHostToDevice, c.stream))) return e;
