@@ -405,31 +405,48 @@ __global__ void __launch_bounds__(BLOCK, 5) k_first(FirstArgs a) {
                 __syncwarp();
             }
         }
-        // first 32 records of the next vertex are prefetched while the current one is processed
-        uint2 nf = make_uint2(0, 0);
-        uint32_t nT = 0;
-        {
-            const int eb0 = off_w[0], ee0 = off_w[1];
-            if (ee0 - eb0 <= FIRST_BIG && eb0 + lane < ee0 && !(thr && ee0 - eb0 <= 32)) {
-                nf = ld_stream(&a.fwd[eb0 + lane]);
-                nT = CONST_T ? a.T0 : ld_stream(&a.fwdT[eb0 + lane]);
+        // The rows left for the warp, in order: every row (then rows for k_first_big / empty rows are skipped
+        // below), or with thread rows only those of 33..FIRST_BIG out-edges, found 32 vertices at a time by a
+        // ballot (they are a few percent of a skewed graph's vertices).  The first 32 records of the next row
+        // are prefetched while the current one is processed.
+        const int nvb = end - base;
+        int it_i = -1, it_i0 = -32;
+        uint32_t it_mk = 0u;
+        auto next_row = [&]() -> int {
+            if (!thr) return ++it_i;
+            while (!it_mk) {
+                it_i0 += 32;
+                if (it_i0 >= nvb) return nvb;
+                const int i = it_i0 + lane;
+                const int d = i < nvb ? off_w[i + 1] - off_w[i] : 0;
+                it_mk = __ballot_sync(IM_FULL, d > 32 && d <= FIRST_BIG);
             }
-        }
-        for (int u = base; u < end; ++u) {
-            const int eb = off_w[u - base], ee = off_w[u - base + 1];
+            const int r = it_i0 + __ffs(it_mk) - 1;
+            it_mk &= it_mk - 1;
+            return r;
+        };
+        auto prefetch = [&](int i, uint2& f, uint32_t& T) {
+            f = make_uint2(0, 0);
+            T = 0;
+            if (i >= nvb) return;
+            const int eb1 = off_w[i], ee1 = off_w[i + 1];
+            if (ee1 - eb1 <= FIRST_BIG && eb1 + lane < ee1) {
+                f = ld_stream(&a.fwd[eb1 + lane]);
+                T = CONST_T ? a.T0 : ld_stream(&a.fwdT[eb1 + lane]);
+            }
+        };
+        uint2 nf;
+        uint32_t nT;
+        int cur_i = next_row();
+        prefetch(cur_i, nf, nT);
+        while (cur_i < nvb) {
+            const int u = base + cur_i;
+            const int eb = off_w[cur_i], ee = off_w[cur_i + 1];
             const uint2 cf = nf;
             const uint32_t cT = nT;
-            nf = make_uint2(0, 0);
-            nT = 0;
-            if (u + 1 < end) {
-                const int eb1 = off_w[u + 1 - base], ee1 = off_w[u + 2 - base];
-                if (ee1 - eb1 <= FIRST_BIG && eb1 + lane < ee1 && !(thr && ee1 - eb1 <= 32)) {
-                    nf = ld_stream(&a.fwd[eb1 + lane]);
-                    nT = CONST_T ? a.T0 : ld_stream(&a.fwdT[eb1 + lane]);
-                }
-            }
+            cur_i = next_row();
+            prefetch(cur_i, nf, nT);
             if (ee - eb > FIRST_BIG) continue;  // done by k_first_big
-            if (thr && ee - eb <= 32) continue;  // done above (first_thread), or empty
             if (ee == eb) {  // no out-edge: the row keeps its value (init rows and zeroed masks are written before)
                 if (MEM) {
                     if (lane < W) a.cm_out[(size_t)u * W + lane] = 0u;
