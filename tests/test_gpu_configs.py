@@ -226,10 +226,11 @@ def test_c5_grid_point(J, p, t):
         return
     # no digest for this point yet: per-pair oracle definitions on sampled registers, rebuilt registers and
     # the per-simulation reach of the selected seeds, then an explicit xfail naming the missing digest
-    sampled_register_check(n, off, tgt, pr, J, 1, 200, rng_seed=J)
+    ns = 200 if p < 0.05 else 32  # a sampled register at p = 0.1 is a BFS over ~40% of the graph
+    sampled_register_check(n, off, tgt, pr, J, 1, ns, rng_seed=J)
     s, sc = im.im_select_seeds(100, t)
     log = im.im_get_step_log(100)
     assert list(sc) == [x["sigma_count"] / J for x in log]
-    rebuilt_register_check(n, off, tgt, pr, J, 1, s, log, 200, 4, J + 1)
+    rebuilt_register_check(n, off, tgt, pr, J, 1, s, log, ns, 4, J + 1)
     sampled_seed_reach_check(n, off, tgt, pr, J, 1, np.asarray(s, np.int32), [0, J - 1])
     digest_missing(tag)
