@@ -111,6 +111,7 @@ int ensure_device() {
     g.max_blocks_bfs = std::max(1, bb) * g.num_sms;
     g.trace = getenv("IM_TRACE") != nullptr;
     if (const char* pf = getenv("IM_PULL_FRAC")) g.pull_frac = atof(pf);
+    if (const char* pw = getenv("IM_PULL_FRAC_WIDE")) g.pull_frac_wide = atof(pw);
     if (const char* tr = getenv("IM_THREAD_ROWS")) g.thread_rows = atoi(tr) != 0;
     if (const char* sp = getenv("IM_SLAB_PASSES")) g.slab_passes = atoi(sp);
     if (const char* sm = getenv("IM_SLAB_MIN_M")) g.slab_min_m = atoll(sm);
@@ -433,6 +434,11 @@ int simulate(bool blocked) {
     auto t0 = clk::now();
     const size_t W = (size_t)g.J / 32;
     const double eps_c = g.eps_c;
+    // Wide candidate windows (p = 0.1: J/8 simulations per edge): a pushed edge walks its window with a chain of
+    // dependent loads per 8-byte word and costs ~2x a gathered one (C3 graph, J = 1024: 61M pushed edges 38 ms,
+    // all 68M gathered 23 ms), so the gather is kept until the frontier's in-edges fall below 0.3 m (0.15 / 0.3 / 0.5 / 0.97: 118.7 / 118.9 / 123.8 / 142.9 ms of sweep kernels)
+    const bool wide_windows = g.constT && ((int64_t)g.J << g.B0) > ((int64_t)DENSE_WIN << 31);
+    const double pull_frac = wide_windows ? std::min(g.pull_frac, g.pull_frac_wide) : g.pull_frac;
     g.sync_sweeps = eps_c > 0.0;
     if (g.sync_sweeps) TRY(dalloc(g.Mold, (size_t)g.n * g.J));
     g.built_eps_c = eps_c;
@@ -495,7 +501,7 @@ int simulate(bool blocked) {
         if (!((double)hc.changed / (double)g.n > eps_c)) return false;  // Alg. 2 line 3 (eps_c = 0: nothing changed)
         if (hc.next_items == 0) return false;                            // changed vertices without in-edges
         n_items = hc.next_items;
-        edges += (double)hc.next_edges > g.pull_frac * (double)g.m ? g.m : (int64_t)hc.next_edges;
+        edges += (double)hc.next_edges > pull_frac * (double)g.m ? g.m : (int64_t)hc.next_edges;
         return true;
     };
     // k_sweep_small for the rest of the build once the frontier (after sweep s, counters hc) is small:
@@ -558,7 +564,7 @@ int simulate(bool blocked) {
         CK(cudaEventRecord(g.pev[sl][0], g.stream));
         // direction-optimised: a frontier whose in-edges cover most of the graph is swept by a full
         // in-place gather (every row owned by one warp, no atomics); sparse frontiers are pushed
-        const bool gather = !piped && s > 1 && !g.sync_sweeps && (double)edges_in > g.pull_frac * (double)g.m;
+        const bool gather = !piped && s > 1 && !g.sync_sweeps && (double)edges_in > pull_frac * (double)g.m;
         gathers[sl] = gather;
         if (s == 1 && slab_G > 0) {  // init + the first full sweeps in bucket-major slabs (im_slab.cu)
             CK(launch_slab_build(g, blocked, g.slab_passes, g.cm[1], g.bits[1]));
@@ -601,7 +607,7 @@ int simulate(bool blocked) {
                 if (r == 2) continue;
             }
             // enter the pipelined mode once the next frontier is clearly sparse (no gather sweep any more)
-            piped = g.pipeline && !g.sync_sweeps && s >= 2 && (double)hc.next_edges < 0.25 * g.pull_frac * (double)g.m;
+            piped = g.pipeline && !g.sync_sweeps && s >= 2 && (double)hc.next_edges < 0.25 * pull_frac * (double)g.m;
             continue;
         }
         CK(cudaMemcpyAsync(&hpc[sl], ctr, sizeof(IterCounters), cudaMemcpyDeviceToHost, g.stream));

@@ -140,6 +140,7 @@ struct Ctx {
     int slice_min_bfs = SEG;   // BFS levels: out-rows longer than this are enumerated by hash slices (IM_SLICE_MIN_BFS)
     int64_t list_max = 65536;  // cap of the lazy argmax candidate list length (IM_LIST_MAX)
     bool thread_rows = true;   // first / gather sweeps: rows <= 32 out-edges one per lane (IM_THREAD_ROWS=0: warp per row)
+    double pull_frac_wide = 0.3;  // the same threshold when the candidate windows are wide (> DENSE_WIN simulations; IM_PULL_FRAC_WIDE)
     double pull_frac = 0.97;   // gather sweep when the push frontier's in-edges exceed this share of m (IM_PULL_FRAC)
     IterCounters* ctr = nullptr;   // [2]
     // selection buffers
