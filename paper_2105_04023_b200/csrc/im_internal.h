@@ -16,7 +16,10 @@ constexpr int SEG = 256;        // max edges per work item (a segment of one ver
 constexpr int TAB_MIN = SEG;  // rows longer than this get a bucket offset table (rows path)
 constexpr int MAX_SLICES = 8; // hash slices per long row (more non-zero mask words: the whole row)
 constexpr int BSL = 32;       // bucket slices per long row with a bucket table (k_slices_buckets)
-constexpr int DENSE_WIN = 32;   // windows wider than this many simulations take the warp-cooperative path
+#ifndef IM_DENSE_WIN
+#define IM_DENSE_WIN 32
+#endif
+constexpr int DENSE_WIN = IM_DENSE_WIN;   // windows wider than this many simulations take the warp-cooperative path
 constexpr int BLOCK = 256;      // threads per block of the persistent work-list kernels
 #ifndef IM_FIRST_BIG
 #define IM_FIRST_BIG 2048
