@@ -93,6 +93,13 @@ __device__ __forceinline__ void merge_word(const FirstArgs& a, const uint32_t* s
     if (__vmaxu4(row[w], val) != row[w]) smem_vmax(&row[w], val);
 }
 
+#ifndef IM_FIRST_DENSE_WIN
+#define IM_FIRST_DENSE_WIN 48
+#endif
+// gather sweeps: windows wider than this are walked by the whole warp.  Unlike the push sweeps and BFS levels (whose
+// per-lane path keeps a window's live bits in one 32-bit word, DENSE_WIN <= 32) the per-lane gather walks any width.
+constexpr int FIRST_DENSE_WIN = IM_FIRST_DENSE_WIN;
+
 // `e` is this lane's edge (or -1); the loop around it must be warp-uniform.  Windows wider than
 // DENSE_WIN simulations (w close to 1) are walked by the whole warp, one word per lane.
 template <bool CONST_T, bool BLOCKED, bool MEM>
@@ -130,7 +137,7 @@ __device__ __forceinline__ void gather_rec(const FirstArgs& a, const uint32_t* s
             }
         }
     }
-    const bool dense = hi - lo > DENSE_WIN;
+    const bool dense = hi - lo > FIRST_DENSE_WIN;
     if (!dense && lo < hi)
         for (int w = lo >> 2; w <= (hi - 1) >> 2; ++w) merge_word<BLOCKED, MEM>(a, sX, sHJ, sVis, row, v, hv, h, T, lo, hi, w);
     uint32_t dmask = __ballot_sync(IM_FULL, dense);
@@ -174,7 +181,7 @@ __device__ __forceinline__ void gather_multi(const FirstArgs& a, const uint32_t*
         if (lo[k] < hi[k]) {
             wcount++;
             if (!MEM) hv[k] = vhash(a, f[k].x);
-            else if (hi[k] - lo[k] <= DENSE_WIN) {  // the first two window words (a 4-simulation window spans two words 3/4 of the time)
+            else if (hi[k] - lo[k] <= FIRST_DENSE_WIN) {  // the first two window words (a 4-simulation window spans two words 3/4 of the time)
                 const uint32_t* rv = reinterpret_cast<const uint32_t*>(a.M) + (size_t)f[k].x * (a.J >> 2);
                 pre[k] = rv[lo[k] >> 2];
                 if (((hi[k] - 1) >> 2) > (lo[k] >> 2)) pre2[k] = rv[(lo[k] >> 2) + 1];
@@ -183,11 +190,11 @@ __device__ __forceinline__ void gather_multi(const FirstArgs& a, const uint32_t*
     }
 #pragma unroll
     for (int k = 0; k < U; k++) {
-        if (lo[k] < hi[k] && hi[k] - lo[k] <= DENSE_WIN)
+        if (lo[k] < hi[k] && hi[k] - lo[k] <= FIRST_DENSE_WIN)
             for (int w = lo[k] >> 2; w <= (hi[k] - 1) >> 2; ++w)
                 merge_word<BLOCKED, MEM>(a, sX, sHJ, sVis, row, f[k].x, hv[k], f[k].y, T[k], lo[k], hi[k], w, w - (lo[k] >> 2) < 2,
                                          w == (lo[k] >> 2) ? pre[k] : pre2[k]);
-        uint32_t dmask = __ballot_sync(IM_FULL, hi[k] - lo[k] > DENSE_WIN);
+        uint32_t dmask = __ballot_sync(IM_FULL, hi[k] - lo[k] > FIRST_DENSE_WIN);
         while (dmask) {
             const int l = __ffs(dmask) - 1;
             dmask &= dmask - 1;

@@ -56,18 +56,6 @@ __global__ void k_src(int32_t n, const int32_t* __restrict__ off, int32_t* __res
         for (int e = off[u] + lane; e < off[u + 1]; e += 32) src[e] = (int32_t)u;
 }
 
-// in-degree histogram (reverse row lengths); equal targets of a warp are aggregated first
-__global__ void k_indeg(int64_t m, const int32_t* __restrict__ tgt, int32_t* __restrict__ indeg) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int lane = threadIdx.x & 31;
-    for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < m; base += stride) {
-        const int64_t e = base + threadIdx.x;
-        const int v = e < m ? tgt[e] : -1;
-        const uint32_t peers = __match_any_sync(IM_FULL, v);
-        if (v >= 0 && lane == __ffs(peers) - 1) atomicAdd(&indeg[v], __popc(peers));
-    }
-}
-
 // ---------------------------------------------------------------- exclusive scan of int32 (3 passes)
 // tile = SCAN_T = BLOCK * 16 values: per-tile sums, a one-block scan of the tile sums, per-tile scan
 // with the tile's offset.  Sums fit int32 (CSR offsets, segment counts <= m < 2^31).
@@ -259,8 +247,8 @@ __device__ __forceinline__ uint2 row_rec(const RowSortArgs& a, int64_t e, uint32
 // shared memory, reserves each digit's run with one global atomic, stages the unit sorted by digit in
 // shared memory and writes every run contiguously (coalesced).  The order inside a reverse row is
 // immaterial except for the bucket order of long rows (k_rev_rows).
-constexpr int PT = 3072;    // records per partition-pass unit (staged in dynamic shared memory: 3072 x 13 B, 5 blocks / SM)
-constexpr size_t PSCAT_SMEM = (size_t)PT * (sizeof(uint2) + sizeof(int) + 1);
+constexpr int PT = 3072;    // records per partition-pass unit (staged in dynamic shared memory: 3072 x 9 B)
+constexpr size_t PSCAT_SMEM = (size_t)PT * (sizeof(uint2) + 1);
 constexpr int PCH = 16384;  // staged records per k_place work unit
 constexpr int NPMAX = 4096; // vertices per k_place partition (shared counters)
 constexpr int PSEG_MAX = 65536;  // segments after two passes (256^2)
@@ -291,15 +279,15 @@ __global__ void __launch_bounds__(BLOCK) k_seg_units(int nseg, const int32_t* __
     if (threadIdx.x == 0) ustart[nseg] = carry;
 }
 
-// the input record / target of position e of a pass: pass 0 reads the forward edges (src, fwd), later
-// passes the previous pass's output
+// the record {u, v} of position e of a pass: pass 0 reads the input edges (src, tgt), later passes the
+// previous pass's output.  The passes carry 8 bytes per edge; the edge hash is recomputed once, by k_place
+// (carrying {u, h} + v moved 12 bytes per edge and pass).
 struct PartIn {
-    const int32_t* src;  // pass 0: source vertex per forward position, else null
-    const uint2* fwd;    // pass 0: forward records {v, h}
-    const uint2* rec;    // later passes: {u, h}
-    const int32_t* v;    // later passes: targets
-    __device__ __forceinline__ int32_t tv(int e) const { return src ? (int32_t)fwd[e].x : v[e]; }
-    __device__ __forceinline__ uint2 rc(int e) const { return src ? make_uint2((uint32_t)src[e], fwd[e].y) : rec[e]; }
+    const int32_t* src;  // pass 0: source vertex per input position, else null
+    const int32_t* tgt;  // pass 0: targets
+    const uint2* rec;    // later passes: {u, v}
+    __device__ __forceinline__ int32_t tv(int e) const { return src ? tgt[e] : (int32_t)rec[e].y; }
+    __device__ __forceinline__ uint2 uv(int e) const { return src ? make_uint2((uint32_t)src[e], (uint32_t)tgt[e]) : rec[e]; }
 };
 
 __global__ void __launch_bounds__(BLOCK) k_pcount(PartIn in, int nseg, const int32_t* __restrict__ soff,
@@ -335,12 +323,11 @@ __global__ void __launch_bounds__(BLOCK) k_pscan(int nseg, const int32_t* __rest
 
 __global__ void __launch_bounds__(BLOCK) k_pscatter(PartIn in, int nseg, const int32_t* __restrict__ soff,
                                                     const int32_t* __restrict__ ustart, int shift, int32_t* __restrict__ cursor,
-                                                    uint2* __restrict__ orec, int32_t* __restrict__ ov) {
+                                                    uint2* __restrict__ orec) {
     __shared__ int hist[256], loff[256], gbase[256];
     extern __shared__ __align__(16) unsigned char dyn[];
     uint2* srec = reinterpret_cast<uint2*>(dyn);
-    int* sv = reinterpret_cast<int*>(dyn + PT * sizeof(uint2));
-    unsigned char* sdig = dyn + PT * (sizeof(uint2) + sizeof(int));
+    unsigned char* sdig = dyn + PT * sizeof(uint2);
     __shared__ int sW[BLOCK / 32];
     __shared__ int tot, sseg;
     const int nunits = ustart[nseg];
@@ -351,45 +338,44 @@ __global__ void __launch_bounds__(BLOCK) k_pscatter(PartIn in, int nseg, const i
         __syncthreads();
         const int sg = sseg, e0 = soff[sg] + (un - ustart[sg]) * PT, e1 = min(soff[sg + 1], e0 + PT);
         constexpr int PU = PT / BLOCK;  // records per thread, all loads in flight together
-        int vv[PU];
+        uint2 rr[PU];
+        bool hv[PU];
 #pragma unroll
         for (int k = 0; k < PU; k++) {
             const int e = e0 + k * BLOCK + threadIdx.x;
-            vv[k] = e < e1 ? in.tv(e) : -1;
+            hv[k] = e < e1;
+            rr[k] = hv[k] ? in.uv(e) : make_uint2(0, 0);
         }
 #pragma unroll
         for (int k = 0; k < PU; k++)
-            if (vv[k] >= 0) atomicAdd(&hist[(vv[k] >> shift) & 255], 1);
+            if (hv[k]) atomicAdd(&hist[(rr[k].y >> shift) & 255], 1);
         __syncthreads();
         const int c = hist[threadIdx.x];
         loff[threadIdx.x] = block_excl_scan(c, sW, &tot);  // contains the barriers
         gbase[threadIdx.x] = c ? atomicAdd(&cursor[(size_t)sg * 256 + threadIdx.x], c) : 0;
         hist[threadIdx.x] = loff[threadIdx.x];  // now the local placement cursor
         __syncthreads();
-        uint2 rr[PU];
-#pragma unroll
-        for (int k = 0; k < PU; k++) {
-            const int e = e0 + k * BLOCK + threadIdx.x;
-            rr[k] = vv[k] >= 0 ? in.rc(e) : make_uint2(0, 0);
-        }
 #pragma unroll
         for (int k = 0; k < PU; k++) {  // stage the unit sorted by digit
-            if (vv[k] < 0) continue;
-            const int d = (vv[k] >> shift) & 255;
+            if (!hv[k]) continue;
+            const int d = (rr[k].y >> shift) & 255;
             const int q = atomicAdd(&hist[d], 1);
             srec[q] = rr[k];
-            sv[q] = vv[k];
             sdig[q] = (unsigned char)d;
         }
         __syncthreads();
         for (int q = threadIdx.x; q < e1 - e0; q += blockDim.x) {  // each digit's run is contiguous here and there
             const int d = sdig[q];
-            const int pos = gbase[d] + (q - loff[d]);
-            orec[pos] = srec[q];
-            ov[pos] = sv[q];
+            orec[gbase[d] + (q - loff[d])] = srec[q];
         }
     }
 }
+
+// in-degrees from the partitioned records: a unit of <= PCH records of one 2^LB-vertex partition is counted per
+// target in shared memory and added with one global atomic per distinct target (a histogram of the unpartitioned
+// targets costs one returning atomic per warp-distinct target, 4.3 ms on the 520M-edge RMAT)
+__global__ void __launch_bounds__(BLOCK) k_part_indeg(int LB, int NP, const int32_t* __restrict__ soff,
+                                                      const int32_t* __restrict__ ustart, PartIn in, int32_t* __restrict__ indeg);
 
 // ---------------------------------------------------------------- bucket-major edge list (im_slab.cu)
 // All edges grouped by the salt bucket h >> Bs of their hash (<= 256 buckets): an edge can only be live in the
@@ -533,10 +519,32 @@ __global__ void __launch_bounds__(BLOCK) k_place(int n, int LB, int NP, const in
         }
         __syncthreads();
         for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-            const int v = in.tv(e);
+            const uint2 r = in.uv(e);
+            const int v = (int)r.y;
             const int pos = atomicAdd(&cnt[v - vb], 1);
-            (roff[v + 1] - roff[v] > TAB_MIN ? ltmp : rev)[pos] = in.rc(e);
+            (roff[v + 1] - roff[v] > TAB_MIN ? ltmp : rev)[pos] = make_uint2(r.x, edge_hash(r.x, r.y));
         }
+    }
+}
+
+__global__ void __launch_bounds__(BLOCK) k_part_indeg(int LB, int NP, const int32_t* __restrict__ soff,
+                                                      const int32_t* __restrict__ ustart, PartIn in, int32_t* __restrict__ indeg) {
+    __shared__ int cnt[NPMAX];
+    __shared__ int sp;
+    const int nunits = ustart[NP];
+    const int V = 1 << LB;
+    for (int un = blockIdx.x; un < nunits; un += gridDim.x) {
+        __syncthreads();
+        if (threadIdx.x == 0) sp = unit_segment(ustart, NP, un);
+        for (int i = threadIdx.x; i < V; i += blockDim.x) cnt[i] = 0;
+        __syncthreads();
+        const int p = sp;
+        const int64_t vb = (int64_t)p << LB;
+        const int e0 = soff[p] + (un - ustart[p]) * PCH, e1 = min(soff[p + 1], e0 + PCH);
+        for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) atomicAdd(&cnt[in.tv(e) - vb], 1);
+        __syncthreads();
+        for (int i = threadIdx.x; i < V; i += blockDim.x)
+            if (cnt[i]) atomicAdd(&indeg[vb + i], cnt[i]);
     }
 }
 
@@ -925,10 +933,6 @@ static cudaError_t prep_rows(Ctx& c, const int32_t* tgt, int32_t* indeg, void** 
     int* cnt = (int*)(lf + n);  // [0] long-row count, [1] batch cursor, [2] table count
     int32_t* cursor = (int32_t*)scr[1];
     uint2* rtmp = (uint2*)scr[2];
-    k_indeg<<<grid_for(c, c.m), BLOCK, 0, c.stream>>>(c.m, tgt, indeg);
-    if ((e = LAUNCHED(c))) return e;
-    size_t t2 = tb;
-    if ((e = scan_exclusive(c, indeg, c.roff, n + 1, scr[4], t2))) return e;
     if ((e = cudaMemsetAsync(cursor, 0, (size_t)n * sizeof(int32_t), c.stream))) return e;
     // huge rows: lists (forward, reverse), their counters and unit starts
     const int max_huge = (int)(c.m / HCH + 2);
@@ -975,9 +979,7 @@ static cudaError_t prep_rows(Ctx& c, const int32_t* tgt, int32_t* indeg, void** 
     const int NP = (int)(((int64_t)n + (1 << LB) - 1) >> LB);
     int32_t* src = (int32_t*)scr[3];
     uint2* recA = (uint2*)scr[5];
-    int32_t* vA = (int32_t*)scr[6];
     uint2* recB = rtmp;
-    int32_t* vB = src;  // free once pass 0 has read the sources
     int32_t* seg = (int32_t*)scr[7];                 // segment offsets of the current pass (<= 65536 + 1)
     int32_t* nseg_off = seg + (PSEG_MAX + 1);        // of the next pass
     int32_t* cnt2 = nseg_off + (PSEG_MAX + 1);       // digit counts / cursors per (segment, digit)
@@ -990,13 +992,12 @@ static cudaError_t prep_rows(Ctx& c, const int32_t* tgt, int32_t* indeg, void** 
         if ((e = cudaMemcpyAsync(seg, zm, sizeof zm, cudaMemcpyHostToDevice, c.stream))) return e;
         if ((e = cudaStreamSynchronize(c.stream))) return e;  // zm goes out of scope
     }
-    PartIn in{src, c.fwd, nullptr, nullptr};
+    PartIn in{src, tgt, nullptr};
     const uint2* rec_final = nullptr;
     int nseg = 1;
     for (int k = 0; k < L; k++) {
         const int shift = NB - 8 * (k + 1);
         uint2* orec = (k & 1) ? recB : recA;
-        int32_t* ov = (k & 1) ? vB : vA;
         k_seg_units<<<1, BLOCK, 0, c.stream>>>(nseg, seg, PT, ustart);
         if ((e = LAUNCHED(c))) return e;
         if ((e = cudaMemsetAsync(cnt2, 0, (size_t)nseg * 256 * sizeof(int32_t), c.stream))) return e;
@@ -1010,15 +1011,22 @@ static cudaError_t prep_rows(Ctx& c, const int32_t* tgt, int32_t* indeg, void** 
             if ((e = cudaFuncSetAttribute(k_pscatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PSCAT_SMEM))) return e;
             attr = true;
         }
-        k_pscatter<<<c.num_sms * 5, BLOCK, PSCAT_SMEM, c.stream>>>(in, nseg, seg, ustart, shift, cnt2, orec, ov);
+        k_pscatter<<<c.num_sms * 6, BLOCK, PSCAT_SMEM, c.stream>>>(in, nseg, seg, ustart, shift, cnt2, orec);
         if ((e = LAUNCHED(c))) return e;
         std::swap(seg, nseg_off);
         nseg *= 256;
-        in = PartIn{nullptr, nullptr, orec, ov};
+        in = PartIn{nullptr, nullptr, orec};
         rec_final = orec;
     }
     // long reverse rows land in a buffer the passes no longer need (not the one k_place reads)
     if (L >= 1 && rec_final == recB) rtmp = recA;
+    // in-degrees and reverse offsets from the partitioned records (segment p of the last pass = partition p)
+    k_seg_units<<<1, BLOCK, 0, c.stream>>>(NP, seg, PCH, ustart);
+    if ((e = LAUNCHED(c))) return e;
+    k_part_indeg<<<c.num_sms * 8, BLOCK, 0, c.stream>>>(LB, NP, seg, ustart, in, indeg);
+    if ((e = LAUNCHED(c))) return e;
+    size_t t2 = tb;
+    if ((e = scan_exclusive(c, indeg, c.roff, n + 1, scr[4], t2))) return e;
     k_seg_units_roff<<<1, BLOCK, 0, c.stream>>>(n, LB, NP, c.roff, PCH, ustart);
     if ((e = LAUNCHED(c))) return e;
     k_place<<<c.num_sms * 8, BLOCK, 0, c.stream>>>(n, LB, NP, ustart, c.roff, cursor, in, c.rev, rtmp);
@@ -1044,8 +1052,8 @@ cudaError_t prep_scratch_sizes(Ctx& c, size_t* sz) {
     sz[1] = ((size_t)c.n + 1) * 4;
     sz[2] = rows_path(c) ? m * 8 : 8;
     sz[3] = rows_path(c) ? m * 4 : 8;  // edge sources of the transpose
-    sz[5] = rows_path(c) ? m * 8 : 8;  // staged records {u, h}
-    sz[6] = rows_path(c) ? m * 4 : 8;  // their targets
+    sz[5] = rows_path(c) ? m * 8 : 8;  // partition-pass records {u, v}
+    sz[6] = 8;  // unused
     sz[7] = (4 * (size_t)PSEG_MAX + 8) * 4;  // segment tables, digit counts, unit starts of the transpose
     sz[8] = ((size_t)(m / HCH + 2) * 259 + 32) * 4;  // huge-row lists, unit starts, counters
     size_t t = 0;

@@ -1,0 +1,3 @@
+set -x
+timeout 900 python -m pytest tests -m gpu -x -q -k "test_gpu_parity or c1 or c2 or c3 or bfs_paths or abi" > gpurun_out/pytest46.log 2>&1; echo rc=$?; tail -3 gpurun_out/pytest46.log
+IM_BENCH_CONFIG=c4 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/b46_c4.json 2> gpurun_out/b46_c4.err; echo bench rc=$?

@@ -25,6 +25,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--K", type=int, default=100)
 ap.add_argument("--points", default="all", choices=["all", "corners"])
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--only", help="comma-separated J:p[:t] filters, e.g. 256:0.1,128:0.1:0.05 (A/B runs)")
 a = ap.parse_args()
 import statistics  # noqa: E402
 
@@ -42,6 +43,9 @@ m = len(tgt)
 grid = gen.C5_GRID
 if a.points == "corners":
     grid = [g for g in grid if g[0] in (64, 1024) and g[2] in (0.01, 0.3)]
+if a.only:
+    flt = [tuple(float(x) for x in f.split(":")) for f in a.only.split(",")]
+    grid = [g for g in grid if any(g[0] == f[0] and g[1] == f[1] and (len(f) < 3 or g[2] == f[2]) for f in flt)]
 rows = []
 for p in sorted({g[1] for g in grid}):
     pr = np.full(m, p, np.float32)
