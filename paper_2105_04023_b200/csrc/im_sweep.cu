@@ -437,68 +437,112 @@ __global__ void k_compact(int32_t n, int J, int slice_min, const uint32_t* __res
 __global__ void k_slices_buckets(int J, int B, int KB, const uint32_t* __restrict__ Xs, const int32_t* __restrict__ big,
                                  const uint32_t* __restrict__ mask, const int32_t* __restrict__ offs, int4* __restrict__ items,
                                  IterCounters* ctr, const int32_t* __restrict__ tidx, const int32_t* __restrict__ tab, int nbk) {
-    __shared__ uint32_t sBm[BLOCK / 32][8];
+    __shared__ uint32_t sM[BLOCK / 32][32];
+    __shared__ int sBs[257];  // first simulation of every bucket (the salts are sorted: the simulations of a bucket are a range)
     __shared__ int sRs[BLOCK / 32][BSL], sRe[BLOCK / 32][BSL];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, W = J >> 5;
-    const int NBW = ((1 << KB) + 31) >> 5;  // words of the bucket set (<= 8)
+    const int NBK = 1 << KB, NBW = (NBK + 31) >> 5;  // buckets, words of the bucket set (<= 8)
     const int nb = ctr->big;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < nb; i += nwarps) {
-        const int v = big[i];
-        const int rb = offs[v], re = offs[v + 1];
-        const int t = __ldg(&tidx[v]);
-        if (lane < 8) sBm[wib][lane] = 0u;
-        __syncwarp();
-        const uint32_t m = lane < W ? mask[(size_t)v * W + lane] : 0u;
-        for (uint32_t tt = m; tt; tt &= tt - 1) {
-            const uint32_t b = __ldg(&Xs[32 * lane + __ffs(tt) - 1]) >> B;
-            atomicOr(&sBm[wib][b >> 5], 1u << (b & 31));
+    if ((int64_t)blockIdx.x * (BLOCK / 32) >= nb) return;  // no row for any warp of this block
+    for (int b = threadIdx.x; b <= NBK; b += blockDim.x) {  // lower bound of bucket b among the sorted salts
+        int lo = 0, hi = J;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if ((__ldg(&Xs[mid]) >> B) < (uint32_t)b) lo = mid + 1; else hi = mid;
         }
+        sBs[b] = lo;
+    }
+    __syncthreads();
+    // One row per warp and block iteration; the block's rows reserve their items with ONE global atomic (a
+    // returning atomic per row on the same counter serialised ~300k rows of an early C4 sweep), the edge count
+    // is added once per block at the end.
+    __shared__ int sCnt[BLOCK / 32], sPos[BLOCK / 32];
+    __shared__ ull sEd[BLOCK / 32];
+    ull edges_acc = 0;  // thread 0
+    for (int64_t base = (int64_t)blockIdx.x * (BLOCK / 32); base < nb; base += (int64_t)gridDim.x * (BLOCK / 32)) {
+        const int64_t i = base + wib;
+        const bool act = i < nb;
+        int v = 0, rb = 0, re = 0, t = -1;
+        if (act) {
+            v = big[i];
+            rb = offs[v];
+            re = offs[v + 1];
+            t = __ldg(&tidx[v]);
+        }
+        sM[wib][lane] = act && lane < W ? mask[(size_t)v * W + lane] : 0u;
         __syncwarp();
-        const uint32_t x = lane < NBW ? sBm[wib][lane] : 0u;
+        // bucket lane + 32 k is marked iff the mask holds a simulation of its range (a loop over the set
+        // simulations with one salt load and one shared atomic each cost up to 32 dependent trips per lane)
+        uint32_t x = 0u;
+        for (int k = 0; k < NBW; k++) {
+            const int b = lane + 32 * k;
+            bool hit = false;
+            if (b < NBK) {
+                const int s = sBs[b], e = sBs[b + 1];
+                if (s < e) {
+                    const int w0 = s >> 5, w1 = (e - 1) >> 5;
+                    for (int w = w0; w <= w1 && !hit; ++w)
+                        hit = (sM[wib][w] & bit_range(w == w0 ? (s & 31) : 0, w == w1 ? ((e - 1) & 31) : 31)) != 0u;
+                }
+            }
+            const uint32_t xk = __ballot_sync(IM_FULL, hit);
+            if (lane == k) x = xk;
+        }
         uint32_t prev = __shfl_up_sync(IM_FULL, x, 1), next = __shfl_down_sync(IM_FULL, x, 1);
         if (lane == 0) prev = 0u;
         if (lane == 31) next = 0u;
         const uint32_t starts = x & ~((x << 1) | (prev >> 31)), ends = x & ~((x >> 1) | (next << 31));
         const int ns = __popc(starts), ne = __popc(ends);
         const int R = __reduce_add_sync(IM_FULL, ns), cov = __reduce_add_sync(IM_FULL, __popc(x));
-        if (R == 0) continue;
-        if (t < 0 || R > BSL || 4 * cov >= 3 * (1 << KB)) {  // the whole row
-            const int nsg = (re - rb + SEG - 1) / SEG;
-            int pos = 0;
-            if (lane == 0) {
-                pos = atomicAdd(&ctr->next_items, nsg);
-                atomicAdd(&ctr->next_edges, (ull)(re - rb));
+        const bool whole = R > 0 && (t < 0 || R > BSL || 4 * cov >= 3 * (1 << KB));  // the whole row
+        int b0 = 0, len = 0, nsl = 0, ninc = 0, ntot = 0;
+        ull es = 0;
+        if (whole) {
+            ntot = (re - rb + SEG - 1) / SEG;
+            es = (ull)(re - rb);
+        } else if (R > 0) {
+            // the k-th run starts at the k-th start bit and ends at the k-th end bit
+            int sp = warp_incl_scan(ns, lane) - ns, ep = warp_incl_scan(ne, lane) - ne;
+            for (uint32_t tt = starts; tt; tt &= tt - 1) sRs[wib][sp++] = 32 * lane + __ffs(tt) - 1;
+            for (uint32_t tt = ends; tt; tt &= tt - 1) sRe[wib][ep++] = 32 * lane + __ffs(tt) - 1;
+            __syncwarp();
+            if (lane < R) {
+                const int32_t* tb = tab + (int64_t)t * nbk;
+                b0 = __ldg(&tb[sRs[wib][lane]]);
+                len = __ldg(&tb[sRe[wib][lane] + 1]) - b0;
             }
-            pos = __shfl_sync(IM_FULL, pos, 0);
-            for (int k = lane; k < nsg; k += 32) items[pos + k] = make_int4(v, rb + k * SEG, min(rb + (k + 1) * SEG, re), 0);
-            continue;
+            nsl = (len + SEG - 1) / SEG;
+            ninc = warp_incl_scan(nsl, lane);
+            ntot = __shfl_sync(IM_FULL, ninc, 31);
+            es = (ull)__reduce_add_sync(IM_FULL, len);
         }
-        // the k-th run starts at the k-th start bit and ends at the k-th end bit
-        int sp = warp_incl_scan(ns, lane) - ns, ep = warp_incl_scan(ne, lane) - ne;
-        for (uint32_t tt = starts; tt; tt &= tt - 1) sRs[wib][sp++] = 32 * lane + __ffs(tt) - 1;
-        for (uint32_t tt = ends; tt; tt &= tt - 1) sRe[wib][ep++] = 32 * lane + __ffs(tt) - 1;
-        __syncwarp();
-        int b0 = 0, len = 0;
-        if (lane < R) {
-            const int32_t* tb = tab + (int64_t)t * nbk;
-            b0 = __ldg(&tb[sRs[wib][lane]]);
-            len = __ldg(&tb[sRe[wib][lane] + 1]) - b0;
+        if (lane == 0) {
+            sCnt[wib] = ntot;
+            sEd[wib] = es;
         }
-        const int nsl = (len + SEG - 1) / SEG;
-        const int ninc = warp_incl_scan(nsl, lane);
-        const int ntot = __shfl_sync(IM_FULL, ninc, 31);
-        const int es = __reduce_add_sync(IM_FULL, len);
-        int pos = 0;
-        if (lane == 0 && ntot) {
-            pos = atomicAdd(&ctr->next_items, ntot);
-            atomicAdd(&ctr->next_edges, (ull)es);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int tot = 0;
+#pragma unroll
+            for (int w = 0; w < BLOCK / 32; w++) {
+                sPos[w] = tot;
+                tot += sCnt[w];
+                edges_acc += sEd[w];
+            }
+            const int g0 = tot ? atomicAdd(&ctr->next_items, tot) : 0;
+#pragma unroll
+            for (int w = 0; w < BLOCK / 32; w++) sPos[w] += g0;
         }
-        pos = __shfl_sync(IM_FULL, pos, 0);
-        int p = pos + ninc - nsl;
-        for (int s0 = b0; s0 < b0 + len; s0 += SEG) items[p++] = make_int4(v, s0, min(s0 + SEG, b0 + len), 0);
-        __syncwarp();
+        __syncthreads();
+        const int pos = sPos[wib];
+        if (whole) {
+            for (int k = lane; k < ntot; k += 32) items[pos + k] = make_int4(v, rb + k * SEG, min(rb + (k + 1) * SEG, re), 0);
+        } else if (ntot) {
+            int p = pos + ninc - nsl;
+            for (int s0 = b0; s0 < b0 + len; s0 += SEG) items[p++] = make_int4(v, s0, min(s0 + SEG, b0 + len), 0);
+        }
     }
+    if (threadIdx.x == 0 && edges_acc) atomicAdd(&ctr->next_edges, edges_acc);
 }
 
 // ------------------------------------------------------------------ small-frontier sweeps in one cluster
