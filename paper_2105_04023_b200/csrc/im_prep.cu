@@ -247,7 +247,13 @@ __device__ __forceinline__ uint2 row_rec(const RowSortArgs& a, int64_t e, uint32
 // shared memory, reserves each digit's run with one global atomic, stages the unit sorted by digit in
 // shared memory and writes every run contiguously (coalesced).  The order inside a reverse row is
 // immaterial except for the bucket order of long rows (k_rev_rows).
-constexpr int PT = 3072;    // records per partition-pass unit (staged in dynamic shared memory: 3072 x 9 B)
+#ifndef PREP_PT
+#define PREP_PT 3072
+#endif
+#ifndef PSCAT_BPS
+#define PSCAT_BPS 8
+#endif
+constexpr int PT = PREP_PT;    // records per partition-pass unit (staged in dynamic shared memory: 3072 x 9 B)
 constexpr size_t PSCAT_SMEM = (size_t)PT * (sizeof(uint2) + 1);
 constexpr int PCH = 16384;  // staged records per k_place work unit
 constexpr int NPMAX = 4096; // vertices per k_place partition (shared counters)
@@ -301,6 +307,7 @@ __global__ void __launch_bounds__(BLOCK) k_pcount(PartIn in, int nseg, const int
         hist[threadIdx.x] = 0;  // BLOCK == 256
         __syncthreads();
         const int sg = sseg, e0 = soff[sg] + (un - ustart[sg]) * PT, e1 = min(soff[sg + 1], e0 + PT);
+#pragma unroll 4
         for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) atomicAdd(&hist[(in.tv(e) >> shift) & 255], 1);
         __syncthreads();
         if (hist[threadIdx.x]) atomicAdd(&counts[(size_t)sg * 256 + threadIdx.x], hist[threadIdx.x]);
@@ -499,6 +506,7 @@ __global__ void __launch_bounds__(BLOCK) k_place(int n, int LB, int NP, const in
                                                  const int32_t* __restrict__ roff, int32_t* __restrict__ cursor, PartIn in,
                                                  uint2* __restrict__ rev, uint2* __restrict__ ltmp) {
     __shared__ int cnt[NPMAX];
+    __shared__ unsigned char lng[NPMAX];  // the target's reverse row is long (sorted later from ltmp)
     __shared__ int sp;
     const int nunits = ustart[NP];
     const int V = 1 << LB;
@@ -511,18 +519,24 @@ __global__ void __launch_bounds__(BLOCK) k_place(int n, int LB, int NP, const in
         const int64_t vb = (int64_t)p << LB;
         const int rb = roff[vb], re = roff[min((int64_t)n, vb + V)];
         const int e0 = rb + (un - ustart[p]) * PCH, e1 = min(re, e0 + PCH);
+#pragma unroll 4
         for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) atomicAdd(&cnt[in.tv(e) - vb], 1);
         __syncthreads();
         for (int i = threadIdx.x; i < V; i += blockDim.x) {  // this unit's run of target vb + i
             const int c = cnt[i];
-            cnt[i] = c ? roff[vb + i] + atomicAdd(&cursor[vb + i], c) : 0;
+            if (c) {
+                const int r0 = roff[vb + i];
+                lng[i] = roff[vb + i + 1] - r0 > TAB_MIN;
+                cnt[i] = r0 + atomicAdd(&cursor[vb + i], c);
+            }
         }
         __syncthreads();
+#pragma unroll 4
         for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
             const uint2 r = in.uv(e);
-            const int v = (int)r.y;
-            const int pos = atomicAdd(&cnt[v - vb], 1);
-            (roff[v + 1] - roff[v] > TAB_MIN ? ltmp : rev)[pos] = make_uint2(r.x, edge_hash(r.x, r.y));
+            const int i = (int)r.y - (int)vb;
+            const int pos = atomicAdd(&cnt[i], 1);
+            (lng[i] ? ltmp : rev)[pos] = make_uint2(r.x, edge_hash(r.x, r.y));
         }
     }
 }
@@ -541,6 +555,7 @@ __global__ void __launch_bounds__(BLOCK) k_part_indeg(int LB, int NP, const int3
         const int p = sp;
         const int64_t vb = (int64_t)p << LB;
         const int e0 = soff[p] + (un - ustart[p]) * PCH, e1 = min(soff[p + 1], e0 + PCH);
+#pragma unroll 4
         for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) atomicAdd(&cnt[in.tv(e) - vb], 1);
         __syncthreads();
         for (int i = threadIdx.x; i < V; i += blockDim.x)
@@ -989,7 +1004,7 @@ static cudaError_t prep_rows(Ctx& c, const int32_t* tgt, int32_t* indeg, void** 
             if ((e = cudaFuncSetAttribute(k_pscatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PSCAT_SMEM))) return e;
             attr = true;
         }
-        k_pscatter<<<c.num_sms * 6, BLOCK, PSCAT_SMEM, c.stream>>>(in, nseg, seg, ustart, shift, cnt2, orec);
+        k_pscatter<<<c.num_sms * PSCAT_BPS, BLOCK, PSCAT_SMEM, c.stream>>>(in, nseg, seg, ustart, shift, cnt2, orec);
         if ((e = LAUNCHED(c))) return e;
         std::swap(seg, nseg_off);
         nseg *= 256;
