@@ -510,7 +510,7 @@ int simulate(bool blocked) {
         const int sl = s & 1;
         if (g.sync_sweeps || g.small_sweep_edges <= 0 || (long long)hc.next_edges > g.small_sweep_edges) return 0;
         CK(cudaEventRecord(g.pev[sl][0], g.stream));
-        CK(launch_sweep_small(g, g.items[sl], hc.next_items, s + 1, blocked, g.small_sweep_edges));
+        CK(launch_sweep_small(g, g.items[sl], hc.next_items, hc.changed, s + 1, blocked, g.small_sweep_edges));
         CK(cudaEventRecord(g.pev[sl][1], g.stream));
         SweepSmallOut so;
         TRY(readback(g.sso, sizeof so, &so));

@@ -253,7 +253,7 @@ cudaError_t launch_sweep(Ctx& c, const int4* items, int n_items, const uint32_t*
                          uint32_t* bits_out, IterCounters* ctr, bool blocked, const IterCounters* nin = nullptr);
 cudaError_t launch_commit(Ctx& c, const uint32_t* bits_new);
 // the remaining sweeps of a build from the work items of sweep s0 - 1's compaction, in one cluster launch
-cudaError_t launch_sweep_small(Ctx& c, const int4* items, int n_items, int s0, bool blocked, long long max_edges);
+cudaError_t launch_sweep_small(Ctx& c, const int4* items, int n_items, int n_changed, int s0, bool blocked, long long max_edges);
 cudaError_t launch_slices_big(Ctx& c, const int32_t* big, const uint32_t* mask, const int32_t* offs, const uint2* rec,
                               int4* items_out, IterCounters* ctr, bool whole_dense);
 cudaError_t launch_estimate(Ctx& c, double* out);

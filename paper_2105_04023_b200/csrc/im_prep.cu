@@ -255,6 +255,7 @@ __device__ __forceinline__ uint2 row_rec(const RowSortArgs& a, int64_t e, uint32
 #endif
 constexpr int PT = PREP_PT;    // records per partition-pass unit (staged in dynamic shared memory: 3072 x 9 B)
 constexpr size_t PSCAT_SMEM = (size_t)PT * (sizeof(uint2) + 1);
+constexpr size_t BSCAT_SMEM = (size_t)PT * (sizeof(uint2) + sizeof(int) + 1);  // k_bscatter stages {u, h}, v and the digit
 constexpr int PCH = 16384;  // staged records per k_place work unit
 constexpr int NPMAX = 4096; // vertices per k_place partition (shared counters)
 constexpr int PSEG_MAX = 65536;  // segments after two passes (256^2)
@@ -470,10 +471,10 @@ static cudaError_t bucket_partition(Ctx& c, const int32_t* src, int32_t* cnt256)
     if ((e = cudaMemcpyAsync(cnt256, cur, sizeof cur, cudaMemcpyHostToDevice, c.stream))) return e;
     static bool attr = false;
     if (!attr) {
-        if ((e = cudaFuncSetAttribute(k_bscatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PSCAT_SMEM))) return e;
+        if ((e = cudaFuncSetAttribute(k_bscatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BSCAT_SMEM))) return e;
         attr = true;
     }
-    k_bscatter<<<c.num_sms * 5, BLOCK, PSCAT_SMEM, c.stream>>>(c.m, src, c.fwd, c.Bs, cnt256, c.brec, c.bv);
+    k_bscatter<<<c.num_sms * 5, BLOCK, BSCAT_SMEM, c.stream>>>(c.m, src, c.fwd, c.Bs, cnt256, c.brec, c.bv);
     if ((e = LAUNCHED(c))) return e;
     return cudaStreamSynchronize(c.stream);  // cur is read by the copy above
 }
