@@ -55,6 +55,8 @@ _vp, _i32, _i64, _u64, _f64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, c
 SIGNATURES = {
     "im_load_csr": (ctypes.c_int, [_i32, _vp, _vp, _vp]),
     "im_load_csr_device": (ctypes.c_int, [_i32, _i64, _vp, _vp, _vp]),
+    "im_load_csr_const": (ctypes.c_int, [_i32, _vp, _vp, ctypes.c_float]),
+    "im_load_csr_const_device": (ctypes.c_int, [_i32, _i64, _vp, _vp, ctypes.c_float]),
     "im_build_sketches": (ctypes.c_int, [_i32, _u64]),
     "im_estimate": (ctypes.c_int, [_vp]),
     "im_estimate_device": (ctypes.c_int, [_vp]),
@@ -138,6 +140,17 @@ class Library:
     def im_load_csr_device(self, n: int, m: int, d_offsets, d_targets, d_probs) -> None:
         """Device arrays (torch CUDA tensors or raw pointers), already resident in HBM."""
         self._check(self.L.im_load_csr_device(n, m, _dptr(d_offsets), _dptr(d_targets) or None, _dptr(d_probs) or None))
+
+    def im_load_csr_const(self, n: int, offsets, targets, w: float) -> None:
+        """Host arrays and one scalar IC probability for every edge (the paper's constant-w settings)."""
+        o, po = _host(offsets, np.int32)
+        t, pt = _host(targets, np.int32)
+        if len(o) != n + 1 or len(t) != int(o[-1]):
+            raise IMError(IM_EINVAL, "array lengths do not match n / offsets[n]")
+        self._check(self.L.im_load_csr_const(n, po, pt or None, float(w)))
+
+    def im_load_csr_const_device(self, n: int, m: int, d_offsets, d_targets, w: float) -> None:
+        self._check(self.L.im_load_csr_const_device(n, m, _dptr(d_offsets), _dptr(d_targets) or None, float(w)))
 
     def im_build_sketches(self, J: int, seed: int) -> None:
         self._check(self.L.im_build_sketches(J, seed & 0xFFFFFFFFFFFFFFFF))

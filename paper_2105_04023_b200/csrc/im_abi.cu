@@ -215,7 +215,8 @@ int readback(const void* dptr, size_t bytes, void* host) {
 }
 
 // ----------------------------------------------------------- a0: load + edge prep
-int load_common(int32_t n, int64_t m, const int32_t* d_off_src, const int32_t* d_tgt, const float* d_prob) {
+// d_prob == nullptr: every edge has probability w_const (im_load_csr_const; m > 1, so the rows path never reads d_prob)
+int load_common(int32_t n, int64_t m, const int32_t* d_off_src, const int32_t* d_tgt, const float* d_prob, float w_const = 0.0f) {
     auto t0 = clk::now();
     int64_t launches0 = g.launches;
     // offsets: own copy
@@ -225,7 +226,7 @@ int load_common(int32_t n, int64_t m, const int32_t* d_off_src, const int32_t* d
     TRY(dalloc(dflags, 4));
     CK(cudaMemsetAsync(dflags, 0, 4 * sizeof(int), g.stream));
     CK(launch_validate(g, g.off, d_tgt, d_prob, dflags));
-    if (m > 0) CK(launch_const_check(g, d_prob, dflags + 1));
+    if (m > 0 && d_prob) CK(launch_const_check(g, d_prob, dflags + 1));
     int hf[4];
     TRY(readback(dflags, sizeof hf, hf));
     if (hf[0]) {
@@ -235,8 +236,8 @@ int load_common(int32_t n, int64_t m, const int32_t* d_off_src, const int32_t* d
     g.constT = (m == 0) || hf[1] == 0;
     g.T0 = 0;
     if (g.constT && m > 0) {
-        float w0;
-        TRY(readback(d_prob, sizeof(float), &w0));
+        float w0 = w_const;
+        if (d_prob) TRY(readback(d_prob, sizeof(float), &w0));
         g.T0 = live_threshold(w0);
     }
     // constant threshold: rows ordered by h >> B0 (im_prep.cu)
@@ -724,6 +725,54 @@ int im_load_csr_device(int32_t n, int64_t m, const int32_t* d_offsets, const int
     g.n = n;
     g.m = m;
     int r = load_common(n, m, d_offsets, d_targets, d_probs);
+    if (r) reset_graph_state();
+    return r;
+}
+
+int im_load_csr_const(int32_t n, const int32_t* offsets, const int32_t* targets, float w) {
+    TRY(ensure_device());
+    if (n < 1) return fail(IM_EINVAL, "n must be >= 1 (got %d)", n);  // before offsets[n] is read
+    if (!offsets || (!targets && offsets[n] > 0)) return fail(IM_EINVAL, "null pointer argument");
+    if (!(w >= 0.0f && w <= 1.0f)) return fail(IM_EINVAL, "invalid graph: probabilities not finite in [0,1]");
+    TRY(check_csr_args(n, offsets[n]));
+    if (offsets[0] != 0) return fail(IM_EINVAL, "offsets[0] must be 0");
+    const int64_t m = offsets[n];
+    if (m <= 1) {  // no bucket-ordered rows below two edges: the array path
+        const float p1 = w;
+        return im_load_csr(n, offsets, targets, &p1);
+    }
+    reset_graph_state();
+    int32_t*& d_off = g.t_off;
+    int32_t*& d_tgt = g.t_tgt;
+    TRY(dalloc(d_off, (size_t)n + 1));
+    TRY(dalloc(d_tgt, (size_t)m));
+    CK(cudaMemcpyAsync(d_off, offsets, ((size_t)n + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, g.stream));
+    CK(cudaMemcpyAsync(d_tgt, targets, (size_t)m * sizeof(int32_t), cudaMemcpyHostToDevice, g.stream));
+    g.n = n;
+    g.m = m;
+    int r = load_common(n, m, d_off, d_tgt, nullptr, w);
+    if (r) reset_graph_state();
+    return r;
+}
+
+int im_load_csr_const_device(int32_t n, int64_t m, const int32_t* d_offsets, const int32_t* d_targets, float w) {
+    TRY(ensure_device());
+    if (!d_offsets || (m > 0 && !d_targets)) return fail(IM_EINVAL, "null pointer argument");
+    if (!(w >= 0.0f && w <= 1.0f)) return fail(IM_EINVAL, "invalid graph: probabilities not finite in [0,1]");
+    TRY(check_csr_args(n, m));
+    reset_graph_state();
+    g.n = n;
+    g.m = m;
+    int r;
+    if (m <= 1) {  // the array path (a one-entry device array)
+        float*& d_prob = g.t_prob;
+        TRY(dalloc(d_prob, (size_t)1));
+        CK(cudaMemcpyAsync(d_prob, &w, sizeof(float), cudaMemcpyHostToDevice, g.stream));
+        TRY(sync());
+        r = load_common(n, m, d_offsets, d_targets, d_prob);
+    } else {
+        r = load_common(n, m, d_offsets, d_targets, nullptr, w);
+    }
     if (r) reset_graph_state();
     return r;
 }

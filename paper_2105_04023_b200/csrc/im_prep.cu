@@ -34,8 +34,10 @@ __global__ void k_validate(int32_t n, int64_t m, const int32_t* __restrict__ off
     for (int64_t e = tid; e < m; e += stride) {
         int32_t v = tgt[e];
         if (v < 0 || v >= n) f |= 2;
-        float w = prob[e];
-        if (!(w >= 0.0f && w <= 1.0f)) f |= 4;  // also rejects NaN
+        if (prob) {  // null: one scalar probability, checked on the host (im_load_csr_const)
+            float w = prob[e];
+            if (!(w >= 0.0f && w <= 1.0f)) f |= 4;  // also rejects NaN
+        }
     }
     if (f) atomicOr(flags, f);
 }

@@ -140,6 +140,47 @@ def test_estimate_parity():
 
 
 # ------------------------------------------------------------------ greedy (Alg. 1)
+def test_constant_w_entry_point_vs_oracle():
+    """im_load_csr_const (one scalar w, the paper's constant-probability settings PAPER.md:457-462) against the
+    oracle run on the explicit array: registers, seeds, scores and reach; degenerate sizes and a bad w."""
+    rng = np.random.default_rng(77)
+    for g, (w, J) in enumerate([(0.005, 64), (0.01, 128), (0.1, 256), (1.0, 32), (0.0, 32), (0.3, 96)]):
+        n = int(rng.integers(2, 2500))
+        m = int(rng.integers(2, 6 * n))
+        off, tgt, pr = brute.random_graph(rng, n, m, w)
+        seed = int(rng.integers(0, 2**63))
+        im.im_load_csr_const(n, off, tgt, w)
+        im.im_build_sketches(J, seed)
+        st = im.im_get_stats()
+        assert st["const_threshold"] == 1
+        Mo, _ = oracle.simulate(n, off, tgt, pr, J, seed)
+        assert np.array_equal(im.im_get_registers(n, J), Mo), (g, n, m, w)
+        K = min(n, 8)
+        s, sc = im.im_select_seeds(K, 0.05)
+        r = oracle.select_seeds(n, off, tgt, pr, J, seed, K, 0.05, want_vis=True)
+        assert list(s) == list(r["seeds"]) and list(sc) == list(r["scores"])
+        assert np.array_equal(reach_bool(n, J), r["vis"].astype(bool))
+    # no edge / one edge (the array path inside), device pointers
+    for off, tgt in (([0, 0, 0], []), ([0, 1, 1], [1])):
+        im.im_load_csr_const(2, off, tgt, 0.5)
+        im.im_build_sketches(32, 3)
+        Mo, _ = oracle.simulate(2, np.array(off, np.int32), np.array(tgt, np.int32), np.full(len(tgt), 0.5, np.float32), 32, 3)
+        assert np.array_equal(im.im_get_registers(2, 32), Mo)
+    import torch
+    n, m = 500, 3000
+    off, tgt, pr = brute.random_graph(rng, n, m, 0.05)
+    d_off, d_tgt = torch.from_numpy(off).cuda(), torch.from_numpy(tgt).cuda()
+    torch.cuda.synchronize()
+    im.im_load_csr_const_device(n, len(tgt), d_off, d_tgt, 0.05)
+    im.im_build_sketches(64, 5)
+    Mo, _ = oracle.simulate(n, off, tgt, pr, 64, 5)
+    assert np.array_equal(im.im_get_registers(n, 64), Mo)
+    for w in (float("nan"), 1.5, -0.1):
+        with pytest.raises(im.IMError) as e:
+            im.im_load_csr_const(n, off, tgt, w)
+        assert e.value.code == im.IM_EINVAL
+
+
 def compare_select(n, off, tgt, pr, J, seed, K, t):
     im.im_load_csr(n, off, tgt, pr)
     im.im_build_sketches(J, seed)
