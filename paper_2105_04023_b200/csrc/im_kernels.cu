@@ -20,7 +20,10 @@ namespace im {
 // ============================================================ a5: Eq. 2 estimate
 // A warp sums EV rows per iteration (16-byte loads, all EV rows' loads in flight before the
 // reductions); lane k finishes row k, so the EV exp2 run in parallel.  Exact integer sums.
-constexpr int EV = 4;
+#ifndef IM_EV
+#define IM_EV 4
+#endif
+constexpr int EV = IM_EV;
 template <bool SUMS>
 __global__ void k_estimate(int32_t n, int32_t J, const uint32_t* __restrict__ M32, double* __restrict__ out, int32_t* sums) {
     const int lane = threadIdx.x & 31, nch = J >> 4;
@@ -29,13 +32,16 @@ __global__ void k_estimate(int32_t n, int32_t J, const uint32_t* __restrict__ M3
     for (int64_t v0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * EV; v0 < n; v0 += warps * EV) {
         uint32_t s[EV];
 #pragma unroll
-        for (int k = 0; k < EV; k++) {
-            s[k] = 0u;
-            if (v0 + k < n)
-                for (int c = lane; c < nch; c += 32) {
-                    const uint4 x = __ldcs(&M16[(v0 + k) * nch + c]);
-                    s[k] += __vsadu4(x.x, 0u) + __vsadu4(x.y, 0u) + __vsadu4(x.z, 0u) + __vsadu4(x.w, 0u);
-                }
+        for (int k = 0; k < EV; k++) s[k] = 0u;
+        for (int c0 = 0; c0 < nch; c0 += 32) {  // the EV rows' loads of this chunk column issued before any is summed
+            const int c = c0 + lane;
+            uint4 x[EV];
+#pragma unroll
+            for (int k = 0; k < EV; k++)
+                x[k] = (c < nch && v0 + k < n) ? __ldcs(&M16[(v0 + k) * nch + c]) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+            for (int k = 0; k < EV; k++)
+                s[k] += __vsadu4(x[k].x, 0u) + __vsadu4(x[k].y, 0u) + __vsadu4(x[k].z, 0u) + __vsadu4(x[k].w, 0u);
         }
 #pragma unroll
         for (int o = 16; o; o >>= 1)
