@@ -233,7 +233,9 @@ int load_common(int32_t n, int64_t m, const int32_t* d_off_src, const int32_t* d
         return fail(IM_EINVAL, "invalid graph:%s%s%s", (hf[0] & 1) ? " offsets (offsets[0]!=0, decreasing, or offsets[n]!=m)" : "",
                     (hf[0] & 2) ? " targets out of [0,n)" : "", (hf[0] & 4) ? " probabilities not finite in [0,1]" : "");
     }
-    g.constT = (m == 0) || hf[1] == 0;
+    // one scalar threshold only with m > 1 (the bucket-ordered rows path); a single edge takes the per-edge path, which
+    // keeps its threshold next to the record (it wrote through the unallocated threshold array before: fixed, tested)
+    g.constT = (m == 0) || (hf[1] == 0 && m > 1);
     g.T0 = 0;
     if (g.constT && m > 0) {
         float w0 = w_const;

@@ -64,6 +64,8 @@ def test_degenerate_graphs():
     cases = [
         (1, [0, 0], [], []),
         (5, [0] * 6, [], []),
+        (2, [0, 1, 1], [1], [0.5]),                   # a single edge (per-edge threshold path)
+        (3, [0, 0, 1, 1], [0], [1.0]),
         (4, [0, 2, 3, 3, 4], [1, 1, 2, 0], [0.0, 0.0, 0.0, 0.0]),
         (4, [0, 2, 3, 3, 4], [1, 1, 2, 0], [1.0, 1.0, 1.0, 1.0]),
         (3, [0, 2, 4, 4], [0, 0, 1, 1], [1.0, 0.7, 1.0, 0.2]),
